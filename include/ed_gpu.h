@@ -1,0 +1,234 @@
+/*
+ * ed_gpu.h — C ABI of the B200-native EinDecomp executor (libed_gpu.so).
+ *
+ * Drop-in replacement for the reference's CPU executor
+ *
+ *   run_report_t execute(exec_graph_t const&, placement_t const&,
+ *                        map<int, tensor_relation_t> const&,
+ *                        exec_options_t const& = {});     // runtime.h:45-49
+ *                                                          // runtime.cc:382-451
+ *
+ * The reference planner (parse -> optimize_dag -> explode -> place_all,
+ * runtime.cc:511-516) is unchanged; its products are flattened into
+ * ed_plan_c by the host adapter and executed here on
+ * B200s. No C++ or torch types cross this boundary: plain structs,
+ * pointers and sizes, status codes plus a NUL-terminated message.
+ *
+ * Ownership: the caller owns every host buffer; the library owns device
+ * memory, streams, CUDA graphs and NCCL communicators. ed_prepare deep-
+ * copies the plan. A context / plan handle is single-caller (not
+ * re-entrant); calls block until their work is complete, like execute().
+ *
+ * Multi-GPU: one process per GPU. Rank r runs the exec vertices whose
+ * machine (placement_t::machine_of, placement.h:9-15) maps to it
+ * (machine % world == r); remote dependencies move over NCCL.
+ */
+#ifndef ED_GPU_H
+#define ED_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ED_ABI_VERSION 1
+
+/* Errors. The adapter rethrows ED_ERR_PLAN as plan_error_t (setup.h:40-42),
+ * ED_ERR_EVAL as eval_error_t (setup.h:45-47; division by zero, ops.cc:10-14,
+ * detected on device), everything else as std::runtime_error. */
+typedef enum {
+  ED_OK = 0,
+  ED_ERR_USAGE = 1,
+  ED_ERR_PLAN = 2,
+  ED_ERR_EVAL = 4,
+  ED_ERR_CUDA = 5,
+  ED_ERR_NCCL = 6,
+  ED_ERR_OOM = 7,
+  ED_ERR_UNSUPPORTED = 8
+} ed_status;
+
+/* Arithmetic of the run (exec_options_t::f32, runtime.h:39-43, generalised).
+ *   FP64 : f64 storage, every op in double, folds in dep order — reproduces
+ *          the reference's default execute() bit for bit.
+ *   FP32 : f32 storage; non-contraction vertices reproduce the reference's
+ *          f32 mode bit for bit; contractions on fp32 CUDA cores.
+ *   TF32 : f32 storage; mul/sum contractions on tcgen05 kind::tf32.
+ *   BF16 : f32 storage, bf16 contraction operands (written by their
+ *          producers), tcgen05 kind::f16 with fp32 accumulation in TMEM. */
+typedef enum {
+  ED_PREC_FP32 = 0,
+  ED_PREC_TF32 = 1,
+  ED_PREC_BF16 = 2,
+  ED_PREC_FP64 = 3
+} ed_precision;
+
+/* Operator enums, in the order of ops.h:8-22. -1 = absent. */
+typedef enum { ED_JOIN_MUL = 0, ED_JOIN_ADD, ED_JOIN_SUB, ED_JOIN_DIV, ED_JOIN_SQDIFF, ED_JOIN_ABSDIFF } ed_join_op;
+typedef enum { ED_AGG_SUM = 0, ED_AGG_MAX } ed_agg_op;
+typedef enum { ED_MAP_RELU = 0, ED_MAP_EXP, ED_MAP_NEG, ED_MAP_SCALE, ED_MAP_IDENTITY } ed_map_op;
+
+/* exec_kind_t, execgraph.h:12 */
+typedef enum { ED_EXEC_INPUT_CHUNK = 0, ED_EXEC_JOIN = 1, ED_EXEC_REFINEMENT = 2 } ed_exec_kind;
+
+typedef enum { ED_DTYPE_F64 = 0, ED_DTYPE_F32 = 1 } ed_dtype;
+
+/* One EinGraph vertex: ein_vertex_t (einsum.h:42-47) + einsum_expr_t
+ * (einsum.h:9-38) + task_graph_t::d (decomp.h:21-30). Labels are interned
+ * as small non-negative ints (equal strings -> equal ids within a vertex). */
+typedef struct {
+  const char* name;
+  int32_t arity;            /* 0 = graph input, 1 = unary map, 2 = binary join */
+  int32_t join_op;          /* ed_join_op or -1 */
+  int32_t map_op;           /* ed_map_op or -1 */
+  int32_t agg_op;           /* ed_agg_op or -1 */
+  double scale_c;           /* unary_op_t::scale_c */
+  int32_t rank;             /* rank of bound */
+  const int64_t* bound;     /* b of this vertex */
+  int32_t rank_z, rank_x, rank_y;
+  const int32_t* lz;        /* out_labels */
+  const int32_t* lx;        /* in_labels[0] */
+  const int32_t* ly;        /* in_labels[1] (binary only) */
+  int32_t rank_d;
+  const int64_t* d;         /* exprs: over l_XY; inputs: storage partition */
+  int32_t inputs[2];        /* graph vertex ids, -1 when absent */
+} ed_vertex_c;
+
+/* exec_vertex_t (execgraph.h:14-34) + placement_t::machine_of. */
+typedef struct {
+  int32_t kind;             /* ed_exec_kind */
+  int32_t owner, producer, consumer, slot;
+  int32_t key_rank;
+  const int64_t* key;
+  int32_t chunk_rank;
+  const int64_t* chunk_bound;
+  int64_t fp, sz;
+  int32_t n_deps;
+  const int32_t* deps;      /* fixed order: refinements fold in this order */
+  int32_t machine;
+} ed_exec_vertex_c;
+
+typedef struct {
+  int32_t n_vertices;
+  const ed_vertex_c* vertices;
+  int32_t n_exec;
+  const ed_exec_vertex_c* exec;   /* ids = array positions, topological */
+  int32_t n_outputs;
+  const int32_t* outputs;         /* eingraph_t::outputs */
+  int32_t n_machines;             /* placement_t::n_machines */
+  double alpha;                   /* placement_t::alpha (max_site_cost) */
+} ed_plan_c;
+
+typedef struct {
+  int32_t precision;        /* ed_precision */
+  int32_t corrupt;          /* exec_options_t::corrupt test hook: +1 on one join output */
+  int32_t profile;          /* 1: time every launch with CUDA events (ed_kernel_stats) */
+  int32_t no_graph;         /* 1: launch eagerly instead of replaying a CUDA graph */
+  int32_t reserved[4];
+} ed_options_c;
+
+/* One input chunk (tensor_relation_t::chunks entry, relation.h:13-19),
+ * row-major over exec vertex exec_id's chunk_bound. */
+typedef struct {
+  int32_t exec_id;
+  int32_t dtype;            /* ed_dtype */
+  const void* data;
+  int64_t n;
+} ed_chunk_in_c;
+
+/* One whole input tensor of graph vertex vertex_id; the library performs
+ * chunk() (relation.cc:31-53) on the device. */
+typedef struct {
+  int32_t vertex_id;
+  int32_t dtype;
+  const void* data;
+  int64_t n;
+} ed_tensor_in_c;
+
+/* One graph output, assembled (relation.cc:55-78) row-major. */
+typedef struct {
+  int32_t vertex_id;
+  int32_t dtype;
+  void* data;
+  int64_t n;
+} ed_output_c;
+
+/* machine_counters_t, runtime.h:16-20 */
+typedef struct {
+  int64_t fp, sent, received;
+} ed_machine_c;
+
+/* run_report_t (runtime.h:27-37) minus the tensors (see ed_download). */
+typedef struct {
+  int32_t n_machines;        /* capacity of machines[] (caller-owned) */
+  ed_machine_c* machines;    /* counters equal the reference's whole-chunk accounting */
+  int64_t total_transferred;
+  int64_t wall_steps;
+  double max_site_cost;
+  double device_ms;          /* event-timed ed_run on this rank */
+  int64_t peer_bytes;        /* bytes this rank actually sent to peers */
+  double contraction_flops;  /* 2 * sum fp of mul/sum joins run by this rank */
+  int32_t gpu_launches;      /* kernels launched by this rank's ed_run */
+} ed_report_c;
+
+/* Per-launch-class timing from a profiled run (options.profile = 1). */
+typedef struct {
+  char name[64];             /* kernel class + graph vertex, e.g. "gemm_bf16:Z1" */
+  int32_t launches;
+  double ms;                 /* summed CUDA-event time */
+  double flops;              /* algorithmic flops summed over launches */
+  double bytes;              /* algorithmic HBM bytes summed over launches */
+} ed_kernel_stat_c;
+
+struct ed_ctx;
+struct ed_plan_h;
+
+int32_t ed_abi_version(void);
+
+/* NCCL bootstrap id (128 bytes) for world > 1, made on rank 0 and
+ * broadcast by the caller. */
+ed_status ed_nccl_unique_id(void* out, size_t len, char* err, size_t errlen);
+
+ed_status ed_ctx_create(int32_t device, int32_t rank, int32_t world,
+                        const void* nccl_id, size_t nccl_id_len,
+                        struct ed_ctx** out, char* err, size_t errlen);
+void ed_ctx_destroy(struct ed_ctx* ctx);
+
+/* Validates the plan (execute()'s checks, runtime.cc:388-395), maps each
+ * expression onto a kernel, allocates every chunk buffer in HBM, builds
+ * tensor maps and the transfer schedule, and records the CUDA graph. */
+ed_status ed_prepare(struct ed_ctx* ctx, const ed_plan_c* plan, const ed_options_c* options,
+                     struct ed_plan_h** out, char* err, size_t errlen);
+void ed_plan_destroy(struct ed_plan_h* h);
+
+/* Seed input chunks (engine_t ctor, runtime.cc:66-84): H2D + convert. */
+ed_status ed_upload(struct ed_plan_h* h, const ed_chunk_in_c* chunks, int32_t n,
+                    char* err, size_t errlen);
+/* Whole input tensors; chunked on device. */
+ed_status ed_upload_tensors(struct ed_plan_h* h, const ed_tensor_in_c* tensors, int32_t n,
+                            char* err, size_t errlen);
+
+/* Run every exec vertex of this rank; device-resident. report may be NULL. */
+ed_status ed_run(struct ed_plan_h* h, ed_report_c* report, char* err, size_t errlen);
+
+/* Assemble graph outputs from their final refinement layers (runtime.cc:432-448)
+ * and copy D2H. On rank r only outputs whose chunks this rank holds are valid
+ * unless world == 1; ed_download gathers to the calling rank when world > 1. */
+ed_status ed_download(struct ed_plan_h* h, ed_output_c* outputs, int32_t n,
+                      char* err, size_t errlen);
+
+/* Copy one exec vertex's produced chunk D2H (per-vertex parity tests).
+ * Returns ED_ERR_USAGE if the chunk is not resident on this rank. */
+ed_status ed_download_chunk(struct ed_plan_h* h, int32_t exec_id, int32_t dtype,
+                            void* data, int64_t n, char* err, size_t errlen);
+
+/* Per-launch-class timings of the last profiled ed_run. */
+ed_status ed_kernel_stats(struct ed_plan_h* h, ed_kernel_stat_c* out, int32_t cap,
+                          int32_t* n_out, char* err, size_t errlen);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ED_GPU_H */
