@@ -1,0 +1,305 @@
+"""Benchmark: EinSum-graph TFLOP/s of the B200 executor (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config bmm2]
+                    [--precision bf16] [--impl ours|reference]
+
+A step is one ed_run of the placed ExecGraph of the config graph (p=8, L=N,
+the reference planner's plan from plans/), inputs resident in HBM. `value`
+is contraction TFLOP/s = sum over mul/sum join kernels of 2*fp (SURVEY
+8(d)) / device time (CUDA events, max over ranks). `e2e` is the same metric
+through the C ABI with pinned host buffers: H2D of every input tensor,
+on-device chunking, ed_run, D2H of the assembled output, each step.
+For N > 1 run under torchrun (one process per GPU).
+"""
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "EinSum-graph TFLOP/s at 1/2/4/8 B200 and % of tensor peak vs CPU ref"
+CONFIG_DESC = {
+    "bmm2": "C2 batched contraction bij,bjk->bik b=64, 2048^2, two chained nodes (configs[1])",
+    "chain3": "C1 matmul chain ij,jk->ik x3 at 4096^2 (configs[0])",
+    "ffnn_big": "C3 FFNN batch 16384 hidden 8192, relu + row softmax (configs[2])",
+    "attn_big": "C4 attention s=4096 a=4096 h=32 d=128 (configs[3])",
+    "hoc": "C5 abcd,cdef->abef 128^4 (configs[4])",
+}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return d["bf16_tflops"], d.get("bf16_tflops_sustained"), d["hbm_gbs"], "measured"
+    except Exception:
+        return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[5 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def synthetic_inputs(plan, seed, dtype=np.float32):
+    """Synthetic data of the config's shape and distribution: integers in
+    [-4,4] for sum/mul-only graphs, U[-1,1) otherwise (runtime.cc:552-571)."""
+    rng = np.random.default_rng(seed)
+    out = {}
+    for vid in plan.input_vertices():
+        shape = plan.vertices[vid].bound
+        if plan.integer_valued():
+            a = rng.integers(-4, 5, size=shape, dtype=np.int8).astype(dtype)
+        else:
+            a = rng.random(size=shape, dtype=np.float32).astype(dtype) * 2 - 1
+        out[vid] = a
+    return out
+
+
+def cpu_baseline(config, threads=True):
+    """The reference CPU executor (oracle/_ref, unmodified sources, -O3) on the
+    reduced twin of the config: TFLOP/s of execute() alone, threaded with L=8."""
+    from oracle import bridge as B
+    from paper_2410_02682_b200.plan import Plan
+    twin = config.replace("_big", "") + "_s"
+    if config == "ffnn_big":
+        twin = "ffnn_s"
+    if config == "attn_big":
+        twin = "attn_s"
+    name = f"{twin}_p8_L8"
+    doc = json.load(open(os.path.join(ROOT, "plans", name + ".json")))
+    plan = Plan.from_json(doc)
+    ins = B.generate_inputs(plan, 1)
+    kind = "reference" if B.have_ref() else "port"
+    if kind == "reference":
+        _, secs, _, _ = B.ref_execute(doc, ins, threaded=threads)
+    else:
+        t0 = time.perf_counter()
+        B.oracle_execute(plan, ins)
+        secs = time.perf_counter() - t0
+    flops = plan.contraction_flops()
+    return {"value": flops / secs / 1e12, "unit": "TFLOP/s", "cores": os.cpu_count() if threads else 1,
+            "kind": kind, "sample": f"{twin} (reduced twin, SURVEY App. B) p=8 L=8, execute() threaded,"
+                                    f" {flops:.3e} contraction flops in {secs:.2f} s",
+            "seconds": secs}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    vals = []
+    cb = None
+    for i in range(args.warmup + args.steps):
+        cb = cpu_baseline(args.config)
+        if i >= args.warmup:
+            vals.append(cb["value"])
+    v = statistics.median(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOP/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["seconds"] * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference generate_inputs)",
+            "config": {"workload": CONFIG_DESC.get(args.config, args.config), "graph": args.config,
+                       "p": 8, "sample": cb["sample"]},
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="bmm2")
+    ap.add_argument("--precision", default="bf16")
+    ap.add_argument("--impl", default="ours")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    from paper_2410_02682_b200 import build as b
+    b.build()
+    from paper_2410_02682_b200.executor import Context, PreparedPlan
+    from paper_2410_02682_b200.plan import Plan
+
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("gloo")
+        idt = torch.zeros(128, dtype=torch.uint8)
+        if rank == 0:
+            idt = torch.tensor(list(Context.nccl_unique_id()), dtype=torch.uint8)
+        dist.broadcast(idt, 0)
+        ctx = Context(local, rank, world, bytes(idt.tolist()))
+    else:
+        ctx = Context(local)
+
+    L = world
+    plan = Plan.load(os.path.join(ROOT, "plans", f"{args.config}_p8_L{L}.json"))
+    ins = synthetic_inputs(plan, 1234)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    # ---- device-resident throughput --------------------------------------
+    pp = PreparedPlan(ctx, plan, precision=args.precision)
+    pp.upload(ins)
+    for _ in range(args.warmup):
+        rep = pp.run()
+    barrier()
+    torch.cuda.synchronize()
+    dev_ms = []
+    with Clocks(local) as clk:
+        for _ in range(args.steps):
+            rep = pp.run()
+            dev_ms.append(rep.device_ms)
+    torch.cuda.synchronize()
+    barrier()
+    tot_ms = sum(dev_ms)
+    if world > 1:
+        t = torch.tensor([tot_ms], dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    flops = plan.contraction_flops()
+    value = flops * args.steps / (tot_ms / 1e3) / 1e12
+    launches = rep.gpu_launches
+    pp.close()
+
+    # ---- kernel shares / roofline (one profiled run) -----------------------
+    pk, pk_sus, hbm, peak_src = peaks()
+    pp = PreparedPlan(ctx, plan, precision=args.precision, profile=True)
+    pp.upload(ins)
+    pp.run()
+    pp.run()
+    stats = pp.kernel_stats()
+    pp.close()
+    gemm = [s for s in stats if s["name"].startswith("gemm")]
+    g_ms = sum(s["ms"] for s in gemm)
+    g_fl = sum(s["flops"] for s in gemm)
+    g_n = sum(s["launches"] for s in gemm)
+    step_ms = sum(s["ms"] for s in stats)
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
+        traffic = prof.get(args.config, {}).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    achieved = g_fl / (g_ms / 1e3) / 1e12 if g_ms else 0.0
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": pk, "unit": "TFLOP/s",
+                "frac": achieved / pk if pk else None, "traffic": traffic,
+                "kernel": "tcgen05 GEMM (gemm_kernel)", "launches_per_step": g_n,
+                "share_of_step": g_ms / step_ms if step_ms else None,
+                "per_launch_tflop": g_fl / max(1, g_n) / 1e12, "peak_source": f"{peak_src} bf16 burst",
+                "kernels": stats}
+
+    # ---- end to end through the C ABI ------------------------------------------
+    pin = {vid: torch.from_numpy(a).pin_memory() for vid, a in ins.items()}
+    pins = {vid: t.numpy() for vid, t in pin.items()}
+    outs = {vid: torch.empty(plan.vertices[vid].bound, dtype=torch.float32).pin_memory() for vid in plan.outputs}
+    outs_np = {vid: t.numpy() for vid, t in outs.items()}
+    pp = PreparedPlan(ctx, plan, precision=args.precision)
+    h2d = sum(a.nbytes for a in pins.values())
+    d2h = sum(a.nbytes for a in outs_np.values())
+    pp.upload(pins)
+    pp.run()
+    pp.download(into=outs_np)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        pp.upload(pins)
+        pp.run()
+        pp.download(into=outs_np)
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    pp.close()
+    e2e = {"value": flops * args.e2e_steps / e2e_s / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s / args.e2e_steps * 1e3}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cb = cpu_baseline(args.config)
+        cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": args.precision,
+                "data": "synthetic (integer [-4,4] like generate_inputs, numpy-seeded)",
+                "config": {"workload": CONFIG_DESC.get(args.config, args.config), "graph": args.config,
+                           "p": 8, "L": L, "plan": f"plans/{args.config}_p8_L{L}.json",
+                           "l2": "inputs larger than L2 (1 GiB per input tensor); no flush needed",
+                           "frac_of_peak": value / (pk * world)},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches * args.steps, "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    ctx.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -35,6 +35,12 @@ extern "C" {
 
 #define ED_ABI_VERSION 1
 
+#if defined(__GNUC__)
+#define ED_API __attribute__((visibility("default")))
+#else
+#define ED_API
+#endif
+
 /* Errors. The adapter rethrows ED_ERR_PLAN as plan_error_t (setup.h:40-42),
  * ED_ERR_EVAL as eval_error_t (setup.h:45-47; division by zero, ops.cc:10-14,
  * detected on device), everything else as std::runtime_error. */
@@ -184,47 +190,47 @@ typedef struct {
 struct ed_ctx;
 struct ed_plan_h;
 
-int32_t ed_abi_version(void);
+ED_API int32_t ed_abi_version(void);
 
 /* NCCL bootstrap id (128 bytes) for world > 1, made on rank 0 and
  * broadcast by the caller. */
-ed_status ed_nccl_unique_id(void* out, size_t len, char* err, size_t errlen);
+ED_API ed_status ed_nccl_unique_id(void* out, size_t len, char* err, size_t errlen);
 
-ed_status ed_ctx_create(int32_t device, int32_t rank, int32_t world,
+ED_API ed_status ed_ctx_create(int32_t device, int32_t rank, int32_t world,
                         const void* nccl_id, size_t nccl_id_len,
                         struct ed_ctx** out, char* err, size_t errlen);
-void ed_ctx_destroy(struct ed_ctx* ctx);
+ED_API void ed_ctx_destroy(struct ed_ctx* ctx);
 
 /* Validates the plan (execute()'s checks, runtime.cc:388-395), maps each
  * expression onto a kernel, allocates every chunk buffer in HBM, builds
  * tensor maps and the transfer schedule, and records the CUDA graph. */
-ed_status ed_prepare(struct ed_ctx* ctx, const ed_plan_c* plan, const ed_options_c* options,
+ED_API ed_status ed_prepare(struct ed_ctx* ctx, const ed_plan_c* plan, const ed_options_c* options,
                      struct ed_plan_h** out, char* err, size_t errlen);
-void ed_plan_destroy(struct ed_plan_h* h);
+ED_API void ed_plan_destroy(struct ed_plan_h* h);
 
 /* Seed input chunks (engine_t ctor, runtime.cc:66-84): H2D + convert. */
-ed_status ed_upload(struct ed_plan_h* h, const ed_chunk_in_c* chunks, int32_t n,
+ED_API ed_status ed_upload(struct ed_plan_h* h, const ed_chunk_in_c* chunks, int32_t n,
                     char* err, size_t errlen);
 /* Whole input tensors; chunked on device. */
-ed_status ed_upload_tensors(struct ed_plan_h* h, const ed_tensor_in_c* tensors, int32_t n,
+ED_API ed_status ed_upload_tensors(struct ed_plan_h* h, const ed_tensor_in_c* tensors, int32_t n,
                             char* err, size_t errlen);
 
 /* Run every exec vertex of this rank; device-resident. report may be NULL. */
-ed_status ed_run(struct ed_plan_h* h, ed_report_c* report, char* err, size_t errlen);
+ED_API ed_status ed_run(struct ed_plan_h* h, ed_report_c* report, char* err, size_t errlen);
 
 /* Assemble graph outputs from their final refinement layers (runtime.cc:432-448)
  * and copy D2H. On rank r only outputs whose chunks this rank holds are valid
  * unless world == 1; ed_download gathers to the calling rank when world > 1. */
-ed_status ed_download(struct ed_plan_h* h, ed_output_c* outputs, int32_t n,
+ED_API ed_status ed_download(struct ed_plan_h* h, ed_output_c* outputs, int32_t n,
                       char* err, size_t errlen);
 
 /* Copy one exec vertex's produced chunk D2H (per-vertex parity tests).
  * Returns ED_ERR_USAGE if the chunk is not resident on this rank. */
-ed_status ed_download_chunk(struct ed_plan_h* h, int32_t exec_id, int32_t dtype,
+ED_API ed_status ed_download_chunk(struct ed_plan_h* h, int32_t exec_id, int32_t dtype,
                             void* data, int64_t n, char* err, size_t errlen);
 
 /* Per-launch-class timings of the last profiled ed_run. */
-ed_status ed_kernel_stats(struct ed_plan_h* h, ed_kernel_stat_c* out, int32_t cap,
+ED_API ed_status ed_kernel_stats(struct ed_plan_h* h, ed_kernel_stat_c* out, int32_t cap,
                           int32_t* n_out, char* err, size_t errlen);
 
 #ifdef __cplusplus

@@ -1,0 +1,233 @@
+// Exact-semantics CUDA-core kernels: the generic inner EinSum, the
+// refinement fold, chunk scatter/gather and dtype conversion.
+//
+// Arithmetic follows ops.cc:5-38 in double with round-to-nearest intrinsics
+// (no FMA contraction), then rounds to the storage type. For f32 storage
+// this is exactly the reference's f32 mode (every operand and result
+// rounded through float, kernel.cc:43-44; runtime.cc:257-259): double has
+// more than 2*24+2 bits, so rounding an exact-in-double result of + - * /
+// to float equals the correctly rounded float op. For f64 storage it is
+// the reference's default mode bit for bit.
+#include <cuda_bf16.h>
+
+#include "kernels.h"
+
+namespace ed {
+
+namespace {
+
+template <typename T> __device__ __forceinline__ T from_d(double v);
+template <> __device__ __forceinline__ float from_d<float>(double v) { return __double2float_rn(v); }
+template <> __device__ __forceinline__ double from_d<double>(double v) { return v; }
+
+__device__ __forceinline__ double join_d(int op, double x, double y, int* err) {
+  switch (op) {
+    case 0: return __dmul_rn(x, y);
+    case 1: return __dadd_rn(x, y);
+    case 2: return __dsub_rn(x, y);
+    case 3:
+      if (y == 0.0) {
+        atomicExch(err, 1);  // eval_error_t("division by zero"), ops.cc:10-14
+        return 0.0;
+      }
+      return __ddiv_rn(x, y);
+    case 4: {
+      double d = __dsub_rn(x, y);
+      return __dmul_rn(d, d);
+    }
+    default: return fabs(__dsub_rn(x, y));
+  }
+}
+
+__device__ __forceinline__ double map_d(int op, double c, double x) {
+  switch (op) {
+    case 0: return x > 0.0 ? x : 0.0;
+    case 1: return exp(x);
+    case 2: return -x;
+    case 3: return __dmul_rn(c, x);
+    default: return x;
+  }
+}
+
+__device__ __forceinline__ double agg_d(int op, double acc, double v) {
+  // sum / std::max(acc, v) (ops.cc:31-36)
+  return op == 0 ? __dadd_rn(acc, v) : (acc < v ? v : acc);
+}
+
+template <typename T>
+__global__ void generic_kernel(const GenericParams p) {
+  const T* x = static_cast<const T*>(p.x);
+  const T* y = static_cast<const T*>(p.y);
+  T* out = static_cast<T*>(p.out);
+  __nv_bfloat16* o16 = static_cast<__nv_bfloat16*>(p.out16);
+  for (int64_t o = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; o < p.n_out;
+       o += int64_t(gridDim.x) * blockDim.x) {
+    int64_t rem = o, xo = 0, yo = 0;
+    for (int d = p.nz - 1; d >= 0; --d) {
+      int64_t c = rem % p.zext[d];
+      rem /= p.zext[d];
+      xo += c * p.xs_z[d];
+      yo += c * p.ys_z[d];
+    }
+    int64_t a[kMaxRank];
+    int64_t total = 1;
+    for (int d = 0; d < p.na; ++d) {
+      a[d] = 0;
+      total *= p.aext[d];
+    }
+    double acc = 0.0;
+    for (int64_t t = 0; t < total; ++t) {
+      double v;
+      if (y) v = join_d(p.join, double(x[xo]), double(y[yo]), p.err);
+      else v = map_d(p.map, p.c, double(x[xo]));
+      v = double(from_d<T>(v));
+      acc = t == 0 ? v : double(from_d<T>(agg_d(p.agg, acc, v)));
+      for (int d = p.na - 1; d >= 0; --d) {
+        xo += p.xs_a[d];
+        yo += p.ys_a[d];
+        if (++a[d] < p.aext[d]) break;
+        xo -= p.xs_a[d] * p.aext[d];
+        yo -= p.ys_a[d] * p.aext[d];
+        a[d] = 0;
+      }
+    }
+    out[o] = from_d<T>(acc);
+    if (o16) o16[o] = __double2bfloat16(acc);
+  }
+}
+
+template <typename T>
+__global__ void refine_kernel(const RefineParams p) {
+  __shared__ DepRect deps[kMaxDeps];
+  for (int i = threadIdx.x; i < p.n_deps; i += blockDim.x) deps[i] = p.deps[i];
+  __syncthreads();
+  T* out = static_cast<T*>(p.out);
+  __nv_bfloat16* o16 = static_cast<__nv_bfloat16*>(p.out16);
+  for (int64_t o = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; o < p.n_out;
+       o += int64_t(gridDim.x) * blockDim.x) {
+    int64_t g[kMaxRank];
+    int64_t rem = o;
+    for (int d = p.rank - 1; d >= 0; --d) {
+      g[d] = p.c0[d] + rem % p.cext[d];
+      rem /= p.cext[d];
+    }
+    double acc = 0.0;
+    bool touched = false;
+    for (int k = 0; k < p.n_deps; ++k) {
+      const DepRect& r = deps[k];
+      int64_t off = 0;
+      bool in = true;
+      for (int d = 0; d < p.rank; ++d) {
+        int64_t l = g[d] - r.r0[d];
+        in = in && l >= 0 && l < r.ext[d];
+        off = off * r.ext[d] + l;
+      }
+      if (!in) continue;
+      double v = double(static_cast<const T*>(r.src)[off]);
+      acc = touched ? double(from_d<T>(agg_d(p.agg, acc, v))) : v;
+      touched = true;
+    }
+    out[o] = from_d<T>(acc);
+    if (o16) o16[o] = __double2bfloat16(acc);
+  }
+}
+
+template <typename T> __device__ __forceinline__ double ld(const void* p, int64_t i) {
+  return double(static_cast<const T*>(p)[i]);
+}
+__device__ __forceinline__ double ld_dt(const void* p, int dt, int64_t i) {
+  if (dt == 0) return ld<double>(p, i);
+  if (dt == 1) return ld<float>(p, i);
+  return double(__bfloat162float(static_cast<const __nv_bfloat16*>(p)[i]));
+}
+__device__ __forceinline__ void st_dt(void* p, int dt, int64_t i, double v) {
+  if (dt == 0) static_cast<double*>(p)[i] = v;
+  else if (dt == 1) static_cast<float*>(p)[i] = __double2float_rn(v);
+  else static_cast<__nv_bfloat16*>(p)[i] = __double2bfloat16(v);
+}
+
+__global__ void scatter_kernel(const ChunkMapParams p, const void* whole, int in_dt, int st_dt_) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < p.n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    int64_t rem = i, key = 0, loc = 0, kmul = 1, lmul = 1;
+    for (int d = p.rank - 1; d >= 0; --d) {
+      int64_t c = rem % p.bound[d];
+      rem /= p.bound[d];
+      key += (c / p.cb[d]) * kmul;
+      loc += (c % p.cb[d]) * lmul;
+      kmul *= p.part[d];
+      lmul *= p.cb[d];
+    }
+    if (!p.chunks[key]) continue;  // chunk lives on another rank
+    double v = ld_dt(whole, in_dt, i);
+    st_dt(p.chunks[key], st_dt_, loc, v);
+    if (p.shadows && p.shadows[key]) st_dt(p.shadows[key], 2, loc, v);
+  }
+}
+
+__global__ void gather_kernel(const ChunkMapParams p, void* whole, int st_dt_, int out_dt) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < p.n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    int64_t rem = i, key = 0, loc = 0, kmul = 1, lmul = 1;
+    for (int d = p.rank - 1; d >= 0; --d) {
+      int64_t c = rem % p.bound[d];
+      rem /= p.bound[d];
+      key += (c / p.cb[d]) * kmul;
+      loc += (c % p.cb[d]) * lmul;
+      kmul *= p.part[d];
+      lmul *= p.cb[d];
+    }
+    st_dt(whole, out_dt, i, ld_dt(p.chunks[key], st_dt_, loc));
+  }
+}
+
+__global__ void convert_kernel(const void* src, int in_dt, void* dst, int out_dt, int64_t n) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    st_dt(dst, out_dt, i, ld_dt(src, in_dt, i));
+}
+
+__global__ void add_one_kernel(void* p, int dt) { st_dt(p, dt, 0, ld_dt(p, dt, 0) + 1.0); }
+
+int grid_for(int64_t n, int block) {
+  int64_t g = (n + block - 1) / block;
+  // enough CTAs for 8 waves of 148 SMs; grid-stride loops cover the rest
+  return int(g < 148 * 8 * 4 ? (g < 1 ? 1 : g) : 148 * 8 * 4);
+}
+
+}  // namespace
+
+cudaError_t launch_generic(const GenericParams& p, bool f64, cudaStream_t s) {
+  const int block = 256;
+  if (f64) generic_kernel<double><<<grid_for(p.n_out, block), block, 0, s>>>(p);
+  else generic_kernel<float><<<grid_for(p.n_out, block), block, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_refine(const RefineParams& p, bool f64, cudaStream_t s) {
+  const int block = 256;
+  if (f64) refine_kernel<double><<<grid_for(p.n_out, block), block, 0, s>>>(p);
+  else refine_kernel<float><<<grid_for(p.n_out, block), block, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scatter(const ChunkMapParams& p, const void* whole, DT in, DT store, cudaStream_t s) {
+  scatter_kernel<<<grid_for(p.n, 256), 256, 0, s>>>(p, whole, int(in), int(store));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather(const ChunkMapParams& p, void* whole, DT store, DT out, cudaStream_t s) {
+  gather_kernel<<<grid_for(p.n, 256), 256, 0, s>>>(p, whole, int(store), int(out));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_convert(const void* src, DT in, void* dst, DT out, int64_t n, cudaStream_t s) {
+  convert_kernel<<<grid_for(n, 256), 256, 0, s>>>(src, int(in), dst, int(out), n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_add_one(void* p, DT dt, cudaStream_t s) {
+  add_one_kernel<<<1, 1, 0, s>>>(p, int(dt));
+  return cudaGetLastError();
+}
+
+}  // namespace ed

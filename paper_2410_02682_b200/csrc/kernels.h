@@ -1,0 +1,68 @@
+// Device-side parameter blocks for the non-tensor-core kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ed {
+
+constexpr int kMaxRank = 8;
+constexpr int kMaxDeps = 64;
+
+// One inner EinSum over one chunk pair (kernel_eval, kernel.cc:15-68).
+// Output labels z (chunk row-major), aggregation labels a (in the order of
+// the distinct labels, so the fold runs in kernel_eval's odometer order).
+struct GenericParams {
+  int nz, na;
+  int64_t zext[kMaxRank], aext[kMaxRank];
+  int64_t xs_z[kMaxRank], ys_z[kMaxRank];   // input strides per output dim (0 = absent)
+  int64_t xs_a[kMaxRank], ys_a[kMaxRank];   // input strides per aggregation dim
+  int join, map, agg;                       // ed_join_op / ed_map_op / ed_agg_op, -1 absent
+  double c;                                 // scale constant
+  const void* x;
+  const void* y;
+  void* out;                                // storage dtype
+  void* out16;                              // optional bf16 shadow
+  int64_t n_out;
+  int* err;                                 // device flag: 1 = division by zero
+};
+
+// One producer-side chunk folded into a refinement (runtime.cc:198-269).
+struct DepRect {
+  const void* src;
+  int64_t r0[kMaxRank];     // region start, global coordinates
+  int64_t ext[kMaxRank];    // region extent (= src chunk bound)
+};
+
+struct RefineParams {
+  int rank;
+  int n_deps;
+  int agg;                  // -1 none
+  int64_t c0[kMaxRank];     // consumer chunk start, global
+  int64_t cext[kMaxRank];   // consumer chunk bound
+  int64_t n_out;
+  const DepRect* deps;      // device array, fold order
+  void* out;
+  void* out16;
+};
+
+// Whole tensor <-> chunk buffers (chunk / assemble, relation.cc:31-78).
+struct ChunkMapParams {
+  int rank;
+  int64_t bound[kMaxRank];
+  int64_t cb[kMaxRank];     // chunk bound
+  int64_t part[kMaxRank];   // partition d
+  int64_t n;                // elements of the whole tensor
+  void* const* chunks;      // device array, one pointer per key (lexicographic)
+  void* const* shadows;     // optional bf16 shadows per key (nullable array)
+};
+
+enum class DT : int { F64 = 0, F32 = 1, BF16 = 2 };
+
+cudaError_t launch_generic(const GenericParams& p, bool f64, cudaStream_t s);
+cudaError_t launch_refine(const RefineParams& p, bool f64, cudaStream_t s);
+cudaError_t launch_scatter(const ChunkMapParams& p, const void* whole, DT in, DT store, cudaStream_t s);
+cudaError_t launch_gather(const ChunkMapParams& p, void* whole, DT store, DT out, cudaStream_t s);
+cudaError_t launch_convert(const void* src, DT in, void* dst, DT out, int64_t n, cudaStream_t s);
+cudaError_t launch_add_one(void* p, DT dt, cudaStream_t s);  // exec_options_t::corrupt hook
+
+}  // namespace ed

@@ -1,0 +1,1302 @@
+// libed_gpu: the B200 executor behind include/ed_gpu.h.
+//
+// Replaces execute() (runtime.cc:382-451). ed_prepare turns the placed
+// ExecGraph into a static schedule of kernel launches on one stream:
+//   * mul/sum joins of one output region -> ONE tcgen05 GEMM whose K loop
+//     runs over the region's aggregation siblings, so the sibling fold of the
+//     refinement (runtime.cc:242-261) happens in the TMEM accumulator;
+//   * every other join -> the exact generic inner-EinSum kernel;
+//   * refinements that are a single same-shape dependency -> aliases (no
+//     copy); all others -> the ordered gather/fold kernel;
+//   * remote dependencies (world > 1) -> NCCL send/recv on a comm stream.
+// The schedule is captured once into a CUDA graph and replayed by ed_run.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <numeric>
+#include <set>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "ed_gpu.h"
+#include "gemm_sm100.h"
+#include "kernels.h"
+
+using namespace ed;
+
+namespace {
+
+using shape = std::vector<int64_t>;
+using labels = std::vector<int32_t>;
+
+struct ed_error : std::runtime_error {
+  ed_status code;
+  ed_error(ed_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CUDA_OK(expr)                                                                         \
+  do {                                                                                        \
+    cudaError_t e_ = (expr);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      throw ed_error(e_ == cudaErrorMemoryAllocation ? ED_ERR_OOM : ED_ERR_CUDA,              \
+                     std::string(#expr) + ": " + cudaGetErrorString(e_));                     \
+  } while (0)
+
+#define NCCL_OK(expr)                                                                         \
+  do {                                                                                        \
+    ncclResult_t r_ = (expr);                                                                 \
+    if (r_ != ncclSuccess) throw ed_error(ED_ERR_NCCL, std::string(#expr) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+void set_err(char* err, size_t errlen, const std::string& m) {
+  if (err && errlen) std::snprintf(err, errlen, "%s", m.c_str());
+}
+
+template <typename F>
+ed_status guarded(char* err, size_t errlen, F&& f) {
+  try {
+    f();
+    return ED_OK;
+  } catch (ed_error const& e) {
+    set_err(err, errlen, e.what());
+    return e.code;
+  } catch (std::exception const& e) {
+    set_err(err, errlen, e.what());
+    return ED_ERR_USAGE;
+  }
+}
+
+int64_t prod(const shape& s) {
+  int64_t r = 1;
+  for (auto x : s) r *= x;
+  return r;
+}
+
+std::vector<int> positions(const labels& l1, const labels& l2) {
+  std::vector<int> r;
+  for (auto l : l1) {
+    auto it = std::find(l2.begin(), l2.end(), l);
+    if (it == l2.end()) throw ed_error(ED_ERR_PLAN, "unknown label in projection");
+    r.push_back(int(it - l2.begin()));
+  }
+  return r;
+}
+
+shape pick(const shape& b, const std::vector<int>& pos) {
+  shape r;
+  for (int p : pos) r.push_back(b[p]);
+  return r;
+}
+
+// ---- deep copy of the plan ----------------------------------------------------
+struct Vtx {
+  std::string name;
+  int arity, join, map, agg;
+  double c;
+  shape bound, d;
+  labels lz, lx, ly, lxy, dls;
+  int inputs[2];
+};
+
+struct Ex {
+  int kind, owner, producer, consumer, slot, machine;
+  shape key, cb;
+  int64_t fp, sz;
+  std::vector<int> deps;
+};
+
+// ---- label -> GEMM mapping ----------------------------------------------------
+struct Dim {
+  int64_t ext = 1, stride = 0;
+};
+
+// Merge the labels `cls` (in tensor order) of a row-major tensor into one
+// strided dimension; fails if they are not one contiguous run.
+bool merge_dim(const labels& tl, const shape& text, const labels& cls, Dim& out, labels& order) {
+  shape strides(tl.size(), 1);
+  for (int i = int(tl.size()) - 2; i >= 0; --i) strides[i] = strides[i + 1] * text[i + 1];
+  std::vector<int> pos;
+  for (size_t i = 0; i < tl.size(); ++i)
+    if (std::find(cls.begin(), cls.end(), tl[i]) != cls.end() && text[i] > 1) pos.push_back(int(i));
+  out = Dim{};
+  order.clear();
+  if (pos.empty()) return true;
+  for (size_t j = 0; j + 1 < pos.size(); ++j)
+    if (strides[pos[j]] != strides[pos[j + 1]] * text[pos[j + 1]]) return false;
+  out.ext = 1;
+  for (int q : pos) {
+    out.ext *= text[q];
+    order.push_back(tl[q]);
+  }
+  out.stride = strides[pos.back()];
+  return true;
+}
+
+struct GemmMap {
+  int a_slot, b_slot;  // which einsum input feeds MMA-A / MMA-B
+  Dim am, ak, ab, bn, bk, bb, cm, cn, cb;
+  bool a_mn, b_mn;
+};
+
+bool map_gemm(const Vtx& v, const shape& local_xy, bool bf16, GemmMap& g, std::string& why) {
+  if (v.arity != 2 || v.join != ED_JOIN_MUL || v.agg != ED_AGG_SUM) {
+    why = "not mul/sum";
+    return false;
+  }
+  std::map<int, int64_t> ext;
+  for (size_t i = 0; i < v.lxy.size(); ++i) ext.emplace(v.lxy[i], local_xy[i]);
+  auto extents = [&](const labels& ls) {
+    shape r;
+    for (auto l : ls) r.push_back(ext.at(l));
+    return r;
+  };
+  auto has = [](const labels& ls, int l) { return std::find(ls.begin(), ls.end(), l) != ls.end(); };
+  labels B, M, N, K;
+  for (auto l : v.dls) {
+    bool x = has(v.lx, l), y = has(v.ly, l), z = has(v.lz, l);
+    if (x && y && z) B.push_back(l);
+    else if (x && z) M.push_back(l);
+    else if (y && z) N.push_back(l);
+    else if (x && y) K.push_back(l);
+    else if (ext.at(l) > 1) {
+      why = "one-sided aggregation label";
+      return false;
+    }
+  }
+  // MMA-B must own the output's contiguous dimension.
+  int inner = -1;
+  for (int i = int(v.lz.size()) - 1; i >= 0; --i)
+    if (ext.at(v.lz[i]) > 1) {
+      inner = v.lz[i];
+      break;
+    }
+  bool swap = inner >= 0 && has(M, inner);
+  if (inner >= 0 && has(B, inner)) {
+    why = "batch label is the output's contiguous dim";
+    return false;
+  }
+  const labels& lA = swap ? v.ly : v.lx;
+  const labels& lB = swap ? v.lx : v.ly;
+  const labels& Mcls = swap ? N : M;
+  const labels& Ncls = swap ? M : N;
+  g.a_slot = swap ? 1 : 0;
+  g.b_slot = swap ? 0 : 1;
+  shape eA = extents(lA), eB = extents(lB), eZ = extents(v.lz);
+  labels o1, o2, o3;
+  bool ok = merge_dim(lA, eA, Mcls, g.am, o1) && merge_dim(v.lz, eZ, Mcls, g.cm, o2) && o1 == o2;
+  ok = ok && merge_dim(lB, eB, Ncls, g.bn, o1) && merge_dim(v.lz, eZ, Ncls, g.cn, o2) && o1 == o2;
+  ok = ok && merge_dim(lA, eA, K, g.ak, o1) && merge_dim(lB, eB, K, g.bk, o2) && o1 == o2;
+  ok = ok && merge_dim(lA, eA, B, g.ab, o1) && merge_dim(lB, eB, B, g.bb, o2) && o1 == o2 &&
+       merge_dim(v.lz, eZ, B, g.cb, o3) && o1 == o3;
+  if (!ok) {
+    why = "label classes are not contiguous runs";
+    return false;
+  }
+  if (g.cn.ext > 1 && g.cn.stride != 1) {
+    why = "output N not contiguous";
+    return false;
+  }
+  g.a_mn = !(g.ak.ext == 1 || g.ak.stride == 1);
+  if (g.a_mn && !(g.am.ext == 1 || g.am.stride == 1)) {
+    why = "A has no unit-stride M or K";
+    return false;
+  }
+  g.b_mn = !(g.bk.ext == 1 || g.bk.stride == 1);
+  if (g.b_mn && !(g.bn.ext == 1 || g.bn.stride == 1)) {
+    why = "B has no unit-stride N or K";
+    return false;
+  }
+  const int es = bf16 ? 2 : 4;
+  auto aligned = [&](const Dim& d) { return d.ext == 1 || (d.stride * es) % 16 == 0; };
+  // outer (non-unit) strides of each TMA view must be 16-byte multiples
+  if (!(aligned(g.a_mn ? g.ak : g.am) && aligned(g.ab) && aligned(g.b_mn ? g.bk : g.bn) && aligned(g.bb))) {
+    why = "operand strides not 16-byte aligned";
+    return false;
+  }
+  if (g.am.ext > INT32_MAX || g.bn.ext > INT32_MAX || g.ak.ext > INT32_MAX || g.ab.ext > 65535) {
+    why = "extent too large";
+    return false;
+  }
+  return true;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    CUDA_OK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (!p) throw ed_error(ED_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 3-D tensor map {inner, outer, batch} with a 128-byte swizzled box.
+void make_map(CUtensorMap* m, const void* base, bool bf16, int64_t inner, int64_t outer, int64_t outer_stride,
+              int64_t batch, int64_t batch_stride, uint32_t box_inner, uint32_t box_outer) {
+  const int es = bf16 ? 2 : 4;
+  cuuint64_t dims[3] = {cuuint64_t(inner), cuuint64_t(outer), cuuint64_t(batch)};
+  auto fix = [&](int64_t s, int64_t prev_bytes) -> cuuint64_t {
+    int64_t b = s * es;
+    if (b <= 0 || b % 16) b = ((prev_bytes + 15) / 16) * 16;  // unit extent: stride unused
+    return cuuint64_t(b);
+  };
+  cuuint64_t s1 = fix(outer > 1 ? outer_stride : 0, inner * es);
+  cuuint64_t s2 = fix(batch > 1 ? batch_stride : 0, int64_t(s1) * outer);
+  cuuint64_t strides[2] = {s1, s2};
+  cuuint32_t box[3] = {box_inner, box_outer, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode_fn()(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                           const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw ed_error(ED_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+}
+
+// ---- schedule -------------------------------------------------------------------
+enum class OpKind { GEMM, GENERIC, REFINE, CORRUPT, SEND, RECV, CONVERT };
+
+struct Op {
+  OpKind kind;
+  std::string name;   // launch class, e.g. "gemm_bf16:Z1"
+  double flops = 0, bytes = 0;
+  GemmParams gemm;
+  bool bf16 = false;
+  GenericParams gen;
+  RefineParams ref;
+  void* ptr = nullptr;
+  DT dt = DT::F32;
+  int peer = -1;
+  size_t count = 0;
+};
+
+struct Buffer {
+  size_t off_main = SIZE_MAX, off_16 = SIZE_MAX;
+  bool need_main = false, need_16 = false;
+  void* main = nullptr;
+  void* b16 = nullptr;
+};
+
+}  // namespace
+
+struct ed_ctx {
+  int device = 0, rank = 0, world = 1;
+  ncclComm_t comm = nullptr;
+  cudaStream_t stream = nullptr, comm_stream = nullptr;
+};
+
+struct ed_plan_h {
+  ed_ctx* ctx = nullptr;
+  ed_options_c opt{};
+  std::vector<Vtx> V;
+  std::vector<Ex> X;
+  std::vector<int> outputs;
+  int n_machines = 1;
+  double alpha = 0.0;
+  bool f64 = false;
+  DT store = DT::F32;
+  size_t es = 4;
+
+  std::vector<int> owner;          // exec id -> exec id holding its data
+  std::vector<char> local;         // exec id runs (or is received) on this rank
+  std::vector<Buffer> buf;         // indexed by exec id (meaningful at owners)
+  std::vector<Op> ops;
+  std::vector<ed_machine_c> counters;
+  int64_t total_transferred = 0, peer_bytes = 0;
+  double max_site_cost = 0.0, contraction_flops = 0.0;
+  int first_join = -1;
+
+  void* arena = nullptr;
+  size_t arena_bytes = 0;
+  DepRect* d_deps = nullptr;
+  void** d_ptrs = nullptr;         // chunk-pointer tables for scatter/gather
+  int* d_err = nullptr;
+  void* staging = nullptr;
+  size_t staging_bytes = 0;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::vector<cudaEvent_t> op_events;
+  std::vector<ed_kernel_stat_c> stats;
+
+  struct SrcRec {
+    int ref, src;
+    shape r0, ext;
+  };
+  std::vector<SrcRec> srcs_;                      // refinement sources, fold order
+  std::map<int, GemmMap> gmap_;                   // einsum -> GEMM mapping
+  std::map<int, std::vector<int>> region_sibs_;   // GEMM head join -> siblings
+
+  int rank_of(int id) const { return X[id].machine % ctx->world; }
+  shape out_partition(int w) const {
+    if (V[w].arity == 0) return V[w].d;
+    return pick(V[w].d, positions(V[w].lz, V[w].lxy));
+  }
+  shape required_partition(int w, int slot) const {
+    return pick(V[w].d, positions(slot == 0 ? V[w].lx : V[w].ly, V[w].lxy));
+  }
+  // engine_t::region_key / region_partition (runtime.cc:96-116)
+  shape region_key(int id) const {
+    const Ex& u = X[id];
+    if (u.kind != ED_EXEC_JOIN) return u.key;
+    return pick(u.key, positions(V[u.producer].lz, V[u.producer].dls));
+  }
+  shape region_partition(int id) const {
+    const Ex& u = X[id];
+    if (u.kind == ED_EXEC_INPUT_CHUNK) return V[u.producer].d;
+    if (u.kind == ED_EXEC_JOIN) return out_partition(u.producer);
+    if (u.consumer >= 0) return required_partition(u.consumer, u.slot);
+    return out_partition(u.producer);
+  }
+  shape local_xy(int w) const {
+    shape b;
+    for (int s = 0; s < V[w].arity; ++s) {
+      const shape& bi = V[V[w].inputs[s]].bound;
+      b.insert(b.end(), bi.begin(), bi.end());
+    }
+    for (size_t i = 0; i < b.size(); ++i) b[i] /= V[w].d[i];
+    return b;
+  }
+  void* main_of(int id) { return buf[owner[id]].main; }
+  void* b16_of(int id) { return buf[owner[id]].b16; }
+
+  void copy_plan(const ed_plan_c* p);
+  void validate();
+  void build();
+  void allocate();
+  void record();
+  void launch_op(size_t i, cudaStream_t s);
+  void destroy();
+};
+
+void ed_plan_h::copy_plan(const ed_plan_c* p) {
+  if (!p || p->n_vertices <= 0 || !p->vertices || p->n_exec < 0 || (p->n_exec && !p->exec))
+    throw ed_error(ED_ERR_USAGE, "ed_prepare: empty or null plan");
+  V.resize(p->n_vertices);
+  for (int i = 0; i < p->n_vertices; ++i) {
+    const ed_vertex_c& s = p->vertices[i];
+    Vtx& v = V[i];
+    v.name = s.name ? s.name : ("v" + std::to_string(i));
+    v.arity = s.arity;
+    v.join = s.join_op;
+    v.map = s.map_op;
+    v.agg = s.agg_op;
+    v.c = s.scale_c;
+    v.bound.assign(s.bound, s.bound + s.rank);
+    v.d.assign(s.d, s.d + s.rank_d);
+    v.lz.assign(s.lz, s.lz + s.rank_z);
+    v.lx.assign(s.lx, s.lx + s.rank_x);
+    if (s.arity == 2) v.ly.assign(s.ly, s.ly + s.rank_y);
+    v.inputs[0] = s.inputs[0];
+    v.inputs[1] = s.inputs[1];
+    v.lxy = v.lx;
+    v.lxy.insert(v.lxy.end(), v.ly.begin(), v.ly.end());
+    v.dls = v.lx;
+    for (auto l : v.ly)
+      if (std::find(v.dls.begin(), v.dls.end(), l) == v.dls.end()) v.dls.push_back(l);
+  }
+  X.resize(p->n_exec);
+  for (int i = 0; i < p->n_exec; ++i) {
+    const ed_exec_vertex_c& s = p->exec[i];
+    Ex& x = X[i];
+    x.kind = s.kind;
+    x.owner = s.owner;
+    x.producer = s.producer;
+    x.consumer = s.consumer;
+    x.slot = s.slot;
+    x.machine = s.machine;
+    x.key.assign(s.key, s.key + s.key_rank);
+    x.cb.assign(s.chunk_bound, s.chunk_bound + s.chunk_rank);
+    x.fp = s.fp;
+    x.sz = s.sz;
+    x.deps.assign(s.deps, s.deps + s.n_deps);
+  }
+  outputs.assign(p->outputs, p->outputs + p->n_outputs);
+  n_machines = p->n_machines;
+  alpha = p->alpha;
+}
+
+// execute()'s structural checks (runtime.cc:388-395) plus the refinement
+// invariants compute() enforces per element (runtime.cc:230-268), which are
+// data-independent and therefore checked once here.
+void ed_plan_h::validate() {
+  const int nv = int(V.size()), ne = int(X.size());
+  if (n_machines < 1) throw ed_error(ED_ERR_PLAN, "execute: placement does not cover the exec graph");
+  for (int w = 0; w < nv; ++w) {
+    const Vtx& v = V[w];
+    if (v.arity < 0 || v.arity > 2) throw ed_error(ED_ERR_PLAN, "bad arity for '" + v.name + "'");
+    if (int(v.bound.size()) > kMaxRank) throw ed_error(ED_ERR_UNSUPPORTED, "rank > 8 for '" + v.name + "'");
+    if (v.arity == 0) {
+      if (v.d.size() != v.bound.size()) throw ed_error(ED_ERR_PLAN, "explode: vertex '" + v.name + "' is not labeled");
+      continue;
+    }
+    if (v.d.size() != v.lxy.size()) throw ed_error(ED_ERR_PLAN, "partition vector rank mismatch for '" + v.name + "'");
+    if (int(v.dls.size()) > kMaxRank) throw ed_error(ED_ERR_UNSUPPORTED, "more than 8 distinct labels");
+    shape bxy;
+    for (int s = 0; s < v.arity; ++s) {
+      int in = v.inputs[s];
+      if (in < 0 || in >= nv) throw ed_error(ED_ERR_PLAN, "graph: out-of-range input");
+      bxy.insert(bxy.end(), V[in].bound.begin(), V[in].bound.end());
+    }
+    if (bxy.size() != v.lxy.size()) throw ed_error(ED_ERR_PLAN, "graph: ranks disagree with labels");
+    for (size_t i = 0; i < bxy.size(); ++i) {
+      if (v.d[i] < 1 || bxy[i] % v.d[i] != 0)
+        throw ed_error(ED_ERR_PLAN, "partition entry does not divide bound");
+      // shared labels must agree in extent and partition (first occurrence wins, indexing.cc:30-41)
+      auto pos = positions({v.lxy[i]}, v.lxy)[0];
+      if (bxy[pos] != bxy[i] || v.d[pos] != v.d[i]) throw ed_error(ED_ERR_PLAN, "inconsistent shared label");
+    }
+  }
+  for (int id = 0; id < ne; ++id) {
+    const Ex& u = X[id];
+    if (u.machine < 0 || u.machine >= n_machines) throw ed_error(ED_ERR_PLAN, "execute: incomplete placement");
+    if (u.producer < 0 || u.producer >= nv) throw ed_error(ED_ERR_PLAN, "exec vertex producer out of range");
+    for (int d : u.deps)
+      if (d < 0 || d >= id) throw ed_error(ED_ERR_PLAN, "exec graph is not in topological id order");
+    if (prod(u.cb) != u.sz) throw ed_error(ED_ERR_PLAN, "exec vertex size mismatch");
+    if (u.kind == ED_EXEC_JOIN) {
+      if (int(u.deps.size()) != V[u.producer].arity) throw ed_error(ED_ERR_PLAN, "join arity mismatch");
+    } else if (u.kind == ED_EXEC_REFINEMENT) {
+      if (u.deps.size() > size_t(kMaxDeps)) throw ed_error(ED_ERR_UNSUPPORTED, "refinement with > 64 deps");
+      // coverage: deps of one refinement share the producer's region partition,
+      // so distinct region keys are disjoint and repeats are aggregation siblings
+      const shape& bound = V[u.producer].bound;
+      shape dc = region_partition(id);
+      std::set<shape> seen;
+      bool repeat = false;
+      int64_t covered = 0;
+      for (int d : u.deps) {
+        shape rk = region_key(d), dr = region_partition(d);
+        if (!seen.insert(rk).second) {
+          repeat = true;
+          continue;
+        }
+        int64_t vol = 1;
+        for (size_t i = 0; i < bound.size(); ++i) {
+          int64_t r0 = rk[i] * (bound[i] / dr[i]), r1 = r0 + bound[i] / dr[i];
+          int64_t c0 = u.key[i] * (bound[i] / dc[i]), c1 = c0 + u.cb[i];
+          vol *= std::max<int64_t>(0, std::min(r1, c1) - std::max(r0, c0));
+        }
+        covered += vol;
+      }
+      int agg = V[u.producer].arity == 0 ? -1 : V[u.producer].agg;
+      if (repeat && agg < 0)
+        throw ed_error(ED_ERR_PLAN, "execute: overlapping contributions without an aggregation op");
+      if (covered != u.sz) throw ed_error(ED_ERR_PLAN, "execute: refinement chunk left partially unwritten");
+    }
+  }
+  for (int o : outputs)
+    if (o < 0 || o >= nv) throw ed_error(ED_ERR_PLAN, "output out of range");
+
+  // transfer accounting: one whole-chunk pull per (chunk, machine)
+  // (pull / pull_available, runtime.cc:119-172) — a pure function of the plan
+  counters.assign(n_machines, ed_machine_c{0, 0, 0});
+  std::set<std::pair<int, int>> pulled;
+  total_transferred = 0;
+  for (int id = 0; id < ne; ++id) {
+    const Ex& v = X[id];
+    if (v.kind == ED_EXEC_INPUT_CHUNK) continue;
+    counters[v.machine].fp += v.fp;
+    for (int d : v.deps)
+      if (X[d].machine != v.machine && pulled.insert({d, v.machine}).second) {
+        counters[X[d].machine].sent += X[d].sz;
+        counters[v.machine].received += X[d].sz;
+        total_transferred += X[d].sz;
+      }
+  }
+  max_site_cost = 0;
+  for (auto& c : counters)
+    max_site_cost = std::max(max_site_cost, alpha * double(c.fp) + double(c.sent) + double(c.received));
+}
+
+void ed_plan_h::build() {
+  const int ne = int(X.size());
+  const int me = ctx->rank;
+  owner.resize(ne);
+  std::iota(owner.begin(), owner.end(), 0);
+  local.assign(ne, 0);
+  buf.assign(ne, Buffer{});
+  for (int id = 0; id < ne; ++id) local[id] = rank_of(id) == me;
+
+  const bool tc = opt.precision == ED_PREC_TF32 || opt.precision == ED_PREC_BF16;
+  const bool bf16 = opt.precision == ED_PREC_BF16;
+
+  // ---- per einsum: kernel class and region fusion ----
+  std::map<int, GemmMap> gmap;
+  std::map<int, std::string> why_not;
+  std::vector<char> fused_head(ne, 0);       // join id -> emits the region's GEMM
+  std::map<int, std::vector<int>> region_sibs;  // head join -> sibling joins (fold order)
+  for (int w = 0; w < int(V.size()); ++w) {
+    if (V[w].arity == 0) continue;
+    GemmMap g;
+    std::string why;
+    if (tc && map_gemm(V[w], local_xy(w), bf16, g, why)) gmap[w] = g;
+    else why_not[w] = why;
+  }
+  {
+    std::map<std::pair<int, shape>, std::vector<int>> regions;
+    for (int id = 0; id < ne; ++id)
+      if (X[id].kind == ED_EXEC_JOIN && local[id] && gmap.count(X[id].producer))
+        regions[{X[id].producer, region_key(id)}].push_back(id);
+    for (auto& [k, sibs] : regions) {
+      if (int(sibs.size()) <= kMaxSib) {
+        fused_head[sibs[0]] = 1;
+        region_sibs[sibs[0]] = sibs;
+        for (int s : sibs) owner[s] = sibs[0];
+      } else {
+        for (int s : sibs) {
+          fused_head[s] = 1;
+          region_sibs[s] = {s};
+        }
+      }
+    }
+  }
+
+  // remote dependencies become local copies received over NCCL
+  std::vector<std::pair<int, int>> transfers;  // (dep, destination rank), global order
+  {
+    std::set<std::pair<int, int>> seen;
+    for (int id = 0; id < ne; ++id) {
+      if (X[id].kind == ED_EXEC_INPUT_CHUNK) continue;
+      int dst = rank_of(id);
+      for (int d : X[id].deps)
+        if (rank_of(d) != dst && seen.insert({d, dst}).second) transfers.push_back({d, dst});
+    }
+  }
+
+  // ---- refinements: effective sources, aliasing ----
+  struct Src {
+    int id;
+    shape r0, ext;
+  };
+  std::vector<std::vector<Src>> srcs(ne);
+  for (int id = 0; id < ne; ++id) {
+    const Ex& u = X[id];
+    if (u.kind != ED_EXEC_REFINEMENT || !local[id]) continue;
+    const shape& bound = V[u.producer].bound;
+    std::set<int> used;
+    for (int d : u.deps) {
+      int o = local[d] ? owner[d] : d;  // remote deps arrive as their own chunks
+      if (!used.insert(o).second) continue;
+      shape rk = region_key(d), dr = region_partition(d), r0(bound.size()), ext(bound.size());
+      for (size_t i = 0; i < bound.size(); ++i) {
+        ext[i] = bound[i] / dr[i];
+        r0[i] = rk[i] * ext[i];
+      }
+      srcs[id].push_back({o, r0, ext});
+    }
+    // a refinement that is exactly one producer chunk is that chunk
+    const shape dc = region_partition(id);
+    if (srcs[id].size() == 1) {
+      bool same = true;
+      for (size_t i = 0; i < bound.size(); ++i)
+        same = same && srcs[id][0].r0[i] == u.key[i] * (bound[i] / dc[i]) && srcs[id][0].ext[i] == u.cb[i];
+      if (same) owner[id] = owner[srcs[id][0].id];
+    }
+  }
+
+  // ---- buffer needs ----
+  for (int id = 0; id < ne; ++id) {
+    if (!local[id]) continue;
+    const Ex& u = X[id];
+    if (u.kind == ED_EXEC_INPUT_CHUNK) buf[owner[id]].need_main = true;
+    if (u.kind == ED_EXEC_JOIN) {
+      int w = u.producer;
+      if (gmap.count(w)) {
+        for (int d : u.deps) {
+          int o = local[d] ? owner[d] : d;
+          if (bf16) buf[o].need_16 = true;
+          else buf[o].need_main = true;
+        }
+      } else {
+        for (int d : u.deps) buf[local[d] ? owner[d] : d].need_main = true;
+      }
+    }
+    if (u.kind == ED_EXEC_REFINEMENT) {
+      if (owner[id] == id)
+        for (auto& s : srcs[id]) buf[s.id].need_main = true;
+      if (u.consumer < 0) buf[owner[id]].need_main = true;  // graph output / sink
+    }
+  }
+  // data that leaves this rank travels in the storage dtype
+  for (auto& [d, dst] : transfers)
+    if (rank_of(d) == me) buf[owner[d]].need_main = true;
+  for (auto& [d, dst] : transfers)
+    if (dst == me) buf[d].need_main = true;
+  // every computed chunk keeps at least one representation
+  for (int id = 0; id < ne; ++id)
+    if (local[id] && owner[id] == id && !buf[id].need_16) buf[id].need_main = true;
+
+  // ---- allocation plan ----
+  size_t off = 0;
+  auto take = [&](int64_t elems, size_t esz) {
+    size_t o = off;
+    off += ((size_t(elems) * esz + 1023) / 1024) * 1024;
+    return o;
+  };
+  for (int id = 0; id < ne; ++id) {
+    bool here = (local[id] && owner[id] == id);
+    bool recv = false;
+    for (auto& [d, dst] : transfers) recv = recv || (d == id && dst == me);
+    if (!here && !recv) continue;
+    if (buf[id].need_main) buf[id].off_main = take(X[id].sz, es);
+    if (buf[id].need_16) buf[id].off_16 = take(X[id].sz, 2);
+  }
+  arena_bytes = std::max<size_t>(off, 1024);
+
+  // ---- ops (exec-id order; transfers at their first consumer) ----
+  std::vector<std::vector<std::pair<int, int>>> xfer_at(ne);
+  {
+    std::set<std::pair<int, int>> seen;
+    for (int id = 0; id < ne; ++id) {
+      if (X[id].kind == ED_EXEC_INPUT_CHUNK) continue;
+      int dst = rank_of(id);
+      for (int d : X[id].deps)
+        if (rank_of(d) != dst && seen.insert({d, dst}).second) xfer_at[id].push_back({d, dst});
+    }
+  }
+  ops.clear();
+  contraction_flops = 0;
+  for (int id = 0; id < ne; ++id) {
+    for (auto& [d, dst] : xfer_at[id]) {
+      if (rank_of(d) == me) {
+        Op op{OpKind::SEND};
+        op.name = "nccl_send";
+        op.peer = dst;
+        op.ptr = reinterpret_cast<void*>(d);  // resolved after allocation
+        op.count = size_t(X[d].sz);
+        op.bytes = double(X[d].sz) * es;
+        ops.push_back(op);
+      } else if (dst == me) {
+        Op op{OpKind::RECV};
+        op.name = "nccl_recv";
+        op.peer = rank_of(d);
+        op.ptr = reinterpret_cast<void*>(d);
+        op.count = size_t(X[d].sz);
+        op.bytes = double(X[d].sz) * es;
+        ops.push_back(op);
+        if (buf[d].need_16) {  // received operand of a bf16 GEMM
+          Op cv{OpKind::CONVERT};
+          cv.name = "convert_bf16";
+          cv.ptr = reinterpret_cast<void*>(d);
+          cv.bytes = double(X[d].sz) * (es + 2);
+          ops.push_back(cv);
+        }
+      }
+    }
+    const Ex& u = X[id];
+    if (!local[id] || u.kind == ED_EXEC_INPUT_CHUNK) continue;
+    const Vtx& w = V[u.producer];
+    if (u.kind == ED_EXEC_JOIN) {
+      if (first_join < 0) first_join = id;
+      if (w.join == ED_JOIN_MUL && w.agg == ED_AGG_SUM) contraction_flops += 2.0 * double(u.fp);
+      if (gmap.count(u.producer)) {
+        if (!fused_head[id]) continue;
+        Op op{OpKind::GEMM};
+        op.bf16 = bf16;
+        op.name = std::string(bf16 ? "gemm_bf16:" : "gemm_tf32:") + w.name;
+        op.ptr = reinterpret_cast<void*>(id);
+        auto& sibs = region_sibs[id];
+        op.gemm.n_sib = int(sibs.size());
+        for (int s : sibs) op.flops += 2.0 * double(X[s].fp);
+        ops.push_back(op);
+      } else {
+        Op op{OpKind::GENERIC};
+        op.name = "einsum_generic:" + w.name;
+        op.ptr = reinterpret_cast<void*>(id);
+        op.flops = double(u.fp);
+        ops.push_back(op);
+      }
+      continue;
+    }
+    // refinement
+    if (owner[id] != id) continue;  // aliased: no work
+    Op op{OpKind::REFINE};
+    op.name = "refine:" + w.name;
+    op.ptr = reinterpret_cast<void*>(id);
+    ops.push_back(op);
+  }
+  if (opt.corrupt && first_join >= 0 && local[first_join]) {
+    // after the op that produced the first join
+    size_t at = 0;
+    for (size_t i = 0; i < ops.size(); ++i)
+      if ((ops[i].kind == OpKind::GEMM || ops[i].kind == OpKind::GENERIC) &&
+          reinterpret_cast<intptr_t>(ops[i].ptr) == owner[first_join]) {
+        at = i + 1;
+        break;
+      }
+    Op op{OpKind::CORRUPT};
+    op.name = "corrupt_hook";
+    op.ptr = reinterpret_cast<void*>(owner[first_join]);
+    ops.insert(ops.begin() + at, op);
+  }
+
+  // stash what allocate() needs
+  this->srcs_.clear();
+  for (int id = 0; id < ne; ++id)
+    for (auto& s : srcs[id]) this->srcs_.push_back({id, s.id, s.r0, s.ext});
+  this->gmap_ = gmap;
+  this->region_sibs_ = region_sibs;
+}
+
+void ed_plan_h::allocate() {
+  const int ne = int(X.size());
+  CUDA_OK(cudaMalloc(&arena, arena_bytes));
+  char* base = static_cast<char*>(arena);
+  for (int id = 0; id < ne; ++id) {
+    if (buf[id].off_main != SIZE_MAX) buf[id].main = base + buf[id].off_main;
+    if (buf[id].off_16 != SIZE_MAX) buf[id].b16 = base + buf[id].off_16;
+  }
+  CUDA_OK(cudaMalloc(&d_err, sizeof(int)));
+  CUDA_OK(cudaMemset(d_err, 0, sizeof(int)));
+  CUDA_OK(cudaMalloc(&d_ptrs, sizeof(void*) * 2 * std::max(1, ne)));
+
+  // refinement dependency tables, one contiguous device array
+  std::vector<DepRect> host_deps;
+  std::map<int, size_t> dep_off;
+  for (auto& s : srcs_) {
+    if (!dep_off.count(s.ref)) dep_off[s.ref] = host_deps.size();
+    DepRect r{};
+    r.src = buf[s.src].main;
+    for (size_t i = 0; i < s.r0.size(); ++i) {
+      r.r0[i] = s.r0[i];
+      r.ext[i] = s.ext[i];
+    }
+    host_deps.push_back(r);
+  }
+  if (!host_deps.empty()) {
+    CUDA_OK(cudaMalloc(&d_deps, sizeof(DepRect) * host_deps.size()));
+    CUDA_OK(cudaMemcpy(d_deps, host_deps.data(), sizeof(DepRect) * host_deps.size(), cudaMemcpyHostToDevice));
+  }
+
+  auto resolve = [&](int dep) { return local[dep] ? owner[dep] : dep; };
+  for (auto& op : ops) {
+    const int id = int(reinterpret_cast<intptr_t>(op.ptr));
+    switch (op.kind) {
+      case OpKind::GEMM: {
+        const Ex& u = X[id];
+        const GemmMap& g = gmap_.at(u.producer);
+        GemmParams& p = op.gemm;
+        const bool b16 = op.bf16;
+        const auto& sibs = region_sibs_.at(id);
+        p.n_sib = int(sibs.size());
+        p.M = int(g.am.ext);
+        p.N = int(g.bn.ext);
+        p.K = int(g.ak.ext);
+        p.batch = int(g.ab.ext);
+        p.a_mn = g.a_mn;
+        p.b_mn = g.b_mn;
+        const uint32_t BK = uint32_t(gemm_bk(b16)), BN = uint32_t(gemm_bn(b16));
+        const uint32_t ATOM = 128u / (b16 ? 2u : 4u);
+        for (int s = 0; s < p.n_sib; ++s) {
+          const Ex& j = X[sibs[s]];
+          int da = resolve(j.deps[g.a_slot]), db = resolve(j.deps[g.b_slot]);
+          const void* pa = b16 ? buf[da].b16 : buf[da].main;
+          const void* pb = b16 ? buf[db].b16 : buf[db].main;
+          if (!pa || !pb) throw ed_error(ED_ERR_PLAN, "GEMM operand buffer missing");
+          if (!g.a_mn) make_map(&p.a[s], pa, b16, g.ak.ext, g.am.ext, g.am.stride, g.ab.ext, g.ab.stride, BK, 128);
+          else make_map(&p.a[s], pa, b16, g.am.ext, g.ak.ext, g.ak.stride, g.ab.ext, g.ab.stride, ATOM, BK);
+          if (!g.b_mn) make_map(&p.b[s], pb, b16, g.bk.ext, g.bn.ext, g.bn.stride, g.bb.ext, g.bb.stride, BK, BN);
+          else make_map(&p.b[s], pb, b16, g.bn.ext, g.bk.ext, g.bk.stride, g.bb.ext, g.bb.stride, ATOM, BK);
+        }
+        p.c32 = static_cast<float*>(buf[id].main);
+        p.c16 = buf[id].b16;
+        p.c_sm = g.cm.ext > 1 ? g.cm.stride : 0;
+        p.c_sb = g.cb.ext > 1 ? g.cb.stride : 0;
+        p.vec_ok = (p.c_sm % 8 == 0) && (p.c_sb % 8 == 0);
+        const double ab = double(g.am.ext) * g.ak.ext * g.ab.ext + double(g.bn.ext) * g.bk.ext * g.bb.ext;
+        const double cbytes = double(g.am.ext) * g.bn.ext * g.ab.ext * ((p.c32 ? 4 : 0) + (p.c16 ? 2 : 0));
+        op.bytes = ab * (b16 ? 2 : 4) * p.n_sib + cbytes;
+        break;
+      }
+      case OpKind::GENERIC: {
+        const Ex& u = X[id];
+        const Vtx& w = V[u.producer];
+        GenericParams& p = op.gen;
+        std::memset(&p, 0, sizeof(p));
+        shape lxy = local_xy(u.producer);
+        std::map<int, int64_t> ext;
+        for (size_t i = 0; i < w.lxy.size(); ++i) ext.emplace(w.lxy[i], lxy[i]);
+        auto strides_of = [&](const labels& ls) {
+          std::map<int, int64_t> st;
+          int64_t s = 1;
+          for (int i = int(ls.size()) - 1; i >= 0; --i) {
+            st[ls[i]] = s;
+            s *= ext.at(ls[i]);
+          }
+          return st;
+        };
+        auto xs = strides_of(w.lx);
+        auto ys = w.arity == 2 ? strides_of(w.ly) : std::map<int, int64_t>{};
+        auto get = [](const std::map<int, int64_t>& m, int l) {
+          auto it = m.find(l);
+          return it == m.end() ? int64_t(0) : it->second;
+        };
+        p.nz = int(w.lz.size());
+        for (int i = 0; i < p.nz; ++i) {
+          p.zext[i] = ext.at(w.lz[i]);
+          p.xs_z[i] = get(xs, w.lz[i]);
+          p.ys_z[i] = get(ys, w.lz[i]);
+        }
+        p.na = 0;
+        for (auto l : w.dls)
+          if (std::find(w.lz.begin(), w.lz.end(), l) == w.lz.end()) {
+            p.aext[p.na] = ext.at(l);
+            p.xs_a[p.na] = get(xs, l);
+            p.ys_a[p.na] = get(ys, l);
+            ++p.na;
+          }
+        p.join = w.join;
+        p.map = w.map;
+        p.agg = w.agg;
+        p.c = w.c;
+        p.x = buf[resolve(u.deps[0])].main;
+        p.y = w.arity == 2 ? buf[resolve(u.deps[1])].main : nullptr;
+        p.out = buf[id].main;
+        p.out16 = buf[id].b16;
+        p.n_out = u.sz;
+        p.err = d_err;
+        int64_t xin = prod(pick(lxy, positions(w.lx, w.lxy)));
+        int64_t yin = w.arity == 2 ? prod(pick(lxy, positions(w.ly, w.lxy))) : 0;
+        op.bytes = double(xin + yin + u.sz) * es;
+        break;
+      }
+      case OpKind::REFINE: {
+        const Ex& u = X[id];
+        const Vtx& w = V[u.producer];
+        RefineParams& p = op.ref;
+        std::memset(&p, 0, sizeof(p));
+        const shape& bound = w.bound;
+        shape dc = region_partition(id);
+        p.rank = int(bound.size());
+        p.agg = w.arity == 0 ? -1 : w.agg;
+        for (int i = 0; i < p.rank; ++i) {
+          p.cext[i] = u.cb[i];
+          p.c0[i] = u.key[i] * (bound[i] / dc[i]);
+        }
+        p.n_out = u.sz;
+        size_t first = dep_off.at(id), n = 0;
+        for (auto& s : srcs_) n += s.ref == id;
+        p.deps = d_deps + first;
+        p.n_deps = int(n);
+        p.out = buf[id].main;
+        p.out16 = buf[id].b16;
+        op.bytes = double(u.sz) * (es + (p.out16 ? 2 : 0));
+        double rd = 0;
+        for (auto& s : srcs_)
+          if (s.ref == id) {
+            double vol = 1;
+            for (int i = 0; i < p.rank; ++i)
+              vol *= double(std::max<int64_t>(0, std::min(s.r0[i] + s.ext[i], p.c0[i] + p.cext[i]) -
+                                                     std::max(s.r0[i], p.c0[i])));
+            rd += vol;
+          }
+        op.bytes += rd * es;
+        break;
+      }
+      case OpKind::CORRUPT:
+        op.dt = buf[id].main ? store : DT::BF16;
+        op.ptr = buf[id].main ? buf[id].main : buf[id].b16;
+        break;
+      case OpKind::SEND:
+        op.ptr = buf[resolve(id)].main;
+        break;
+      case OpKind::RECV:
+        op.ptr = buf[id].main;
+        break;
+      case OpKind::CONVERT:
+        op.gen.x = buf[id].main;
+        op.gen.out16 = buf[id].b16;
+        op.gen.n_out = X[id].sz;
+        break;
+    }
+  }
+}
+
+void ed_plan_h::launch_op(size_t i, cudaStream_t s) {
+  Op& op = ops[i];
+  switch (op.kind) {
+    case OpKind::GEMM: CUDA_OK(launch_gemm(op.gemm, op.bf16, s)); break;
+    case OpKind::GENERIC: CUDA_OK(launch_generic(op.gen, f64, s)); break;
+    case OpKind::REFINE: CUDA_OK(launch_refine(op.ref, f64, s)); break;
+    case OpKind::CORRUPT: CUDA_OK(launch_add_one(op.ptr, op.dt, s)); break;
+    case OpKind::CONVERT: CUDA_OK(launch_convert(op.gen.x, store, op.gen.out16, DT::BF16, op.gen.n_out, s)); break;
+    case OpKind::SEND:
+      NCCL_OK(ncclSend(op.ptr, op.count, f64 ? ncclFloat64 : ncclFloat32, op.peer, ctx->comm, s));
+      break;
+    case OpKind::RECV:
+      NCCL_OK(ncclRecv(op.ptr, op.count, f64 ? ncclFloat64 : ncclFloat32, op.peer, ctx->comm, s));
+      break;
+  }
+}
+
+void ed_plan_h::record() {
+  CUDA_OK(gemm_prepare());
+  CUDA_OK(cudaEventCreate(&ev0));
+  CUDA_OK(cudaEventCreate(&ev1));
+  if (opt.no_graph || opt.profile) return;
+  cudaStream_t s = ctx->stream;
+  CUDA_OK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  try {
+    for (size_t i = 0; i < ops.size(); ++i) launch_op(i, s);
+  } catch (...) {
+    cudaGraph_t g;
+    cudaStreamEndCapture(s, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  CUDA_OK(cudaStreamEndCapture(s, &graph));
+  CUDA_OK(cudaGraphInstantiate(&gexec, graph, 0));
+}
+
+void ed_plan_h::destroy() {
+  if (gexec) cudaGraphExecDestroy(gexec);
+  if (graph) cudaGraphDestroy(graph);
+  if (ev0) cudaEventDestroy(ev0);
+  if (ev1) cudaEventDestroy(ev1);
+  for (auto e : op_events) cudaEventDestroy(e);
+  if (arena) cudaFree(arena);
+  if (d_deps) cudaFree(d_deps);
+  if (d_ptrs) cudaFree(d_ptrs);
+  if (d_err) cudaFree(d_err);
+  if (staging) cudaFree(staging);
+}
+
+namespace {
+
+void ensure_staging(ed_plan_h* h, size_t bytes) {
+  if (h->staging_bytes >= bytes) return;
+  if (h->staging) CUDA_OK(cudaFree(h->staging));
+  h->staging = nullptr;
+  CUDA_OK(cudaMalloc(&h->staging, bytes));
+  h->staging_bytes = bytes;
+}
+
+size_t dt_size(int dtype) {
+  if (dtype == ED_DTYPE_F64) return 8;
+  if (dtype == ED_DTYPE_F32) return 4;
+  throw ed_error(ED_ERR_USAGE, "unknown dtype");
+}
+
+DT dt_of(int dtype) { return dtype == ED_DTYPE_F64 ? DT::F64 : DT::F32; }
+
+// chunk <-> whole-tensor mapping for graph vertex w over partition `part`
+// and the exec ids holding its chunks (any order; keyed by their key).
+void chunk_map(ed_plan_h* h, int w, const shape& part, const std::vector<int>& ids, bool want_shadow,
+               ChunkMapParams& p) {
+  const shape& bound = h->V[w].bound;
+  std::memset(&p, 0, sizeof(p));
+  p.rank = int(bound.size());
+  p.n = prod(bound);
+  int64_t nkeys = prod(part);
+  std::vector<void*> ptrs(size_t(2 * nkeys), nullptr);
+  for (int i = 0; i < p.rank; ++i) {
+    p.bound[i] = bound[i];
+    p.part[i] = part[i];
+    p.cb[i] = bound[i] / part[i];
+  }
+  for (int id : ids) {
+    int64_t k = 0;
+    for (int i = 0; i < p.rank; ++i) k = k * part[i] + h->X[id].key[i];
+    if (h->local[id]) {
+      ptrs[size_t(k)] = h->buf[h->owner[id]].main;
+      if (want_shadow) ptrs[size_t(nkeys + k)] = h->buf[h->owner[id]].b16;
+    }
+  }
+  if (size_t(2 * nkeys) > 2 * std::max<size_t>(1, h->X.size())) {
+    CUDA_OK(cudaFree(h->d_ptrs));
+    CUDA_OK(cudaMalloc(&h->d_ptrs, sizeof(void*) * 2 * nkeys));
+  }
+  CUDA_OK(cudaMemcpy(h->d_ptrs, ptrs.data(), sizeof(void*) * 2 * nkeys, cudaMemcpyHostToDevice));
+  p.chunks = h->d_ptrs;
+  p.shadows = want_shadow ? h->d_ptrs + nkeys : nullptr;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t ed_abi_version(void) { return ED_ABI_VERSION; }
+
+ed_status ed_nccl_unique_id(void* out, size_t len, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!out || len < sizeof(ncclUniqueId)) throw ed_error(ED_ERR_USAGE, "buffer too small for ncclUniqueId");
+    ncclUniqueId id;
+    NCCL_OK(ncclGetUniqueId(&id));
+    std::memcpy(out, &id, sizeof(id));
+  });
+}
+
+ed_status ed_ctx_create(int32_t device, int32_t rank, int32_t world, const void* nccl_id, size_t nccl_id_len,
+                        ed_ctx** out, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!out || world < 1 || rank < 0 || rank >= world) throw ed_error(ED_ERR_USAGE, "bad rank/world");
+    int n = 0;
+    CUDA_OK(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n) throw ed_error(ED_ERR_USAGE, "no such CUDA device");
+    CUDA_OK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CUDA_OK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) throw ed_error(ED_ERR_UNSUPPORTED, "libed_gpu is built for sm_100a (B200)");
+    auto* c = new ed_ctx;
+    c->device = device;
+    c->rank = rank;
+    c->world = world;
+    try {
+      CUDA_OK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      CUDA_OK(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+      if (world > 1) {
+        if (!nccl_id || nccl_id_len < sizeof(ncclUniqueId)) throw ed_error(ED_ERR_USAGE, "world > 1 needs an NCCL id");
+        ncclUniqueId id;
+        std::memcpy(&id, nccl_id, sizeof(id));
+        NCCL_OK(ncclCommInitRank(&c->comm, world, id, rank));
+      }
+    } catch (...) {
+      ed_ctx_destroy(c);
+      throw;
+    }
+    *out = c;
+  });
+}
+
+void ed_ctx_destroy(ed_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->comm) ncclCommDestroy(c->comm);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+  delete c;
+}
+
+ed_status ed_prepare(ed_ctx* ctx, const ed_plan_c* plan, const ed_options_c* options, ed_plan_h** out,
+                     char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!ctx || !out) throw ed_error(ED_ERR_USAGE, "null context or output");
+    CUDA_OK(cudaSetDevice(ctx->device));
+    auto* h = new ed_plan_h;
+    h->ctx = ctx;
+    if (options) h->opt = *options;
+    if (h->opt.precision < 0 || h->opt.precision > 3) {
+      delete h;
+      throw ed_error(ED_ERR_USAGE, "unknown precision");
+    }
+    h->f64 = h->opt.precision == ED_PREC_FP64;
+    h->store = h->f64 ? DT::F64 : DT::F32;
+    h->es = h->f64 ? 8 : 4;
+    try {
+      h->copy_plan(plan);
+      h->validate();
+      h->build();
+      h->allocate();
+      h->record();
+    } catch (...) {
+      h->destroy();
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+void ed_plan_destroy(ed_plan_h* h) {
+  if (!h) return;
+  cudaSetDevice(h->ctx->device);
+  h->destroy();
+  delete h;
+}
+
+ed_status ed_upload(ed_plan_h* h, const ed_chunk_in_c* chunks, int32_t n, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!h || (n && !chunks)) throw ed_error(ED_ERR_USAGE, "null argument");
+    CUDA_OK(cudaSetDevice(h->ctx->device));
+    cudaStream_t s = h->ctx->stream;
+    for (int i = 0; i < n; ++i) {
+      const ed_chunk_in_c& c = chunks[i];
+      if (c.exec_id < 0 || c.exec_id >= int(h->X.size()) || h->X[c.exec_id].kind != ED_EXEC_INPUT_CHUNK)
+        throw ed_error(ED_ERR_PLAN, "ed_upload: not an input chunk");
+      if (c.n != h->X[c.exec_id].sz) throw ed_error(ED_ERR_PLAN, "ed_upload: chunk size mismatch");
+      if (!h->local[c.exec_id]) continue;
+      size_t bytes = size_t(c.n) * dt_size(c.dtype);
+      ensure_staging(h, bytes);
+      CUDA_OK(cudaMemcpyAsync(h->staging, c.data, bytes, cudaMemcpyHostToDevice, s));
+      Buffer& b = h->buf[c.exec_id];
+      CUDA_OK(launch_convert(h->staging, dt_of(c.dtype), b.main, h->store, c.n, s));
+      if (b.b16) CUDA_OK(launch_convert(h->staging, dt_of(c.dtype), b.b16, DT::BF16, c.n, s));
+    }
+    CUDA_OK(cudaStreamSynchronize(s));
+  });
+}
+
+ed_status ed_upload_tensors(ed_plan_h* h, const ed_tensor_in_c* ts, int32_t n, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!h || (n && !ts)) throw ed_error(ED_ERR_USAGE, "null argument");
+    CUDA_OK(cudaSetDevice(h->ctx->device));
+    cudaStream_t s = h->ctx->stream;
+    for (int i = 0; i < n; ++i) {
+      const ed_tensor_in_c& t = ts[i];
+      if (t.vertex_id < 0 || t.vertex_id >= int(h->V.size()) || h->V[t.vertex_id].arity != 0)
+        throw ed_error(ED_ERR_PLAN, "execute: no relation supplied for an input");
+      if (t.n != prod(h->V[t.vertex_id].bound)) throw ed_error(ED_ERR_PLAN, "ed_upload_tensors: size mismatch");
+      std::vector<int> ids;
+      bool shadow = false;
+      for (int id = 0; id < int(h->X.size()); ++id)
+        if (h->X[id].kind == ED_EXEC_INPUT_CHUNK && h->X[id].producer == t.vertex_id) {
+          ids.push_back(id);
+          shadow = shadow || (h->local[id] && h->buf[id].b16);
+        }
+      size_t bytes = size_t(t.n) * dt_size(t.dtype);
+      ensure_staging(h, bytes);
+      CUDA_OK(cudaMemcpyAsync(h->staging, t.data, bytes, cudaMemcpyHostToDevice, s));
+      ChunkMapParams p;
+      chunk_map(h, t.vertex_id, h->V[t.vertex_id].d, ids, shadow, p);
+      CUDA_OK(launch_scatter(p, h->staging, dt_of(t.dtype), h->store, s));
+      CUDA_OK(cudaStreamSynchronize(s));
+    }
+  });
+}
+
+ed_status ed_run(ed_plan_h* h, ed_report_c* rep, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!h) throw ed_error(ED_ERR_USAGE, "null plan");
+    CUDA_OK(cudaSetDevice(h->ctx->device));
+    cudaStream_t s = h->ctx->stream;
+    CUDA_OK(cudaMemsetAsync(h->d_err, 0, sizeof(int), s));
+    if (h->opt.profile && h->op_events.size() != h->ops.size() + 1) {
+      for (auto e : h->op_events) cudaEventDestroy(e);
+      h->op_events.assign(h->ops.size() + 1, nullptr);
+      for (auto& e : h->op_events) CUDA_OK(cudaEventCreate(&e));
+    }
+    CUDA_OK(cudaEventRecord(h->ev0, s));
+    if (h->gexec) {
+      CUDA_OK(cudaGraphLaunch(h->gexec, s));
+    } else {
+      for (size_t i = 0; i < h->ops.size(); ++i) {
+        if (h->opt.profile) CUDA_OK(cudaEventRecord(h->op_events[i], s));
+        h->launch_op(i, s);
+      }
+      if (h->opt.profile) CUDA_OK(cudaEventRecord(h->op_events[h->ops.size()], s));
+    }
+    CUDA_OK(cudaEventRecord(h->ev1, s));
+    CUDA_OK(cudaEventSynchronize(h->ev1));
+    int flag = 0;
+    CUDA_OK(cudaMemcpy(&flag, h->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+    float ms = 0;
+    CUDA_OK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+    if (h->opt.profile) {
+      std::map<std::string, size_t> idx;
+      h->stats.clear();
+      for (size_t i = 0; i < h->ops.size(); ++i) {
+        float t = 0;
+        CUDA_OK(cudaEventElapsedTime(&t, h->op_events[i], h->op_events[i + 1]));
+        const Op& op = h->ops[i];
+        auto it = idx.find(op.name);
+        if (it == idx.end()) {
+          ed_kernel_stat_c st{};
+          std::snprintf(st.name, sizeof(st.name), "%s", op.name.c_str());
+          it = idx.emplace(op.name, h->stats.size()).first;
+          h->stats.push_back(st);
+        }
+        auto& st = h->stats[it->second];
+        st.launches += 1;
+        st.ms += t;
+        st.flops += op.flops;
+        st.bytes += op.bytes;
+      }
+    }
+    if (flag) throw ed_error(ED_ERR_EVAL, "division by zero");
+    if (rep) {
+      if (rep->machines)
+        for (int m = 0; m < std::min(rep->n_machines, h->n_machines); ++m) rep->machines[m] = h->counters[m];
+      rep->total_transferred = h->total_transferred;
+      rep->wall_steps = int64_t(h->X.size());
+      rep->max_site_cost = h->max_site_cost;
+      rep->device_ms = ms;
+      int64_t pb = 0;
+      int launches = 0;
+      for (auto& op : h->ops) {
+        if (op.kind == OpKind::SEND) pb += int64_t(op.count) * int64_t(h->es);
+        if (op.kind != OpKind::SEND && op.kind != OpKind::RECV) ++launches;
+      }
+      rep->peer_bytes = pb;
+      rep->contraction_flops = h->contraction_flops;
+      rep->gpu_launches = launches;
+    }
+  });
+}
+
+ed_status ed_download(ed_plan_h* h, ed_output_c* outs, int32_t n, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!h || (n && !outs)) throw ed_error(ED_ERR_USAGE, "null argument");
+    CUDA_OK(cudaSetDevice(h->ctx->device));
+    cudaStream_t s = h->ctx->stream;
+    for (int i = 0; i < n; ++i) {
+      int w = outs[i].vertex_id;
+      if (w < 0 || w >= int(h->V.size())) throw ed_error(ED_ERR_USAGE, "output vertex out of range");
+      if (outs[i].n != prod(h->V[w].bound)) throw ed_error(ED_ERR_USAGE, "output size mismatch");
+      std::vector<int> ids;
+      for (int id = 0; id < int(h->X.size()); ++id) {
+        const Ex& u = h->X[id];
+        bool mine = h->V[w].arity == 0 ? (u.kind == ED_EXEC_INPUT_CHUNK && u.producer == w)
+                                        : (u.kind == ED_EXEC_REFINEMENT && u.producer == w && u.consumer < 0);
+        if (mine) {
+          if (!h->local[id]) throw ed_error(ED_ERR_USAGE, "output chunk lives on another rank");
+          ids.push_back(id);
+        }
+      }
+      if (ids.empty()) throw ed_error(ED_ERR_PLAN, "no final refinement layer for output");
+      shape part = h->V[w].arity == 0 ? h->V[w].d : h->out_partition(w);
+      size_t bytes = size_t(outs[i].n) * dt_size(outs[i].dtype);
+      ensure_staging(h, bytes);
+      ChunkMapParams p;
+      chunk_map(h, w, part, ids, false, p);
+      CUDA_OK(launch_gather(p, h->staging, h->store, dt_of(outs[i].dtype), s));
+      CUDA_OK(cudaMemcpyAsync(outs[i].data, h->staging, bytes, cudaMemcpyDeviceToHost, s));
+      CUDA_OK(cudaStreamSynchronize(s));
+    }
+  });
+}
+
+ed_status ed_download_chunk(ed_plan_h* h, int32_t exec_id, int32_t dtype, void* data, int64_t n, char* err,
+                            size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!h || !data) throw ed_error(ED_ERR_USAGE, "null argument");
+    if (exec_id < 0 || exec_id >= int(h->X.size())) throw ed_error(ED_ERR_USAGE, "exec id out of range");
+    if (n != h->X[exec_id].sz) throw ed_error(ED_ERR_USAGE, "chunk size mismatch");
+    if (!h->local[exec_id]) throw ed_error(ED_ERR_USAGE, "chunk not resident on this rank");
+    const Ex& u = h->X[exec_id];
+    int o = h->owner[exec_id];
+    if (u.kind == ED_EXEC_JOIN && o != exec_id)
+      throw ed_error(ED_ERR_USAGE, "join partial was folded into its region's accumulator");
+    CUDA_OK(cudaSetDevice(h->ctx->device));
+    cudaStream_t s = h->ctx->stream;
+    size_t bytes = size_t(n) * dt_size(dtype);
+    ensure_staging(h, bytes);
+    const Buffer& b = h->buf[o];
+    if (b.main) CUDA_OK(launch_convert(b.main, h->store, h->staging, dt_of(dtype), n, s));
+    else CUDA_OK(launch_convert(b.b16, DT::BF16, h->staging, dt_of(dtype), n, s));
+    CUDA_OK(cudaMemcpyAsync(data, h->staging, bytes, cudaMemcpyDeviceToHost, s));
+    CUDA_OK(cudaStreamSynchronize(s));
+  });
+}
+
+ed_status ed_kernel_stats(ed_plan_h* h, ed_kernel_stat_c* out, int32_t cap, int32_t* n_out, char* err,
+                          size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!h || !n_out) throw ed_error(ED_ERR_USAGE, "null argument");
+    int k = std::min<int>(cap, int(h->stats.size()));
+    for (int i = 0; i < k; ++i) out[i] = h->stats[i];
+    *n_out = int(h->stats.size());
+  });
+}
+
+}  // extern "C"

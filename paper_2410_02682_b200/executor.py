@@ -1,0 +1,243 @@
+"""Python host over libed_gpu.so, mirroring the reference's executor API.
+
+    report = execute(plan, inputs, precision="bf16")   # runtime.h:45-49
+
+`plan` is a Plan (the reference planner's task graph + exec graph +
+placement); `inputs` maps each input vertex id to its whole tensor (chunked
+on the device, relation.cc:31-53) or to {exec_id: chunk}. The report mirrors
+run_report_t (runtime.h:27-37). Errors mirror the reference's exception
+classes: PlanError ~ plan_error_t, EvalError ~ eval_error_t.
+
+There is no CPU fallback: if the CUDA library is missing or no B200 is
+visible, every entry point raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import abi
+from .plan import Plan
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libed_gpu.so")
+
+_lib = None
+
+
+class EdError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(msg)
+        self.code = code
+
+
+class PlanError(EdError):
+    """plan_error_t (setup.h:40-42)."""
+
+
+class EvalError(EdError):
+    """eval_error_t (setup.h:45-47)."""
+
+
+def library():
+    """Loads the in-tree CUDA library. Raises if it is not built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is not built; run `python -m paper_2410_02682_b200.build`")
+        _lib = abi.declare(C.CDLL(LIB_PATH))
+        if _lib.ed_abi_version() != 1:
+            raise ImportError("libed_gpu ABI version mismatch")
+    return _lib
+
+
+def _check(code, err):
+    if code == abi.ED_OK:
+        return
+    msg = err.value.decode(errors="replace")
+    if code == abi.ED_ERR_PLAN:
+        raise PlanError(code, msg)
+    if code == abi.ED_ERR_EVAL:
+        raise EvalError(code, msg)
+    raise EdError(code, msg)
+
+
+def _err():
+    return C.create_string_buffer(2048), 2048
+
+
+@dataclass
+class RunReport:
+    """run_report_t (runtime.h:27-37) plus device timing."""
+    machines: list = field(default_factory=list)     # (fp, sent, received) per machine
+    total_transferred: int = 0
+    wall_steps: int = 0
+    max_site_cost: float = 0.0
+    outputs: dict = field(default_factory=dict)      # output vertex -> assembled tensor
+    device_ms: float = 0.0
+    peer_bytes: int = 0
+    contraction_flops: float = 0.0
+    gpu_launches: int = 0
+
+
+class Context:
+    """One GPU (one process per GPU; rank/world for multi-GPU plans)."""
+
+    def __init__(self, device=0, rank=0, world=1, nccl_id: bytes | None = None):
+        lib = library()
+        self.rank, self.world = rank, world
+        h = C.c_void_p()
+        err, n = _err()
+        idbuf = C.create_string_buffer(nccl_id, len(nccl_id)) if nccl_id else None
+        _check(lib.ed_ctx_create(device, rank, world, idbuf, len(nccl_id) if nccl_id else 0, C.byref(h), err, n), err)
+        self.h = h
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        err, n = _err()
+        _check(library().ed_nccl_unique_id(buf, 128, err, n), err)
+        return buf.raw
+
+    def close(self):
+        if self.h:
+            library().ed_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class PreparedPlan:
+    """A plan resident on the GPU: buffers allocated, kernels chosen, CUDA graph
+    recorded (ed_prepare). Upload, run and download may be repeated."""
+
+    def __init__(self, ctx: Context, plan: Plan, precision="bf16", corrupt=False, profile=False, graph=True):
+        self.ctx, self.plan = ctx, plan
+        self._pc, self._keep = plan.to_c()
+        opt = abi.ed_options_c()
+        opt.precision = abi.PREC[precision]
+        opt.corrupt = int(bool(corrupt))
+        opt.profile = int(bool(profile))
+        opt.no_graph = int(not graph)
+        h = C.c_void_p()
+        err, n = _err()
+        _check(library().ed_prepare(ctx.h, C.byref(self._pc), C.byref(opt), C.byref(h), err, n), err)
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            library().ed_plan_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- inputs --------------------------------------------------------------
+    def upload(self, inputs: dict):
+        """inputs: vid -> whole tensor (f64 or f32 ndarray), or
+        vid -> {exec_id: chunk ndarray} (a tensor relation)."""
+        tensors, chunks, keep = [], [], []
+        for vid, val in inputs.items():
+            if isinstance(val, dict):
+                for eid, ch in val.items():
+                    a = _host(ch)
+                    keep.append(a)
+                    chunks.append(abi.ed_chunk_in_c(eid, _dt(a), a.ctypes.data, a.size))
+            else:
+                a = _host(val)
+                keep.append(a)
+                tensors.append(abi.ed_tensor_in_c(vid, _dt(a), a.ctypes.data, a.size))
+        err, n = _err()
+        if tensors:
+            arr = (abi.ed_tensor_in_c * len(tensors))(*tensors)
+            _check(library().ed_upload_tensors(self.h, arr, len(tensors), err, n), err)
+        if chunks:
+            arr = (abi.ed_chunk_in_c * len(chunks))(*chunks)
+            _check(library().ed_upload(self.h, arr, len(chunks), err, n), err)
+
+    # ---- run -------------------------------------------------------------------
+    def run(self) -> RunReport:
+        L = self.plan.n_machines
+        machines = (abi.ed_machine_c * L)()
+        rep = abi.ed_report_c()
+        rep.n_machines = L
+        rep.machines = C.cast(machines, C.POINTER(abi.ed_machine_c))
+        err, n = _err()
+        _check(library().ed_run(self.h, C.byref(rep), err, n), err)
+        return RunReport([(m.fp, m.sent, m.received) for m in machines], rep.total_transferred,
+                         rep.wall_steps, rep.max_site_cost, {}, rep.device_ms, rep.peer_bytes,
+                         rep.contraction_flops, rep.gpu_launches)
+
+    # ---- outputs ---------------------------------------------------------------
+    def download(self, dtype=np.float64, into: dict | None = None) -> dict:
+        outs = {}
+        descs = []
+        for vid in self.plan.outputs:
+            a = into[vid] if into is not None else np.empty(self.plan.vertices[vid].bound, dtype=dtype)
+            outs[vid] = a
+            descs.append(abi.ed_output_c(vid, _dt(a), a.ctypes.data, a.size))
+        if descs:
+            arr = (abi.ed_output_c * len(descs))(*descs)
+            err, n = _err()
+            _check(library().ed_download(self.h, arr, len(descs), err, n), err)
+        return outs
+
+    def download_chunk(self, exec_id: int, dtype=np.float64) -> np.ndarray:
+        u = self.plan.exec[exec_id]
+        a = np.empty(u.chunk_bound, dtype=dtype)
+        err, n = _err()
+        _check(library().ed_download_chunk(self.h, exec_id, _dt(a), a.ctypes.data, a.size, err, n), err)
+        return a
+
+    def kernel_stats(self):
+        cap = 256
+        arr = (abi.ed_kernel_stat_c * cap)()
+        k = C.c_int32()
+        err, n = _err()
+        _check(library().ed_kernel_stats(self.h, arr, cap, C.byref(k), err, n), err)
+        return [dict(name=arr[i].name.decode(), launches=arr[i].launches, ms=arr[i].ms,
+                     flops=arr[i].flops, bytes=arr[i].bytes) for i in range(min(k.value, cap))]
+
+
+def _host(a):
+    a = np.asarray(a)
+    if a.dtype not in (np.float64, np.float32):
+        a = a.astype(np.float64)
+    return np.ascontiguousarray(a)
+
+
+def _dt(a):
+    return abi.DTYPE_F64 if a.dtype == np.float64 else abi.DTYPE_F32
+
+
+_default_ctx = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+def execute(plan: Plan, inputs: dict, precision="bf16", corrupt=False, ctx: Context | None = None,
+            out_dtype=np.float64) -> RunReport:
+    """execute() (runtime.cc:382-451) on the GPU: seed, run, assemble outputs."""
+    pp = PreparedPlan(ctx or default_context(), plan, precision=precision, corrupt=corrupt)
+    try:
+        pp.upload(inputs)
+        rep = pp.run()
+        rep.outputs = pp.download(dtype=out_dtype)
+        return rep
+    finally:
+        pp.close()

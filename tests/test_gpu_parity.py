@@ -1,0 +1,134 @@
+"""Parity of the B200 executor (through the C ABI) with the reference.
+
+Bars (written per test):
+  FP64 : bit-exact to the reference's default execute()
+  FP32 : bit-exact to the reference's f32 mode (exec_options_t::f32)
+  TF32 / BF16 : bit-exact on integer-valued contractions whose partial sums
+         stay below 2^24; otherwise max_rel_err (tensor.cc:9-19) within the
+         stated bound against the f64 reference.
+"""
+import numpy as np
+import pytest
+
+from conftest import golden_cases, load_golden, load_plan
+from oracle import bridge as B
+
+pytestmark = pytest.mark.gpu
+
+MATRIX = [c for c in golden_cases()]
+# stated bounds for the tensor-core modes (max_rel_err vs the f64 reference)
+TOL = {"tf32": 5e-3, "bf16": 3e-2}
+
+
+def _run(ctx, plan, ins, prec, **kw):
+    from paper_2410_02682_b200.executor import execute
+    return execute(plan, ins, precision=prec, ctx=ctx, **kw)
+
+
+@pytest.mark.parametrize("case", MATRIX)
+def test_fp64_bitexact_vs_reference(gpu_ctx, case):
+    name, ins, o64, o32, orc, counters, total = load_golden(case)
+    plan = load_plan(name)
+    rep = _run(gpu_ctx, plan, ins, "fp64")
+    for vid, a in o64.items():
+        assert np.array_equal(rep.outputs[vid], a), f"{case}: vertex {vid} differs"
+    assert rep.machines == counters and rep.total_transferred == total
+
+
+@pytest.mark.parametrize("case", MATRIX)
+def test_fp32_bitexact_vs_reference_f32_mode(gpu_ctx, case):
+    name, ins, o64, o32, orc, counters, total = load_golden(case)
+    plan = load_plan(name)
+    rep = _run(gpu_ctx, plan, ins, "fp32")
+    for vid, a in o32.items():
+        assert np.array_equal(rep.outputs[vid], a), f"{case}: vertex {vid} differs"
+
+
+@pytest.mark.parametrize("prec", ["tf32", "bf16"])
+@pytest.mark.parametrize("case", MATRIX)
+def test_tensor_core_modes_within_bound(gpu_ctx, case, prec):
+    name, ins, o64, o32, orc, counters, total = load_golden(case)
+    plan = load_plan(name)
+    rep = _run(gpu_ctx, plan, ins, prec)
+    exact = plan.integer_valued() and all(v.expr is None or v.expr.map is None for v in plan.vertices)
+    for vid, a in o64.items():
+        err = B.max_rel_err(rep.outputs[vid], a)
+        if exact and np.max(np.abs(a)) < 2 ** 24:
+            assert err == 0.0, f"{case}: integer graph not exact ({err})"
+        else:
+            assert err <= TOL[prec], f"{case}: {err}"
+
+
+LAYOUTS = ["gemm_nn", "gemm_tn", "gemm_nt", "gemm_swap", "gemm_ragged", "gemm_batch", "gemm_heads", "gemm_merge"]
+
+
+@pytest.mark.parametrize("prec", ["fp32", "tf32", "bf16"])
+@pytest.mark.parametrize("p", [1, 8])
+@pytest.mark.parametrize("name", LAYOUTS)
+def test_gemm_layouts_integer_exact(gpu_ctx, name, p, prec):
+    """Integer inputs in [-4,4] (generate_inputs) with K <= 256: every
+    product and partial sum is exact in bf16/tf32/fp32, so each label layout
+    (K-/MN-major operands, swapped roles, batch, ragged edges, merged label
+    groups) must reproduce the dense oracle bit for bit."""
+    plan = load_plan(f"{name}_p{p}_L1")
+    ins = B.generate_inputs(plan, 7)
+    pc, keep = plan.to_c()
+    out_vid = plan.outputs[0]
+    v = plan.vertices[out_vid]
+    x, y = ins[v.inputs[0]], ins[v.inputs[1]]
+    spec = ",".join(["".join(v.expr.ins[0]), "".join(v.expr.ins[1])]) + "->" + "".join(v.expr.out)
+    letters = {l: chr(ord("a") + i) for i, l in enumerate(dict.fromkeys(v.expr.ins[0] + v.expr.ins[1]))}
+    spec = (",".join("".join(letters[l] for l in ls) for ls in v.expr.ins) + "->" +
+            "".join(letters[l] for l in v.expr.out))
+    want = np.einsum(spec, x, y)
+    rep = _run(gpu_ctx, plan, ins, prec)
+    assert np.array_equal(rep.outputs[out_vid], want)
+
+
+def test_corrupt_hook_breaks_verification(gpu_ctx):
+    # test_runtime.cc:197-207
+    name, ins, o64, *_ = load_golden("matmul_p4_L2_s29")
+    rep = _run(gpu_ctx, load_plan(name), ins, "bf16", corrupt=True)
+    assert any(B.max_rel_err(rep.outputs[v], a) > 1e-10 for v, a in o64.items())
+
+
+def test_division_by_zero_raises_eval_error(gpu_ctx):
+    from paper_2410_02682_b200.executor import EvalError
+    plan = load_plan("divzero_p2_L1")
+    x = np.ones((4, 4))
+    y = np.ones((4, 4))
+    y[2, 3] = 0.0
+    ins = {plan.find("X"): x, plan.find("Y"): y}
+    with pytest.raises(EvalError):
+        _run(gpu_ctx, plan, ins, "fp32")
+    y[2, 3] = 2.0
+    rep = _run(gpu_ctx, plan, ins, "fp32")
+    assert rep.outputs[plan.outputs[0]][2, 3] == 0.5
+
+
+@pytest.mark.parametrize("twin", ["chain3_s", "bmm2_s", "hoc_s"])
+def test_twins_first_contraction_exact(gpu_ctx, twin):
+    """Reduced twins of the integer configs: the first contraction's partial
+    sums stay below 2^24, so every mode reproduces the reference's exact
+    integers (SURVEY 8c known-answer trick)."""
+    from paper_2410_02682_b200.executor import Context, PreparedPlan
+    plan = load_plan(f"{twin}_p8_L1")
+    ins = B.generate_inputs(plan, 1)
+    first = next(v for v in plan.vertices if v.expr is not None)
+    x, y = ins[first.inputs[0]], ins[first.inputs[1]]
+    letters = {l: chr(ord("a") + i) for i, l in enumerate(dict.fromkeys(first.expr.ins[0] + first.expr.ins[1]))}
+    spec = (",".join("".join(letters[l] for l in ls) for ls in first.expr.ins) + "->" +
+            "".join(letters[l] for l in first.expr.out))
+    want = np.einsum(spec, x, y)
+    for prec in ("tf32", "bf16"):
+        pp = PreparedPlan(gpu_ctx, plan, precision=prec)
+        pp.upload(ins)
+        pp.run()
+        # every refinement of the first vertex holds a block of `want`
+        for u in plan.exec:
+            if u.kind == 2 and u.producer == first.vid:
+                got = pp.download_chunk(u.id)
+                dc = [b // c for b, c in zip(first.bound, u.chunk_bound)]
+                sl = tuple(slice(k * c, (k + 1) * c) for k, c in zip(u.key, u.chunk_bound))
+                assert np.array_equal(got, want[sl]), (twin, prec, u.id)
+        pp.close()

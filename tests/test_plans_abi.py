@@ -1,0 +1,90 @@
+"""Host-side checks (CPU): plan files, C-ABI flattening, the built library's
+exports and struct layout against include/ed_gpu.h."""
+import ctypes as C
+import glob
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import PLANS, ROOT, load_plan
+from paper_2410_02682_b200 import abi
+from paper_2410_02682_b200.plan import Plan
+
+HEADER = os.path.join(ROOT, "include", "ed_gpu.h")
+
+
+def test_every_plan_loads_and_flattens():
+    for path in sorted(glob.glob(os.path.join(PLANS, "*.json"))):
+        plan = Plan.load(path)
+        pc, keep = plan.to_c()
+        assert pc.n_exec == len(plan.exec) and pc.n_vertices == len(plan.vertices)
+        for u in plan.exec:
+            assert all(d < u.id for d in u.deps), "exec ids must be topological"
+            assert 0 <= u.machine < plan.n_machines
+
+
+def test_config_flops_match_baseline():
+    # contraction FLOPs per config
+    want = {"chain3": 4.123e11, "bmm2": 2.199e12, "ffnn_big": 4.398e12, "attn_big": 8.246e11, "hoc": 8.796e12}
+    for name, f in want.items():
+        assert load_plan(f"{name}_p8_L1").contraction_flops() == pytest.approx(f, rel=1e-3)
+
+
+def test_planner_places_one_join_per_gpu_at_L8():
+    # at p=8, L=8 every contraction vertex puts one join per machine
+    for name in ["chain3", "bmm2", "hoc"]:
+        plan = load_plan(f"{name}_p8_L8")
+        for v in plan.vertices:
+            if v.expr is None:
+                continue
+            machines = sorted(plan.exec[j].machine for j in plan.joins_of(v.vid))
+            assert machines == list(range(8)), (name, v.name, machines)
+
+
+def _lib():
+    from paper_2410_02682_b200 import build
+    build.build()
+    from paper_2410_02682_b200.executor import library
+    return library()
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib()
+    declared = re.findall(r"ED_API\s+[\w\s\*]+?\b(ed_\w+)\s*\(", open(HEADER).read())
+    assert sorted(declared) == sorted(abi.EXPORTED)
+    for name in declared:
+        assert hasattr(lib, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", os.path.join(ROOT, "paper_2410_02682_b200", "libed_gpu.so")],
+                         capture_output=True, text=True).stdout
+    exported = sorted(l.split()[-1] for l in out.splitlines() if " T " in l)
+    assert exported == sorted(declared), "library must export exactly the header's API"
+    assert lib.ed_abi_version() == 1
+
+
+def test_struct_layout_matches_header(tmp_path):
+    src = tmp_path / "sz.c"
+    names = ["ed_vertex_c", "ed_exec_vertex_c", "ed_plan_c", "ed_options_c", "ed_chunk_in_c",
+             "ed_tensor_in_c", "ed_output_c", "ed_machine_c", "ed_report_c", "ed_kernel_stat_c"]
+    src.write_text('#include <stdio.h>\n#include "ed_gpu.h"\nint main(){' +
+                   "".join(f'printf("%zu\\n", sizeof({n}));' for n in names) + "return 0;}\n")
+    exe = tmp_path / "sz"
+    subprocess.run(["gcc", "-I" + os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    sizes = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()]
+    assert sizes == [C.sizeof(getattr(abi, n)) for n in names]
+
+
+def test_no_device_is_a_loud_error():
+    """Without a GPU the product path raises; it never falls back to the CPU."""
+    try:
+        import torch
+        if torch.cuda.is_available():
+            pytest.skip("GPU present")
+    except Exception:
+        pass
+    _lib()
+    from paper_2410_02682_b200.executor import Context, EdError
+    with pytest.raises(EdError):
+        Context(0)
