@@ -91,7 +91,7 @@ __global__ void generic_kernel(const GenericParams p) {
         a[d] = 0;
       }
     }
-    out[o] = from_d<T>(acc);
+    if (out) out[o] = from_d<T>(acc);
     if (o16) o16[o] = __double2bfloat16(acc);
   }
 }
@@ -127,7 +127,7 @@ __global__ void refine_kernel(const RefineParams p) {
       acc = touched ? double(from_d<T>(agg_d(p.agg, acc, v))) : v;
       touched = true;
     }
-    out[o] = from_d<T>(acc);
+    if (out) out[o] = from_d<T>(acc);
     if (o16) o16[o] = __double2bfloat16(acc);
   }
 }

@@ -215,6 +215,10 @@ bool map_gemm(const Vtx& v, const shape& local_xy, bool bf16, GemmMap& g, std::s
     why = "B has no unit-stride N or K";
     return false;
   }
+  if (!bf16 && (g.a_mn || g.b_mn)) {
+    why = "tf32 MN-major operand";  // K-major only for kind::tf32 (bf16 supports both)
+    return false;
+  }
   const int es = bf16 ? 2 : 4;
   auto aligned = [&](const Dim& d) { return d.ext == 1 || (d.stride * es) % 16 == 0; };
   // outer (non-unit) strides of each TMA view must be 16-byte multiples
