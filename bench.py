@@ -59,7 +59,7 @@ class Clocks:
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -166,7 +166,7 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="bmm2")
     ap.add_argument("--precision", default="bf16")
@@ -207,17 +207,18 @@ def main():
     # ---- device-resident throughput --------------------------------------
     pp = PreparedPlan(ctx, plan, precision=args.precision)
     pp.upload(ins)
-    for _ in range(args.warmup):
-        rep = pp.run()
-    barrier()
-    torch.cuda.synchronize()
-    dev_ms = []
     with Clocks(local) as clk:
+        time.sleep(0.5)  # let the sampler start before the timed region
+        for _ in range(args.warmup):
+            rep = pp.run()
+        barrier()
+        torch.cuda.synchronize()
+        dev_ms = []
         for _ in range(args.steps):
             rep = pp.run()
             dev_ms.append(rep.device_ms)
-    torch.cuda.synchronize()
-    barrier()
+        torch.cuda.synchronize()
+        barrier()
     tot_ms = sum(dev_ms)
     if world > 1:
         t = torch.tensor([tot_ms], dtype=torch.float64)

@@ -1,15 +1,22 @@
-// Block contraction of a mul/sum join on the 5th-gen tensor cores.
+// Block contractions of mul/sum joins on the 5th-gen tensor cores.
 //
-// Replaces kernel_eval's mul/sum case (kernel.cc:48-65) for one output
-// region: C = sum_s A_s * B_s over the aggregation siblings s of the region
-// (the join tuples folded by the region's refinement, runtime.cc:242-261),
-// concatenated along K so the fold happens in the TMEM accumulator.
+// Replaces kernel_eval's mul/sum case (kernel.cc:48-65). One persistent
+// launch covers every output region of one einsum on this rank; each region
+// is C = sum_s A_s * B_s over its aggregation siblings s (the join tuples its
+// refinement folds, runtime.cc:242-261), K-concatenated so the fold happens
+// in the TMEM accumulator and no partial ever reaches HBM.
 //
-// Label permutations are folded into 3-D TMA tensor maps (inner dim, outer
-// dim, batch) — K-major or MN-major per operand — so no transpose copy ever
-// runs. Warp roles: warp 0 TMA producer, warp 1 TMEM allocator + single-
-// thread tcgen05.mma issuer, warps 2-5 epilogue (TMEM -> registers -> HBM),
-// STAGES-deep smem ring with full/empty mbarriers.
+// Label permutations are folded into 3-D TMA tensor maps {inner, outer,
+// batch} — K-major or MN-major per operand — so no transpose copy runs.
+// kCta = 2 pairs two SMs as one cluster (tcgen05 cta_group::2): a 256x256
+// tile per pair, each CTA loading half of A and half of B, so per-SM operand
+// traffic drops by a third and the smem ring gets six stages.
+// Warp roles (192 threads, 1 CTA per SM):
+//   warp 0     TMA producer over a STAGES-deep smem ring (full/empty mbarriers)
+//   warp 1     TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 2-5  epilogue: TMEM -> registers -> HBM (fp32 and/or bf16 shadow)
+// Two TMEM accumulators (2 x BN columns) let the epilogue of tile i overlap
+// the MMAs of tile i+1. Tiles are scheduled round-robin over the grid.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -20,193 +27,294 @@ namespace ed {
 
 namespace {
 
-constexpr int BM = 128;
-constexpr int STAGES = 4;
+constexpr int BM = 128;  // accumulator rows per CTA (TMEM lanes)
+constexpr int BN = 256;  // accumulator columns
 constexpr int kThreads = 192;
+constexpr int kAccStages = 2;
 
-template <bool kBF16, int BN>
+template <bool kBF16, int kCta>
 struct Cfg {
   static constexpr int ES = kBF16 ? 2 : 4;          // element bytes
   static constexpr int BK = 128 / ES;               // one 128-byte swizzle row of K
   static constexpr int UMMA_K = kBF16 ? 16 : 8;     // 32 bytes of K per MMA
+  static constexpr int TILE_M = BM * kCta;          // output rows per cluster tile
+  static constexpr int B_ROWS = BN / kCta;          // B rows (N) loaded per CTA
   static constexpr int A_BYTES = BM * 128;
-  static constexpr int B_BYTES = BN * 128;
+  static constexpr int B_BYTES = B_ROWS * 128;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = kCta == 2 ? 6 : 4;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr int MN_ATOM = 128 / ES;          // MN elements per 128-byte atom
 };
 
-template <bool kBF16, int BN>
-__global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ GemmParams p) {
-  using C_ = Cfg<kBF16, BN>;
+struct TileCoord {
+  int region, b, m0, n0;
+};
+
+template <int TILE_M>
+__device__ __forceinline__ TileCoord tile_coord(const GemmLaunch& p, int t, int tiles_m, int tiles_n) {
+  TileCoord c;
+  const int per_batch = tiles_m * tiles_n;
+  const int per_region = per_batch * p.batch;
+  c.region = t / per_region;
+  int r = t - c.region * per_region;
+  c.b = r / per_batch;
+  r -= c.b * per_batch;
+  c.m0 = (r / tiles_n) * TILE_M;
+  c.n0 = (r % tiles_n) * BN;
+  return c;
+}
+
+template <bool kBF16, int kCta>
+__global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ GemmLaunch p) {
+  using C_ = Cfg<kBF16, kCta>;
+  constexpr int STAGES = C_::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * C_::STAGE_BYTES);
   uint64_t* empty_bar = full_bar + STAGES;
-  uint64_t* tmem_full = empty_bar + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* acc_full = empty_bar + STAGES;
+  uint64_t* acc_empty = acc_full + kAccStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + kAccStages);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  const int n0 = blockIdx.x * BN;
-  const int m0 = blockIdx.y * BM;
-  const int bz = blockIdx.z;
+  const uint32_t rank = kCta == 2 ? cluster_ctarank() : 0;
+  const int tiles_m = (p.M + C_::TILE_M - 1) / C_::TILE_M;
+  const int tiles_n = (p.N + BN - 1) / BN;
+  const int total = tiles_m * tiles_n * p.batch * p.n_regions;
   const int kblocks = (p.K + C_::BK - 1) / C_::BK;
-  const int iters = kblocks * p.n_sib;
+  const int first = blockIdx.x / kCta, stride = gridDim.x / kCta;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int s = 0; s < kAccStages; ++s) {
+      mbar_init(&acc_full[s], 1);
+      mbar_init(&acc_empty[s], 4 * kCta);  // one arrive per epilogue warp of the pair
+    }
     fence_mbar_init();
   }
-  if (warp == 0 && lane == 0) {
-    for (int s = 0; s < p.n_sib; ++s) {
-      tma_prefetch(&p.a[s]);
-      tma_prefetch(&p.b[s]);
-    }
-  }
-  if (warp == 1) tmem_alloc<BN>(tmem_slot);
+  if (warp == 1) tmem_alloc<kAccStages * BN, kCta>(tmem_slot);
   tc_fence_before();
-  __syncthreads();
+  if (kCta == 2) cluster_sync();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    // ---- TMA producer ----
+    // ---- TMA producer (both CTAs of a pair load their halves) ----
     if (lane == 0) {
-      for (int it = 0; it < iters; ++it) {
-        const int s = it % STAGES;
-        const uint32_t ph = (it / STAGES) & 1;
-        mbar_wait(&empty_bar[s], ph ^ 1);
-        const int sib = it / kblocks;
-        const int k0 = (it % kblocks) * C_::BK;
-        uint8_t* sa = smem + s * C_::STAGE_BYTES;
-        uint8_t* sb = sa + C_::A_BYTES;
-        mbar_expect_tx(&full_bar[s], C_::STAGE_BYTES);
-        if (!p.a_mn) {
-          tma_load_3d(sa, &p.a[sib], &full_bar[s], k0, m0, bz);
-        } else {
-          for (int i = 0; i < BM / C_::MN_ATOM; ++i)
-            tma_load_3d(sa + i * C_::BK * 128, &p.a[sib], &full_bar[s], m0 + i * C_::MN_ATOM, k0, bz);
-        }
-        if (!p.b_mn) {
-          tma_load_3d(sb, &p.b[sib], &full_bar[s], k0, n0, bz);
-        } else {
-          for (int i = 0; i < BN / C_::MN_ATOM; ++i)
-            tma_load_3d(sb + i * C_::BK * 128, &p.b[sib], &full_bar[s], n0 + i * C_::MN_ATOM, k0, bz);
+      int it = 0;
+      for (int t = first; t < total; t += stride) {
+        const TileCoord tc = tile_coord<C_::TILE_M>(p, t, tiles_m, tiles_n);
+        const GemmRegion reg = p.regions[tc.region];
+        const int am = tc.m0 + int(rank) * BM, bn = tc.n0 + int(rank) * C_::B_ROWS;
+        for (int sib = 0; sib < reg.n_sib; ++sib) {
+          const CUtensorMap* ma = p.maps + reg.map0 + 2 * sib;
+          const CUtensorMap* mb = ma + 1;
+          for (int kb = 0; kb < kblocks; ++kb, ++it) {
+            const int s = it % STAGES;
+            const uint32_t ph = (it / STAGES) & 1;
+            mbar_wait(&empty_bar[s], ph ^ 1);
+            const int k0 = kb * C_::BK;
+            uint8_t* sa = smem + s * C_::STAGE_BYTES;
+            uint8_t* sb = sa + C_::A_BYTES;
+            if (rank == 0) mbar_expect_tx(&full_bar[s], C_::STAGE_BYTES * kCta);
+            auto load = [&](void* dst, const CUtensorMap* m, int c0, int c1) {
+              if (kCta == 2) tma_load_3d_2sm(dst, m, &full_bar[s], c0, c1, tc.b);
+              else tma_load_3d(dst, m, &full_bar[s], c0, c1, tc.b);
+            };
+            if (!p.a_mn) {
+              load(sa, ma, k0, am);
+            } else {
+#pragma unroll
+              for (int i = 0; i < BM / C_::MN_ATOM; ++i) load(sa + i * C_::BK * 128, ma, am + i * C_::MN_ATOM, k0);
+            }
+            if (!p.b_mn) {
+              load(sb, mb, k0, bn);
+            } else {
+#pragma unroll
+              for (int i = 0; i < C_::B_ROWS / C_::MN_ATOM; ++i)
+                load(sb + i * C_::BK * 128, mb, bn + i * C_::MN_ATOM, k0);
+            }
+          }
         }
       }
     }
   } else if (warp == 1) {
-    // ---- MMA issuer (one thread) ----
-    if (lane == 0) {
-      const uint32_t idesc = umma_idesc(kBF16 ? 1u : 2u, BM, BN, p.a_mn, p.b_mn);
+    // ---- MMA issuer (one thread of the leader CTA) ----
+    if (lane == 0 && rank == 0) {
+      const uint32_t idesc = umma_idesc(kBF16 ? 1u : 2u, BM * kCta, BN, p.a_mn, p.b_mn);
       // K-major: 8-row x 128-byte swizzle atoms stacked along MN (SBO 1024),
       // K advances 32 bytes per MMA inside the atom.
       // MN-major: 128-byte MN atoms of BK K-rows (LBO = BK*128), 8-row K
       // groups (SBO 1024), K advances UMMA_K rows per MMA.
       const uint32_t a_lbo = p.a_mn ? C_::BK * 128 : 16, b_lbo = p.b_mn ? C_::BK * 128 : 16;
       const uint32_t a_step = p.a_mn ? C_::UMMA_K * 128 : 32, b_step = p.b_mn ? C_::UMMA_K * 128 : 32;
-      for (int it = 0; it < iters; ++it) {
-        const int s = it % STAGES;
-        const uint32_t ph = (it / STAGES) & 1;
-        mbar_wait(&full_bar[s], ph);
+      int it = 0, local = 0;
+      for (int t = first; t < total; t += stride, ++local) {
+        const TileCoord tc = tile_coord<C_::TILE_M>(p, t, tiles_m, tiles_n);
+        const int n_sib = p.regions[tc.region].n_sib;
+        const int as = local & 1;
+        const uint32_t aph = (local >> 1) & 1;
+        if (kCta == 2) mbar_wait_cluster(&acc_empty[as], aph ^ 1);
+        else mbar_wait(&acc_empty[as], aph ^ 1);
         tc_fence_after();
-        const uint32_t sa = smem_u32(smem + s * C_::STAGE_BYTES);
-        const uint32_t sb = sa + C_::A_BYTES;
+        const uint32_t d_tmem = tmem + uint32_t(as * BN);
+        const int iters = kblocks * n_sib;
+        for (int i = 0; i < iters; ++i, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(&full_bar[s], ph);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + s * C_::STAGE_BYTES);
+          const uint32_t sb = sa + C_::A_BYTES;
 #pragma unroll
-        for (int k = 0; k < C_::BK / C_::UMMA_K; ++k) {
-          const uint64_t ad = umma_desc_sw128(sa + k * a_step, a_lbo, 1024);
-          const uint64_t bd = umma_desc_sw128(sb + k * b_step, b_lbo, 1024);
-          if (kBF16) mma_f16(tmem, ad, bd, idesc, (it | k) != 0);
-          else mma_tf32(tmem, ad, bd, idesc, (it | k) != 0);
+          for (int k = 0; k < C_::BK / C_::UMMA_K; ++k) {
+            const uint64_t ad = umma_desc_sw128(sa + k * a_step, a_lbo, 1024);
+            const uint64_t bd = umma_desc_sw128(sb + k * b_step, b_lbo, 1024);
+            const uint32_t acc = (i | k) != 0;
+            if (kCta == 2) {
+              if (kBF16) mma_f16_2sm(d_tmem, ad, bd, idesc, acc);
+              else mma_tf32_2sm(d_tmem, ad, bd, idesc, acc);
+            } else {
+              if (kBF16) mma_f16(d_tmem, ad, bd, idesc, acc);
+              else mma_tf32(d_tmem, ad, bd, idesc, acc);
+            }
+          }
+          if (kCta == 2) mma_commit_2sm(&empty_bar[s]);
+          else mma_commit(&empty_bar[s]);
         }
-        mma_commit(&empty_bar[s]);
+        if (kCta == 2) mma_commit_2sm(&acc_full[as]);
+        else mma_commit(&acc_full[as]);
       }
-      mma_commit(tmem_full);
     }
   } else {
-    // ---- epilogue: TMEM -> registers -> HBM ----
+    // ---- epilogue: TMEM -> registers -> HBM (each CTA its 128 rows) ----
     const int wq = warp & 3;  // TMEM lane quarter this warp may access
-    const int row = m0 + wq * 32 + lane;
-    mbar_wait(tmem_full, 0);
-    tc_fence_after();
-    float* c32 = p.c32 ? p.c32 + (long long)bz * p.c_sb + (long long)row * p.c_sm : nullptr;
-    __nv_bfloat16* c16 = p.c16 ? static_cast<__nv_bfloat16*>(p.c16) + (long long)bz * p.c_sb + (long long)row * p.c_sm : nullptr;
+    const uint32_t empty_leader = kCta == 2 ? mapa(smem_u32(acc_empty), 0) : 0;
+    int local = 0;
+    for (int t = first; t < total; t += stride, ++local) {
+      const TileCoord tc = tile_coord<C_::TILE_M>(p, t, tiles_m, tiles_n);
+      const GemmRegion reg = p.regions[tc.region];
+      const int as = local & 1;
+      const uint32_t aph = (local >> 1) & 1;
+      mbar_wait(&acc_full[as], aph);
+      tc_fence_after();
+      const int row = tc.m0 + int(rank) * BM + wq * 32 + lane;
+      const long long base = (long long)tc.b * p.c_sb + (long long)row * p.c_sm;
+      float* c32 = reg.c32 ? reg.c32 + base : nullptr;
+      __nv_bfloat16* c16 = reg.c16 ? static_cast<__nv_bfloat16*>(reg.c16) + base : nullptr;
+      const uint32_t tbase = tmem + (uint32_t(wq * 32) << 16) + uint32_t(as * BN);
 #pragma unroll 1
-    for (int c = 0; c < BN / 32; ++c) {
-      uint32_t r[32];
-      tmem_ld_32x32b_x32(tmem + (uint32_t(wq * 32) << 16) + uint32_t(c * 32), r);
-      tmem_ld_wait();
-      const int col = n0 + c * 32;
-      if (row >= p.M || col >= p.N) continue;
-      const bool full = col + 32 <= p.N && p.vec_ok;
-      if (c32) {
-        if (full) {
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tbase + uint32_t(c * 32), r);
+        tmem_ld_wait();
+        const int col = tc.n0 + c * 32;
+        if (row >= p.M || col >= p.N) continue;
+        const bool full = col + 32 <= p.N && p.vec_ok;
+        if (c32) {
+          if (full) {
 #pragma unroll
-          for (int j = 0; j < 32; j += 4)
-            *reinterpret_cast<float4*>(c32 + col + j) =
-                make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
-                            __uint_as_float(r[j + 3]));
-        } else {
-          for (int j = 0; j < 32 && col + j < p.N; ++j) c32[col + j] = __uint_as_float(r[j]);
+            for (int j = 0; j < 32; j += 4)
+              *reinterpret_cast<float4*>(c32 + col + j) =
+                  make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
+                              __uint_as_float(r[j + 3]));
+          } else {
+            for (int j = 0; j < 32 && col + j < p.N; ++j) c32[col + j] = __uint_as_float(r[j]);
+          }
+        }
+        if (c16) {
+          if (full) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) {
+              uint4 v;
+              __nv_bfloat162 h0 = __floats2bfloat162_rn(__uint_as_float(r[j]), __uint_as_float(r[j + 1]));
+              __nv_bfloat162 h1 = __floats2bfloat162_rn(__uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+              __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(r[j + 4]), __uint_as_float(r[j + 5]));
+              __nv_bfloat162 h3 = __floats2bfloat162_rn(__uint_as_float(r[j + 6]), __uint_as_float(r[j + 7]));
+              v.x = *reinterpret_cast<uint32_t*>(&h0);
+              v.y = *reinterpret_cast<uint32_t*>(&h1);
+              v.z = *reinterpret_cast<uint32_t*>(&h2);
+              v.w = *reinterpret_cast<uint32_t*>(&h3);
+              *reinterpret_cast<uint4*>(c16 + col + j) = v;
+            }
+          } else {
+            for (int j = 0; j < 32 && col + j < p.N; ++j) c16[col + j] = __float2bfloat16_rn(__uint_as_float(r[j]));
+          }
         }
       }
-      if (c16) {
-        if (full) {
-#pragma unroll
-          for (int j = 0; j < 32; j += 8) {
-            __nv_bfloat162 h[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              h[q] = __floats2bfloat162_rn(__uint_as_float(r[j + 2 * q]), __uint_as_float(r[j + 2 * q + 1]));
-            *reinterpret_cast<uint4*>(c16 + col + j) = *reinterpret_cast<uint4*>(h);
-          }
-        } else {
-          for (int j = 0; j < 32 && col + j < p.N; ++j) c16[col + j] = __float2bfloat16_rn(__uint_as_float(r[j]));
-        }
+      // this warp is done reading accumulator `as` (tell the leader's MMA issuer)
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (kCta == 2) mbar_arrive_cluster(empty_leader + uint32_t(as * sizeof(uint64_t)));
+        else mbar_arrive(&acc_empty[as]);
       }
     }
   }
 
   tc_fence_before();
-  __syncthreads();
+  if (kCta == 2) cluster_sync();
+  else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<BN>(tmem);
+    tmem_dealloc<kAccStages * BN, kCta>(tmem);
   }
 }
 
-template <bool kBF16, int BN>
+template <bool kBF16, int kCta>
 cudaError_t prepare_t() {
-  return cudaFuncSetAttribute(gemm_kernel<kBF16, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              Cfg<kBF16, BN>::SMEM);
+  return cudaFuncSetAttribute(gemm_kernel<kBF16, kCta>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              Cfg<kBF16, kCta>::SMEM);
 }
 
-template <bool kBF16, int BN>
-cudaError_t launch_t(const GemmParams& p, cudaStream_t stream) {
-  using C_ = Cfg<kBF16, BN>;
-  auto k = gemm_kernel<kBF16, BN>;
-  dim3 grid((p.N + BN - 1) / BN, (p.M + BM - 1) / BM, p.batch);
-  k<<<grid, kThreads, C_::SMEM, stream>>>(p);
-  return cudaGetLastError();
+template <bool kBF16, int kCta>
+cudaError_t launch_t(const GemmLaunch& p, int num_sms, cudaStream_t stream) {
+  using C_ = Cfg<kBF16, kCta>;
+  const long long tiles =
+      (long long)((p.M + C_::TILE_M - 1) / C_::TILE_M) * ((p.N + BN - 1) / BN) * p.batch * p.n_regions;
+  const int clusters = int(tiles < num_sms / kCta ? tiles : num_sms / kCta);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(clusters * kCta);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = C_::SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kCta;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, gemm_kernel<kBF16, kCta>, p);
 }
 
 }  // namespace
 
-int gemm_bn(bool bf16) { (void)bf16; return 256; }
 int gemm_bk(bool bf16) { return bf16 ? 64 : 32; }
+int gemm_bn(bool) { return BN; }
+bool gemm_paired(int M) { return M > BM; }
+int gemm_b_box(int M) { return gemm_paired(M) ? BN / 2 : BN; }
+int gemm_bm() { return BM; }
 
 cudaError_t gemm_prepare() {
-  cudaError_t e = prepare_t<true, 256>();
-  return e != cudaSuccess ? e : prepare_t<false, 256>();
+  cudaError_t e;
+  if ((e = prepare_t<true, 1>()) != cudaSuccess) return e;
+  if ((e = prepare_t<false, 1>()) != cudaSuccess) return e;
+  if ((e = prepare_t<true, 2>()) != cudaSuccess) return e;
+  return prepare_t<false, 2>();
 }
 
-cudaError_t launch_gemm(const GemmParams& p, bool bf16, cudaStream_t stream) {
-  return bf16 ? launch_t<true, 256>(p, stream) : launch_t<false, 256>(p, stream);
+cudaError_t launch_gemm(const GemmLaunch& p, int num_sms, cudaStream_t stream) {
+  // pair SMs when the output has rows for both halves of a 256-row tile
+  const bool pair = gemm_paired(p.M);
+  if (p.bf16) return pair ? launch_t<true, 2>(p, num_sms, stream) : launch_t<true, 1>(p, num_sms, stream);
+  return pair ? launch_t<false, 2>(p, num_sms, stream) : launch_t<false, 1>(p, num_sms, stream);
 }
 
 }  // namespace ed

@@ -7,21 +7,33 @@ namespace ed {
 
 constexpr int kMaxSib = 8;  // aggregation siblings folded in one accumulator
 
-struct GemmParams {
-  CUtensorMap a[kMaxSib];   // MMA-A operand of each sibling (M x K), 3-D {inner, outer, batch}
-  CUtensorMap b[kMaxSib];   // MMA-B operand of each sibling (N x K)
+// One output region of an einsum: the sum over its aggregation siblings s of
+// A_s * B_s (K-concatenated), written to c32 and/or its bf16 shadow c16.
+struct GemmRegion {
   int n_sib;
+  int map0;        // maps[map0 + 2*s] = A_s, maps[map0 + 2*s + 1] = B_s
+  float* c32;
+  void* c16;
+};
+
+// One launch: every region of one einsum on this rank (same chunk shapes).
+struct GemmLaunch {
+  const CUtensorMap* maps;    // device array, 64-byte aligned
+  const GemmRegion* regions;  // device array
+  int n_regions;
   int M, N, K, batch;
-  int a_mn, b_mn;           // 1: operand is MN-major (M or N contiguous)
-  int vec_ok;               // 1: output rows 16-byte aligned (vector stores)
-  float* c32;               // fp32 output (nullable)
-  void* c16;                // bf16 shadow output (nullable)
-  long long c_sm, c_sb;     // output element strides for M and batch; N stride is 1
+  int a_mn, b_mn;             // 1: operand is MN-major (M or N contiguous)
+  int vec_ok;                 // 1: output rows 16-byte aligned (vector stores)
+  long long c_sm, c_sb;       // output element strides for M and batch; N stride is 1
+  int bf16;                   // operand type: 1 bf16 (kind::f16), 0 fp32 (kind::tf32)
 };
 
 int gemm_bk(bool bf16);
 int gemm_bn(bool bf16);
+int gemm_bm();
+bool gemm_paired(int M);  // 2-SM (cta_group::2) tiles for this M
+int gemm_b_box(int M);    // B rows (N) one CTA loads per K-major TMA box
 cudaError_t gemm_prepare();  // sets the dynamic-smem attribute (call before capture)
-cudaError_t launch_gemm(const GemmParams& p, bool bf16, cudaStream_t stream);
+cudaError_t launch_gemm(const GemmLaunch& p, int num_sms, cudaStream_t stream);
 
 }  // namespace ed

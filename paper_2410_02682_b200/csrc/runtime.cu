@@ -274,7 +274,10 @@ struct Op {
   OpKind kind;
   std::string name;   // launch class, e.g. "gemm_bf16:Z1"
   double flops = 0, bytes = 0;
-  GemmParams gemm;
+  GemmLaunch gemm{};
+  std::vector<int> heads;              // GEMM: region heads (join ids), fold order
+  std::vector<CUtensorMap> maps;       // GEMM: host copies, uploaded by allocate()
+  std::vector<GemmRegion> regions;
   bool bf16 = false;
   GenericParams gen;
   RefineParams ref;
@@ -294,7 +297,7 @@ struct Buffer {
 }  // namespace
 
 struct ed_ctx {
-  int device = 0, rank = 0, world = 1;
+  int device = 0, rank = 0, world = 1, num_sms = 148;
   ncclComm_t comm = nullptr;
   cudaStream_t stream = nullptr, comm_stream = nullptr;
 };
@@ -323,6 +326,8 @@ struct ed_plan_h {
   void* arena = nullptr;
   size_t arena_bytes = 0;
   DepRect* d_deps = nullptr;
+  void* d_maps = nullptr;          // CUtensorMap[] of all GEMM launches
+  void* d_regions = nullptr;       // GemmRegion[] of all GEMM launches
   void** d_ptrs = nullptr;         // chunk-pointer tables for scatter/gather
   int* d_err = nullptr;
   void* staging = nullptr;
@@ -671,6 +676,7 @@ void ed_plan_h::build() {
   }
   ops.clear();
   contraction_flops = 0;
+  std::set<int> gemm_emitted;
   for (int id = 0; id < ne; ++id) {
     for (auto& [d, dst] : xfer_at[id]) {
       if (rank_of(d) == me) {
@@ -705,14 +711,18 @@ void ed_plan_h::build() {
       if (first_join < 0) first_join = id;
       if (w.join == ED_JOIN_MUL && w.agg == ED_AGG_SUM) contraction_flops += 2.0 * double(u.fp);
       if (gmap.count(u.producer)) {
-        if (!fused_head[id]) continue;
+        if (!fused_head[id] || gemm_emitted.count(u.producer)) continue;
+        gemm_emitted.insert(u.producer);
+        // one persistent launch for every region of this einsum on this rank
         Op op{OpKind::GEMM};
         op.bf16 = bf16;
         op.name = std::string(bf16 ? "gemm_bf16:" : "gemm_tf32:") + w.name;
         op.ptr = reinterpret_cast<void*>(id);
-        auto& sibs = region_sibs[id];
-        op.gemm.n_sib = int(sibs.size());
-        for (int s : sibs) op.flops += 2.0 * double(X[s].fp);
+        for (int h = 0; h < ne; ++h)
+          if (fused_head[h] && X[h].producer == u.producer) {
+            op.heads.push_back(h);
+            for (int s : region_sibs[h]) op.flops += 2.0 * double(X[s].fp);
+          }
         ops.push_back(op);
       } else {
         Op op{OpKind::GENERIC};
@@ -734,8 +744,9 @@ void ed_plan_h::build() {
     // after the op that produced the first join
     size_t at = 0;
     for (size_t i = 0; i < ops.size(); ++i)
-      if ((ops[i].kind == OpKind::GEMM || ops[i].kind == OpKind::GENERIC) &&
-          reinterpret_cast<intptr_t>(ops[i].ptr) == owner[first_join]) {
+      if ((ops[i].kind == OpKind::GEMM &&
+           std::count(ops[i].heads.begin(), ops[i].heads.end(), owner[first_join])) ||
+          (ops[i].kind == OpKind::GENERIC && reinterpret_cast<intptr_t>(ops[i].ptr) == owner[first_join])) {
         at = i + 1;
         break;
       }
@@ -784,43 +795,63 @@ void ed_plan_h::allocate() {
   }
 
   auto resolve = [&](int dep) { return local[dep] ? owner[dep] : dep; };
+  size_t gemm_maps_total = 0, gemm_regions_total = 0;
   for (auto& op : ops) {
     const int id = int(reinterpret_cast<intptr_t>(op.ptr));
     switch (op.kind) {
       case OpKind::GEMM: {
         const Ex& u = X[id];
         const GemmMap& g = gmap_.at(u.producer);
-        GemmParams& p = op.gemm;
+        GemmLaunch& p = op.gemm;
         const bool b16 = op.bf16;
-        const auto& sibs = region_sibs_.at(id);
-        p.n_sib = int(sibs.size());
+        p.bf16 = b16;
         p.M = int(g.am.ext);
         p.N = int(g.bn.ext);
         p.K = int(g.ak.ext);
         p.batch = int(g.ab.ext);
         p.a_mn = g.a_mn;
         p.b_mn = g.b_mn;
-        const uint32_t BK = uint32_t(gemm_bk(b16)), BN = uint32_t(gemm_bn(b16));
-        const uint32_t ATOM = 128u / (b16 ? 2u : 4u);
-        for (int s = 0; s < p.n_sib; ++s) {
-          const Ex& j = X[sibs[s]];
-          int da = resolve(j.deps[g.a_slot]), db = resolve(j.deps[g.b_slot]);
-          const void* pa = b16 ? buf[da].b16 : buf[da].main;
-          const void* pb = b16 ? buf[db].b16 : buf[db].main;
-          if (!pa || !pb) throw ed_error(ED_ERR_PLAN, "GEMM operand buffer missing");
-          if (!g.a_mn) make_map(&p.a[s], pa, b16, g.ak.ext, g.am.ext, g.am.stride, g.ab.ext, g.ab.stride, BK, 128);
-          else make_map(&p.a[s], pa, b16, g.am.ext, g.ak.ext, g.ak.stride, g.ab.ext, g.ab.stride, ATOM, BK);
-          if (!g.b_mn) make_map(&p.b[s], pb, b16, g.bk.ext, g.bn.ext, g.bn.stride, g.bb.ext, g.bb.stride, BK, BN);
-          else make_map(&p.b[s], pb, b16, g.bn.ext, g.bk.ext, g.bk.stride, g.bb.ext, g.bb.stride, ATOM, BK);
-        }
-        p.c32 = static_cast<float*>(buf[id].main);
-        p.c16 = buf[id].b16;
         p.c_sm = g.cm.ext > 1 ? g.cm.stride : 0;
         p.c_sb = g.cb.ext > 1 ? g.cb.stride : 0;
         p.vec_ok = (p.c_sm % 8 == 0) && (p.c_sb % 8 == 0);
+        const uint32_t BK = uint32_t(gemm_bk(b16)), BM = uint32_t(gemm_bm());
+        const uint32_t ATOM = 128u / (b16 ? 2u : 4u);
+        op.maps.clear();
+        op.regions.clear();
+        int total_sib = 0;
+        for (int head : op.heads) {
+          const auto& sibs = region_sibs_.at(head);
+          GemmRegion r{};
+          r.n_sib = int(sibs.size());
+          r.map0 = int(op.maps.size());
+          for (int sidx : sibs) {
+            const Ex& j = X[sidx];
+            int da = resolve(j.deps[g.a_slot]), db = resolve(j.deps[g.b_slot]);
+            const void* pa = b16 ? buf[da].b16 : buf[da].main;
+            const void* pb = b16 ? buf[db].b16 : buf[db].main;
+            if (!pa || !pb) throw ed_error(ED_ERR_PLAN, "GEMM operand buffer missing");
+            CUtensorMap ma, mb;
+            if (!g.a_mn) make_map(&ma, pa, b16, g.ak.ext, g.am.ext, g.am.stride, g.ab.ext, g.ab.stride, BK, BM);
+            else make_map(&ma, pa, b16, g.am.ext, g.ak.ext, g.ak.stride, g.ab.ext, g.ab.stride, ATOM, BK);
+            if (!g.b_mn)
+              make_map(&mb, pb, b16, g.bk.ext, g.bn.ext, g.bn.stride, g.bb.ext, g.bb.stride, BK,
+                       uint32_t(gemm_b_box(p.M)));
+            else make_map(&mb, pb, b16, g.bn.ext, g.bk.ext, g.bk.stride, g.bb.ext, g.bb.stride, ATOM, BK);
+            op.maps.push_back(ma);
+            op.maps.push_back(mb);
+            ++total_sib;
+          }
+          r.c32 = static_cast<float*>(buf[head].main);
+          r.c16 = buf[head].b16;
+          op.regions.push_back(r);
+        }
+        p.n_regions = int(op.regions.size());
         const double ab = double(g.am.ext) * g.ak.ext * g.ab.ext + double(g.bn.ext) * g.bk.ext * g.bb.ext;
-        const double cbytes = double(g.am.ext) * g.bn.ext * g.ab.ext * ((p.c32 ? 4 : 0) + (p.c16 ? 2 : 0));
-        op.bytes = ab * (b16 ? 2 : 4) * p.n_sib + cbytes;
+        const double cbytes = double(g.am.ext) * g.bn.ext * g.ab.ext *
+                              ((op.regions[0].c32 ? 4 : 0) + (op.regions[0].c16 ? 2 : 0));
+        op.bytes = ab * (b16 ? 2 : 4) * total_sib + cbytes * p.n_regions;
+        gemm_maps_total += op.maps.size();
+        gemm_regions_total += op.regions.size();
         break;
       }
       case OpKind::GENERIC: {
@@ -925,12 +956,29 @@ void ed_plan_h::allocate() {
         break;
     }
   }
+  // tensor maps and region tables of every GEMM launch, in device memory
+  if (gemm_maps_total) {
+    CUDA_OK(cudaMalloc(&d_maps, sizeof(CUtensorMap) * gemm_maps_total));
+    CUDA_OK(cudaMalloc(&d_regions, sizeof(GemmRegion) * gemm_regions_total));
+    size_t mo = 0, ro = 0;
+    for (auto& op : ops) {
+      if (op.kind != OpKind::GEMM) continue;
+      CUtensorMap* dm = static_cast<CUtensorMap*>(d_maps) + mo;
+      GemmRegion* dr = static_cast<GemmRegion*>(d_regions) + ro;
+      CUDA_OK(cudaMemcpy(dm, op.maps.data(), sizeof(CUtensorMap) * op.maps.size(), cudaMemcpyHostToDevice));
+      CUDA_OK(cudaMemcpy(dr, op.regions.data(), sizeof(GemmRegion) * op.regions.size(), cudaMemcpyHostToDevice));
+      op.gemm.maps = dm;
+      op.gemm.regions = dr;
+      mo += op.maps.size();
+      ro += op.regions.size();
+    }
+  }
 }
 
 void ed_plan_h::launch_op(size_t i, cudaStream_t s) {
   Op& op = ops[i];
   switch (op.kind) {
-    case OpKind::GEMM: CUDA_OK(launch_gemm(op.gemm, op.bf16, s)); break;
+    case OpKind::GEMM: CUDA_OK(launch_gemm(op.gemm, ctx->num_sms, s)); break;
     case OpKind::GENERIC: CUDA_OK(launch_generic(op.gen, f64, s)); break;
     case OpKind::REFINE: CUDA_OK(launch_refine(op.ref, f64, s)); break;
     case OpKind::CORRUPT: CUDA_OK(launch_add_one(op.ptr, op.dt, s)); break;
@@ -971,6 +1019,8 @@ void ed_plan_h::destroy() {
   for (auto e : op_events) cudaEventDestroy(e);
   if (arena) cudaFree(arena);
   if (d_deps) cudaFree(d_deps);
+  if (d_maps) cudaFree(d_maps);
+  if (d_regions) cudaFree(d_regions);
   if (d_ptrs) cudaFree(d_ptrs);
   if (d_err) cudaFree(d_err);
   if (staging) cudaFree(staging);
@@ -1054,6 +1104,7 @@ ed_status ed_ctx_create(int32_t device, int32_t rank, int32_t world, const void*
     if (prop.major != 10) throw ed_error(ED_ERR_UNSUPPORTED, "libed_gpu is built for sm_100a (B200)");
     auto* c = new ed_ctx;
     c->device = device;
+    c->num_sms = prop.multiProcessorCount;
     c->rank = rank;
     c->world = world;
     try {
