@@ -43,7 +43,8 @@ struct Cfg {
   static constexpr int B_BYTES = B_ROWS * 128;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = kCta == 2 ? 6 : 4;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int STORE_BYTES = 4 * 2 * 4096;  // 4 epilogue warps x 2 staging tiles of 32x128 B
+  static constexpr int SMEM = STAGES * STAGE_BYTES + STORE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr int MN_ATOM = 128 / ES;          // MN elements per 128-byte atom
 };
 
@@ -71,7 +72,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   constexpr int STAGES = C_::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * C_::STAGE_BYTES);
+  uint8_t* stage_out = smem + STAGES * C_::STAGE_BYTES;  // epilogue staging (1024-aligned)
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(stage_out + C_::STORE_BYTES);
   uint64_t* empty_bar = full_bar + STAGES;
   uint64_t* acc_full = empty_bar + STAGES;
   uint64_t* acc_empty = acc_full + kAccStages;
@@ -197,6 +199,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     const int wq = warp & 3;  // TMEM lane quarter this warp may access
     const uint32_t empty_leader = kCta == 2 ? mapa(smem_u32(acc_empty), 0) : 0;
     int local = 0;
+    uint32_t stage_ctr = 0;
     for (int t = first; t < total; t += stride, ++local) {
       const TileCoord tc = tile_coord<C_::TILE_M>(p, t, tiles_m, tiles_n);
       const GemmRegion reg = p.regions[tc.region];
@@ -209,43 +212,62 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       float* c32 = reg.c32 ? reg.c32 + base : nullptr;
       __nv_bfloat16* c16 = reg.c16 ? static_cast<__nv_bfloat16*>(reg.c16) + base : nullptr;
       const uint32_t tbase = tmem + (uint32_t(wq * 32) << 16) + uint32_t(as * BN);
+      if (reg.cmap32 >= 0 || reg.cmap16 >= 0) {
+        // TMEM -> registers -> 128B-swizzled smem tile -> TMA store (full lines,
+        // clipped at the region bounds); two staging tiles per warp alternate.
+        const int trow = tc.m0 + int(rank) * BM + wq * 32;
+        for (int pass = 0; pass < 2; ++pass) {
+          const int cm = pass == 0 ? reg.cmap32 : reg.cmap16;
+          if (cm < 0) continue;
+          const int cols = pass == 0 ? 32 : 64;  // 128 bytes of fp32 / bf16
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(tbase + uint32_t(c * 32), r);
-        tmem_ld_wait();
-        const int col = tc.n0 + c * 32;
-        if (row >= p.M || col >= p.N) continue;
-        const bool full = col + 32 <= p.N && p.vec_ok;
-        if (c32) {
-          if (full) {
+          for (int c = 0; c < BN / cols; ++c) {
+            uint32_t r[64];
+            tmem_ld_32x32b_x32(tbase + uint32_t(c * cols), *reinterpret_cast<uint32_t(*)[32]>(r));
+            if (pass == 1) tmem_ld_32x32b_x32(tbase + uint32_t(c * cols + 32), *reinterpret_cast<uint32_t(*)[32]>(r + 32));
+            tmem_ld_wait();
+            uint8_t* tile = stage_out + (wq * 2 + (stage_ctr & 1)) * 4096;
+            if (lane == 0) bulk_wait_read<1>();
+            __syncwarp();
+            uint8_t* rowp = tile + lane * 128;
 #pragma unroll
-            for (int j = 0; j < 32; j += 4)
-              *reinterpret_cast<float4*>(c32 + col + j) =
-                  make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
-                              __uint_as_float(r[j + 3]));
-          } else {
-            for (int j = 0; j < 32 && col + j < p.N; ++j) c32[col + j] = __uint_as_float(r[j]);
+            for (int j = 0; j < 8; ++j) {
+              uint4 v;
+              if (pass == 0) {
+                v = make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
+              } else {
+                __nv_bfloat162 h0 = __floats2bfloat162_rn(__uint_as_float(r[8 * j]), __uint_as_float(r[8 * j + 1]));
+                __nv_bfloat162 h1 = __floats2bfloat162_rn(__uint_as_float(r[8 * j + 2]), __uint_as_float(r[8 * j + 3]));
+                __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(r[8 * j + 4]), __uint_as_float(r[8 * j + 5]));
+                __nv_bfloat162 h3 = __floats2bfloat162_rn(__uint_as_float(r[8 * j + 6]), __uint_as_float(r[8 * j + 7]));
+                v.x = *reinterpret_cast<uint32_t*>(&h0);
+                v.y = *reinterpret_cast<uint32_t*>(&h1);
+                v.z = *reinterpret_cast<uint32_t*>(&h2);
+                v.w = *reinterpret_cast<uint32_t*>(&h3);
+              }
+              *reinterpret_cast<uint4*>(rowp + ((j ^ (lane & 7)) << 4)) = v;
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_3d(p.maps + cm, tile, tc.n0 + c * cols, trow, tc.b);
+              bulk_commit();
+            }
+            ++stage_ctr;
           }
         }
-        if (c16) {
-          if (full) {
-#pragma unroll
-            for (int j = 0; j < 32; j += 8) {
-              uint4 v;
-              __nv_bfloat162 h0 = __floats2bfloat162_rn(__uint_as_float(r[j]), __uint_as_float(r[j + 1]));
-              __nv_bfloat162 h1 = __floats2bfloat162_rn(__uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
-              __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(r[j + 4]), __uint_as_float(r[j + 5]));
-              __nv_bfloat162 h3 = __floats2bfloat162_rn(__uint_as_float(r[j + 6]), __uint_as_float(r[j + 7]));
-              v.x = *reinterpret_cast<uint32_t*>(&h0);
-              v.y = *reinterpret_cast<uint32_t*>(&h1);
-              v.z = *reinterpret_cast<uint32_t*>(&h2);
-              v.w = *reinterpret_cast<uint32_t*>(&h3);
-              *reinterpret_cast<uint4*>(c16 + col + j) = v;
-            }
-          } else {
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tbase + uint32_t(c * 32), r);
+          tmem_ld_wait();
+          const int col = tc.n0 + c * 32;
+          if (row >= p.M || col >= p.N) continue;
+          if (c32)
+            for (int j = 0; j < 32 && col + j < p.N; ++j) c32[col + j] = __uint_as_float(r[j]);
+          if (c16)
             for (int j = 0; j < 32 && col + j < p.N; ++j) c16[col + j] = __float2bfloat16_rn(__uint_as_float(r[j]));
-          }
         }
       }
       // this warp is done reading accumulator `as` (tell the leader's MMA issuer)
@@ -256,6 +278,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         else mbar_arrive(&acc_empty[as]);
       }
     }
+    if (lane == 0) bulk_wait<0>();
   }
 
   tc_fence_before();

@@ -12,6 +12,8 @@ constexpr int kMaxSib = 8;  // aggregation siblings folded in one accumulator
 struct GemmRegion {
   int n_sib;
   int map0;        // maps[map0 + 2*s] = A_s, maps[map0 + 2*s + 1] = B_s
+  int cmap32;      // output tensor map for TMA stores (-1: direct stores)
+  int cmap16;
   float* c32;
   void* c16;
 };
@@ -33,6 +35,7 @@ int gemm_bn(bool bf16);
 int gemm_bm();
 bool gemm_paired(int M);  // 2-SM (cta_group::2) tiles for this M
 int gemm_b_box(int M);    // B rows (N) one CTA loads per K-major TMA box
+constexpr int kStoreRows = 32;   // epilogue TMA-store box: 32 rows x 128 bytes
 cudaError_t gemm_prepare();  // sets the dynamic-smem attribute (call before capture)
 cudaError_t launch_gemm(const GemmLaunch& p, int num_sms, cudaStream_t stream);
 

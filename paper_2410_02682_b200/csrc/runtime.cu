@@ -843,6 +843,20 @@ void ed_plan_h::allocate() {
           }
           r.c32 = static_cast<float*>(buf[head].main);
           r.c16 = buf[head].b16;
+          // output tensor maps for the TMA-store epilogue (16-byte strides only)
+          auto out_map = [&](void* base, bool o16) {
+            const int oes = o16 ? 2 : 4;
+            bool ok = base && (g.cm.ext == 1 || (g.cm.stride * oes) % 16 == 0) &&
+                      (g.cb.ext == 1 || (g.cb.stride * oes) % 16 == 0);
+            if (!ok) return -1;
+            CUtensorMap mc;
+            make_map(&mc, base, o16, g.bn.ext, g.am.ext, g.cm.stride, g.ab.ext, g.cb.stride, o16 ? 64u : 32u,
+                     uint32_t(kStoreRows));
+            op.maps.push_back(mc);
+            return int(op.maps.size()) - 1;
+          };
+          r.cmap32 = out_map(r.c32, false);
+          r.cmap16 = out_map(r.c16, true);
           op.regions.push_back(r);
         }
         p.n_regions = int(op.regions.size());
