@@ -1,0 +1,37 @@
+// Grouped memory-bound join kernels (see ewise.cu).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ed {
+
+// Per-join operand pointers of a grouped launch (blockIdx.y = join).
+struct JoinPtrs {
+  const void* x;
+  const void* y;
+  void* out;     // storage dtype (nullable)
+  void* out16;   // bf16 shadow (nullable)
+};
+
+struct EwiseParams {
+  const JoinPtrs* joins;  // device array
+  int64_t n;              // elements per join output
+  int binary;             // 1: join op with y
+  int y_mode;             // 1: y has Z's layout, 2: y broadcast over Z's trailing `inner` elements
+  int64_t inner;
+  int join, map;
+  double c;
+  int* err;               // division-by-zero flag
+};
+
+struct RowReduceParams {
+  const JoinPtrs* joins;
+  int64_t rows, len;      // Z elements, aggregated elements per Z element (trailing in X)
+  int map, agg;
+  double c;
+};
+
+cudaError_t launch_ewise(const EwiseParams& p, int n_joins, bool f64, bool exact, cudaStream_t s);
+cudaError_t launch_rowreduce(const RowReduceParams& p, int n_joins, bool f64, bool exact, cudaStream_t s);
+
+}  // namespace ed

@@ -132,6 +132,51 @@ __global__ void refine_kernel(const RefineParams p) {
   }
 }
 
+template <typename T>
+__global__ void __launch_bounds__(256) rect_kernel(const RectParams p) {
+  const RectGroup& g = p.groups[blockIdx.y];
+  T* out = static_cast<T*>(p.out);
+  __nv_bfloat16* o16 = static_cast<__nv_bfloat16*>(p.out16);
+  const int r = p.rank;
+  const int64_t inner = g.ext[r - 1];
+  constexpr int V = 16 / sizeof(T);
+  const int64_t r_begin = int64_t(blockIdx.x) * p.rows_per_block;
+  const int64_t r_end = r_begin + p.rows_per_block < g.rows ? r_begin + p.rows_per_block : g.rows;
+  for (int64_t row = r_begin; row < r_end; ++row) {
+    int64_t rem = row, so = g.src_off, dofs = g.dst_off;
+    for (int d = r - 2; d >= 0; --d) {
+      const int64_t c = rem % g.ext[d];
+      rem /= g.ext[d];
+      so += c * g.sstr[d];
+      dofs += c * g.dstr[d];
+    }
+    if (p.vec) {
+      for (int64_t i = int64_t(threadIdx.x) * V; i < inner; i += int64_t(blockDim.x) * V) {
+        T acc[V], v[V];
+        *reinterpret_cast<uint4*>(acc) = *reinterpret_cast<const uint4*>(static_cast<const T*>(g.src[0]) + so + i);
+        for (int k = 1; k < g.n_src; ++k) {
+          *reinterpret_cast<uint4*>(v) = *reinterpret_cast<const uint4*>(static_cast<const T*>(g.src[k]) + so + i);
+#pragma unroll
+          for (int e = 0; e < V; ++e) acc[e] = from_d<T>(agg_d(p.agg, double(acc[e]), double(v[e])));
+        }
+        if (out) *reinterpret_cast<uint4*>(out + dofs + i) = *reinterpret_cast<uint4*>(acc);
+        if (o16) {
+#pragma unroll
+          for (int e = 0; e < V; ++e) o16[dofs + i + e] = __double2bfloat16(double(acc[e]));
+        }
+      }
+    } else {
+      for (int64_t i = threadIdx.x; i < inner; i += blockDim.x) {
+        double acc = double(static_cast<const T*>(g.src[0])[so + i]);
+        for (int k = 1; k < g.n_src; ++k)
+          acc = double(from_d<T>(agg_d(p.agg, acc, double(static_cast<const T*>(g.src[k])[so + i]))));
+        if (out) out[dofs + i] = from_d<T>(acc);
+        if (o16) o16[dofs + i] = __double2bfloat16(acc);
+      }
+    }
+  }
+}
+
 template <typename T> __device__ __forceinline__ double ld(const void* p, int64_t i) {
   return double(static_cast<const T*>(p)[i]);
 }
@@ -207,6 +252,13 @@ cudaError_t launch_refine(const RefineParams& p, bool f64, cudaStream_t s) {
   const int block = 256;
   if (f64) refine_kernel<double><<<grid_for(p.n_out, block), block, 0, s>>>(p);
   else refine_kernel<float><<<grid_for(p.n_out, block), block, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rect(const RectParams& p, int n_groups, int64_t max_rows, bool f64, cudaStream_t s) {
+  dim3 grid(unsigned((max_rows + p.rows_per_block - 1) / p.rows_per_block), unsigned(n_groups));
+  if (f64) rect_kernel<double><<<grid, 256, 0, s>>>(p);
+  else rect_kernel<float><<<grid, 256, 0, s>>>(p);
   return cudaGetLastError();
 }
 

@@ -45,6 +45,28 @@ struct RefineParams {
   void* out16;
 };
 
+// Fast refinement: the overlap rectangle of one producer region with the
+// consumer chunk, folding the region's aggregation siblings in dep order.
+constexpr int kRectSrc = 8;
+struct RectGroup {
+  int n_src;
+  const void* src[kRectSrc];
+  int64_t src_off, dst_off;           // element offset of the rectangle's origin
+  int64_t ext[kMaxRank];              // rectangle extents
+  int64_t sstr[kMaxRank], dstr[kMaxRank];  // row-major strides of source region / consumer chunk
+  int64_t rows;                       // prod(ext[0..rank-2])
+};
+
+struct RectParams {
+  int rank;
+  int agg;
+  int vec;                            // 1: inner runs and offsets are 16-byte aligned
+  int rows_per_block;
+  const RectGroup* groups;            // device array
+  void* out;
+  void* out16;
+};
+
 // Whole tensor <-> chunk buffers (chunk / assemble, relation.cc:31-78).
 struct ChunkMapParams {
   int rank;
@@ -60,6 +82,7 @@ enum class DT : int { F64 = 0, F32 = 1, BF16 = 2 };
 
 cudaError_t launch_generic(const GenericParams& p, bool f64, cudaStream_t s);
 cudaError_t launch_refine(const RefineParams& p, bool f64, cudaStream_t s);
+cudaError_t launch_rect(const RectParams& p, int n_groups, int64_t max_rows, bool f64, cudaStream_t s);
 cudaError_t launch_scatter(const ChunkMapParams& p, const void* whole, DT in, DT store, cudaStream_t s);
 cudaError_t launch_gather(const ChunkMapParams& p, void* whole, DT store, DT out, cudaStream_t s);
 cudaError_t launch_convert(const void* src, DT in, void* dst, DT out, int64_t n, cudaStream_t s);

@@ -29,6 +29,7 @@
 
 #include "ed_gpu.h"
 #include "gemm_sm100.h"
+#include "ewise.h"
 #include "kernels.h"
 
 using namespace ed;
@@ -268,7 +269,7 @@ void make_map(CUtensorMap* m, const void* base, bool bf16, int64_t inner, int64_
 }
 
 // ---- schedule -------------------------------------------------------------------
-enum class OpKind { GEMM, GENERIC, REFINE, CORRUPT, SEND, RECV, CONVERT };
+enum class OpKind { GEMM, GENERIC, REFINE, CORRUPT, SEND, RECV, CONVERT, EWISE, ROWREDUCE };
 
 struct Op {
   OpKind kind;
@@ -281,6 +282,12 @@ struct Op {
   bool bf16 = false;
   GenericParams gen;
   RefineParams ref;
+  EwiseParams ew{};
+  RectParams rect{};
+  std::vector<RectGroup> groups;       // REFINE fast path (empty: generic fold kernel)
+  int64_t max_rows = 0;
+  RowReduceParams rr{};
+  std::vector<JoinPtrs> jptrs;         // EWISE / ROWREDUCE: per-join operands
   void* ptr = nullptr;
   DT dt = DT::F32;
   int peer = -1;
@@ -293,6 +300,47 @@ struct Buffer {
   void* main = nullptr;
   void* b16 = nullptr;
 };
+
+// Memory-bound join shapes with a dedicated grouped kernel (ewise.cu).
+struct MemMap {
+  OpKind kind;
+  int y_mode = 0;
+  int64_t inner = 1, rows = 1, len = 1;
+};
+
+bool map_memory(const Vtx& v, const shape& local_xy, bool f64, MemMap& m) {
+  std::map<int, int64_t> ext;
+  for (size_t i = 0; i < v.lxy.size(); ++i) ext.emplace(v.lxy[i], local_xy[i]);
+  auto prod_of = [&](const labels& ls, size_t from, size_t to) {
+    int64_t r = 1;
+    for (size_t i = from; i < to; ++i) r *= ext.at(ls[i]);
+    return r;
+  };
+  const bool has_agg = v.agg >= 0;
+  if (!has_agg) {
+    if (v.lx != v.lz) return false;
+    m.kind = OpKind::EWISE;
+    if (v.arity == 1) return true;
+    if (v.ly == v.lz) {
+      m.y_mode = 1;
+      return true;
+    }
+    // y's labels a prefix of z's: broadcast over the trailing block
+    if (v.ly.size() < v.lz.size() && std::equal(v.ly.begin(), v.ly.end(), v.lz.begin())) {
+      m.y_mode = 2;
+      m.inner = prod_of(v.lz, v.ly.size(), v.lz.size());
+      return m.inner % (f64 ? 2 : 4) == 0;
+    }
+    return false;
+  }
+  if (v.arity != 1) return false;
+  // z's labels a prefix of x's: fold x's trailing labels (kernel_eval order)
+  if (v.lz.size() >= v.lx.size() || !std::equal(v.lz.begin(), v.lz.end(), v.lx.begin())) return false;
+  m.kind = OpKind::ROWREDUCE;
+  m.rows = prod_of(v.lx, 0, v.lz.size());
+  m.len = prod_of(v.lx, v.lz.size(), v.lx.size());
+  return true;
+}
 
 }  // namespace
 
@@ -345,6 +393,9 @@ struct ed_plan_h {
   std::vector<SrcRec> srcs_;                      // refinement sources, fold order
   std::map<int, GemmMap> gmap_;                   // einsum -> GEMM mapping
   std::map<int, std::vector<int>> region_sibs_;   // GEMM head join -> siblings
+  std::map<int, MemMap> memmap_;                  // einsum -> memory-bound kernel shape
+  void* d_joinptrs = nullptr;                     // JoinPtrs[] of grouped memory-bound launches
+  void* d_rects = nullptr;                        // RectGroup[] of fast refinements
 
   int rank_of(int id) const { return X[id].machine % ctx->world; }
   shape out_partition(int w) const {
@@ -551,6 +602,8 @@ void ed_plan_h::build() {
     std::string why;
     if (tc && map_gemm(V[w], local_xy(w), bf16, g, why)) gmap[w] = g;
     else why_not[w] = why;
+    MemMap mm;
+    if (!gmap.count(w) && map_memory(V[w], local_xy(w), f64, mm)) memmap_[w] = mm;
   }
   {
     std::map<std::pair<int, shape>, std::vector<int>> regions;
@@ -724,6 +777,19 @@ void ed_plan_h::build() {
             for (int s : region_sibs[h]) op.flops += 2.0 * double(X[s].fp);
           }
         ops.push_back(op);
+      } else if (memmap_.count(u.producer)) {
+        if (gemm_emitted.count(u.producer)) continue;
+        gemm_emitted.insert(u.producer);
+        const MemMap& mm = memmap_.at(u.producer);
+        Op op{mm.kind};
+        op.name = std::string(mm.kind == OpKind::EWISE ? "ewise:" : "rowreduce:") + w.name;
+        op.ptr = reinterpret_cast<void*>(id);
+        for (int h = 0; h < ne; ++h)
+          if (local[h] && X[h].kind == ED_EXEC_JOIN && X[h].producer == u.producer) {
+            op.heads.push_back(h);
+            op.flops += double(X[h].fp);
+          }
+        ops.push_back(op);
       } else {
         Op op{OpKind::GENERIC};
         op.name = "einsum_generic:" + w.name;
@@ -744,7 +810,7 @@ void ed_plan_h::build() {
     // after the op that produced the first join
     size_t at = 0;
     for (size_t i = 0; i < ops.size(); ++i)
-      if ((ops[i].kind == OpKind::GEMM &&
+      if (((ops[i].kind == OpKind::GEMM || ops[i].kind == OpKind::EWISE || ops[i].kind == OpKind::ROWREDUCE) &&
            std::count(ops[i].heads.begin(), ops[i].heads.end(), owner[first_join])) ||
           (ops[i].kind == OpKind::GENERIC && reinterpret_cast<intptr_t>(ops[i].ptr) == owner[first_join])) {
         at = i + 1;
@@ -795,7 +861,7 @@ void ed_plan_h::allocate() {
   }
 
   auto resolve = [&](int dep) { return local[dep] ? owner[dep] : dep; };
-  size_t gemm_maps_total = 0, gemm_regions_total = 0;
+  size_t gemm_maps_total = 0, gemm_regions_total = 0, jptrs_total = 0, rect_total = 0;
   for (auto& op : ops) {
     const int id = int(reinterpret_cast<intptr_t>(op.ptr));
     switch (op.kind) {
@@ -951,6 +1017,68 @@ void ed_plan_h::allocate() {
             rd += vol;
           }
         op.bytes += rd * es;
+        // fast path: group sources by region (siblings fold in dep order)
+        op.groups.clear();
+        op.max_rows = 0;
+        bool fast = true;
+        std::vector<std::pair<shape, std::vector<const void*>>> regions;
+        std::vector<const SrcRec*> firsts;
+        for (auto& sr : srcs_) {
+          if (sr.ref != id) continue;
+          auto it = std::find_if(regions.begin(), regions.end(), [&](auto& q) { return q.first == sr.r0; });
+          if (it == regions.end()) {
+            regions.push_back({sr.r0, {}});
+            firsts.push_back(&sr);
+            it = regions.end() - 1;
+          }
+          it->second.push_back(buf[sr.src].main);
+        }
+        const int V = int(16 / es);
+        bool vec = true;
+        for (size_t gi = 0; gi < regions.size() && fast; ++gi) {
+          const SrcRec& f = *firsts[gi];
+          if (int(regions[gi].second.size()) > kRectSrc) {
+            fast = false;
+            break;
+          }
+          RectGroup rg{};
+          rg.n_src = int(regions[gi].second.size());
+          for (int k = 0; k < rg.n_src; ++k) rg.src[k] = regions[gi].second[k];
+          int64_t ss = 1, ds = 1;
+          for (int i = p.rank - 1; i >= 0; --i) {
+            rg.sstr[i] = ss;
+            rg.dstr[i] = ds;
+            ss *= f.ext[i];
+            ds *= p.cext[i];
+          }
+          rg.src_off = rg.dst_off = 0;
+          rg.rows = 1;
+          for (int i = 0; i < p.rank; ++i) {
+            int64_t lo = std::max(f.r0[i], p.c0[i]);
+            int64_t hi = std::min(f.r0[i] + f.ext[i], p.c0[i] + p.cext[i]);
+            rg.ext[i] = hi - lo;
+            rg.src_off += (lo - f.r0[i]) * rg.sstr[i];
+            rg.dst_off += (lo - p.c0[i]) * rg.dstr[i];
+            if (i < p.rank - 1) rg.rows *= rg.ext[i];
+          }
+          if (std::any_of(rg.ext, rg.ext + p.rank, [](int64_t e) { return e <= 0; })) continue;
+          vec = vec && rg.ext[p.rank - 1] % V == 0 && rg.src_off % V == 0 && rg.dst_off % V == 0 &&
+                (p.rank == 1 || (f.ext[p.rank - 1] % V == 0 && p.cext[p.rank - 1] % V == 0));
+          op.max_rows = std::max(op.max_rows, rg.rows);
+          op.groups.push_back(rg);
+        }
+        if (fast && !op.groups.empty() && p.rank >= 1) {
+          op.rect.rank = p.rank;
+          op.rect.agg = p.agg;
+          op.rect.vec = vec;
+          const int64_t inner = op.groups[0].ext[p.rank - 1];
+          op.rect.rows_per_block = int(std::max<int64_t>(1, std::min<int64_t>(64, 8192 / std::max<int64_t>(1, inner))));
+          op.rect.out = p.out;
+          op.rect.out16 = p.out16;
+          rect_total += op.groups.size();
+        } else {
+          op.groups.clear();
+        }
         break;
       }
       case OpKind::CORRUPT:
@@ -968,6 +1096,72 @@ void ed_plan_h::allocate() {
         op.gen.out16 = buf[id].b16;
         op.gen.n_out = X[id].sz;
         break;
+      case OpKind::EWISE:
+      case OpKind::ROWREDUCE: {
+        const Ex& u = X[id];
+        const Vtx& w = V[u.producer];
+        const MemMap& mm = memmap_.at(u.producer);
+        op.jptrs.clear();
+        double in_el = 0;
+        shape lxy = local_xy(u.producer);
+        int64_t xin = prod(pick(lxy, positions(w.lx, w.lxy)));
+        int64_t yin = w.arity == 2 ? prod(pick(lxy, positions(w.ly, w.lxy))) : 0;
+        for (int h : op.heads) {
+          const Ex& j = X[h];
+          JoinPtrs jp{};
+          jp.x = buf[resolve(j.deps[0])].main;
+          jp.y = w.arity == 2 ? buf[resolve(j.deps[1])].main : nullptr;
+          jp.out = buf[h].main;
+          jp.out16 = buf[h].b16;
+          op.jptrs.push_back(jp);
+          in_el += double(xin + yin);
+          op.bytes += double(j.sz) * ((jp.out ? es : 0) + (jp.out16 ? 2 : 0));
+        }
+        op.bytes += in_el * es;
+        if (mm.kind == OpKind::EWISE) {
+          EwiseParams& p = op.ew;
+          p.n = u.sz;
+          p.binary = w.arity == 2;
+          p.y_mode = mm.y_mode;
+          p.inner = mm.inner;
+          p.join = w.join;
+          p.map = w.map;
+          p.c = w.c;
+          p.err = d_err;
+        } else {
+          RowReduceParams& p = op.rr;
+          p.rows = mm.rows;
+          p.len = mm.len;
+          p.map = w.map;
+          p.agg = w.agg;
+          p.c = w.c;
+        }
+        jptrs_total += op.jptrs.size();
+        break;
+      }
+    }
+  }
+  if (rect_total) {
+    CUDA_OK(cudaMalloc(&d_rects, sizeof(RectGroup) * rect_total));
+    size_t o = 0;
+    for (auto& op : ops) {
+      if (op.groups.empty()) continue;
+      RectGroup* d = static_cast<RectGroup*>(d_rects) + o;
+      CUDA_OK(cudaMemcpy(d, op.groups.data(), sizeof(RectGroup) * op.groups.size(), cudaMemcpyHostToDevice));
+      op.rect.groups = d;
+      o += op.groups.size();
+    }
+  }
+  if (jptrs_total) {
+    CUDA_OK(cudaMalloc(&d_joinptrs, sizeof(JoinPtrs) * jptrs_total));
+    size_t o = 0;
+    for (auto& op : ops) {
+      if (op.jptrs.empty()) continue;
+      JoinPtrs* d = static_cast<JoinPtrs*>(d_joinptrs) + o;
+      CUDA_OK(cudaMemcpy(d, op.jptrs.data(), sizeof(JoinPtrs) * op.jptrs.size(), cudaMemcpyHostToDevice));
+      op.ew.joins = d;
+      op.rr.joins = d;
+      o += op.jptrs.size();
     }
   }
   // tensor maps and region tables of every GEMM launch, in device memory
@@ -994,8 +1188,17 @@ void ed_plan_h::launch_op(size_t i, cudaStream_t s) {
   switch (op.kind) {
     case OpKind::GEMM: CUDA_OK(launch_gemm(op.gemm, ctx->num_sms, s)); break;
     case OpKind::GENERIC: CUDA_OK(launch_generic(op.gen, f64, s)); break;
-    case OpKind::REFINE: CUDA_OK(launch_refine(op.ref, f64, s)); break;
+    case OpKind::REFINE:
+      if (!op.groups.empty()) CUDA_OK(launch_rect(op.rect, int(op.groups.size()), op.max_rows, f64, s));
+      else CUDA_OK(launch_refine(op.ref, f64, s));
+      break;
     case OpKind::CORRUPT: CUDA_OK(launch_add_one(op.ptr, op.dt, s)); break;
+    case OpKind::EWISE:
+      CUDA_OK(launch_ewise(op.ew, int(op.jptrs.size()), f64, opt.precision == ED_PREC_FP32, s));
+      break;
+    case OpKind::ROWREDUCE:
+      CUDA_OK(launch_rowreduce(op.rr, int(op.jptrs.size()), f64, opt.precision == ED_PREC_FP32, s));
+      break;
     case OpKind::CONVERT: CUDA_OK(launch_convert(op.gen.x, store, op.gen.out16, DT::BF16, op.gen.n_out, s)); break;
     case OpKind::SEND:
       NCCL_OK(ncclSend(op.ptr, op.count, f64 ? ncclFloat64 : ncclFloat32, op.peer, ctx->comm, s));
@@ -1034,6 +1237,8 @@ void ed_plan_h::destroy() {
   if (arena) cudaFree(arena);
   if (d_deps) cudaFree(d_deps);
   if (d_maps) cudaFree(d_maps);
+  if (d_joinptrs) cudaFree(d_joinptrs);
+  if (d_rects) cudaFree(d_rects);
   if (d_regions) cudaFree(d_regions);
   if (d_ptrs) cudaFree(d_ptrs);
   if (d_err) cudaFree(d_err);
