@@ -111,8 +111,16 @@ __global__ void __launch_bounds__(256) ewise_kernel(const EwiseParams p) {
         for (int i = 0; i < V; ++i) yv[i] = yy;
       }
     }
+    if (!kExact && sizeof(T) == 4 && p.binary && p.join == 3 && p.y_mode == 2) {
+      // broadcast divide (softmax normalisation): one reciprocal per vector
+      if (yv[0] == T(0)) atomicExch(p.err, 1);
+      const float inv = __frcp_rn(float(yv[0]));
 #pragma unroll
-    for (int i = 0; i < V; ++i) r[i] = apply<T, kExact>(p, xv[i], p.binary ? yv[i] : T(0));
+      for (int i = 0; i < V; ++i) r[i] = T(__fmul_rn(float(xv[i]), inv));
+    } else {
+#pragma unroll
+      for (int i = 0; i < V; ++i) r[i] = apply<T, kExact>(p, xv[i], p.binary ? yv[i] : T(0));
+    }
     if (out) __stcs(reinterpret_cast<uint4*>(out + o), *reinterpret_cast<uint4*>(r));
     if (o16) {
 #pragma unroll
@@ -129,13 +137,64 @@ __global__ void __launch_bounds__(256) ewise_kernel(const EwiseParams p) {
   }
 }
 
-// 32 rows per block; tiles of 32 rows x TC columns are loaded coalesced into
-// smem by all 8 warps, then each of warp 0's lanes folds its row in order.
+// Order-free folds (max in every mode, sum in the tensor-core modes): one
+// warp per row, 16-byte loads, shuffle tree.
 template <typename T, bool kExact>
-__global__ void __launch_bounds__(256) rowreduce_kernel(const RowReduceParams p) {
-  constexpr int R = 32;
-  constexpr int TC = sizeof(T) == 4 ? 128 : 64;
-  __shared__ T tile[2][R][TC + 1];
+__global__ void __launch_bounds__(256) rowreduce_warp_kernel(const RowReduceParams p) {
+  const JoinPtrs jp = p.joins[blockIdx.y];
+  const T* __restrict__ x = static_cast<const T*>(jp.x);
+  T* out = static_cast<T*>(jp.out);
+  __nv_bfloat16* o16 = static_cast<__nv_bfloat16*>(jp.out16);
+  constexpr int V = 16 / sizeof(T);
+  const int lane = threadIdx.x % 32;
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x / 32);
+  const bool vec = p.len % V == 0;
+  for (int64_t row = int64_t(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32; row < p.rows; row += warps) {
+    const T* xr = x + row * p.len;
+    double acc = 0.0;
+    bool any = false;
+    auto fold = [&](T xv) {
+      double v;
+      if (kExact || sizeof(T) == 8) v = double(rnd<T>(map_x(p.map, p.c, double(xv))));
+      else v = double(map_f(p.map, float(p.c), float(xv)));
+      if (!any) acc = v;
+      else acc = p.agg == 0 ? double(float(acc) + float(v)) : (acc < v ? v : acc);
+      any = true;
+    };
+    if (vec) {
+      for (int64_t i = int64_t(lane) * V; i < p.len; i += 32 * V) {
+        T xv[V];
+        *reinterpret_cast<uint4*>(xv) = __ldcs(reinterpret_cast<const uint4*>(xr + i));
+#pragma unroll
+        for (int e = 0; e < V; ++e) fold(xv[e]);
+      }
+    } else {
+      for (int64_t i = lane; i < p.len; i += 32) fold(xr[i]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      double other = __shfl_xor_sync(0xffffffffu, acc, o);
+      bool other_any = __shfl_xor_sync(0xffffffffu, any, o);
+      if (other_any) {
+        if (!any) acc = other;
+        else acc = p.agg == 0 ? double(float(acc) + float(other)) : (acc < other ? other : acc);
+        any = true;
+      }
+    }
+    if (lane == 0) {
+      if (out) out[row] = rnd<T>(acc);
+      if (o16) o16[row] = __double2bfloat16(acc);
+    }
+  }
+}
+
+// Exact-order sums (the fp32/fp64 modes): each thread owns a row and folds it
+// in odometer order (index 0..L-1) from coalesced smem-transposed tiles of
+// 128 rows x 32 columns.
+template <typename T>
+__global__ void __launch_bounds__(128) rowreduce_seq_kernel(const RowReduceParams p) {
+  constexpr int R = 128, TC = 32;
+  __shared__ T tile[R][TC + 1];
   const JoinPtrs jp = p.joins[blockIdx.y];
   const T* __restrict__ x = static_cast<const T*>(jp.x);
   T* out = static_cast<T*>(jp.out);
@@ -143,52 +202,26 @@ __global__ void __launch_bounds__(256) rowreduce_kernel(const RowReduceParams p)
   const int64_t row0 = int64_t(blockIdx.x) * R;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int64_t L = p.len;
-  const int ntiles = int((L + TC - 1) / TC);
   double acc = 0.0;
-  auto load = [&](int t, int b) {
-    // warp w loads rows w, w+8, w+16, w+24 of the tile
-    const int64_t c0 = int64_t(t) * TC;
-    for (int rr = warp; rr < R; rr += 8) {
+  for (int64_t c0 = 0; c0 < L; c0 += TC) {
+    for (int rr = warp; rr < R; rr += 4) {
       const int64_t row = row0 + rr;
-      for (int c = lane; c < TC; c += 32) {
-        T v = T(0);
-        if (row < p.rows && c0 + c < L) v = x[row * L + c0 + c];
-        tile[b][rr][c] = v;
-      }
+      T v = T(0);
+      if (row < p.rows && c0 + lane < L) v = x[row * L + c0 + lane];
+      tile[rr][lane] = v;
     }
-  };
-  load(0, 0);
-  __syncthreads();
-  for (int t = 0; t < ntiles; ++t) {
-    if (t + 1 < ntiles && warp > 0) {
-      // warps 1..7 prefetch the next tile while warp 0 folds this one
-      const int64_t c0 = int64_t(t + 1) * TC;
-      for (int rr = warp - 1; rr < R; rr += 7) {
-        const int64_t row = row0 + rr;
-        for (int c = lane; c < TC; c += 32) {
-          T v = T(0);
-          if (row < p.rows && c0 + c < L) v = x[row * L + c0 + c];
-          tile[(t + 1) & 1][rr][c] = v;
-        }
-      }
-    }
-    if (warp == 0) {
-      const int n = int(L - int64_t(t) * TC < TC ? L - int64_t(t) * TC : TC);
-      for (int c = 0; c < n; ++c) {
-        const T xv = tile[t & 1][lane][c];
-        double v;
-        if (kExact || sizeof(T) == 8) v = double(rnd<T>(map_x(p.map, p.c, double(xv))));
-        else v = double(map_f(p.map, float(p.c), float(xv)));
-        if (t == 0 && c == 0) acc = v;
-        else if (p.agg == 0) acc = kExact || sizeof(T) == 8 ? double(rnd<T>(__dadd_rn(acc, v))) : double(float(acc) + float(v));
-        else acc = acc < v ? v : acc;
-      }
+    __syncthreads();
+    const int n = int(L - c0 < TC ? L - c0 : TC);
+    for (int c = 0; c < n; ++c) {
+      const double v = double(rnd<T>(map_x(p.map, p.c, double(tile[threadIdx.x][c]))));
+      acc = (c0 == 0 && c == 0) ? v : (p.agg == 0 ? double(rnd<T>(__dadd_rn(acc, v))) : (acc < v ? v : acc));
     }
     __syncthreads();
   }
-  if (warp == 0 && row0 + lane < p.rows) {
-    if (out) out[row0 + lane] = rnd<T>(acc);
-    if (o16) o16[row0 + lane] = __double2bfloat16(acc);
+  const int64_t row = row0 + threadIdx.x;
+  if (row < p.rows) {
+    if (out) out[row] = rnd<T>(acc);
+    if (o16) o16[row] = __double2bfloat16(acc);
   }
 }
 
@@ -209,10 +242,16 @@ cudaError_t launch_ewise(const EwiseParams& p, int n_joins, bool f64, bool exact
 }
 
 cudaError_t launch_rowreduce(const RowReduceParams& p, int n_joins, bool f64, bool exact, cudaStream_t s) {
-  dim3 grid(unsigned((p.rows + 31) / 32), n_joins);
-  if (f64) rowreduce_kernel<double, true><<<grid, 256, 0, s>>>(p);
-  else if (exact) rowreduce_kernel<float, true><<<grid, 256, 0, s>>>(p);
-  else rowreduce_kernel<float, false><<<grid, 256, 0, s>>>(p);
+  if ((exact || f64) && p.agg == 0) {
+    dim3 grid(unsigned((p.rows + 127) / 128), n_joins);
+    if (f64) rowreduce_seq_kernel<double><<<grid, 128, 0, s>>>(p);
+    else rowreduce_seq_kernel<float><<<grid, 128, 0, s>>>(p);
+  } else {
+    dim3 grid(blocks_for(p.rows, 8, n_joins), n_joins);
+    if (f64) rowreduce_warp_kernel<double, true><<<grid, 256, 0, s>>>(p);
+    else if (exact) rowreduce_warp_kernel<float, true><<<grid, 256, 0, s>>>(p);
+    else rowreduce_warp_kernel<float, false><<<grid, 256, 0, s>>>(p);
+  }
   return cudaGetLastError();
 }
 

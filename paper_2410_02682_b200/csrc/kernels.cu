@@ -138,12 +138,17 @@ __global__ void __launch_bounds__(256) rect_kernel(const RectParams p) {
   T* out = static_cast<T*>(p.out);
   __nv_bfloat16* o16 = static_cast<__nv_bfloat16*>(p.out16);
   const int r = p.rank;
-  const int64_t inner = g.ext[r - 1];
   constexpr int V = 16 / sizeof(T);
+  const int W = p.vec ? V : 1;                      // elements per slot
+  const int64_t per_row = g.ext[r - 1] / W;         // slots per row
   const int64_t r_begin = int64_t(blockIdx.x) * p.rows_per_block;
+  if (r_begin >= g.rows) return;
   const int64_t r_end = r_begin + p.rows_per_block < g.rows ? r_begin + p.rows_per_block : g.rows;
-  for (int64_t row = r_begin; row < r_end; ++row) {
-    int64_t rem = row, so = g.src_off, dofs = g.dst_off;
+  const int64_t slots = (r_end - r_begin) * per_row;
+  for (int64_t sl = threadIdx.x; sl < slots; sl += blockDim.x) {
+    const int64_t row = r_begin + sl / per_row;
+    const int64_t i = (sl % per_row) * W;
+    int64_t rem = row, so = g.src_off + i, dofs = g.dst_off + i;
     for (int d = r - 2; d >= 0; --d) {
       const int64_t c = rem % g.ext[d];
       rem /= g.ext[d];
@@ -151,28 +156,24 @@ __global__ void __launch_bounds__(256) rect_kernel(const RectParams p) {
       dofs += c * g.dstr[d];
     }
     if (p.vec) {
-      for (int64_t i = int64_t(threadIdx.x) * V; i < inner; i += int64_t(blockDim.x) * V) {
-        T acc[V], v[V];
-        *reinterpret_cast<uint4*>(acc) = *reinterpret_cast<const uint4*>(static_cast<const T*>(g.src[0]) + so + i);
-        for (int k = 1; k < g.n_src; ++k) {
-          *reinterpret_cast<uint4*>(v) = *reinterpret_cast<const uint4*>(static_cast<const T*>(g.src[k]) + so + i);
+      T acc[V], v[V];
+      *reinterpret_cast<uint4*>(acc) = *reinterpret_cast<const uint4*>(static_cast<const T*>(g.src[0]) + so);
+      for (int k = 1; k < g.n_src; ++k) {
+        *reinterpret_cast<uint4*>(v) = *reinterpret_cast<const uint4*>(static_cast<const T*>(g.src[k]) + so);
 #pragma unroll
-          for (int e = 0; e < V; ++e) acc[e] = from_d<T>(agg_d(p.agg, double(acc[e]), double(v[e])));
-        }
-        if (out) *reinterpret_cast<uint4*>(out + dofs + i) = *reinterpret_cast<uint4*>(acc);
-        if (o16) {
+        for (int e = 0; e < V; ++e) acc[e] = from_d<T>(agg_d(p.agg, double(acc[e]), double(v[e])));
+      }
+      if (out) *reinterpret_cast<uint4*>(out + dofs) = *reinterpret_cast<uint4*>(acc);
+      if (o16) {
 #pragma unroll
-          for (int e = 0; e < V; ++e) o16[dofs + i + e] = __double2bfloat16(double(acc[e]));
-        }
+        for (int e = 0; e < V; ++e) o16[dofs + e] = __double2bfloat16(double(acc[e]));
       }
     } else {
-      for (int64_t i = threadIdx.x; i < inner; i += blockDim.x) {
-        double acc = double(static_cast<const T*>(g.src[0])[so + i]);
-        for (int k = 1; k < g.n_src; ++k)
-          acc = double(from_d<T>(agg_d(p.agg, acc, double(static_cast<const T*>(g.src[k])[so + i]))));
-        if (out) out[dofs + i] = from_d<T>(acc);
-        if (o16) o16[dofs + i] = __double2bfloat16(acc);
-      }
+      double acc = double(static_cast<const T*>(g.src[0])[so]);
+      for (int k = 1; k < g.n_src; ++k)
+        acc = double(from_d<T>(agg_d(p.agg, acc, double(static_cast<const T*>(g.src[k])[so]))));
+      if (out) out[dofs] = from_d<T>(acc);
+      if (o16) o16[dofs] = __double2bfloat16(acc);
     }
   }
 }

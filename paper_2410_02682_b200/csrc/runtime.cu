@@ -1072,7 +1072,8 @@ void ed_plan_h::allocate() {
           op.rect.agg = p.agg;
           op.rect.vec = vec;
           const int64_t inner = op.groups[0].ext[p.rank - 1];
-          op.rect.rows_per_block = int(std::max<int64_t>(1, std::min<int64_t>(64, 8192 / std::max<int64_t>(1, inner))));
+          // ~32 KiB of output per block
+          op.rect.rows_per_block = int(std::max<int64_t>(1, (32768 / int64_t(es)) / std::max<int64_t>(1, inner)));
           op.rect.out = p.out;
           op.rect.out16 = p.out16;
           rect_total += op.groups.size();
