@@ -161,3 +161,24 @@ def test_twins_first_contraction_exact(gpu_ctx, twin):
                     exp = _bf16(exp)
                 assert np.array_equal(got, exp), (twin, prec, u.id)
         pp.close()
+
+
+def test_reference_flow_with_gpu_executor(gpu_ctx, tmp_path):
+    """The reference's own run_end_to_end flow (build_pipeline, generate_inputs,
+    chunk) with execute() and the C++ adapter execute_gpu() side by side
+    (integration/ed_check.cc): bit-identical outputs in f64 and f32 mode
+    (exp-bearing graphs within last-bit bounds), identical machine counters,
+    and an audit within the cost-model bounds, over the acceptance matrix."""
+    import json
+    import os
+    import subprocess
+    from conftest import ROOT
+    exe = os.path.join(ROOT, "oracle", "_ref", "ed_check")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/ed_check not built (needs /root/reference at build time)")
+    for g in ["matmul", "ffnn", "softmax", "attention"]:
+        doc = json.load(open(os.path.join(ROOT, "plans", f"{g}_p1_L1.json")))
+        (tmp_path / f"{g}.eg").write_text(doc["graph_text"])
+    r = subprocess.run([exe, str(tmp_path)], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert "72/72 passed" in r.stdout
