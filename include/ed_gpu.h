@@ -187,6 +187,15 @@ typedef struct {
   double bytes;              /* algorithmic HBM bytes summed over launches */
 } ed_kernel_stat_c;
 
+/* One step of a rank's logical schedule (ed_plan_schedule). */
+typedef enum { ED_SCHED_COMPUTE = 0, ED_SCHED_SEND = 1, ED_SCHED_RECV = 2 } ed_sched_kind;
+typedef struct {
+  int32_t kind;              /* ed_sched_kind */
+  int32_t exec_id;           /* vertex computed, or chunk sent / received */
+  int32_t peer;              /* SEND: destination rank, RECV: source rank, else -1 */
+  int64_t elems;             /* chunk elements moved (SEND / RECV) */
+} ed_sched_op_c;
+
 struct ed_ctx;
 struct ed_plan_h;
 
@@ -219,8 +228,9 @@ ED_API ed_status ed_upload_tensors(struct ed_plan_h* h, const ed_tensor_in_c* te
 ED_API ed_status ed_run(struct ed_plan_h* h, ed_report_c* report, char* err, size_t errlen);
 
 /* Assemble graph outputs from their final refinement layers (runtime.cc:432-448)
- * and copy D2H. On rank r only outputs whose chunks this rank holds are valid
- * unless world == 1; ed_download gathers to the calling rank when world > 1. */
+ * and copy D2H. With world > 1 this is collective: every rank calls it, chunks
+ * held by other ranks travel to rank 0 over NCCL, and only rank 0's buffers
+ * are written. */
 ED_API ed_status ed_download(struct ed_plan_h* h, ed_output_c* outputs, int32_t n,
                       char* err, size_t errlen);
 
@@ -228,6 +238,14 @@ ED_API ed_status ed_download(struct ed_plan_h* h, ed_output_c* outputs, int32_t 
  * Returns ED_ERR_USAGE if the chunk is not resident on this rank. */
 ED_API ed_status ed_download_chunk(struct ed_plan_h* h, int32_t exec_id, int32_t dtype,
                             void* data, int64_t n, char* err, size_t errlen);
+
+/* Host-only (no GPU needed): rank `rank`'s logical schedule in a world of
+ * `world` processes — its exec vertices in execution order, interleaved with
+ * the NCCL sends/receives of remote dependencies, which every rank issues in
+ * the same global order (a transfer is placed before its first consumer).
+ * ed_run executes exactly this order (with joins grouped into launches). */
+ED_API ed_status ed_plan_schedule(const ed_plan_c* plan, int32_t rank, int32_t world, ed_sched_op_c* out,
+                                  int32_t cap, int32_t* n_out, char* err, size_t errlen);
 
 /* Per-launch-class timings of the last profiled ed_run. */
 ED_API ed_status ed_kernel_stats(struct ed_plan_h* h, ed_kernel_stat_c* out, int32_t cap,

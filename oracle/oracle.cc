@@ -180,6 +180,109 @@ void block_copy(shape const& bound, shape const& d, shape const& key,
   } while(advance(local, cb));
 }
 
+// Plan-level helpers shared by the whole-plan and per-vertex entry points.
+struct plan_view {
+  const ed_plan_c* plan;
+  explicit plan_view(const ed_plan_c* p) : plan(p) {}
+  shape bound_of(int vid) const { auto const& v = plan->vertices[vid]; return shape(v.bound, v.bound + v.rank); }
+  shape d_of(int vid) const { auto const& v = plan->vertices[vid]; return shape(v.d, v.d + v.rank_d); }
+  shape key_of(int id) const { auto const& x = plan->exec[id]; return shape(x.key, x.key + x.key_rank); }
+  shape cb_of(int id) const { auto const& x = plan->exec[id]; return shape(x.chunk_bound, x.chunk_bound + x.chunk_rank); }
+
+  // task_graph_t::out_partition / required_input_partition (decomp.cc:3-14)
+  shape out_partition(int vid) const {
+    if(plan->vertices[vid].arity == 0) return d_of(vid);
+    expr_view e(&plan->vertices[vid]);
+    return pick(d_of(vid), positions(e.lz, e.lxy));
+  }
+  shape required_partition(int vid, int slot) const {
+    expr_view e(&plan->vertices[vid]);
+    return pick(d_of(vid), positions(slot == 0 ? e.lx : e.ly, e.lxy));
+  }
+  // engine_t::region_key / region_partition (runtime.cc:96-116)
+  shape region_key(int id) const {
+    auto const& u = plan->exec[id];
+    if(u.kind != ED_EXEC_JOIN) return key_of(id);
+    expr_view e(&plan->vertices[u.producer]);
+    return pick(key_of(id), positions(e.lz, e.dls));
+  }
+  shape region_partition(int id) const {
+    auto const& u = plan->exec[id];
+    if(u.kind == ED_EXEC_INPUT_CHUNK) return d_of(u.producer);
+    if(u.kind == ED_EXEC_JOIN) return out_partition(u.producer);
+    if(u.consumer >= 0) return required_partition(u.consumer, u.slot);
+    return out_partition(u.producer);
+  }
+
+  // compute() (runtime.cc:183-270) for one join or refinement, given its
+  // dependency chunks in dep order
+  void compute(int id, const double* const* deps, double* out, bool r32) const {
+    auto const& v = plan->exec[id];
+    auto const* V = plan->vertices;
+    std::fill(out, out + v.sz, 0.0);
+    if(v.kind == ED_EXEC_JOIN) {
+      // join branch: spec.local_xy = b_XY / d (runtime.cc:51-63, 185-196)
+      int w = v.producer;
+      expr_view e(&V[w]);
+      shape bxy;
+      for(int s = 0; s != V[w].arity; ++s) {
+        auto b = bound_of(V[w].inputs[s]);
+        bxy.insert(bxy.end(), b.begin(), b.end());
+      }
+      shape d = d_of(w);
+      for(size_t i = 0; i != bxy.size(); ++i) bxy[i] /= d[i];
+      einsum_loop(e, bxy, deps[0], e.binary ? deps[1] : nullptr, out, r32);
+      return;
+    }
+    // refinement branch: paste each dep's overlap rectangle, folding
+    // aggregation siblings in dep order (runtime.cc:198-269)
+    int w = v.producer;
+    shape bound = bound_of(w);
+    shape dc = region_partition(id);
+    int agg = V[w].arity == 0 ? -1 : V[w].agg_op;
+    shape cbound = cb_of(id), ckey = key_of(id);
+    std::vector<char> touched(size_t(v.sz), 0);
+    shape c0(bound.size());
+    for(size_t i = 0; i != bound.size(); ++i) c0[i] = ckey[i] * (bound[i] / dc[i]);
+    for(int k = 0; k != v.n_deps; ++k) {
+      int uid = v.deps[k];
+      shape rk = region_key(uid), dr = region_partition(uid);
+      shape r0(bound.size()), lo(bound.size()), span(bound.size());
+      bool empty = false;
+      for(size_t i = 0; i != bound.size(); ++i) {
+        r0[i] = rk[i] * (bound[i] / dr[i]);
+        lo[i] = std::max(r0[i], c0[i]);
+        int64_t hi = std::min(r0[i] + bound[i] / dr[i], c0[i] + cbound[i]);
+        span[i] = hi - lo[i];
+        if(span[i] <= 0) empty = true;
+      }
+      if(empty) continue;
+      shape ub = cb_of(uid);
+      shape rel(bound.size(), 0), ui(bound.size()), ci(bound.size());
+      const double* u = deps[k];
+      do {
+        for(size_t i = 0; i != bound.size(); ++i) {
+          ui[i] = lo[i] + rel[i] - r0[i];
+          ci[i] = lo[i] + rel[i] - c0[i];
+        }
+        double val = u[offset_of(ui, ub)];
+        int64_t off = offset_of(ci, cbound);
+        if(!touched[size_t(off)]) {
+          out[off] = val;
+          touched[size_t(off)] = 1;
+        } else {
+          if(agg < 0) throw plan_err("execute: overlapping contributions without an aggregation op");
+          double r = agg_op(agg, out[off], val);
+          out[off] = r32 ? double(float(r)) : r;
+        }
+      } while(advance(rel, span));
+    }
+    for(char t: touched) {
+      if(!t) throw plan_err("execute: refinement chunk left partially unwritten");
+    }
+  }
+};
+
 } // namespace
 
 extern "C" {
@@ -249,38 +352,9 @@ int oracle_execute(const ed_plan_c* plan, const ed_tensor_in_c* inputs, int32_t 
                    double* const* chunk_out, ed_machine_c* counters,
                    int64_t* total_transferred, char* err, size_t errlen) {
   return guarded(err, errlen, [&] {
-    int nv = plan->n_vertices, ne = plan->n_exec;
-    auto const* V = plan->vertices;
+    plan_view pv(plan);
+    int ne = plan->n_exec;
     auto const* X = plan->exec;
-    auto bound_of = [&](int vid) { return shape(V[vid].bound, V[vid].bound + V[vid].rank); };
-    auto d_of = [&](int vid) { return shape(V[vid].d, V[vid].d + V[vid].rank_d); };
-    auto key_of = [&](int id) { return shape(X[id].key, X[id].key + X[id].key_rank); };
-    auto cb_of = [&](int id) { return shape(X[id].chunk_bound, X[id].chunk_bound + X[id].chunk_rank); };
-
-    // task_graph_t::out_partition / required_input_partition (decomp.cc:3-14)
-    auto out_partition = [&](int vid) {
-      if(V[vid].arity == 0) return d_of(vid);
-      expr_view e(&V[vid]);
-      return pick(d_of(vid), positions(e.lz, e.lxy));
-    };
-    auto required_partition = [&](int vid, int slot) {
-      expr_view e(&V[vid]);
-      return pick(d_of(vid), positions(slot == 0 ? e.lx : e.ly, e.lxy));
-    };
-    // engine_t::region_key / region_partition (runtime.cc:96-116)
-    auto region_key = [&](int id) {
-      if(X[id].kind != ED_EXEC_JOIN) return key_of(id);
-      expr_view e(&V[X[id].producer]);
-      return pick(key_of(id), positions(e.lz, e.dls));
-    };
-    auto region_partition = [&](int id) {
-      auto const& u = X[id];
-      if(u.kind == ED_EXEC_INPUT_CHUNK) return d_of(u.producer);
-      if(u.kind == ED_EXEC_JOIN) return out_partition(u.producer);
-      if(u.consumer >= 0) return required_partition(u.consumer, u.slot);
-      return out_partition(u.producer);
-    };
-
     std::vector<std::vector<double>> produced{size_t(ne)};
     // seed: chunk each input tensor (engine_t ctor, runtime.cc:66-84)
     std::map<int, const double*> in_data;
@@ -294,77 +368,14 @@ int oracle_execute(const ed_plan_c* plan, const ed_tensor_in_c* inputs, int32_t 
       auto it = in_data.find(vid);
       if(it == in_data.end()) throw plan_err("execute: no relation supplied for an input");
       produced[id].resize(size_t(X[id].sz));
-      block_copy(bound_of(vid), d_of(vid), key_of(id), it->second, produced[id].data(), true);
+      block_copy(pv.bound_of(vid), pv.d_of(vid), pv.key_of(id), it->second, produced[id].data(), true);
     }
-
-    bool r32 = f32 != 0;
     for(int id = 0; id != ne; ++id) {
-      auto const& v = X[id];
-      if(v.kind == ED_EXEC_INPUT_CHUNK) continue;
-      produced[id].assign(size_t(v.sz), 0.0);
-      if(v.kind == ED_EXEC_JOIN) {
-        // compute() join branch (runtime.cc:185-196): spec.local_xy = b_XY / d
-        int w = v.producer;
-        expr_view e(&V[w]);
-        shape bxy;
-        for(int s = 0; s != V[w].arity; ++s) {
-          auto b = bound_of(V[w].inputs[s]);
-          bxy.insert(bxy.end(), b.begin(), b.end());
-        }
-        shape d = d_of(w);
-        for(size_t i = 0; i != bxy.size(); ++i) bxy[i] /= d[i];
-        einsum_loop(e, bxy, produced[v.deps[0]].data(),
-                    e.binary ? produced[v.deps[1]].data() : nullptr,
-                    produced[id].data(), r32);
-        continue;
-      }
-      // compute() refinement branch (runtime.cc:198-269): paste each dep's
-      // overlap rectangle, folding aggregation siblings in dep order
-      int w = v.producer;
-      shape bound = bound_of(w);
-      shape dc = region_partition(id);
-      int agg = V[w].arity == 0 ? -1 : V[w].agg_op;
-      shape cbound = cb_of(id), ckey = key_of(id);
-      std::vector<char> touched(size_t(v.sz), 0);
-      double* o = produced[id].data();
-      shape c0(bound.size());
-      for(size_t i = 0; i != bound.size(); ++i) c0[i] = ckey[i] * (bound[i] / dc[i]);
-      for(int k = 0; k != v.n_deps; ++k) {
-        int uid = v.deps[k];
-        shape rk = region_key(uid), dr = region_partition(uid);
-        shape r0(bound.size()), lo(bound.size()), span(bound.size());
-        bool empty = false;
-        for(size_t i = 0; i != bound.size(); ++i) {
-          r0[i] = rk[i] * (bound[i] / dr[i]);
-          lo[i] = std::max(r0[i], c0[i]);
-          int64_t hi = std::min(r0[i] + bound[i] / dr[i], c0[i] + cbound[i]);
-          span[i] = hi - lo[i];
-          if(span[i] <= 0) empty = true;
-        }
-        if(empty) continue;
-        shape ub = cb_of(uid);
-        shape rel(bound.size(), 0), ui(bound.size()), ci(bound.size());
-        const double* u = produced[uid].data();
-        do {
-          for(size_t i = 0; i != bound.size(); ++i) {
-            ui[i] = lo[i] + rel[i] - r0[i];
-            ci[i] = lo[i] + rel[i] - c0[i];
-          }
-          double val = u[offset_of(ui, ub)];
-          int64_t off = offset_of(ci, cbound);
-          if(!touched[size_t(off)]) {
-            o[off] = val;
-            touched[size_t(off)] = 1;
-          } else {
-            if(agg < 0) throw plan_err("execute: overlapping contributions without an aggregation op");
-            double r = agg_op(agg, o[off], val);
-            o[off] = r32 ? double(float(r)) : r;
-          }
-        } while(advance(rel, span));
-      }
-      for(char t: touched) {
-        if(!t) throw plan_err("execute: refinement chunk left partially unwritten");
-      }
+      if(X[id].kind == ED_EXEC_INPUT_CHUNK) continue;
+      produced[id].assign(size_t(X[id].sz), 0.0);
+      std::vector<const double*> deps;
+      for(int k = 0; k != X[id].n_deps; ++k) deps.push_back(produced[X[id].deps[k]].data());
+      pv.compute(id, deps.data(), produced[id].data(), f32 != 0);
     }
 
     // counters: one whole-chunk pull per (chunk, machine) (runtime.cc:119-172)
@@ -399,17 +410,25 @@ int oracle_execute(const ed_plan_c* plan, const ed_tensor_in_c* inputs, int32_t 
       int vid = outputs[i].vertex_id;
       if(outputs[i].dtype != ED_DTYPE_F64) throw plan_err("oracle: outputs must be f64");
       double* dst = static_cast<double*>(outputs[i].data);
-      shape bound = bound_of(vid);
-      shape part = out_partition(vid);
+      shape bound = pv.bound_of(vid);
+      shape part = pv.out_partition(vid);
       for(int id = 0; id != ne; ++id) {
         auto const& u = X[id];
-        bool mine = V[vid].arity == 0
+        bool mine = plan->vertices[vid].arity == 0
           ? (u.kind == ED_EXEC_INPUT_CHUNK && u.producer == vid)
           : (u.kind == ED_EXEC_REFINEMENT && u.producer == vid && u.consumer < 0);
-        if(mine) block_copy(bound, part, key_of(id), produced[id].data(), dst, false);
+        if(mine) block_copy(bound, part, pv.key_of(id), produced[id].data(), dst, false);
       }
     }
-    (void)nv;
+  });
+}
+
+int oracle_exec_vertex(const ed_plan_c* plan, int32_t exec_id, const double* const* deps, double* out,
+                       int32_t f32, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if(exec_id < 0 || exec_id >= plan->n_exec) throw plan_err("exec id out of range");
+    if(plan->exec[exec_id].kind == ED_EXEC_INPUT_CHUNK) throw plan_err("input chunks are not computed");
+    plan_view(plan).compute(exec_id, deps, out, f32 != 0);
   });
 }
 

@@ -55,6 +55,11 @@ int oracle_execute(const ed_plan_c* plan, const ed_tensor_in_c* inputs, int32_t 
                    double* const* chunk_out, ed_machine_c* counters,
                    int64_t* total_transferred, char* err, size_t errlen);
 
+/* compute() (runtime.cc:183-270) for ONE join or refinement, given its
+ * dependency chunks in dep order (used to replay a rank's schedule). */
+int oracle_exec_vertex(const ed_plan_c* plan, int32_t exec_id, const double* const* deps, double* out,
+                       int32_t f32, char* err, size_t errlen);
+
 #ifdef __cplusplus
 }
 #endif

@@ -123,11 +123,18 @@ class ed_kernel_stat_c(C.Structure):
     ]
 
 
+class ed_sched_op_c(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("exec_id", C.c_int32), ("peer", C.c_int32), ("elems", C.c_int64)]
+
+
+SCHED_COMPUTE, SCHED_SEND, SCHED_RECV = 0, 1, 2
+
+
 # Every symbol include/ed_gpu.h declares (tests/test_abi.py checks exports).
 EXPORTED = [
     "ed_abi_version", "ed_nccl_unique_id", "ed_ctx_create", "ed_ctx_destroy",
     "ed_prepare", "ed_plan_destroy", "ed_upload", "ed_upload_tensors", "ed_run",
-    "ed_download", "ed_download_chunk", "ed_kernel_stats",
+    "ed_download", "ed_download_chunk", "ed_plan_schedule", "ed_kernel_stats",
 ]
 
 
@@ -149,6 +156,8 @@ def declare(lib):
     lib.ed_run.argtypes = [P, C.POINTER(ed_report_c)] + err
     lib.ed_download.argtypes = [P, C.POINTER(ed_output_c), C.c_int32] + err
     lib.ed_download_chunk.argtypes = [P, C.c_int32, C.c_int32, C.c_void_p, C.c_int64] + err
+    lib.ed_plan_schedule.argtypes = [C.POINTER(ed_plan_c), C.c_int32, C.c_int32, C.POINTER(ed_sched_op_c),
+                                     C.c_int32, i32p] + err
     lib.ed_kernel_stats.argtypes = [P, C.POINTER(ed_kernel_stat_c), C.c_int32, i32p] + err
     for name in EXPORTED[1:]:
         f = getattr(lib, name)

@@ -430,6 +430,20 @@ struct ed_plan_h {
   void* main_of(int id) { return buf[owner[id]].main; }
   void* b16_of(int id) { return buf[owner[id]].b16; }
 
+  // remote dependencies per consumer: (dep, destination rank), placed before
+  // the dep's first consumer on that rank, in exec-id order on every rank
+  std::vector<std::vector<std::pair<int, int>>> transfers_by_consumer() const {
+    const int ne = int(X.size());
+    std::vector<std::vector<std::pair<int, int>>> at(ne);
+    std::set<std::pair<int, int>> seen;
+    for (int id = 0; id < ne; ++id) {
+      if (X[id].kind == ED_EXEC_INPUT_CHUNK) continue;
+      int dst = rank_of(id);
+      for (int d : X[id].deps)
+        if (rank_of(d) != dst && seen.insert({d, dst}).second) at[id].push_back({d, dst});
+    }
+    return at;
+  }
   void copy_plan(const ed_plan_c* p);
   void validate();
   void build();
@@ -610,8 +624,15 @@ void ed_plan_h::build() {
     for (int id = 0; id < ne; ++id)
       if (X[id].kind == ED_EXEC_JOIN && local[id] && gmap.count(X[id].producer))
         regions[{X[id].producer, region_key(id)}].push_back(id);
+    // consumers of each join (a sibling may only be folded into its region's
+    // accumulator when everything that reads it runs on this rank)
+    std::vector<char> remote_reader(ne, 0);
+    for (int id = 0; id < ne; ++id)
+      for (int d : X[id].deps)
+        if (rank_of(id) != me) remote_reader[d] = 1;
     for (auto& [k, sibs] : regions) {
-      if (int(sibs.size()) <= kMaxSib) {
+      bool all_local = std::none_of(sibs.begin(), sibs.end(), [&](int s) { return remote_reader[s]; });
+      if (int(sibs.size()) <= kMaxSib && (all_local || sibs.size() == 1)) {
         fused_head[sibs[0]] = 1;
         region_sibs[sibs[0]] = sibs;
         for (int s : sibs) owner[s] = sibs[0];
@@ -717,16 +738,7 @@ void ed_plan_h::build() {
   arena_bytes = std::max<size_t>(off, 1024);
 
   // ---- ops (exec-id order; transfers at their first consumer) ----
-  std::vector<std::vector<std::pair<int, int>>> xfer_at(ne);
-  {
-    std::set<std::pair<int, int>> seen;
-    for (int id = 0; id < ne; ++id) {
-      if (X[id].kind == ED_EXEC_INPUT_CHUNK) continue;
-      int dst = rank_of(id);
-      for (int d : X[id].deps)
-        if (rank_of(d) != dst && seen.insert({d, dst}).second) xfer_at[id].push_back({d, dst});
-    }
-  }
+  const auto xfer_at = transfers_by_consumer();
   ops.clear();
   contraction_flops = 0;
   std::set<int> gemm_emitted;
@@ -1267,7 +1279,7 @@ DT dt_of(int dtype) { return dtype == ED_DTYPE_F64 ? DT::F64 : DT::F32; }
 // chunk <-> whole-tensor mapping for graph vertex w over partition `part`
 // and the exec ids holding its chunks (any order; keyed by their key).
 void chunk_map(ed_plan_h* h, int w, const shape& part, const std::vector<int>& ids, bool want_shadow,
-               ChunkMapParams& p) {
+               ChunkMapParams& p, const std::vector<void*>* remote = nullptr) {
   const shape& bound = h->V[w].bound;
   std::memset(&p, 0, sizeof(p));
   p.rank = int(bound.size());
@@ -1279,10 +1291,13 @@ void chunk_map(ed_plan_h* h, int w, const shape& part, const std::vector<int>& i
     p.part[i] = part[i];
     p.cb[i] = bound[i] / part[i];
   }
-  for (int id : ids) {
+  for (size_t n = 0; n < ids.size(); ++n) {
+    const int id = ids[n];
     int64_t k = 0;
     for (int i = 0; i < p.rank; ++i) k = k * part[i] + h->X[id].key[i];
-    if (h->local[id]) {
+    if (remote && (*remote)[n]) {
+      ptrs[size_t(k)] = (*remote)[n];
+    } else if (h->local[id]) {
       ptrs[size_t(k)] = h->buf[h->owner[id]].main;
       if (want_shadow) ptrs[size_t(nkeys + k)] = h->buf[h->owner[id]].b16;
     }
@@ -1514,6 +1529,7 @@ ed_status ed_download(ed_plan_h* h, ed_output_c* outs, int32_t n, char* err, siz
     if (!h || (n && !outs)) throw ed_error(ED_ERR_USAGE, "null argument");
     CUDA_OK(cudaSetDevice(h->ctx->device));
     cudaStream_t s = h->ctx->stream;
+    const int me = h->ctx->rank, world = h->ctx->world;
     for (int i = 0; i < n; ++i) {
       int w = outs[i].vertex_id;
       if (w < 0 || w >= int(h->V.size())) throw ed_error(ED_ERR_USAGE, "output vertex out of range");
@@ -1523,19 +1539,40 @@ ed_status ed_download(ed_plan_h* h, ed_output_c* outs, int32_t n, char* err, siz
         const Ex& u = h->X[id];
         bool mine = h->V[w].arity == 0 ? (u.kind == ED_EXEC_INPUT_CHUNK && u.producer == w)
                                         : (u.kind == ED_EXEC_REFINEMENT && u.producer == w && u.consumer < 0);
-        if (mine) {
-          if (!h->local[id]) throw ed_error(ED_ERR_USAGE, "output chunk lives on another rank");
-          ids.push_back(id);
-        }
+        if (mine) ids.push_back(id);
       }
       if (ids.empty()) throw ed_error(ED_ERR_PLAN, "no final refinement layer for output");
+      // world > 1: every rank calls; chunks held elsewhere travel to rank 0
+      std::vector<void*> remote(ids.size(), nullptr);
+      if (world > 1) {
+        NCCL_OK(ncclGroupStart());
+        for (size_t k = 0; k < ids.size(); ++k) {
+          int id = ids[k], src = h->rank_of(id);
+          if (src == 0) continue;
+          if (me == src)
+            NCCL_OK(ncclSend(h->main_of(id), size_t(h->X[id].sz), h->f64 ? ncclFloat64 : ncclFloat32, 0,
+                             h->ctx->comm, s));
+          if (me == 0) {
+            CUDA_OK(cudaMallocAsync(&remote[k], size_t(h->X[id].sz) * h->es, s));
+            NCCL_OK(ncclRecv(remote[k], size_t(h->X[id].sz), h->f64 ? ncclFloat64 : ncclFloat32, src,
+                             h->ctx->comm, s));
+          }
+        }
+        NCCL_OK(ncclGroupEnd());
+        if (me != 0) {
+          CUDA_OK(cudaStreamSynchronize(s));
+          continue;
+        }
+      }
       shape part = h->V[w].arity == 0 ? h->V[w].d : h->out_partition(w);
       size_t bytes = size_t(outs[i].n) * dt_size(outs[i].dtype);
       ensure_staging(h, bytes);
       ChunkMapParams p;
-      chunk_map(h, w, part, ids, false, p);
+      chunk_map(h, w, part, ids, false, p, &remote);
       CUDA_OK(launch_gather(p, h->staging, h->store, dt_of(outs[i].dtype), s));
       CUDA_OK(cudaMemcpyAsync(outs[i].data, h->staging, bytes, cudaMemcpyDeviceToHost, s));
+      for (void* r : remote)
+        if (r) CUDA_OK(cudaFreeAsync(r, s));
       CUDA_OK(cudaStreamSynchronize(s));
     }
   });
@@ -1561,6 +1598,31 @@ ed_status ed_download_chunk(ed_plan_h* h, int32_t exec_id, int32_t dtype, void* 
     else CUDA_OK(launch_convert(b.b16, DT::BF16, h->staging, dt_of(dtype), n, s));
     CUDA_OK(cudaMemcpyAsync(data, h->staging, bytes, cudaMemcpyDeviceToHost, s));
     CUDA_OK(cudaStreamSynchronize(s));
+  });
+}
+
+ed_status ed_plan_schedule(const ed_plan_c* plan, int32_t rank, int32_t world, ed_sched_op_c* out, int32_t cap,
+                           int32_t* n_out, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!n_out || world < 1 || rank < 0 || rank >= world) throw ed_error(ED_ERR_USAGE, "bad rank/world");
+    ed_ctx c;
+    c.rank = rank;
+    c.world = world;
+    ed_plan_h h;
+    h.ctx = &c;
+    h.copy_plan(plan);
+    h.validate();
+    const auto at = h.transfers_by_consumer();
+    std::vector<ed_sched_op_c> ops;
+    for (int id = 0; id < int(h.X.size()); ++id) {
+      for (auto& [d, dst] : at[id]) {
+        if (h.rank_of(d) == rank) ops.push_back({ED_SCHED_SEND, d, dst, h.X[d].sz});
+        else if (dst == rank) ops.push_back({ED_SCHED_RECV, d, h.rank_of(d), h.X[d].sz});
+      }
+      if (h.X[id].kind != ED_EXEC_INPUT_CHUNK && h.rank_of(id) == rank) ops.push_back({ED_SCHED_COMPUTE, id, -1, 0});
+    }
+    for (int i = 0; i < std::min<int>(cap, int(ops.size())); ++i) out[i] = ops[i];
+    *n_out = int(ops.size());
   });
 }
 

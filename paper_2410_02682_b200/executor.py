@@ -220,6 +220,19 @@ def _dt(a):
     return abi.DTYPE_F64 if a.dtype == np.float64 else abi.DTYPE_F32
 
 
+def plan_schedule(plan: Plan, rank: int, world: int):
+    """Rank `rank`'s logical schedule (host-only; no GPU needed):
+    [(kind, exec_id, peer, elems)] with kind in {"compute", "send", "recv"}."""
+    pc, keep = plan.to_c()
+    cap = 4 * len(plan.exec) + 16
+    arr = (abi.ed_sched_op_c * cap)()
+    n = C.c_int32()
+    err, en = _err()
+    _check(library().ed_plan_schedule(C.byref(pc), rank, world, arr, cap, C.byref(n), err, en), err)
+    names = {abi.SCHED_COMPUTE: "compute", abi.SCHED_SEND: "send", abi.SCHED_RECV: "recv"}
+    return [(names[arr[i].kind], arr[i].exec_id, arr[i].peer, arr[i].elems) for i in range(n.value)]
+
+
 _default_ctx = None
 
 
