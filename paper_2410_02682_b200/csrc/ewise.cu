@@ -225,6 +225,72 @@ __global__ void __launch_bounds__(128) rowreduce_seq_kernel(const RowReduceParam
   }
 }
 
+// One 128-thread block per row; the row lives in registers (EPT per thread),
+// so X is read once and Y written once (the five unfused vertices move the
+// row eight times).
+template <int EPT>
+__global__ void __launch_bounds__(128) softmax_kernel(const SoftmaxParams p) {
+  constexpr int NV = EPT / 4;
+  __shared__ float red[4];
+  const JoinPtrs jp = p.joins[blockIdx.y];
+  const int t = threadIdx.x, lane = t % 32, warp = t / 32;
+  for (int64_t row = blockIdx.x; row < p.rows; row += gridDim.x) {
+    const float* xr = static_cast<const float*>(jp.x) + row * p.len;
+    float v[EPT];
+    float mx = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int i = (j * 128 + t) * 4;
+      float4 q = i < p.len ? __ldcs(reinterpret_cast<const float4*>(xr + i)) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+      v[4 * j] = q.x;
+      v[4 * j + 1] = q.y;
+      v[4 * j + 2] = q.z;
+      v[4 * j + 3] = q.w;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) mx = fmaxf(mx, v[4 * j + e]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) red[warp] = mx;
+    __syncthreads();
+    mx = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+    __syncthreads();
+    float sum = 0.f;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int i = (j * 128 + t) * 4;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        v[4 * j + e] = i < p.len ? expf(v[4 * j + e] - mx) : 0.f;
+        sum += v[4 * j + e];
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0) red[warp] = sum;
+    __syncthreads();
+    sum = (red[0] + red[1]) + (red[2] + red[3]);
+    __syncthreads();
+    const float inv = __frcp_rn(sum);
+    float* yo = jp.out ? static_cast<float*>(jp.out) + row * p.len : nullptr;
+    __nv_bfloat16* y16 = jp.out16 ? static_cast<__nv_bfloat16*>(jp.out16) + row * p.len : nullptr;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int i = (j * 128 + t) * 4;
+      if (i >= p.len) continue;
+      const float a = v[4 * j] * inv, b = v[4 * j + 1] * inv, c = v[4 * j + 2] * inv, d = v[4 * j + 3] * inv;
+      if (yo) __stcs(reinterpret_cast<float4*>(yo + i), make_float4(a, b, c, d));
+      if (y16) {
+        __nv_bfloat162 h0 = __floats2bfloat162_rn(a, b), h1 = __floats2bfloat162_rn(c, d);
+        uint2 w;
+        w.x = *reinterpret_cast<uint32_t*>(&h0);
+        w.y = *reinterpret_cast<uint32_t*>(&h1);
+        *reinterpret_cast<uint2*>(y16 + i) = w;
+      }
+    }
+  }
+}
+
 int blocks_for(int64_t work, int per_block, int joins) {
   int64_t b = (work + per_block - 1) / per_block;
   const int64_t cap = (148 * 8 + joins - 1) / joins;  // ~8 CTAs per SM across the launch
@@ -238,6 +304,17 @@ cudaError_t launch_ewise(const EwiseParams& p, int n_joins, bool f64, bool exact
   if (f64) ewise_kernel<double, true><<<grid, 256, 0, s>>>(p);
   else if (exact) ewise_kernel<float, true><<<grid, 256, 0, s>>>(p);
   else ewise_kernel<float, false><<<grid, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_softmax(const SoftmaxParams& p, int n_joins, cudaStream_t s) {
+  const unsigned rows = unsigned(p.rows < 65535 * 8 ? p.rows : 65535 * 8);
+  dim3 grid(rows, n_joins);
+  if (p.len <= 128 * 8) softmax_kernel<8><<<grid, 128, 0, s>>>(p);
+  else if (p.len <= 128 * 16) softmax_kernel<16><<<grid, 128, 0, s>>>(p);
+  else if (p.len <= 128 * 32) softmax_kernel<32><<<grid, 128, 0, s>>>(p);
+  else if (p.len <= 128 * 64) softmax_kernel<64><<<grid, 128, 0, s>>>(p);
+  else return cudaErrorInvalidValue;
   return cudaGetLastError();
 }
 

@@ -31,6 +31,15 @@ struct RowReduceParams {
   double c;
 };
 
+// Fused row softmax (max, sub, exp, sum, div of one row block in registers):
+// Y = exp(X - max_row) / sum_row exp(X - max_row), rows of `len` elements.
+struct SoftmaxParams {
+  const JoinPtrs* joins;  // x = the chain's input chunk, out/out16 = Y's chunk
+  int64_t rows;
+  int len;
+};
+
+cudaError_t launch_softmax(const SoftmaxParams& p, int n_joins, cudaStream_t s);
 cudaError_t launch_ewise(const EwiseParams& p, int n_joins, bool f64, bool exact, cudaStream_t s);
 cudaError_t launch_rowreduce(const RowReduceParams& p, int n_joins, bool f64, bool exact, cudaStream_t s);
 

@@ -66,6 +66,26 @@ __device__ __forceinline__ TileCoord tile_coord(const GemmLaunch& p, int t, int 
   return c;
 }
 
+// unary map of a fused consumer vertex (ops.cc:18-28) on 32 accumulator
+// values; the op is uniform, so branch once outside the unrolled loops.
+__device__ __forceinline__ void epi32(const GemmLaunch& p, uint32_t* r) {
+  const int op = p.epi_map;
+  const float c = p.epi_c;
+  if (op == 0) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const float x = __uint_as_float(r[j]);
+      r[j] = __float_as_uint(x > 0.0f ? x : 0.0f);
+    }
+  } else if (op == 2) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) r[j] ^= 0x80000000u;
+  } else if (op == 3) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(c * __uint_as_float(r[j]));
+  }
+}
+
 template <bool kBF16, int kCta>
 __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ GemmLaunch p) {
   using C_ = Cfg<kBF16, kCta>;
@@ -226,6 +246,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             tmem_ld_32x32b_x32(tbase + uint32_t(c * cols), *reinterpret_cast<uint32_t(*)[32]>(r));
             if (pass == 1) tmem_ld_32x32b_x32(tbase + uint32_t(c * cols + 32), *reinterpret_cast<uint32_t(*)[32]>(r + 32));
             tmem_ld_wait();
+            if (p.epi_map >= 0) {
+              epi32(p, r);
+              if (pass == 1) epi32(p, r + 32);
+            }
             uint8_t* tile = stage_out + (wq * 2 + (stage_ctr & 1)) * 4096;
             if (lane == 0) bulk_wait_read<1>();
             __syncwarp();
@@ -262,12 +286,15 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           uint32_t r[32];
           tmem_ld_32x32b_x32(tbase + uint32_t(c * 32), r);
           tmem_ld_wait();
+          if (p.epi_map >= 0) epi32(p, r);
           const int col = tc.n0 + c * 32;
           if (row >= p.M || col >= p.N) continue;
-          if (c32)
-            for (int j = 0; j < 32 && col + j < p.N; ++j) c32[col + j] = __uint_as_float(r[j]);
-          if (c16)
-            for (int j = 0; j < 32 && col + j < p.N; ++j) c16[col + j] = __float2bfloat16_rn(__uint_as_float(r[j]));
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {  // constant indices keep r[] in registers
+            if (col + j >= p.N) break;
+            if (c32) c32[col + j] = __uint_as_float(r[j]);
+            if (c16) c16[col + j] = __float2bfloat16_rn(__uint_as_float(r[j]));
+          }
         }
       }
       // this warp is done reading accumulator `as` (tell the leader's MMA issuer)

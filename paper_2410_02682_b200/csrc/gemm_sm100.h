@@ -28,6 +28,8 @@ struct GemmLaunch {
   int vec_ok;                 // 1: output rows 16-byte aligned (vector stores)
   long long c_sm, c_sb;       // output element strides for M and batch; N stride is 1
   int bf16;                   // operand type: 1 bf16 (kind::f16), 0 fp32 (kind::tf32)
+  int epi_map;                // fused map on the accumulator (ed_map_op) or -1
+  float epi_c;                // scale constant of a fused scale map
 };
 
 int gemm_bk(bool bf16);

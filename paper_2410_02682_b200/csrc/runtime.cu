@@ -269,7 +269,7 @@ void make_map(CUtensorMap* m, const void* base, bool bf16, int64_t inner, int64_
 }
 
 // ---- schedule -------------------------------------------------------------------
-enum class OpKind { GEMM, GENERIC, REFINE, CORRUPT, SEND, RECV, CONVERT, EWISE, ROWREDUCE };
+enum class OpKind { GEMM, GENERIC, REFINE, CORRUPT, SEND, RECV, CONVERT, EWISE, ROWREDUCE, SOFTMAX };
 
 struct Op {
   OpKind kind;
@@ -287,6 +287,7 @@ struct Op {
   std::vector<RectGroup> groups;       // REFINE fast path (empty: generic fold kernel)
   int64_t max_rows = 0;
   RowReduceParams rr{};
+  SoftmaxParams sm{};
   std::vector<JoinPtrs> jptrs;         // EWISE / ROWREDUCE: per-join operands
   void* ptr = nullptr;
   DT dt = DT::F32;
@@ -394,6 +395,13 @@ struct ed_plan_h {
   std::map<int, GemmMap> gmap_;                   // einsum -> GEMM mapping
   std::map<int, std::vector<int>> region_sibs_;   // GEMM head join -> siblings
   std::map<int, MemMap> memmap_;                  // einsum -> memory-bound kernel shape
+  struct Softmax {
+    int y;
+    int64_t len;
+    std::vector<std::pair<int, int>> pairs;       // (Y join, x chunk ref)
+  };
+  std::map<int, Softmax> softmax_;                // Y vertex -> fused row-softmax chain
+  std::map<int, std::pair<int, double>> epi_;     // GEMM einsum -> epilogue map (op, c)
   void* d_joinptrs = nullptr;                     // JoinPtrs[] of grouped memory-bound launches
   void* d_rects = nullptr;                        // RectGroup[] of fast refinements
 
@@ -663,35 +671,146 @@ void ed_plan_h::build() {
     shape r0, ext;
   };
   std::vector<std::vector<Src>> srcs(ne);
-  for (int id = 0; id < ne; ++id) {
-    const Ex& u = X[id];
-    if (u.kind != ED_EXEC_REFINEMENT || !local[id]) continue;
-    const shape& bound = V[u.producer].bound;
-    std::set<int> used;
-    for (int d : u.deps) {
-      int o = local[d] ? owner[d] : d;  // remote deps arrive as their own chunks
-      if (!used.insert(o).second) continue;
-      shape rk = region_key(d), dr = region_partition(d), r0(bound.size()), ext(bound.size());
-      for (size_t i = 0; i < bound.size(); ++i) {
-        ext[i] = bound[i] / dr[i];
-        r0[i] = rk[i] * ext[i];
+  const std::vector<int> owner0 = owner;  // after sibling fusion
+  std::vector<char> virt(ne, 0);          // exec vertices fused away (never computed)
+  std::map<int, std::pair<int, double>> epi;  // GEMM einsum -> (map op, c) applied in its epilogue
+  auto alias_pass = [&](const std::map<int, int>& virtual_join_src) {
+    owner = owner0;
+    for (int id = 0; id < ne; ++id) {
+      srcs[id].clear();
+      const Ex& u = X[id];
+      if (!local[id]) continue;
+      if (u.kind == ED_EXEC_JOIN) {
+        auto it = virtual_join_src.find(id);
+        if (it != virtual_join_src.end()) owner[id] = owner[u.deps[it->second]];
+        continue;
       }
-      srcs[id].push_back({o, r0, ext});
+      if (u.kind != ED_EXEC_REFINEMENT) continue;
+      const shape& bound = V[u.producer].bound;
+      std::set<int> used;
+      for (int d : u.deps) {
+        int o = local[d] ? owner[d] : d;  // remote deps arrive as their own chunks
+        if (!used.insert(o).second) continue;
+        shape rk = region_key(d), dr = region_partition(d), r0(bound.size()), ext(bound.size());
+        for (size_t i = 0; i < bound.size(); ++i) {
+          ext[i] = bound[i] / dr[i];
+          r0[i] = rk[i] * ext[i];
+        }
+        srcs[id].push_back({o, r0, ext});
+      }
+      // a refinement that is exactly one producer chunk is that chunk
+      const shape dc = region_partition(id);
+      if (srcs[id].size() == 1) {
+        bool same = true;
+        for (size_t i = 0; i < bound.size(); ++i)
+          same = same && srcs[id][0].r0[i] == u.key[i] * (bound[i] / dc[i]) && srcs[id][0].ext[i] == u.cb[i];
+        if (same) owner[id] = owner[srcs[id][0].id];
+      }
     }
-    // a refinement that is exactly one producer chunk is that chunk
-    const shape dc = region_partition(id);
-    if (srcs[id].size() == 1) {
-      bool same = true;
-      for (size_t i = 0; i < bound.size(); ++i)
-        same = same && srcs[id][0].r0[i] == u.key[i] * (bound[i] / dc[i]) && srcs[id][0].ext[i] == u.cb[i];
-      if (same) owner[id] = owner[srcs[id][0].id];
+  };
+  alias_pass({});
+
+  // ---- cross-vertex fusion (tensor-core modes; exact modes keep every vertex) ----
+  std::map<int, int> virtual_join_src;  // fused join -> dep slot whose buffer it becomes
+  if (tc) {
+    const int nv = int(V.size());
+    std::vector<std::vector<int>> readers(nv);
+    for (int w = 0; w < nv; ++w)
+      for (int k = 0; k < V[w].arity; ++k) readers[V[w].inputs[k]].push_back(w);
+    auto is_output = [&](int w) { return std::find(outputs.begin(), outputs.end(), w) != outputs.end(); };
+    auto all_local = [&](int w) {
+      for (int id = 0; id < ne; ++id)
+        if (X[id].producer == w && !local[id]) return false;
+      return true;
+    };
+    auto joins_of = [&](int w) {
+      std::vector<int> r;
+      for (int id = 0; id < ne; ++id)
+        if (X[id].kind == ED_EXEC_JOIN && X[id].producer == w) r.push_back(id);
+      return r;
+    };
+    auto sole_reader = [&](int w, int r) {
+      return readers[w].size() == 1 && readers[w][0] == r && !is_output(w);
+    };
+    // (1) map epilogue: v = map(u), u a region-fused GEMM read only by v
+    for (int v = 0; v < nv; ++v) {
+      if (!memmap_.count(v) || memmap_[v].kind != OpKind::EWISE || V[v].arity != 1) continue;
+      const int u = V[v].inputs[0];
+      if (!gmap.count(u) || !sole_reader(u, v) || !all_local(u) || !all_local(v)) continue;
+      if (V[v].map == ED_MAP_EXP) continue;  // only cheap maps go into the epilogue
+      bool ok = true;
+      for (int j : joins_of(v)) {
+        const int o = owner[X[j].deps[0]];
+        ok = ok && fused_head[o] && X[o].producer == u;
+      }
+      if (!ok) continue;
+      epi[u] = {V[v].map, V[v].c};
+      for (int j : joins_of(v)) virtual_join_src[j] = 0;
+      memmap_.erase(v);
+    }
+    alias_pass(virtual_join_src);
+    // (2) row softmax: M = max(X), S = sub(X, M), E = exp(S), Sg = sum(E), Y = div(E, Sg)
+    for (int y = 0; y < nv; ++y) {
+      auto is = [&](int w, OpKind k, int arity, int op) {
+        return w >= 0 && memmap_.count(w) && memmap_[w].kind == k && V[w].arity == arity &&
+               (arity == 2 ? V[w].join == op : (k == OpKind::ROWREDUCE ? V[w].agg == op : V[w].map == op));
+      };
+      if (!is(y, OpKind::EWISE, 2, ED_JOIN_DIV) || memmap_[y].y_mode != 2) continue;
+      const int e = V[y].inputs[0], sg = V[y].inputs[1];
+      if (!is(e, OpKind::EWISE, 1, ED_MAP_EXP) || !is(sg, OpKind::ROWREDUCE, 1, ED_AGG_SUM)) continue;
+      if (V[sg].map != ED_MAP_IDENTITY || V[sg].inputs[0] != e) continue;
+      const int sv = V[e].inputs[0];
+      if (!is(sv, OpKind::EWISE, 2, ED_JOIN_SUB) || memmap_[sv].y_mode != 2) continue;
+      const int xv = V[sv].inputs[0], m = V[sv].inputs[1];
+      if (!is(m, OpKind::ROWREDUCE, 1, ED_AGG_MAX) || V[m].map != ED_MAP_IDENTITY || V[m].inputs[0] != xv) continue;
+      if (!sole_reader(m, sv) || !sole_reader(sv, e) || !sole_reader(sg, y) || is_output(e) ||
+          readers[e].size() != 2)
+        continue;
+      if (!all_local(m) || !all_local(sv) || !all_local(e) || !all_local(sg) || !all_local(y)) continue;
+      const int64_t L = memmap_[sg].len;
+      if (memmap_[m].len != L || memmap_[sv].inner != L || memmap_[y].inner != L) continue;
+      if (L % 4 != 0 || L > 128 * 64 || f64) continue;  // the fused kernel keeps a row in registers
+      // every Y join must see one aligned row block: the same x chunk under M and S
+      bool ok = true;
+      std::vector<std::pair<int, int>> pairs;  // (y join, x buffer owner)
+      auto join_at = [&](int ref, int w) {
+        const int o = owner[ref];
+        return (X[o].kind == ED_EXEC_JOIN && X[o].producer == w) ? o : -1;
+      };
+      for (int yj : joins_of(y)) {
+        const int ej = join_at(X[yj].deps[0], e), sgj = join_at(X[yj].deps[1], sg);
+        const int sj = ej >= 0 ? join_at(X[ej].deps[0], sv) : -1;
+        const int mj = sj >= 0 ? join_at(X[sj].deps[1], m) : -1;
+        ok = ok && ej >= 0 && sgj >= 0 && sj >= 0 && mj >= 0 && owner[X[sgj].deps[0]] == ej &&
+             owner[X[mj].deps[0]] == owner[X[sj].deps[0]] && X[yj].sz == X[sj].sz && X[yj].sz % L == 0;
+        if (!ok) break;
+        pairs.push_back({yj, X[sj].deps[0]});
+      }
+      if (!ok || pairs.empty()) continue;
+      Softmax sm;
+      sm.y = y;
+      sm.len = L;
+      sm.pairs = pairs;
+      softmax_[y] = sm;
+      for (int w : {m, sv, e, sg})
+        for (int id = 0; id < ne; ++id)
+          if (X[id].producer == w && X[id].kind != ED_EXEC_INPUT_CHUNK) virt[id] = 1;
+      memmap_.erase(m);
+      memmap_.erase(sv);
+      memmap_.erase(e);
+      memmap_.erase(sg);
     }
   }
 
   // ---- buffer needs ----
   for (int id = 0; id < ne; ++id) {
-    if (!local[id]) continue;
+    if (!local[id] || virt[id] || virtual_join_src.count(id)) continue;
     const Ex& u = X[id];
+    if (u.kind == ED_EXEC_JOIN && softmax_.count(u.producer)) {
+      for (auto& [yj, xr] : softmax_[u.producer].pairs)
+        if (yj == id) buf[owner[xr]].need_main = true;
+      continue;
+    }
     if (u.kind == ED_EXEC_INPUT_CHUNK) buf[owner[id]].need_main = true;
     if (u.kind == ED_EXEC_JOIN) {
       int w = u.producer;
@@ -718,7 +837,7 @@ void ed_plan_h::build() {
     if (dst == me) buf[d].need_main = true;
   // every computed chunk keeps at least one representation
   for (int id = 0; id < ne; ++id)
-    if (local[id] && owner[id] == id && !buf[id].need_16) buf[id].need_main = true;
+    if (local[id] && !virt[id] && owner[id] == id && !buf[id].need_16) buf[id].need_main = true;
 
   // ---- allocation plan ----
   size_t off = 0;
@@ -728,7 +847,7 @@ void ed_plan_h::build() {
     return o;
   };
   for (int id = 0; id < ne; ++id) {
-    bool here = (local[id] && owner[id] == id);
+    bool here = (local[id] && owner[id] == id && !virt[id]);
     bool recv = false;
     for (auto& [d, dst] : transfers) recv = recv || (d == id && dst == me);
     if (!here && !recv) continue;
@@ -773,8 +892,19 @@ void ed_plan_h::build() {
     if (!local[id] || u.kind == ED_EXEC_INPUT_CHUNK) continue;
     const Vtx& w = V[u.producer];
     if (u.kind == ED_EXEC_JOIN) {
-      if (first_join < 0) first_join = id;
       if (w.join == ED_JOIN_MUL && w.agg == ED_AGG_SUM) contraction_flops += 2.0 * double(u.fp);
+      if (virt[id] || virtual_join_src.count(id)) continue;  // computed inside a fused kernel
+      if (first_join < 0) first_join = id;
+      if (softmax_.count(u.producer)) {
+        if (gemm_emitted.count(u.producer)) continue;
+        gemm_emitted.insert(u.producer);
+        Op op{OpKind::SOFTMAX};
+        op.name = "softmax_rows:" + w.name;
+        op.ptr = reinterpret_cast<void*>(id);
+        for (auto& [yj, xr] : softmax_[u.producer].pairs) op.heads.push_back(yj);
+        ops.push_back(op);
+        continue;
+      }
       if (gmap.count(u.producer)) {
         if (!fused_head[id] || gemm_emitted.count(u.producer)) continue;
         gemm_emitted.insert(u.producer);
@@ -812,7 +942,7 @@ void ed_plan_h::build() {
       continue;
     }
     // refinement
-    if (owner[id] != id) continue;  // aliased: no work
+    if (owner[id] != id || virt[id]) continue;  // aliased or fused away: no work
     Op op{OpKind::REFINE};
     op.name = "refine:" + w.name;
     op.ptr = reinterpret_cast<void*>(id);
@@ -822,7 +952,8 @@ void ed_plan_h::build() {
     // after the op that produced the first join
     size_t at = 0;
     for (size_t i = 0; i < ops.size(); ++i)
-      if (((ops[i].kind == OpKind::GEMM || ops[i].kind == OpKind::EWISE || ops[i].kind == OpKind::ROWREDUCE) &&
+      if (((ops[i].kind == OpKind::GEMM || ops[i].kind == OpKind::EWISE || ops[i].kind == OpKind::ROWREDUCE ||
+            ops[i].kind == OpKind::SOFTMAX) &&
            std::count(ops[i].heads.begin(), ops[i].heads.end(), owner[first_join])) ||
           (ops[i].kind == OpKind::GENERIC && reinterpret_cast<intptr_t>(ops[i].ptr) == owner[first_join])) {
         at = i + 1;
@@ -839,6 +970,7 @@ void ed_plan_h::build() {
   for (int id = 0; id < ne; ++id)
     for (auto& s : srcs[id]) this->srcs_.push_back({id, s.id, s.r0, s.ext});
   this->gmap_ = gmap;
+  this->epi_ = epi;
   this->region_sibs_ = region_sibs;
 }
 
@@ -892,6 +1024,12 @@ void ed_plan_h::allocate() {
         p.c_sm = g.cm.ext > 1 ? g.cm.stride : 0;
         p.c_sb = g.cb.ext > 1 ? g.cb.stride : 0;
         p.vec_ok = (p.c_sm % 8 == 0) && (p.c_sb % 8 == 0);
+        p.epi_map = -1;
+        if (epi_.count(u.producer)) {
+          p.epi_map = epi_.at(u.producer).first;
+          p.epi_c = float(epi_.at(u.producer).second);
+          op.name += "+map";
+        }
         const uint32_t BK = uint32_t(gemm_bk(b16)), BM = uint32_t(gemm_bm());
         const uint32_t ATOM = 128u / (b16 ? 2u : 4u);
         op.maps.clear();
@@ -1109,6 +1247,22 @@ void ed_plan_h::allocate() {
         op.gen.out16 = buf[id].b16;
         op.gen.n_out = X[id].sz;
         break;
+      case OpKind::SOFTMAX: {
+        const Softmax& sm = softmax_.at(X[id].producer);
+        op.jptrs.clear();
+        for (auto& [yj, xr] : sm.pairs) {
+          JoinPtrs jp{};
+          jp.x = buf[resolve(xr)].main;
+          jp.out = buf[yj].main;
+          jp.out16 = buf[yj].b16;
+          op.jptrs.push_back(jp);
+          op.bytes += double(X[yj].sz) * (es + (jp.out ? es : 0) + (jp.out16 ? 2 : 0));
+        }
+        op.sm.rows = X[sm.pairs[0].first].sz / sm.len;
+        op.sm.len = int(sm.len);
+        jptrs_total += op.jptrs.size();
+        break;
+      }
       case OpKind::EWISE:
       case OpKind::ROWREDUCE: {
         const Ex& u = X[id];
@@ -1174,6 +1328,7 @@ void ed_plan_h::allocate() {
       CUDA_OK(cudaMemcpy(d, op.jptrs.data(), sizeof(JoinPtrs) * op.jptrs.size(), cudaMemcpyHostToDevice));
       op.ew.joins = d;
       op.rr.joins = d;
+      op.sm.joins = d;
       o += op.jptrs.size();
     }
   }
@@ -1209,6 +1364,7 @@ void ed_plan_h::launch_op(size_t i, cudaStream_t s) {
     case OpKind::EWISE:
       CUDA_OK(launch_ewise(op.ew, int(op.jptrs.size()), f64, opt.precision == ED_PREC_FP32, s));
       break;
+    case OpKind::SOFTMAX: CUDA_OK(launch_softmax(op.sm, int(op.jptrs.size()), s)); break;
     case OpKind::ROWREDUCE:
       CUDA_OK(launch_rowreduce(op.rr, int(op.jptrs.size()), f64, opt.precision == ED_PREC_FP32, s));
       break;
@@ -1594,6 +1750,7 @@ ed_status ed_download_chunk(ed_plan_h* h, int32_t exec_id, int32_t dtype, void* 
     size_t bytes = size_t(n) * dt_size(dtype);
     ensure_staging(h, bytes);
     const Buffer& b = h->buf[o];
+    if (!b.main && !b.b16) throw ed_error(ED_ERR_USAGE, "chunk was fused into a consumer kernel and never materialised");
     if (b.main) CUDA_OK(launch_convert(b.main, h->store, h->staging, dt_of(dtype), n, s));
     else CUDA_OK(launch_convert(b.b16, DT::BF16, h->staging, dt_of(dtype), n, s));
     CUDA_OK(cudaMemcpyAsync(data, h->staging, bytes, cudaMemcpyDeviceToHost, s));
