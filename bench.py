@@ -54,7 +54,7 @@ class Clocks:
         self.proc = None
 
     def __enter__(self):
-        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+        q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
@@ -71,7 +71,13 @@ class Clocks:
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) >= 9:
-                self.samples.append(parts)
+                self.samples.append((time.time(), parts))
+
+    def mark(self, begin):
+        if begin:
+            self.t0 = time.time()
+        else:
+            self.t1 = time.time()
 
     def __exit__(self, *a):
         if self.proc:
@@ -82,14 +88,19 @@ class Clocks:
                 self.proc.kill()
 
     def summary(self):
-        if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        # samples that arrived while the timed region ran (nvidia-smi output
+        # lags by up to one period, so allow 50 ms of slack)
+        t0, t1 = getattr(self, "t0", 0.0), getattr(self, "t1", 1e18)
+        inside = [s for t, s in self.samples if t0 <= t <= t1 + 0.05]
+        if not inside:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(s[1]) for s in inside if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in inside if s[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[5 + i].lower().startswith("active")})
+        reasons = sorted({names[i] for s in inside for i in range(4) if s[5 + i].lower().startswith("active")})
+        pw = [float(s[3]) for s in inside if s[3].replace(".", "").isdigit()]
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(inside), "power_w_max": max(pw) if pw else None}
 
 
 def dist_env():
@@ -166,7 +177,7 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="bmm2")
     ap.add_argument("--precision", default="bf16")
@@ -214,10 +225,12 @@ def main():
         barrier()
         torch.cuda.synchronize()
         dev_ms = []
+        clk.mark(True)
         for _ in range(args.steps):
             rep = pp.run()
             dev_ms.append(rep.device_ms)
         torch.cuda.synchronize()
+        clk.mark(False)
         barrier()
     tot_ms = sum(dev_ms)
     if world > 1:

@@ -402,6 +402,7 @@ struct ed_plan_h {
   };
   std::map<int, Softmax> softmax_;                // Y vertex -> fused row-softmax chain
   std::map<int, std::pair<int, double>> epi_;     // GEMM einsum -> epilogue map (op, c)
+  std::vector<char> opaque_;                      // exec id whose value was fused into a consumer
   void* d_joinptrs = nullptr;                     // JoinPtrs[] of grouped memory-bound launches
   void* d_rects = nullptr;                        // RectGroup[] of fast refinements
 
@@ -673,6 +674,7 @@ void ed_plan_h::build() {
   std::vector<std::vector<Src>> srcs(ne);
   const std::vector<int> owner0 = owner;  // after sibling fusion
   std::vector<char> virt(ne, 0);          // exec vertices fused away (never computed)
+  opaque_.assign(ne, 0);
   std::map<int, std::pair<int, double>> epi;  // GEMM einsum -> (map op, c) applied in its epilogue
   auto alias_pass = [&](const std::map<int, int>& virtual_join_src) {
     owner = owner0;
@@ -746,6 +748,9 @@ void ed_plan_h::build() {
       if (!ok) continue;
       epi[u] = {V[v].map, V[v].c};
       for (int j : joins_of(v)) virtual_join_src[j] = 0;
+      // u's own values never exist: its chunks hold map(u)
+      for (int id = 0; id < ne; ++id)
+        if (X[id].producer == u && X[id].kind != ED_EXEC_INPUT_CHUNK) opaque_[id] = 1;
       memmap_.erase(v);
     }
     alias_pass(virtual_join_src);
@@ -1743,8 +1748,9 @@ ed_status ed_download_chunk(ed_plan_h* h, int32_t exec_id, int32_t dtype, void* 
     if (!h->local[exec_id]) throw ed_error(ED_ERR_USAGE, "chunk not resident on this rank");
     const Ex& u = h->X[exec_id];
     int o = h->owner[exec_id];
-    if (u.kind == ED_EXEC_JOIN && o != exec_id)
+    if (u.kind == ED_EXEC_JOIN && o != exec_id && h->X[o].producer == u.producer)
       throw ed_error(ED_ERR_USAGE, "join partial was folded into its region's accumulator");
+    if (h->opaque_[exec_id]) throw ed_error(ED_ERR_USAGE, "chunk was fused into its consumer's kernel");
     CUDA_OK(cudaSetDevice(h->ctx->device));
     cudaStream_t s = h->ctx->stream;
     size_t bytes = size_t(n) * dt_size(dtype);
