@@ -174,8 +174,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       // K advances 32 bytes per MMA inside the atom.
       // MN-major: 128-byte MN atoms of BK K-rows (LBO = BK*128), 8-row K
       // groups (SBO 1024), K advances UMMA_K rows per MMA.
+      // MN-major tf32 uses the 32B-atom swizzle: K groups of 4 rows (SBO 512).
       const uint32_t a_lbo = p.a_mn ? C_::BK * 128 : 16, b_lbo = p.b_mn ? C_::BK * 128 : 16;
       const uint32_t a_step = p.a_mn ? C_::UMMA_K * 128 : 32, b_step = p.b_mn ? C_::UMMA_K * 128 : 32;
+      const uint32_t a_lt = (!kBF16 && p.a_mn) ? 1u : 2u, b_lt = (!kBF16 && p.b_mn) ? 1u : 2u;
+      const uint32_t a_sbo = a_lt == 1 ? 512u : 1024u, b_sbo = b_lt == 1 ? 512u : 1024u;
       int it = 0, local = 0;
       for (int t = first; t < total; t += stride, ++local) {
         const TileCoord tc = tile_coord<C_::TILE_M>(p, t, tiles_m, tiles_n);
@@ -196,8 +199,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           const uint32_t sb = sa + C_::A_BYTES;
 #pragma unroll
           for (int k = 0; k < C_::BK / C_::UMMA_K; ++k) {
-            const uint64_t ad = umma_desc_sw128(sa + k * a_step, a_lbo, 1024);
-            const uint64_t bd = umma_desc_sw128(sb + k * b_step, b_lbo, 1024);
+            const uint64_t ad = umma_desc_sw128(sa + k * a_step, a_lbo, a_sbo, a_lt);
+            const uint64_t bd = umma_desc_sw128(sb + k * b_step, b_lbo, b_sbo, b_lt);
             const uint32_t acc = (i | k) != 0;
             if (kCta == 2) {
               if (kBF16) mma_f16_2sm(d_tmem, ad, bd, idesc, acc);

@@ -212,14 +212,16 @@ __device__ __forceinline__ void tmem_ld_wait() {
 // ---- UMMA descriptors (tcgen05 shared-memory matrix descriptor) ------------
 // bits [0,14) start>>4, [16,30) LBO>>4, [32,46) SBO>>4, [46,48) version=1,
 // [49,52) base offset, [52] lbo mode, [61,64) layout (2 = SWIZZLE_128B).
+// layout 2 = SWIZZLE_128B, 1 = SWIZZLE_128B_BASE32B (the only MN-major
+// layout for 32-bit operands: 32-byte granules swizzled over 4-row groups)
 __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr, uint32_t lbo_bytes,
-                                                    uint32_t sbo_bytes) {
+                                                    uint32_t sbo_bytes, uint32_t layout = 2) {
   uint64_t d = 0;
   d |= uint64_t((smem_addr >> 4) & 0x3FFF);
   d |= uint64_t((lbo_bytes >> 4) & 0x3FFF) << 16;
   d |= uint64_t((sbo_bytes >> 4) & 0x3FFF) << 32;
   d |= uint64_t(1) << 46;
-  d |= uint64_t(2) << 61;
+  d |= uint64_t(layout) << 61;
   return d;
 }
 

@@ -216,10 +216,6 @@ bool map_gemm(const Vtx& v, const shape& local_xy, bool bf16, GemmMap& g, std::s
     why = "B has no unit-stride N or K";
     return false;
   }
-  if (!bf16 && (g.a_mn || g.b_mn)) {
-    why = "tf32 MN-major operand";  // K-major only for kind::tf32 (bf16 supports both)
-    return false;
-  }
   const int es = bf16 ? 2 : 4;
   auto aligned = [&](const Dim& d) { return d.ext == 1 || (d.stride * es) % 16 == 0; };
   // outer (non-unit) strides of each TMA view must be 16-byte multiples
@@ -248,7 +244,8 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // 3-D tensor map {inner, outer, batch} with a 128-byte swizzled box.
 void make_map(CUtensorMap* m, const void* base, bool bf16, int64_t inner, int64_t outer, int64_t outer_stride,
-              int64_t batch, int64_t batch_stride, uint32_t box_inner, uint32_t box_outer) {
+              int64_t batch, int64_t batch_stride, uint32_t box_inner, uint32_t box_outer,
+              CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   const int es = bf16 ? 2 : 4;
   cuuint64_t dims[3] = {cuuint64_t(inner), cuuint64_t(outer), cuuint64_t(batch)};
   auto fix = [&](int64_t s, int64_t prev_bytes) -> cuuint64_t {
@@ -263,7 +260,7 @@ void make_map(CUtensorMap* m, const void* base, bool bf16, int64_t inner, int64_
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = encode_fn()(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
                            const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw ed_error(ED_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
 }
@@ -1052,12 +1049,14 @@ void ed_plan_h::allocate() {
             const void* pb = b16 ? buf[db].b16 : buf[db].main;
             if (!pa || !pb) throw ed_error(ED_ERR_PLAN, "GEMM operand buffer missing");
             CUtensorMap ma, mb;
+            // MN-major fp32 operands need the 32-byte-atom swizzle (see gemm_sm100.cu)
+            const CUtensorMapSwizzle mn_swz = b16 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
             if (!g.a_mn) make_map(&ma, pa, b16, g.ak.ext, g.am.ext, g.am.stride, g.ab.ext, g.ab.stride, BK, BM);
-            else make_map(&ma, pa, b16, g.am.ext, g.ak.ext, g.ak.stride, g.ab.ext, g.ab.stride, ATOM, BK);
+            else make_map(&ma, pa, b16, g.am.ext, g.ak.ext, g.ak.stride, g.ab.ext, g.ab.stride, ATOM, BK, mn_swz);
             if (!g.b_mn)
               make_map(&mb, pb, b16, g.bk.ext, g.bn.ext, g.bn.stride, g.bb.ext, g.bb.stride, BK,
                        uint32_t(gemm_b_box(p.M)));
-            else make_map(&mb, pb, b16, g.bn.ext, g.bk.ext, g.bk.stride, g.bb.ext, g.bb.stride, ATOM, BK);
+            else make_map(&mb, pb, b16, g.bn.ext, g.bk.ext, g.bk.stride, g.bb.ext, g.bb.stride, ATOM, BK, mn_swz);
             op.maps.push_back(ma);
             op.maps.push_back(mb);
             ++total_sib;
