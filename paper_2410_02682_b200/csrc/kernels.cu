@@ -227,6 +227,33 @@ __global__ void gather_kernel(const ChunkMapParams p, void* whole, int st_dt_, i
   }
 }
 
+// one row of one rectangle per block-iteration; threads along the inner run
+__global__ void __launch_bounds__(256) blockcopy_kernel(const BlockCopyParams p) {
+  const BlockCopy& g = p.groups[blockIdx.y];
+  const int r = p.rank;
+  const int64_t inner = g.ext[r - 1];
+  for (int64_t row = blockIdx.x; row < g.rows; row += gridDim.x) {
+    int64_t rem = row, so = g.src_off, dofs = g.dst_off;
+    for (int d = r - 2; d >= 0; --d) {
+      const int64_t c = rem % g.ext[d];
+      rem /= g.ext[d];
+      so += c * g.sstr[d];
+      dofs += c * g.dstr[d];
+    }
+    if (p.in_dt == 1 && p.out_dt == 1 && !g.dst16 && (so % 4) == 0 && (dofs % 4) == 0 && inner % 4 == 0) {
+      const float4* s4 = reinterpret_cast<const float4*>(static_cast<const float*>(g.src) + so);
+      float4* d4 = reinterpret_cast<float4*>(static_cast<float*>(g.dst) + dofs);
+      for (int64_t i = threadIdx.x; i < inner / 4; i += blockDim.x) d4[i] = s4[i];
+      continue;
+    }
+    for (int64_t i = threadIdx.x; i < inner; i += blockDim.x) {
+      const double v = ld_dt(g.src, p.in_dt, so + i);
+      if (g.dst) st_dt(g.dst, p.out_dt, dofs + i, v);
+      if (g.dst16) st_dt(g.dst16, 2, dofs + i, v);
+    }
+  }
+}
+
 __global__ void convert_kernel(const void* src, int in_dt, void* dst, int out_dt, int64_t n) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
     st_dt(dst, out_dt, i, ld_dt(src, in_dt, i));
@@ -270,6 +297,13 @@ cudaError_t launch_scatter(const ChunkMapParams& p, const void* whole, DT in, DT
 
 cudaError_t launch_gather(const ChunkMapParams& p, void* whole, DT store, DT out, cudaStream_t s) {
   gather_kernel<<<grid_for(p.n, 256), 256, 0, s>>>(p, whole, int(store), int(out));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_blockcopy(const BlockCopyParams& p, int n_groups, int64_t max_rows, cudaStream_t s) {
+  const int64_t per = (148 * 16 + n_groups - 1) / n_groups;
+  dim3 grid(unsigned(max_rows < per ? (max_rows < 1 ? 1 : max_rows) : per), unsigned(n_groups));
+  blockcopy_kernel<<<grid, 256, 0, s>>>(p);
   return cudaGetLastError();
 }
 

@@ -80,11 +80,30 @@ struct ChunkMapParams {
 
 enum class DT : int { F64 = 0, F32 = 1, BF16 = 2 };
 
+// Rectangle copies between a whole tensor and its chunks (chunk / assemble,
+// relation.cc:31-78), with dtype conversion and an optional bf16 shadow.
+struct BlockCopy {
+  const void* src;
+  void* dst;
+  void* dst16;                       // optional bf16 shadow of dst
+  int64_t src_off, dst_off;
+  int64_t ext[kMaxRank];
+  int64_t sstr[kMaxRank], dstr[kMaxRank];
+  int64_t rows;                      // prod(ext[0..rank-2])
+};
+
+struct BlockCopyParams {
+  int rank;
+  int in_dt, out_dt;                 // DT
+  const BlockCopy* groups;           // device array
+};
+
 cudaError_t launch_generic(const GenericParams& p, bool f64, cudaStream_t s);
 cudaError_t launch_refine(const RefineParams& p, bool f64, cudaStream_t s);
 cudaError_t launch_rect(const RectParams& p, int n_groups, int64_t max_rows, bool f64, cudaStream_t s);
 cudaError_t launch_scatter(const ChunkMapParams& p, const void* whole, DT in, DT store, cudaStream_t s);
 cudaError_t launch_gather(const ChunkMapParams& p, void* whole, DT store, DT out, cudaStream_t s);
+cudaError_t launch_blockcopy(const BlockCopyParams& p, int n_groups, int64_t max_rows, cudaStream_t s);
 cudaError_t launch_convert(const void* src, DT in, void* dst, DT out, int64_t n, cudaStream_t s);
 cudaError_t launch_add_one(void* p, DT dt, cudaStream_t s);  // exec_options_t::corrupt hook
 

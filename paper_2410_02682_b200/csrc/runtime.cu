@@ -402,6 +402,8 @@ struct ed_plan_h {
   std::vector<char> opaque_;                      // exec id whose value was fused into a consumer
   void* d_joinptrs = nullptr;                     // JoinPtrs[] of grouped memory-bound launches
   void* d_rects = nullptr;                        // RectGroup[] of fast refinements
+  void* d_copy_desc = nullptr;                    // BlockCopy[] scratch for upload / download
+  size_t copy_desc_bytes = 0;
 
   int rank_of(int id) const { return X[id].machine % ctx->world; }
   shape out_partition(int w) const {
@@ -1412,6 +1414,7 @@ void ed_plan_h::destroy() {
   if (d_maps) cudaFree(d_maps);
   if (d_joinptrs) cudaFree(d_joinptrs);
   if (d_rects) cudaFree(d_rects);
+  if (d_copy_desc) cudaFree(d_copy_desc);
   if (d_regions) cudaFree(d_regions);
   if (d_ptrs) cudaFree(d_ptrs);
   if (d_err) cudaFree(d_err);
@@ -1435,6 +1438,76 @@ size_t dt_size(int dtype) {
 }
 
 DT dt_of(int dtype) { return dtype == ED_DTYPE_F64 ? DT::F64 : DT::F32; }
+
+// chunk <-> whole-tensor rectangle copies (BlockCopy) for graph vertex w over
+// partition `part`; to_chunks: whole (staging) -> chunk buffers, else back.
+void block_copies(ed_plan_h* h, int w, const shape& part, const std::vector<int>& ids, bool to_chunks,
+                  const void* whole_src, void* whole_dst, DT whole_dt, cudaStream_t s,
+                  const std::vector<void*>* remote = nullptr) {
+  const shape& bound = h->V[w].bound;
+  const int rank = int(bound.size());
+  if (rank == 0) throw ed_error(ED_ERR_UNSUPPORTED, "rank-0 tensors");
+  shape cb(rank), ws(rank), cs(rank);
+  for (int i = 0; i < rank; ++i) cb[i] = bound[i] / part[i];
+  int64_t a = 1, b = 1;
+  for (int i = rank - 1; i >= 0; --i) {
+    ws[i] = a;
+    cs[i] = b;
+    a *= bound[i];
+    b *= cb[i];
+  }
+  std::vector<BlockCopy> groups;
+  int64_t max_rows = 1;
+  for (size_t n = 0; n < ids.size(); ++n) {
+    const int id = ids[n];
+    void* chunk = (remote && (*remote)[n]) ? (*remote)[n] : (h->local[id] ? h->buf[h->owner[id]].main : nullptr);
+    if (!chunk) continue;
+    BlockCopy g{};
+    int64_t woff = 0, rows = 1;
+    for (int i = 0; i < rank; ++i) {
+      woff += h->X[id].key[i] * cb[i] * ws[i];
+      g.ext[i] = cb[i];
+      if (i < rank - 1) rows *= cb[i];
+    }
+    g.rows = rows;
+    max_rows = std::max(max_rows, rows);
+    if (to_chunks) {
+      g.src = whole_src;
+      g.dst = chunk;
+      g.dst16 = h->buf[h->owner[id]].b16;
+      g.src_off = woff;
+      g.dst_off = 0;
+      for (int i = 0; i < rank; ++i) {
+        g.sstr[i] = ws[i];
+        g.dstr[i] = cs[i];
+      }
+    } else {
+      g.src = chunk;
+      g.dst = whole_dst;
+      g.src_off = 0;
+      g.dst_off = woff;
+      for (int i = 0; i < rank; ++i) {
+        g.sstr[i] = cs[i];
+        g.dstr[i] = ws[i];
+      }
+    }
+    groups.push_back(g);
+  }
+  if (groups.empty()) return;
+  const size_t need = sizeof(BlockCopy) * groups.size();
+  if (h->copy_desc_bytes < need) {
+    if (h->d_copy_desc) CUDA_OK(cudaFree(h->d_copy_desc));
+    CUDA_OK(cudaMalloc(&h->d_copy_desc, need));
+    h->copy_desc_bytes = need;
+  }
+  CUDA_OK(cudaMemcpyAsync(h->d_copy_desc, groups.data(), need, cudaMemcpyHostToDevice, s));
+  BlockCopyParams p{};
+  p.rank = rank;
+  p.in_dt = int(to_chunks ? whole_dt : h->store);
+  p.out_dt = int(to_chunks ? h->store : whole_dt);
+  p.groups = static_cast<const BlockCopy*>(h->d_copy_desc);
+  CUDA_OK(launch_blockcopy(p, int(groups.size()), max_rows, s));
+}
 
 // chunk <-> whole-tensor mapping for graph vertex w over partition `part`
 // and the exec ids holding its chunks (any order; keyed by their key).
@@ -1607,9 +1680,8 @@ ed_status ed_upload_tensors(ed_plan_h* h, const ed_tensor_in_c* ts, int32_t n, c
       size_t bytes = size_t(t.n) * dt_size(t.dtype);
       ensure_staging(h, bytes);
       CUDA_OK(cudaMemcpyAsync(h->staging, t.data, bytes, cudaMemcpyHostToDevice, s));
-      ChunkMapParams p;
-      chunk_map(h, t.vertex_id, h->V[t.vertex_id].d, ids, shadow, p);
-      CUDA_OK(launch_scatter(p, h->staging, dt_of(t.dtype), h->store, s));
+      (void)shadow;
+      block_copies(h, t.vertex_id, h->V[t.vertex_id].d, ids, true, h->staging, nullptr, dt_of(t.dtype), s);
       CUDA_OK(cudaStreamSynchronize(s));
     }
   });
@@ -1727,9 +1799,7 @@ ed_status ed_download(ed_plan_h* h, ed_output_c* outs, int32_t n, char* err, siz
       shape part = h->V[w].arity == 0 ? h->V[w].d : h->out_partition(w);
       size_t bytes = size_t(outs[i].n) * dt_size(outs[i].dtype);
       ensure_staging(h, bytes);
-      ChunkMapParams p;
-      chunk_map(h, w, part, ids, false, p, &remote);
-      CUDA_OK(launch_gather(p, h->staging, h->store, dt_of(outs[i].dtype), s));
+      block_copies(h, w, part, ids, false, nullptr, h->staging, dt_of(outs[i].dtype), s, &remote);
       CUDA_OK(cudaMemcpyAsync(outs[i].data, h->staging, bytes, cudaMemcpyDeviceToHost, s));
       for (void* r : remote)
         if (r) CUDA_OK(cudaFreeAsync(r, s));
