@@ -40,6 +40,8 @@ def ref():
         lib.edref_plan.argtypes = [C.c_char_p, C.c_int64, C.c_int64, C.c_double, C.c_char_p,
                                    C.POINTER(C.c_void_p)] + err
         lib.edref_free.argtypes = [C.c_void_p]
+        lib.edref_artifacts.argtypes = [C.c_char_p, C.c_int64, C.c_int64, C.c_double, C.c_char_p,
+                                        C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)] + err
         lib.edref_generate_input.argtypes = [C.c_char_p, C.c_uint64, C.c_int, C.c_void_p, C.c_int64] + err
         lib.edref_execute.argtypes = [C.c_char_p, C.c_int64, C.c_int64, C.c_double, C.c_char_p,
                                       C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_int,
@@ -94,6 +96,19 @@ def ref_plan_json(graph_text: str, p: int, n_machines: int, alpha: float = 0.01,
     if pinned:
         d["pinned"] = pinned
     return d
+
+
+def ref_artifacts(graph_text: str, p: int, n_machines: int, alpha: float = 0.01, pinned=None):
+    """(taskgraph/1, execgraph/1 with machines) as the reference's json_io writes them."""
+    tg, eg = C.c_void_p(), C.c_void_p()
+    err = C.create_string_buffer(1024)
+    pj = json.dumps(pinned).encode() if pinned else None
+    _check(ref().edref_artifacts(graph_text.encode(), p, n_machines, alpha, pj, C.byref(tg), C.byref(eg), err, 1024),
+           err)
+    out = (json.loads(C.cast(tg, C.c_char_p).value.decode()), json.loads(C.cast(eg, C.c_char_p).value.decode()))
+    ref().edref_free(tg)
+    ref().edref_free(eg)
+    return out
 
 
 def ref_generate_input(graph_text: str, seed: int, vid: int, shape) -> np.ndarray:

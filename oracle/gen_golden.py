@@ -86,3 +86,19 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def artifacts():
+    """tests/golden/artifacts/: the reference's own taskgraph/1 + execgraph/1
+    (json_io.cc) for plan-ingestion tests."""
+    out = os.path.join(OUT, "artifacts")
+    os.makedirs(out, exist_ok=True)
+    for name in ["attention_p8_L4", "ffnn_p4_L2", "chain8_pinned_L4", "attn_big_p8_L8", "bmm2_repart_p8_L2"]:
+        doc = json.load(open(os.path.join(ROOT, "plans", name + ".json")))
+        tg, eg = B.ref_artifacts(doc["graph_text"], doc["p"], doc["n_machines"], doc["alpha"], doc.get("pinned"))
+        json.dump(tg, open(os.path.join(out, name + ".taskgraph.json"), "w"))
+        json.dump(eg, open(os.path.join(out, name + ".execgraph.json"), "w"))
+
+
+if __name__ == "__main__" and "--artifacts" in sys.argv:
+    artifacts()

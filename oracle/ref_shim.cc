@@ -201,6 +201,19 @@ int edref_plan(const char* graph_text, int64_t p, int64_t n_machines, double alp
   });
 }
 
+// The reference's own on-disk artifacts for a plan: taskgraph/1
+// (json_io.cc:63-103, what `eindecomp optimize --out` writes) and execgraph/1
+// with machines (json_io.cc:131-155, what `eindecomp place --out` writes).
+int edref_artifacts(const char* graph_text, int64_t p, int64_t n_machines, double alpha,
+                    const char* pinned_json, char** taskgraph, char** execgraph, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    auto g = parse_eingraph(graph_text);
+    auto pipe = make_pipeline(g, p, n_machines, alpha, pinned_json);
+    *taskgraph = dup_string(taskgraph_to_json(pipe.tg).dump());
+    *execgraph = dup_string(execgraph_to_json(pipe.exec, &pipe.placement).dump());
+  });
+}
+
 // Element count of graph vertex vid (so callers can size buffers).
 int64_t edref_vertex_numel(const char* graph_text, int vid) {
   try {

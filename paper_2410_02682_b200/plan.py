@@ -111,6 +111,77 @@ class Plan:
                     obj.get("objective", 0), obj)
 
     @staticmethod
+    def from_reference_artifacts(taskgraph, execgraph, alpha=0.01, n_machines=None) -> "Plan":
+        """Plan ingestion from the reference's own artifacts: taskgraph/1
+        (json_io.cc:63-103, `eindecomp optimize --out`) and execgraph/1 with
+        machines (json_io.cc:131-155, `eindecomp place --out`). Fields the
+        execgraph/1 schema omits are re-derived as explode() sets them
+        (execgraph.cc:150-185): a refinement's consumer/slot from the join
+        that reads it, its owner (the consumer for input-side layers), and
+        every chunk_bound from the task graph's partitions."""
+        if isinstance(taskgraph, (str, bytes)):
+            taskgraph = json.loads(taskgraph)
+        if isinstance(execgraph, (str, bytes)):
+            execgraph = json.loads(execgraph)
+        if taskgraph.get("schema") != "taskgraph/1" or execgraph.get("schema") != "execgraph/1":
+            raise ValueError("expected taskgraph/1 and execgraph/1 documents")
+        names = [jv["id"] for jv in taskgraph["vertices"]]
+        index = {n: i for i, n in enumerate(names)}
+        verts = []
+        for vid, jv in enumerate(taskgraph["vertices"]):
+            je = jv["einsum"]
+            expr = None
+            if je is not None:
+                mp, c = je.get("map"), 0.0
+                if mp is not None and mp.startswith("scale("):
+                    mp, c = "scale", float(mp[6:-1])
+                expr = Expr(je["out"], je["inns"], je.get("join"), mp, c, je.get("agg"))
+            verts.append(Vertex(vid, jv["id"], list(jv["bound"]), [index[n] for n in jv["inputs"]], expr,
+                                list(jv["d"]), list(jv["out_partition"])))
+        kinds = {"input-chunk": 0, "join-kernel": 1, "refinement": 2}
+        raw = execgraph["vertices"]
+        readers = {}
+        for jv in raw:
+            if kinds[jv["kind"]] == 1:
+                for slot, d in enumerate(jv["deps"]):
+                    readers.setdefault(d, (index[jv["vertex"]], slot))
+
+        def project(d, ls, lxy):
+            return [d[lxy.index(l)] for l in ls]
+
+        ex = []
+        for jv in raw:
+            kind = kinds[jv["kind"]]
+            prod = index[jv["vertex"]]
+            v = verts[prod]
+            consumer, slot, owner = -1, -1, prod
+            if kind == 0:
+                cb = [b // d for b, d in zip(v.bound, v.d)]
+            elif kind == 1:
+                e = v.expr
+                lxy = e.xy_labels()
+                bxy = [b for i in v.inputs for b in verts[i].bound]
+                local = [b // d for b, d in zip(bxy, v.d)]
+                cb = project(local, e.out, lxy)
+            else:
+                if jv["id"] in readers:
+                    consumer, slot = readers[jv["id"]]
+                    ce = verts[consumer].expr
+                    part = project(verts[consumer].d, ce.ins[slot], ce.xy_labels())
+                    if v.expr is None:
+                        owner = consumer
+                else:
+                    part = v.out_partition
+                cb = [b // d for b, d in zip(v.bound, part)]
+            ex.append(ExecVertex(jv["id"], kind, owner, prod, consumer, slot, list(jv["key"]), cb, jv["fp"],
+                                 jv["sz"], list(jv["deps"]), jv.get("machine", 0)))
+        if n_machines is None:
+            n_machines = 1 + max((u.machine for u in ex), default=0)
+        outputs = [index[n] for n in taskgraph["outputs"]]
+        return Plan(None, n_machines, alpha, verts, outputs, ex, taskgraph.get("predicted_cost", 0),
+                    {"taskgraph": taskgraph, "execgraph": execgraph})
+
+    @staticmethod
     def load(path) -> "Plan":
         with open(path) as f:
             return Plan.from_json(json.load(f))

@@ -88,3 +88,38 @@ def test_no_device_is_a_loud_error():
     from paper_2410_02682_b200.executor import Context, EdError
     with pytest.raises(EdError):
         Context(0)
+
+
+ARTIFACTS = ["attention_p8_L4", "ffnn_p4_L2", "chain8_pinned_L4", "attn_big_p8_L8", "bmm2_repart_p8_L2"]
+
+
+@pytest.mark.parametrize("name", ARTIFACTS)
+def test_plan_ingestion_from_reference_artifacts(name):
+    """a plan rebuilt from the reference's own on-disk
+    artifacts (taskgraph/1 + execgraph/1 with machines, json_io.cc) equals the
+    plan the executor otherwise receives, field for field."""
+    import json
+    d = os.path.join(ROOT, "tests", "golden", "artifacts")
+    tg = json.load(open(os.path.join(d, name + ".taskgraph.json")))
+    eg = json.load(open(os.path.join(d, name + ".execgraph.json")))
+    want = load_plan(name)
+    got = Plan.from_reference_artifacts(tg, eg, alpha=want.alpha, n_machines=want.n_machines)
+    assert [v.d for v in got.vertices] == [v.d for v in want.vertices]
+    assert got.outputs == want.outputs
+    key = lambda u: (u.kind, u.owner, u.producer, u.consumer, u.slot, u.key, u.chunk_bound, u.fp, u.sz,
+                     u.deps, u.machine)
+    assert [key(u) for u in got.exec] == [key(u) for u in want.exec]
+
+
+@pytest.mark.skipif(not __import__("oracle.bridge", fromlist=["x"]).have_ref(), reason="oracle/_ref not built")
+def test_plan_ingestion_all_plans_live():
+    import json
+    from oracle import bridge as B
+    for path in sorted(glob.glob(os.path.join(PLANS, "*.json")))[::7]:
+        doc = json.load(open(path))
+        tg, eg = B.ref_artifacts(doc["graph_text"], doc["p"], doc["n_machines"], doc["alpha"], doc.get("pinned"))
+        a = Plan.from_json(doc)
+        b = Plan.from_reference_artifacts(tg, eg, alpha=doc["alpha"], n_machines=doc["n_machines"])
+        key = lambda u: (u.kind, u.owner, u.producer, u.consumer, u.slot, u.key, u.chunk_bound, u.fp, u.sz,
+                         u.deps, u.machine)
+        assert [key(u) for u in a.exec] == [key(u) for u in b.exec], path
