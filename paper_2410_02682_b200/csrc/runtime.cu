@@ -17,6 +17,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -29,6 +30,7 @@
 
 #include "ed_gpu.h"
 #include "gemm_sm100.h"
+#include "attn_sm100.h"
 #include "ewise.h"
 #include "kernels.h"
 
@@ -266,13 +268,15 @@ void make_map(CUtensorMap* m, const void* base, bool bf16, int64_t inner, int64_
 }
 
 // ---- schedule -------------------------------------------------------------------
-enum class OpKind { GEMM, GENERIC, REFINE, CORRUPT, SEND, RECV, CONVERT, EWISE, ROWREDUCE, SOFTMAX };
+enum class OpKind { GEMM, GENERIC, REFINE, CORRUPT, SEND, RECV, CONVERT, EWISE, ROWREDUCE, SOFTMAX, FLASH };
 
 struct Op {
   OpKind kind;
   std::string name;   // launch class, e.g. "gemm_bf16:Z1"
   double flops = 0, bytes = 0;
   GemmLaunch gemm{};
+  AttnLaunch attn{};
+  std::vector<AttnRegion> aregions;
   std::vector<int> heads;              // GEMM: region heads (join ids), fold order
   std::vector<CUtensorMap> maps;       // GEMM: host copies, uploaded by allocate()
   std::vector<GemmRegion> regions;
@@ -394,15 +398,24 @@ struct ed_plan_h {
   std::map<int, MemMap> memmap_;                  // einsum -> memory-bound kernel shape
   struct Softmax {
     int y;
+    int x;                                        // the chain's input vertex
     int64_t len;
     std::vector<std::pair<int, int>> pairs;       // (Y join, x chunk ref)
   };
+  struct Flash {                                  // T1 -> softmax -> O in one kernel
+    int t1, y, o;
+    float scale;
+    std::vector<std::array<int, 4>> regions;      // (Q ref, K ref, V ref, O region head)
+  };
+  std::map<int, Flash> flash_;                    // O vertex -> fused attention block
+  std::set<int> flash_skip_;                      // einsums computed inside a Flash op
   std::map<int, Softmax> softmax_;                // Y vertex -> fused row-softmax chain
   std::map<int, std::pair<int, double>> epi_;     // GEMM einsum -> epilogue map (op, c)
   std::vector<char> opaque_;                      // exec id whose value was fused into a consumer
   void* d_joinptrs = nullptr;                     // JoinPtrs[] of grouped memory-bound launches
   void* d_rects = nullptr;                        // RectGroup[] of fast refinements
   void* d_copy_desc = nullptr;                    // BlockCopy[] scratch for upload / download
+  void* d_attn = nullptr;                         // tensor maps + regions of fused attention launches
   size_t copy_desc_bytes = 0;
 
   int rank_of(int id) const { return X[id].machine % ctx->world; }
@@ -793,6 +806,7 @@ void ed_plan_h::build() {
       if (!ok || pairs.empty()) continue;
       Softmax sm;
       sm.y = y;
+      sm.x = xv;
       sm.len = L;
       sm.pairs = pairs;
       softmax_[y] = sm;
@@ -804,12 +818,72 @@ void ed_plan_h::build() {
       memmap_.erase(e);
       memmap_.erase(sg);
     }
+    // (3) attention block: T1 = Q K^T (GEMM, maybe with a fused scale), the
+    // softmax chain on T1 (or its scaled map), O = T3 V (GEMM, K = the row
+    // label) -> one kernel; T1 and T3 are never materialised (bf16 only)
+    for (auto& [yv, sm] : softmax_) {
+      if (!bf16) break;
+      if (readers[yv].size() != 1 || is_output(yv)) continue;
+      const int o = readers[yv][0];
+      if (!gmap.count(o) || V[o].inputs[gmap[o].a_slot] != yv || !all_local(o)) continue;
+      int t1 = sm.x;
+      float scale = 1.0f;
+      if (!gmap.count(t1)) {
+        // x is a map vertex fused into its GEMM's epilogue (T2 = scale(T1))
+        const int u = V[t1].arity == 1 ? V[t1].inputs[0] : -1;
+        if (u < 0 || !epi.count(u) || epi[u].first != ED_MAP_SCALE) continue;
+        scale = float(epi[u].second);
+        t1 = u;
+      } else if (epi.count(t1)) {
+        continue;
+      }
+      if (!gmap.count(t1) || !all_local(t1)) continue;
+      const GemmMap& gs = gmap[t1];
+      const GemmMap& go = gmap[o];
+      const int64_t H = gs.ab.ext, S = gs.am.ext, T = gs.bn.ext, Dd = gs.ak.ext;
+      if (gs.a_mn || gs.b_mn || !go.b_mn || go.a_mn || go.ab.ext != H || go.am.ext != S || go.ak.ext != T ||
+          go.bn.ext != Dd || T != sm.len || !attn_supported(int(S), int(T), int(Dd)))
+        continue;
+      // region correspondence: O region <- T3 chunk <- T1 region (single siblings)
+      std::map<int, int> t1_of_y;
+      for (auto& [yj, xr] : sm.pairs) t1_of_y[yj] = owner[xr];
+      Flash f{t1, yv, o, scale, {}};
+      bool ok = true;
+      for (int oh = 0; oh < ne && ok; ++oh) {
+        if (!fused_head[oh] || X[oh].producer != o) continue;
+        ok = region_sibs[oh].size() == 1;
+        const int yj = owner[X[oh].deps[go.a_slot]];
+        auto it = t1_of_y.find(yj);
+        ok = ok && it != t1_of_y.end();
+        if (!ok) break;
+        const int th = it->second;
+        ok = fused_head[th] && X[th].producer == t1 && region_sibs[th].size() == 1;
+        if (!ok) break;
+        f.regions.push_back({X[th].deps[gs.a_slot], X[th].deps[gs.b_slot], X[oh].deps[go.b_slot], oh});
+      }
+      if (!ok || f.regions.empty()) continue;
+      flash_[o] = f;
+      flash_skip_.insert(t1);
+      flash_skip_.insert(yv);
+      flash_skip_.insert(o);
+      // T1's regions/refinements and T3's joins/refinements are never materialised
+      for (int id = 0; id < ne; ++id) {
+        const int w = X[id].producer;
+        if ((w == t1 || w == yv) && X[id].kind != ED_EXEC_INPUT_CHUNK) virt[id] = 1;
+      }
+    }
   }
 
   // ---- buffer needs ----
   for (int id = 0; id < ne; ++id) {
     if (!local[id] || virt[id] || virtual_join_src.count(id)) continue;
     const Ex& u = X[id];
+    if (u.kind == ED_EXEC_JOIN && flash_.count(u.producer)) {
+      for (auto& r : flash_[u.producer].regions)
+        if (r[3] == id)
+          for (int k = 0; k < 3; ++k) buf[local[r[k]] ? owner[r[k]] : r[k]].need_16 = true;
+      continue;
+    }
     if (u.kind == ED_EXEC_JOIN && softmax_.count(u.producer)) {
       for (auto& [yj, xr] : softmax_[u.producer].pairs)
         if (yj == id) buf[owner[xr]].need_main = true;
@@ -909,6 +983,20 @@ void ed_plan_h::build() {
         ops.push_back(op);
         continue;
       }
+      if (flash_.count(u.producer)) {
+        if (!fused_head[id] || gemm_emitted.count(u.producer)) continue;
+        gemm_emitted.insert(u.producer);
+        const Flash& f = flash_.at(u.producer);
+        Op op{OpKind::FLASH};
+        op.name = "attention_fused:" + V[f.t1].name + ".." + w.name;
+        op.ptr = reinterpret_cast<void*>(id);
+        for (auto& r : f.regions) op.heads.push_back(r[3]);
+        for (int h = 0; h < ne; ++h)
+          if (X[h].kind == ED_EXEC_JOIN && (X[h].producer == f.t1 || X[h].producer == f.o))
+            op.flops += 2.0 * double(X[h].fp);
+        ops.push_back(op);
+        continue;
+      }
       if (gmap.count(u.producer)) {
         if (!fused_head[id] || gemm_emitted.count(u.producer)) continue;
         gemm_emitted.insert(u.producer);
@@ -957,7 +1045,7 @@ void ed_plan_h::build() {
     size_t at = 0;
     for (size_t i = 0; i < ops.size(); ++i)
       if (((ops[i].kind == OpKind::GEMM || ops[i].kind == OpKind::EWISE || ops[i].kind == OpKind::ROWREDUCE ||
-            ops[i].kind == OpKind::SOFTMAX) &&
+            ops[i].kind == OpKind::SOFTMAX || ops[i].kind == OpKind::FLASH) &&
            std::count(ops[i].heads.begin(), ops[i].heads.end(), owner[first_join])) ||
           (ops[i].kind == OpKind::GENERIC && reinterpret_cast<intptr_t>(ops[i].ptr) == owner[first_join])) {
         at = i + 1;
@@ -1010,6 +1098,7 @@ void ed_plan_h::allocate() {
 
   auto resolve = [&](int dep) { return local[dep] ? owner[dep] : dep; };
   size_t gemm_maps_total = 0, gemm_regions_total = 0, jptrs_total = 0, rect_total = 0;
+  size_t attn_maps_total = 0, attn_regions_total = 0;
   for (auto& op : ops) {
     const int id = int(reinterpret_cast<intptr_t>(op.ptr));
     switch (op.kind) {
@@ -1253,6 +1342,60 @@ void ed_plan_h::allocate() {
         op.gen.out16 = buf[id].b16;
         op.gen.n_out = X[id].sz;
         break;
+      case OpKind::FLASH: {
+        const Flash& f = flash_.at(X[id].producer);
+        const GemmMap& gs = gmap_.at(f.t1);
+        const GemmMap& go = gmap_.at(f.o);
+        AttnLaunch& a = op.attn;
+        a.H = int(gs.ab.ext);
+        a.S = int(gs.am.ext);
+        a.T = int(gs.bn.ext);
+        a.D = int(gs.ak.ext);
+        a.scale = f.scale;
+        op.maps.clear();
+        op.aregions.clear();
+        for (auto& r : f.regions) {
+          AttnRegion ar{};
+          const void* q = buf[resolve(r[0])].b16;
+          const void* k = buf[resolve(r[1])].b16;
+          const void* v = buf[resolve(r[2])].b16;
+          if (!q || !k || !v) throw ed_error(ED_ERR_PLAN, "attention operand buffer missing");
+          CUtensorMap m;
+          make_map(&m, q, true, gs.ak.ext, gs.am.ext, gs.am.stride, gs.ab.ext, gs.ab.stride, 64, 128);
+          ar.q = int(op.maps.size());
+          op.maps.push_back(m);
+          make_map(&m, k, true, gs.bk.ext, gs.bn.ext, gs.bn.stride, gs.bb.ext, gs.bb.stride, 64, 128);
+          ar.k = int(op.maps.size());
+          op.maps.push_back(m);
+          make_map(&m, v, true, go.bn.ext, go.bk.ext, go.bk.stride, go.bb.ext, go.bb.stride, 64, 128);
+          ar.v = int(op.maps.size());
+          op.maps.push_back(m);
+          auto out_map = [&](void* base, bool o16) {
+            const int oes = o16 ? 2 : 4;
+            bool ok = base && (go.cm.ext == 1 || (go.cm.stride * oes) % 16 == 0) &&
+                      (go.cb.ext == 1 || (go.cb.stride * oes) % 16 == 0);
+            if (!ok) return -1;
+            CUtensorMap mc;
+            make_map(&mc, base, o16, go.bn.ext, go.am.ext, go.cm.stride, go.ab.ext, go.cb.stride, o16 ? 64u : 32u,
+                     uint32_t(kStoreRows));
+            op.maps.push_back(mc);
+            return int(op.maps.size()) - 1;
+          };
+          ar.o32 = out_map(buf[r[3]].main, false);
+          ar.o16 = out_map(buf[r[3]].b16, true);
+          if ((buf[r[3]].main && ar.o32 < 0) || (buf[r[3]].b16 && ar.o16 < 0))
+            throw ed_error(ED_ERR_UNSUPPORTED, "attention output not 16-byte aligned");
+          op.aregions.push_back(ar);
+        }
+        a.n_regions = int(op.aregions.size());
+        op.bytes = 0;
+        for (auto& r : f.regions)
+          op.bytes += double(X[r[0]].sz + X[r[1]].sz + X[r[2]].sz) * 2 + double(X[r[3]].sz) * (buf[r[3]].main ? 4 : 0) +
+                      double(X[r[3]].sz) * (buf[r[3]].b16 ? 2 : 0);
+        attn_maps_total += op.maps.size();
+        attn_regions_total += op.aregions.size();
+        break;
+      }
       case OpKind::SOFTMAX: {
         const Softmax& sm = softmax_.at(X[id].producer);
         op.jptrs.clear();
@@ -1314,6 +1457,22 @@ void ed_plan_h::allocate() {
       }
     }
   }
+  if (attn_maps_total) {
+    CUDA_OK(cudaMalloc(&d_attn, sizeof(CUtensorMap) * attn_maps_total + sizeof(AttnRegion) * attn_regions_total));
+    size_t mo = 0, ro = 0;
+    CUtensorMap* maps = static_cast<CUtensorMap*>(d_attn);
+    AttnRegion* regs = reinterpret_cast<AttnRegion*>(maps + attn_maps_total);
+    for (auto& op : ops) {
+      if (op.kind != OpKind::FLASH) continue;
+      CUDA_OK(cudaMemcpy(maps + mo, op.maps.data(), sizeof(CUtensorMap) * op.maps.size(), cudaMemcpyHostToDevice));
+      CUDA_OK(cudaMemcpy(regs + ro, op.aregions.data(), sizeof(AttnRegion) * op.aregions.size(),
+                         cudaMemcpyHostToDevice));
+      op.attn.maps = maps + mo;
+      op.attn.regions = regs + ro;
+      mo += op.maps.size();
+      ro += op.aregions.size();
+    }
+  }
   if (rect_total) {
     CUDA_OK(cudaMalloc(&d_rects, sizeof(RectGroup) * rect_total));
     size_t o = 0;
@@ -1370,6 +1529,7 @@ void ed_plan_h::launch_op(size_t i, cudaStream_t s) {
     case OpKind::EWISE:
       CUDA_OK(launch_ewise(op.ew, int(op.jptrs.size()), f64, opt.precision == ED_PREC_FP32, s));
       break;
+    case OpKind::FLASH: CUDA_OK(launch_attn(op.attn, ctx->num_sms, s)); break;
     case OpKind::SOFTMAX: CUDA_OK(launch_softmax(op.sm, int(op.jptrs.size()), s)); break;
     case OpKind::ROWREDUCE:
       CUDA_OK(launch_rowreduce(op.rr, int(op.jptrs.size()), f64, opt.precision == ED_PREC_FP32, s));
@@ -1386,6 +1546,7 @@ void ed_plan_h::launch_op(size_t i, cudaStream_t s) {
 
 void ed_plan_h::record() {
   CUDA_OK(gemm_prepare());
+  CUDA_OK(attn_prepare());
   CUDA_OK(cudaEventCreate(&ev0));
   CUDA_OK(cudaEventCreate(&ev1));
   if (opt.no_graph || opt.profile) return;
@@ -1415,6 +1576,7 @@ void ed_plan_h::destroy() {
   if (d_joinptrs) cudaFree(d_joinptrs);
   if (d_rects) cudaFree(d_rects);
   if (d_copy_desc) cudaFree(d_copy_desc);
+  if (d_attn) cudaFree(d_attn);
   if (d_regions) cudaFree(d_regions);
   if (d_ptrs) cudaFree(d_ptrs);
   if (d_err) cudaFree(d_err);

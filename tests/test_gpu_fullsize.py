@@ -180,7 +180,7 @@ def _op_fp64(plan, v, args, torch):
 PER_VERTEX_BOUND = 2e-2  # max|got - want| / max|want|, bf16 operands, fp32 accumulation
 
 
-@pytest.mark.parametrize("name", ["ffnn_big", "attn_big", "chain3"])
+@pytest.mark.parametrize("name", ["ffnn_big", "attn_big", "chain3", "attn_s"])
 def test_per_vertex_full_size(gpu_ctx, name):
     """Per-vertex parity at full size: every materialised vertex
     against fp64 evaluated on the GPU's OWN inputs to it, so conditioning of
@@ -218,3 +218,22 @@ def test_per_vertex_full_size(gpu_ctx, name):
         checked += 1
     pp.close()
     assert checked >= 3
+
+
+@pytest.mark.parametrize("name", ["attn_big", "attn_s"])
+def test_attention_block_runs_fused(gpu_ctx, name):
+    """The T1 -> scale -> softmax -> O chain runs as one fused kernel (bf16),
+    and the logits are never materialised."""
+    from paper_2410_02682_b200.executor import PreparedPlan, EdError
+    plan = load_plan(f"{name}_p8_L1")
+    pp = PreparedPlan(gpu_ctx, plan, precision="bf16", profile=True)
+    pp.upload(_inputs(plan))
+    pp.run()
+    names = [k["name"] for k in pp.kernel_stats()]
+    assert any(n.startswith("attention_fused") for n in names), names
+    assert not any(n.startswith("softmax_rows") for n in names), names
+    t1 = plan.find("T1")
+    ref = next(u.id for u in plan.exec if u.kind == 2 and u.producer == t1)
+    with pytest.raises(EdError):
+        pp.download_chunk(ref)
+    pp.close()
