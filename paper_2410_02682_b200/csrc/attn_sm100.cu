@@ -8,9 +8,11 @@
 // P_j = exp(c*S_j - m) / l as bf16 into 128B-swizzled smem and accumulates
 // O += P_j V_j in TMEM. No O rescaling is ever needed.
 //
-// Warp roles (192 threads): warp 0 TMA producer, warp 1 TMEM allocator and
-// single-thread MMA issuer, warps 2-5 softmax (thread = row) and epilogue
-// (TMEM -> swizzled smem -> TMA store, reusing the P buffers).
+// Warp roles (320 threads): warp 0 TMA producer, warp 1 TMEM allocator and
+// single-thread MMA issuer, warps 2-9 softmax and epilogue: two warps per
+// TMEM lane quarter, each owning half of every key block's columns (row
+// statistics merged once per job through smem); the epilogue goes TMEM ->
+// swizzled smem (the warp's own rows of the P buffers) -> TMA store.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -23,7 +25,8 @@ namespace {
 
 constexpr int BQ = 128;   // query rows per job (TMEM lanes)
 constexpr int BKV = 128;  // keys per block
-constexpr int kThreads = 192;
+constexpr int kThreads = 320;
+constexpr int kSoftmaxWarps = 8;
 
 template <int D>
 struct ACfg {
@@ -32,7 +35,7 @@ struct ACfg {
   static constexpr int V_BYTES = BKV * D * 2;  // D/64 MN atoms of 128 key-rows x 128 B
   static constexpr int P_BYTES = BQ * BKV * 2; // 2 K-chunks of 16 KiB
   static constexpr int STAGE = K_BYTES + V_BYTES;
-  static constexpr int SMEM = Q_BYTES + 2 * STAGE + 2 * P_BYTES + 1024 + 512;
+  static constexpr int SMEM = Q_BYTES + 2 * STAGE + 2 * P_BYTES + 1024 + 256;
   static constexpr int S_COL = 0;               // TMEM columns: S0 [0,128), S1 [128,256), O [256, 256+D)
   static constexpr int O_COL = 2 * BKV;
 };
@@ -83,12 +86,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 4);
-      mbar_init(&p_full[i], 4);
+      mbar_init(&s_empty[i], kSoftmaxWarps);
+      mbar_init(&p_full[i], kSoftmaxWarps);
       mbar_init(&p_empty[i], 1);
     }
     mbar_init(o_full, 1);
-    mbar_init(o_empty, 4);
+    mbar_init(o_empty, kSoftmaxWarps);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -190,98 +193,115 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
       }
     }
   } else {
-    // ---------------- softmax + epilogue (thread = query row) ----------------
-    const int wq = warp & 3;
+    // ---------------- softmax + epilogue ----------------
+    // warp w: TMEM lane quarter w % 4 (its rows), column half (w - 2) / 4
+    const int wq = warp & 3, half = (warp - 2) / 4;
     const int r = wq * 32 + lane;
     const uint32_t lane_base = uint32_t(wq * 32) << 16;
     const float sc2 = p.scale * 1.4426950408889634f;  // c * log2(e)
+    auto ex2 = [](float x) {
+      float y;
+      asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+      return y;
+    };
     int sc = 0, pc = 0, local = 0;
     for (int jb = blockIdx.x; jb < jobs; jb += gridDim.x, ++local) {
       const Job J = job_of(p, jb);
       const AttnRegion R = p.regions[J.region];
       float m = -INFINITY, l = 0.f;
-      // pass 1: running max and sum (log2 domain)
+      // pass 1: running max and sum over this warp's 64 columns (log2 domain)
       for (int j = 0; j < nb; ++j, ++sc) {
         const int sb = sc & 1;
         mbar_wait(&s_full[sb], (sc >> 1) & 1);
         tc_fence_after();
-#pragma unroll
-        for (int c = 0; c < BKV / 32; ++c) {
-          uint32_t v[32];
-          tmem_ld_32x32b_x32(tmem + lane_base + uint32_t(C_::S_COL + sb * BKV + c * 32), v);
-          tmem_ld_wait();
-          float mx = m;
-#pragma unroll
-          for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(v[e]) * sc2);
-          float acc = 0.f;
-#pragma unroll
-          for (int e = 0; e < 32; ++e) acc += exp2f(__uint_as_float(v[e]) * sc2 - mx);
-          l = l * exp2f(m - mx) + acc;
-          m = mx;
-        }
+        uint32_t v[64];
+        const uint32_t col = uint32_t(C_::S_COL + sb * BKV + half * 64);
+        tmem_ld_32x32b_x32(tmem + lane_base + col, *reinterpret_cast<uint32_t(*)[32]>(v));
+        tmem_ld_32x32b_x32(tmem + lane_base + col + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+        tmem_ld_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&s_empty[sb]);
+        float mx = m;
+#pragma unroll
+        for (int e = 0; e < 64; ++e) mx = fmaxf(mx, __uint_as_float(v[e]) * sc2);
+        float acc = 0.f;
+#pragma unroll
+        for (int e = 0; e < 64; ++e) acc += ex2(fmaf(__uint_as_float(v[e]), sc2, -mx));
+        l = l * ex2(m - mx) + acc;
+        m = mx;
       }
-      const float inv_l = 1.0f / l;
       // my rows of the P buffers were staging for the last epilogue's stores
       if (lane == 0) bulk_wait_read<0>();
       __syncwarp();
-      // pass 2: P = exp2(c*log2e*S - m) / l  -> bf16, 128B-swizzled K-major
+      // merge the two halves' row statistics through this warp's own rows of
+      // P buffer 0 (every warp has drained its stores before the barrier)
+      {
+        float* mine = reinterpret_cast<float*>(sP + half * 16384 + wq * 4096);
+        const float* other = reinterpret_cast<const float*>(sP + (half ^ 1) * 16384 + wq * 4096);
+        mine[lane] = m;
+        mine[32 + lane] = l;
+        asm volatile("bar.sync 1, %0;" ::"n"(kSoftmaxWarps * 32) : "memory");
+        const float m2 = other[lane], l2 = other[32 + lane];
+        asm volatile("bar.sync 1, %0;" ::"n"(kSoftmaxWarps * 32) : "memory");
+        const float M = fmaxf(m, m2);
+        l = l * ex2(m - M) + l2 * ex2(m2 - M);
+        m = M;
+      }
+      const float inv_l = 1.0f / l;
+      // pass 2: P = exp2(c*log2e*S - m) / l -> bf16 into K-chunk `half`
       for (int j = 0; j < nb; ++j, ++sc, ++pc) {
         const int sb = sc & 1, pb = pc & 1;
         mbar_wait(&s_full[sb], (sc >> 1) & 1);
-        mbar_wait(&p_empty[pb], ((pc >> 1) & 1) ^ 1);
         tc_fence_after();
-        uint8_t* prow = sP + pb * C_::P_BYTES + r * 128;
-#pragma unroll
-        for (int c = 0; c < BKV / 32; ++c) {
-          uint32_t v[32];
-          tmem_ld_32x32b_x32(tmem + lane_base + uint32_t(C_::S_COL + sb * BKV + c * 32), v);
-          tmem_ld_wait();
-          uint8_t* chunk = prow + (c / 2) * 16384;
-#pragma unroll
-          for (int g = 0; g < 4; ++g) {
-            uint32_t w[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const float a = exp2f(__uint_as_float(v[8 * g + 2 * q]) * sc2 - m) * inv_l;
-              const float b = exp2f(__uint_as_float(v[8 * g + 2 * q + 1]) * sc2 - m) * inv_l;
-              __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
-              w[q] = *reinterpret_cast<uint32_t*>(&h2);
-            }
-            const int gran = (c % 2) * 4 + g;
-            *reinterpret_cast<uint4*>(chunk + ((gran ^ (r & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
-          }
-        }
-        fence_proxy_async_smem();
+        uint32_t v[64];
+        const uint32_t col = uint32_t(C_::S_COL + sb * BKV + half * 64);
+        tmem_ld_32x32b_x32(tmem + lane_base + col, *reinterpret_cast<uint32_t(*)[32]>(v));
+        tmem_ld_32x32b_x32(tmem + lane_base + col + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+        tmem_ld_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&s_empty[sb]);
-          mbar_arrive(&p_full[pb]);
+        if (lane == 0) mbar_arrive(&s_empty[sb]);
+        uint32_t w[32];
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          const float a = ex2(fmaf(__uint_as_float(v[2 * q]), sc2, -m)) * inv_l;
+          const float b = ex2(fmaf(__uint_as_float(v[2 * q + 1]), sc2, -m)) * inv_l;
+          __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
+          w[q] = *reinterpret_cast<uint32_t*>(&h2);
         }
+        mbar_wait(&p_empty[pb], ((pc >> 1) & 1) ^ 1);
+        uint8_t* prow = sP + pb * C_::P_BYTES + half * 16384 + r * 128;
+#pragma unroll
+        for (int g = 0; g < 8; ++g)
+          *reinterpret_cast<uint4*>(prow + ((g ^ (r & 7)) << 4)) =
+              make_uint4(w[4 * g], w[4 * g + 1], w[4 * g + 2], w[4 * g + 3]);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[pb]);
       }
-      // epilogue: O rows -> swizzled staging (this warp's rows of the P
-      // buffers, free once every P V MMA of the job has completed) -> TMA
+      // epilogue: this warp's half of O's columns -> staging in its own rows
+      // of its own P K-chunk (free once every P V MMA of the job completed)
       mbar_wait(o_full, local & 1);
       tc_fence_after();
-      uint8_t* tiles[4] = {sP + wq * 4096, sP + 16384 + wq * 4096, sP + C_::P_BYTES + wq * 4096,
-                           sP + C_::P_BYTES + 16384 + wq * 4096};
+      uint8_t* tiles[2] = {sP + half * 16384 + wq * 4096, sP + C_::P_BYTES + half * 16384 + wq * 4096};
       int t_used = 0;
       for (int pass = 0; pass < 2; ++pass) {
         const int cm = pass == 0 ? R.o32 : R.o16;
         if (cm < 0) continue;
         const int cols = pass == 0 ? 32 : 64;
+        const int per_half = (D / cols + 1) / 2;
 #pragma unroll 1
-        for (int c = 0; c < D / cols; ++c) {
+        for (int ci = 0; ci < per_half; ++ci) {
+          const int c = half * per_half + ci;
+          if (c * cols >= D) break;
           uint32_t v[64];
           tmem_ld_32x32b_x32(tmem + lane_base + uint32_t(C_::O_COL + c * cols), *reinterpret_cast<uint32_t(*)[32]>(v));
           if (pass == 1)
             tmem_ld_32x32b_x32(tmem + lane_base + uint32_t(C_::O_COL + c * cols + 32),
                                *reinterpret_cast<uint32_t(*)[32]>(v + 32));
           tmem_ld_wait();
-          if (t_used == 4) {  // recycle staging tiles
+          if (t_used == 2) {  // recycle staging tiles
             if (lane == 0) bulk_wait_read<0>();
             __syncwarp();
             t_used = 0;
