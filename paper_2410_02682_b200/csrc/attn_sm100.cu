@@ -3,10 +3,12 @@
 // kernel per (region, head, 128-row tile), so the [h, s, s2] logits and
 // probabilities never reach HBM.
 //
-// Per job: S_j = Q K_j^T (128 x 128 keys, TMEM), two passes over the key
-// blocks: pass 1 keeps the running row max / sum, pass 2 writes
-// P_j = exp(c*S_j - m) / l as bf16 into 128B-swizzled smem and accumulates
-// O += P_j V_j in TMEM. No O rescaling is ever needed.
+// Per job: for each key block j, S_j = Q K_j^T (128 x 128 keys, TMEM); each
+// column half h of the block keeps its own running reference max m_h and
+// accumulates O_h += exp2(c*log2e*S_j - m_h) V_j in its own TMEM
+// accumulator. A row's O_h is rescaled (TMEM read-modify-write) only when its
+// max grows by more than 2^8, so P stays in bf16 range without a second
+// pass. The halves merge in the epilogue: O = (O_0 2^(m_0-M) + O_1 2^(m_1-M)) / L.
 //
 // Warp roles (320 threads): warp 0 TMA producer, warp 1 TMEM allocator and
 // single-thread MMA issuer, warps 2-9 softmax and epilogue: two warps per
@@ -36,8 +38,8 @@ struct ACfg {
   static constexpr int P_BYTES = BQ * BKV * 2; // 2 K-chunks of 16 KiB
   static constexpr int STAGE = K_BYTES + V_BYTES;
   static constexpr int SMEM = Q_BYTES + 2 * STAGE + 2 * P_BYTES + 1024 + 256;
-  static constexpr int S_COL = 0;               // TMEM columns: S0 [0,128), S1 [128,256), O [256, 256+D)
-  static constexpr int O_COL = 2 * BKV;
+  static constexpr int S_COL = 0;               // TMEM columns: S0 [0,128), S1 [128,256),
+  static constexpr int O_COL = 2 * BKV;         // O_0 [256, 256+D), O_1 [256+D, 256+2D)
 };
 
 struct Job {
@@ -69,11 +71,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
   uint64_t* kv_empty = bar + 4;   // [2]
   uint64_t* s_full = bar + 6;     // [2]
   uint64_t* s_empty = bar + 8;    // [2]
-  uint64_t* p_full = bar + 10;    // [2]
-  uint64_t* p_empty = bar + 12;   // [2]
-  uint64_t* o_full = bar + 14;
-  uint64_t* o_empty = bar + 15;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
+  uint64_t* p_full = bar + 10;    // [buffer][half]
+  uint64_t* p_empty = bar + 14;   // [buffer][half]
+  uint64_t* o_full = bar + 18;
+  uint64_t* o_empty = bar + 19;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 20);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int nb = p.T / BKV;
@@ -87,7 +89,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
       mbar_init(&kv_empty[i], 1);
       mbar_init(&s_full[i], 1);
       mbar_init(&s_empty[i], kSoftmaxWarps);
-      mbar_init(&p_full[i], kSoftmaxWarps);
+    }
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&p_full[i], kSoftmaxWarps / 2);
       mbar_init(&p_empty[i], 1);
     }
     mbar_init(o_full, 1);
@@ -114,21 +118,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         mbar_expect_tx(q_full, C_::Q_BYTES);
 #pragma unroll
         for (int c = 0; c < D / 64; ++c) tma_load_3d(sQ + c * 16384, mq, q_full, c * 64, J.s0, J.h);
-        for (int pass = 0; pass < 2; ++pass) {
-          for (int j = 0; j < nb; ++j, ++it) {
-            const int st = it & 1;
-            mbar_wait(&kv_empty[st], ((it >> 1) & 1) ^ 1);
-            uint8_t* sk = sKV + st * C_::STAGE;
-            uint8_t* sv = sk + C_::K_BYTES;
-            mbar_expect_tx(&kv_full[st], pass == 0 ? C_::K_BYTES : C_::STAGE);
+        for (int j = 0; j < nb; ++j, ++it) {
+          const int st = it & 1;
+          mbar_wait(&kv_empty[st], ((it >> 1) & 1) ^ 1);
+          uint8_t* sk = sKV + st * C_::STAGE;
+          uint8_t* sv = sk + C_::K_BYTES;
+          mbar_expect_tx(&kv_full[st], C_::STAGE);
 #pragma unroll
-            for (int c = 0; c < D / 64; ++c) tma_load_3d(sk + c * 16384, mk, &kv_full[st], c * 64, j * BKV, J.h);
-            if (pass == 1) {
+          for (int c = 0; c < D / 64; ++c) tma_load_3d(sk + c * 16384, mk, &kv_full[st], c * 64, j * BKV, J.h);
 #pragma unroll
-              for (int a = 0; a < D / 64; ++a)
-                tma_load_3d(sv + a * (BKV * 128), mv, &kv_full[st], a * 64, j * BKV, J.h);
-            }
-          }
+          for (int a = 0; a < D / 64; ++a) tma_load_3d(sv + a * (BKV * 128), mv, &kv_full[st], a * 64, j * BKV, J.h);
         }
       }
     }
@@ -155,14 +154,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
       };
       for (int jb = blockIdx.x; jb < jobs; jb += gridDim.x, ++local) {
         mbar_wait(q_full, local & 1);
-        tc_fence_after();
-        // pass 1: scores for the row statistics
-        for (int j = 0; j < nb; ++j, ++it) {
-          issue_s(it & 1);
-          mma_commit(&kv_empty[it & 1]);
-        }
-        // pass 2: scores again, then O += P V
-        mbar_wait(o_empty, (local & 1) ^ 1);
+        mbar_wait(o_empty, (local & 1) ^ 1);  // the last job's epilogue drained O_0, O_1
         tc_fence_after();
         const int it0 = it;
         issue_s(it0 & 1);
@@ -173,18 +165,20 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             issue_s(st ^ 1);
           }
           const int pb = pc & 1;
-          mbar_wait(&p_full[pb], (pc >> 1) & 1);
-          tc_fence_after();
           const uint32_t pa = smem_u32(sP + pb * C_::P_BYTES);
           const uint32_t va = smem_u32(sKV + st * C_::STAGE + C_::K_BYTES);
+          for (int h = 0; h < 2; ++h) {  // O_h += P_h V_h over the 64 keys of half h
+            mbar_wait(&p_full[pb * 2 + h], (pc >> 1) & 1);
+            tc_fence_after();
 #pragma unroll
-          for (int k = 0; k < BKV / 16; ++k) {
-            const uint64_t ad = umma_desc_sw128(pa + (k / 4) * 16384 + (k % 4) * 32, 16, 1024);
-            const uint64_t bd = umma_desc_sw128(va + k * 2048, BKV * 128, 1024);
-            mma_f16(tmem + C_::O_COL, ad, bd, idesc_o, (j | k) != 0);
+            for (int k = 0; k < 4; ++k) {
+              const uint64_t ad = umma_desc_sw128(pa + h * 16384 + k * 32, 16, 1024);
+              const uint64_t bd = umma_desc_sw128(va + (h * 4 + k) * 2048, BKV * 128, 1024);
+              mma_f16(tmem + C_::O_COL + h * D, ad, bd, idesc_o, (j | k) != 0);
+            }
+            mma_commit(&p_empty[pb * 2 + h]);
           }
           mma_commit(&kv_empty[st]);
-          mma_commit(&p_empty[pb]);
           ++pc;
         }
         it = it0 + nb;
@@ -204,52 +198,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
       asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
       return y;
     };
+    const uint32_t o_col = uint32_t(C_::O_COL + half * D);
     int sc = 0, pc = 0, local = 0;
     for (int jb = blockIdx.x; jb < jobs; jb += gridDim.x, ++local) {
       const Job J = job_of(p, jb);
       const AttnRegion R = p.regions[J.region];
-      float m = -INFINITY, l = 0.f;
-      // pass 1: running max and sum over this warp's 64 columns (log2 domain)
-      for (int j = 0; j < nb; ++j, ++sc) {
-        const int sb = sc & 1;
-        mbar_wait(&s_full[sb], (sc >> 1) & 1);
-        tc_fence_after();
-        uint32_t v[64];
-        const uint32_t col = uint32_t(C_::S_COL + sb * BKV + half * 64);
-        tmem_ld_32x32b_x32(tmem + lane_base + col, *reinterpret_cast<uint32_t(*)[32]>(v));
-        tmem_ld_32x32b_x32(tmem + lane_base + col + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
-        tmem_ld_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&s_empty[sb]);
-        float mx = m;
-#pragma unroll
-        for (int e = 0; e < 64; ++e) mx = fmaxf(mx, __uint_as_float(v[e]) * sc2);
-        float acc = 0.f;
-#pragma unroll
-        for (int e = 0; e < 64; ++e) acc += ex2(fmaf(__uint_as_float(v[e]), sc2, -mx));
-        l = l * ex2(m - mx) + acc;
-        m = mx;
-      }
+      float m = -INFINITY, l = 0.f;  // this half's reference max (log2 domain) and sum
       // my rows of the P buffers were staging for the last epilogue's stores
       if (lane == 0) bulk_wait_read<0>();
       __syncwarp();
-      // merge the two halves' row statistics through this warp's own rows of
-      // P buffer 0 (every warp has drained its stores before the barrier)
-      {
-        float* mine = reinterpret_cast<float*>(sP + half * 16384 + wq * 4096);
-        const float* other = reinterpret_cast<const float*>(sP + (half ^ 1) * 16384 + wq * 4096);
-        mine[lane] = m;
-        mine[32 + lane] = l;
-        asm volatile("bar.sync 1, %0;" ::"n"(kSoftmaxWarps * 32) : "memory");
-        const float m2 = other[lane], l2 = other[32 + lane];
-        asm volatile("bar.sync 1, %0;" ::"n"(kSoftmaxWarps * 32) : "memory");
-        const float M = fmaxf(m, m2);
-        l = l * ex2(m - M) + l2 * ex2(m2 - M);
-        m = M;
-      }
-      const float inv_l = 1.0f / l;
-      // pass 2: P = exp2(c*log2e*S - m) / l -> bf16 into K-chunk `half`
       for (int j = 0; j < nb; ++j, ++sc, ++pc) {
         const int sb = sc & 1, pb = pc & 1;
         mbar_wait(&s_full[sb], (sc >> 1) & 1);
@@ -262,28 +219,75 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&s_empty[sb]);
+        float mx = -INFINITY;
+#pragma unroll
+        for (int e = 0; e < 64; ++e) mx = fmaxf(mx, __uint_as_float(v[e]) * sc2);
+        if (j == 0) {
+          m = mx;
+        } else {
+          const bool grow = mx > m + 8.0f;
+          if (__any_sync(0xffffffffu, grow)) {
+            // rescale this half's O rows once every earlier P V MMA is done
+            const int pq = pc - 1;
+            mbar_wait(&p_empty[(pq & 1) * 2 + half], (pq >> 1) & 1);
+            tc_fence_after();
+            const float f = grow ? ex2(m - mx) : 1.0f;
+#pragma unroll 1
+            for (int c = 0; c < D / 32; ++c) {
+              uint32_t o[32];
+              tmem_ld_32x32b_x32(tmem + lane_base + o_col + uint32_t(c * 32), o);
+              tmem_ld_wait();
+#pragma unroll
+              for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * f);
+              tmem_st_32x32b_x32(tmem + lane_base + o_col + uint32_t(c * 32), o);
+            }
+            tmem_st_wait();
+            l *= f;
+            if (grow) m = mx;
+          }
+        }
         uint32_t w[32];
+        float acc = 0.f;
 #pragma unroll
         for (int q = 0; q < 32; ++q) {
-          const float a = ex2(fmaf(__uint_as_float(v[2 * q]), sc2, -m)) * inv_l;
-          const float b = ex2(fmaf(__uint_as_float(v[2 * q + 1]), sc2, -m)) * inv_l;
+          const float a = ex2(fmaf(__uint_as_float(v[2 * q]), sc2, -m));
+          const float b = ex2(fmaf(__uint_as_float(v[2 * q + 1]), sc2, -m));
+          acc += a + b;
           __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
           w[q] = *reinterpret_cast<uint32_t*>(&h2);
         }
-        mbar_wait(&p_empty[pb], ((pc >> 1) & 1) ^ 1);
+        l += acc;
+        mbar_wait(&p_empty[pb * 2 + half], ((pc >> 1) & 1) ^ 1);
         uint8_t* prow = sP + pb * C_::P_BYTES + half * 16384 + r * 128;
 #pragma unroll
         for (int g = 0; g < 8; ++g)
           *reinterpret_cast<uint4*>(prow + ((g ^ (r & 7)) << 4)) =
               make_uint4(w[4 * g], w[4 * g + 1], w[4 * g + 2], w[4 * g + 3]);
         fence_proxy_async_smem();
+        tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[pb]);
+        if (lane == 0) mbar_arrive(&p_full[pb * 2 + half]);
       }
-      // epilogue: this warp's half of O's columns -> staging in its own rows
-      // of its own P K-chunk (free once every P V MMA of the job completed)
+      // merge the halves' statistics through this warp's own rows of P buffer 0
       mbar_wait(o_full, local & 1);
       tc_fence_after();
+      float f_own, f_other;
+      {
+        float* mine = reinterpret_cast<float*>(sP + half * 16384 + wq * 4096);
+        const float* other = reinterpret_cast<const float*>(sP + (half ^ 1) * 16384 + wq * 4096);
+        mine[lane] = m;
+        mine[32 + lane] = l;
+        asm volatile("bar.sync 1, %0;" ::"n"(kSoftmaxWarps * 32) : "memory");
+        const float m2 = other[lane], l2 = other[32 + lane];
+        asm volatile("bar.sync 1, %0;" ::"n"(kSoftmaxWarps * 32) : "memory");
+        const float M = fmaxf(m, m2);
+        const float L = l * ex2(m - M) + l2 * ex2(m2 - M);
+        f_own = ex2(m - M) / L;
+        f_other = ex2(m2 - M) / L;
+      }
+      const float f0 = half == 0 ? f_own : f_other, f1 = half == 0 ? f_other : f_own;
+      // epilogue: this warp's half of O's columns, O_0 f0 + O_1 f1 -> staging in
+      // its own rows of its own P K-chunk (free: every P V MMA has completed)
       uint8_t* tiles[2] = {sP + half * 16384 + wq * 4096, sP + C_::P_BYTES + half * 16384 + wq * 4096};
       int t_used = 0;
       for (int pass = 0; pass < 2; ++pass) {
@@ -296,11 +300,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           const int c = half * per_half + ci;
           if (c * cols >= D) break;
           uint32_t v[64];
-          tmem_ld_32x32b_x32(tmem + lane_base + uint32_t(C_::O_COL + c * cols), *reinterpret_cast<uint32_t(*)[32]>(v));
-          if (pass == 1)
-            tmem_ld_32x32b_x32(tmem + lane_base + uint32_t(C_::O_COL + c * cols + 32),
-                               *reinterpret_cast<uint32_t(*)[32]>(v + 32));
-          tmem_ld_wait();
+          for (int part = 0; part < (pass == 0 ? 1 : 2); ++part) {
+            uint32_t a0[32], a1[32];
+            const uint32_t cc = uint32_t(c * cols + part * 32);
+            tmem_ld_32x32b_x32(tmem + lane_base + uint32_t(C_::O_COL) + cc, a0);
+            tmem_ld_32x32b_x32(tmem + lane_base + uint32_t(C_::O_COL + D) + cc, a1);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+              v[part * 32 + e] = __float_as_uint(__uint_as_float(a0[e]) * f0 + __uint_as_float(a1[e]) * f1);
+          }
           if (t_used == 2) {  // recycle staging tiles
             if (lane == 0) bulk_wait_read<0>();
             __syncwarp();
