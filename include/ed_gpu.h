@@ -62,12 +62,16 @@ typedef enum {
  *          f32 mode bit for bit; contractions on fp32 CUDA cores.
  *   TF32 : f32 storage; mul/sum contractions on tcgen05 kind::tf32.
  *   BF16 : f32 storage, bf16 contraction operands (written by their
- *          producers), tcgen05 kind::f16 with fp32 accumulation in TMEM. */
+ *          producers), tcgen05 kind::f16 with fp32 accumulation in TMEM.
+ *   F32X3: f32 storage; contractions as three kind::tf32 products
+ *          hi*hi + hi*lo + lo*hi (lo = x - tf32(x)) accumulated in TMEM:
+ *          fp32-level accuracy at tensor-core speed. */
 typedef enum {
   ED_PREC_FP32 = 0,
   ED_PREC_TF32 = 1,
   ED_PREC_BF16 = 2,
-  ED_PREC_FP64 = 3
+  ED_PREC_FP64 = 3,
+  ED_PREC_F32X3 = 4
 } ed_precision;
 
 /* Operator enums, in the order of ops.h:8-22. -1 = absent. */

@@ -8,7 +8,7 @@ import ctypes as C
 ED_OK, ED_ERR_USAGE, ED_ERR_PLAN, ED_ERR_EVAL = 0, 1, 2, 4
 ED_ERR_CUDA, ED_ERR_NCCL, ED_ERR_OOM, ED_ERR_UNSUPPORTED = 5, 6, 7, 8
 
-PREC = {"fp32": 0, "tf32": 1, "bf16": 2, "fp64": 3}
+PREC = {"fp32": 0, "tf32": 1, "bf16": 2, "fp64": 3, "fp32x3": 4}
 JOIN = {"mul": 0, "add": 1, "sub": 2, "div": 3, "sqdiff": 4, "absdiff": 5}
 AGG = {"sum": 0, "max": 1}
 MAP = {"relu": 0, "exp": 1, "neg": 2, "scale": 3, "identity": 4}

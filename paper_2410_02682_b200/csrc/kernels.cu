@@ -259,6 +259,22 @@ __global__ void convert_kernel(const void* src, int in_dt, void* dst, int out_dt
     st_dt(dst, out_dt, i, ld_dt(src, in_dt, i));
 }
 
+__global__ void split_lo_kernel(const float4* __restrict__ x, float4* __restrict__ lo, int64_t n4) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n4; i += int64_t(gridDim.x) * blockDim.x) {
+    float4 v = x[i], r;
+    r.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+    r.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+    r.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+    r.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+    lo[i] = r;
+  }
+}
+
+__global__ void split_lo_tail(const float* x, float* lo, int64_t from, int64_t n) {
+  for (int64_t i = from + threadIdx.x; i < n; i += blockDim.x)
+    lo[i] = x[i] - __uint_as_float(__float_as_uint(x[i]) & 0xFFFFE000u);
+}
+
 __global__ void add_one_kernel(void* p, int dt) { st_dt(p, dt, 0, ld_dt(p, dt, 0) + 1.0); }
 
 int grid_for(int64_t n, int block) {
@@ -309,6 +325,14 @@ cudaError_t launch_blockcopy(const BlockCopyParams& p, int n_groups, int64_t max
 
 cudaError_t launch_convert(const void* src, DT in, void* dst, DT out, int64_t n, cudaStream_t s) {
   convert_kernel<<<grid_for(n, 256), 256, 0, s>>>(src, int(in), dst, int(out), n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_split_lo(const float* x, float* lo, int64_t n, cudaStream_t s) {
+  const int64_t n4 = n / 4;
+  if (n4) split_lo_kernel<<<grid_for(n4, 256), 256, 0, s>>>(reinterpret_cast<const float4*>(x),
+                                                            reinterpret_cast<float4*>(lo), n4);
+  if (n % 4) split_lo_tail<<<1, 32, 0, s>>>(x, lo, n4 * 4, n);
   return cudaGetLastError();
 }
 

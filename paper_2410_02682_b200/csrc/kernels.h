@@ -104,6 +104,8 @@ cudaError_t launch_rect(const RectParams& p, int n_groups, int64_t max_rows, boo
 cudaError_t launch_scatter(const ChunkMapParams& p, const void* whole, DT in, DT store, cudaStream_t s);
 cudaError_t launch_gather(const ChunkMapParams& p, void* whole, DT store, DT out, cudaStream_t s);
 cudaError_t launch_blockcopy(const BlockCopyParams& p, int n_groups, int64_t max_rows, cudaStream_t s);
+// 3xTF32 split: lo = x - tf32(x) (the low mantissa bits kind::tf32 drops)
+cudaError_t launch_split_lo(const float* x, float* lo, int64_t n, cudaStream_t s);
 cudaError_t launch_convert(const void* src, DT in, void* dst, DT out, int64_t n, cudaStream_t s);
 cudaError_t launch_add_one(void* p, DT dt, cudaStream_t s);  // exec_options_t::corrupt hook
 

@@ -268,7 +268,7 @@ void make_map(CUtensorMap* m, const void* base, bool bf16, int64_t inner, int64_
 }
 
 // ---- schedule -------------------------------------------------------------------
-enum class OpKind { GEMM, GENERIC, REFINE, CORRUPT, SEND, RECV, CONVERT, EWISE, ROWREDUCE, SOFTMAX, FLASH };
+enum class OpKind { GEMM, GENERIC, REFINE, CORRUPT, SEND, RECV, CONVERT, EWISE, ROWREDUCE, SOFTMAX, FLASH, SPLIT };
 
 struct Op {
   OpKind kind;
@@ -297,10 +297,11 @@ struct Op {
 };
 
 struct Buffer {
-  size_t off_main = SIZE_MAX, off_16 = SIZE_MAX;
-  bool need_main = false, need_16 = false;
+  size_t off_main = SIZE_MAX, off_16 = SIZE_MAX, off_lo = SIZE_MAX;
+  bool need_main = false, need_16 = false, need_lo = false;
   void* main = nullptr;
   void* b16 = nullptr;
+  void* lo = nullptr;   // F32X3: x - tf32(x)
 };
 
 // Memory-bound join shapes with a dedicated grouped kernel (ewise.cu).
@@ -623,8 +624,10 @@ void ed_plan_h::build() {
   buf.assign(ne, Buffer{});
   for (int id = 0; id < ne; ++id) local[id] = rank_of(id) == me;
 
-  const bool tc = opt.precision == ED_PREC_TF32 || opt.precision == ED_PREC_BF16;
+  const bool x3 = opt.precision == ED_PREC_F32X3;
+  const bool tc = opt.precision == ED_PREC_TF32 || opt.precision == ED_PREC_BF16 || x3;
   const bool bf16 = opt.precision == ED_PREC_BF16;
+  const int max_sib = x3 ? kMaxSib / 3 : kMaxSib;  // F32X3 runs 3 products per sibling
 
   // ---- per einsum: kernel class and region fusion ----
   std::map<int, GemmMap> gmap;
@@ -653,7 +656,7 @@ void ed_plan_h::build() {
         if (rank_of(id) != me) remote_reader[d] = 1;
     for (auto& [k, sibs] : regions) {
       bool all_local = std::none_of(sibs.begin(), sibs.end(), [&](int s) { return remote_reader[s]; });
-      if (int(sibs.size()) <= kMaxSib && (all_local || sibs.size() == 1)) {
+      if (int(sibs.size()) <= max_sib && (all_local || sibs.size() == 1)) {
         fused_head[sibs[0]] = 1;
         region_sibs[sibs[0]] = sibs;
         for (int s : sibs) owner[s] = sibs[0];
@@ -897,6 +900,7 @@ void ed_plan_h::build() {
           int o = local[d] ? owner[d] : d;
           if (bf16) buf[o].need_16 = true;
           else buf[o].need_main = true;
+          if (x3) buf[o].need_lo = true;
         }
       } else {
         for (int d : u.deps) buf[local[d] ? owner[d] : d].need_main = true;
@@ -931,6 +935,7 @@ void ed_plan_h::build() {
     if (!here && !recv) continue;
     if (buf[id].need_main) buf[id].off_main = take(X[id].sz, es);
     if (buf[id].need_16) buf[id].off_16 = take(X[id].sz, 2);
+    if (buf[id].need_lo) buf[id].off_lo = take(X[id].sz, 4);
   }
   arena_bytes = std::max<size_t>(off, 1024);
 
@@ -939,6 +944,7 @@ void ed_plan_h::build() {
   ops.clear();
   contraction_flops = 0;
   std::set<int> gemm_emitted;
+  std::set<int> split_done;
   for (int id = 0; id < ne; ++id) {
     for (auto& [d, dst] : xfer_at[id]) {
       if (rank_of(d) == me) {
@@ -1000,6 +1006,22 @@ void ed_plan_h::build() {
       if (gmap.count(u.producer)) {
         if (!fused_head[id] || gemm_emitted.count(u.producer)) continue;
         gemm_emitted.insert(u.producer);
+        // F32X3: lo shadows of produced operands are made just before use
+        if (x3) {
+          for (int h = 0; h < ne; ++h) {
+            if (!fused_head[h] || X[h].producer != u.producer) continue;
+            for (int sidx : region_sibs[h])
+              for (int d : X[sidx].deps) {
+                const int o = local[d] ? owner[d] : d;
+                if (X[o].kind == ED_EXEC_INPUT_CHUNK || !split_done.insert(o).second) continue;
+                Op sp{OpKind::SPLIT};
+                sp.name = "split_tf32";
+                sp.ptr = reinterpret_cast<void*>(o);
+                sp.bytes = double(X[o].sz) * 8;
+                ops.push_back(sp);
+              }
+          }
+        }
         // one persistent launch for every region of this einsum on this rank
         Op op{OpKind::GEMM};
         op.bf16 = bf16;
@@ -1073,6 +1095,7 @@ void ed_plan_h::allocate() {
   for (int id = 0; id < ne; ++id) {
     if (buf[id].off_main != SIZE_MAX) buf[id].main = base + buf[id].off_main;
     if (buf[id].off_16 != SIZE_MAX) buf[id].b16 = base + buf[id].off_16;
+    if (buf[id].off_lo != SIZE_MAX) buf[id].lo = base + buf[id].off_lo;
   }
   CUDA_OK(cudaMalloc(&d_err, sizeof(int)));
   CUDA_OK(cudaMemset(d_err, 0, sizeof(int)));
@@ -1133,11 +1156,15 @@ void ed_plan_h::allocate() {
           GemmRegion r{};
           r.n_sib = int(sibs.size());
           r.map0 = int(op.maps.size());
-          for (int sidx : sibs) {
-            const Ex& j = X[sidx];
+          const bool x3 = opt.precision == ED_PREC_F32X3;
+          r.n_sib = int(sibs.size()) * (x3 ? 3 : 1);
+          for (int pseudo = 0; pseudo < int(sibs.size()) * (x3 ? 3 : 1); ++pseudo) {
+            const Ex& j = X[sibs[x3 ? pseudo / 3 : pseudo]];
             int da = resolve(j.deps[g.a_slot]), db = resolve(j.deps[g.b_slot]);
             const void* pa = b16 ? buf[da].b16 : buf[da].main;
             const void* pb = b16 ? buf[db].b16 : buf[db].main;
+            if (x3 && pseudo % 3 == 1) pb = buf[db].lo;  // hi * lo
+            if (x3 && pseudo % 3 == 2) pa = buf[da].lo;  // lo * hi
             if (!pa || !pb) throw ed_error(ED_ERR_PLAN, "GEMM operand buffer missing");
             CUtensorMap ma, mb;
             // MN-major fp32 operands need the 32-byte-atom swizzle (see gemm_sm100.cu)
@@ -1327,6 +1354,11 @@ void ed_plan_h::allocate() {
         }
         break;
       }
+      case OpKind::SPLIT:
+        op.gen.x = buf[id].main;
+        op.gen.out = buf[id].lo;
+        op.gen.n_out = X[id].sz;
+        break;
       case OpKind::CORRUPT:
         op.dt = buf[id].main ? store : DT::BF16;
         op.ptr = buf[id].main ? buf[id].main : buf[id].b16;
@@ -1530,6 +1562,9 @@ void ed_plan_h::launch_op(size_t i, cudaStream_t s) {
       CUDA_OK(launch_ewise(op.ew, int(op.jptrs.size()), f64, opt.precision == ED_PREC_FP32, s));
       break;
     case OpKind::FLASH: CUDA_OK(launch_attn(op.attn, ctx->num_sms, s)); break;
+    case OpKind::SPLIT:
+      CUDA_OK(launch_split_lo(static_cast<const float*>(op.gen.x), static_cast<float*>(op.gen.out), op.gen.n_out, s));
+      break;
     case OpKind::SOFTMAX: CUDA_OK(launch_softmax(op.sm, int(op.jptrs.size()), s)); break;
     case OpKind::ROWREDUCE:
       CUDA_OK(launch_rowreduce(op.rr, int(op.jptrs.size()), f64, opt.precision == ED_PREC_FP32, s));
@@ -1771,7 +1806,7 @@ ed_status ed_prepare(ed_ctx* ctx, const ed_plan_c* plan, const ed_options_c* opt
     auto* h = new ed_plan_h;
     h->ctx = ctx;
     if (options) h->opt = *options;
-    if (h->opt.precision < 0 || h->opt.precision > 3) {
+    if (h->opt.precision < 0 || h->opt.precision > 4) {
       delete h;
       throw ed_error(ED_ERR_USAGE, "unknown precision");
     }
@@ -1817,6 +1852,7 @@ ed_status ed_upload(ed_plan_h* h, const ed_chunk_in_c* chunks, int32_t n, char* 
       Buffer& b = h->buf[c.exec_id];
       CUDA_OK(launch_convert(h->staging, dt_of(c.dtype), b.main, h->store, c.n, s));
       if (b.b16) CUDA_OK(launch_convert(h->staging, dt_of(c.dtype), b.b16, DT::BF16, c.n, s));
+      if (b.lo) CUDA_OK(launch_split_lo(static_cast<const float*>(b.main), static_cast<float*>(b.lo), c.n, s));
     }
     CUDA_OK(cudaStreamSynchronize(s));
   });
@@ -1844,6 +1880,10 @@ ed_status ed_upload_tensors(ed_plan_h* h, const ed_tensor_in_c* ts, int32_t n, c
       CUDA_OK(cudaMemcpyAsync(h->staging, t.data, bytes, cudaMemcpyHostToDevice, s));
       (void)shadow;
       block_copies(h, t.vertex_id, h->V[t.vertex_id].d, ids, true, h->staging, nullptr, dt_of(t.dtype), s);
+      for (int id : ids)
+        if (h->local[id] && h->buf[id].lo)
+          CUDA_OK(launch_split_lo(static_cast<const float*>(h->buf[id].main), static_cast<float*>(h->buf[id].lo),
+                                  h->X[id].sz, s));
       CUDA_OK(cudaStreamSynchronize(s));
     }
   });

@@ -17,7 +17,7 @@ pytestmark = pytest.mark.gpu
 
 MATRIX = [c for c in golden_cases()]
 # stated bounds for the tensor-core modes (max_rel_err vs the f64 reference)
-TOL = {"tf32": 1e-2, "bf16": 3e-2}
+TOL = {"tf32": 1e-2, "bf16": 3e-2, "fp32x3": 1e-5}
 
 
 def _bf16(a):
@@ -68,7 +68,7 @@ def test_fp32_bitexact_vs_reference_f32_mode(gpu_ctx, case):
         _assert_matches(rep.outputs[vid], a, case, vid, "fp32", plan)
 
 
-@pytest.mark.parametrize("prec", ["tf32", "bf16"])
+@pytest.mark.parametrize("prec", ["tf32", "bf16", "fp32x3"])
 @pytest.mark.parametrize("case", MATRIX)
 def test_tensor_core_modes_within_bound(gpu_ctx, case, prec):
     name, ins, o64, o32, orc, counters, total = load_golden(case)
@@ -86,7 +86,7 @@ def test_tensor_core_modes_within_bound(gpu_ctx, case, prec):
 LAYOUTS = ["gemm_nn", "gemm_tn", "gemm_nt", "gemm_swap", "gemm_ragged", "gemm_batch", "gemm_heads", "gemm_merge"]
 
 
-@pytest.mark.parametrize("prec", ["fp32", "tf32", "bf16"])
+@pytest.mark.parametrize("prec", ["fp32", "tf32", "bf16", "fp32x3"])
 @pytest.mark.parametrize("p", [1, 8])
 @pytest.mark.parametrize("name", LAYOUTS)
 def test_gemm_layouts_integer_exact(gpu_ctx, name, p, prec):
