@@ -277,7 +277,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              tma_store_3d(p.maps + cm, tile, tc.n0 + c * cols, trow, tc.b);
+              // outputs stream out: keep L2 for the operand tiles other CTAs re-read
+              tma_store_3d_hint(p.maps + cm, tile, tc.n0 + c * cols, trow, tc.b, policy_evict_first());
               bulk_commit();
             }
             ++stage_ctr;

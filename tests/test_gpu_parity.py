@@ -182,3 +182,52 @@ def test_reference_flow_with_gpu_executor(gpu_ctx, tmp_path):
     r = subprocess.run([exe, str(tmp_path)], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert "72/72 passed" in r.stdout
+
+
+def _mutated(name, fn):
+    import copy
+    plan = load_plan(name)
+    plan = copy.deepcopy(plan)
+    fn(plan)
+    return plan
+
+
+@pytest.mark.parametrize("what", ["placement", "topology", "coverage", "overlap", "divides"])
+def test_structural_errors_are_plan_errors(gpu_ctx, what):
+    """execute()'s structural checks (runtime.cc:388-395, 230-268) surface as
+    ED_ERR_PLAN -> PlanError (plan_error_t), at prepare time."""
+    from paper_2410_02682_b200.executor import PlanError, PreparedPlan
+    if what == "placement":
+        plan = _mutated("matmul_p4_L2", lambda p: setattr(p.exec[-1], "machine", 7))
+    elif what == "topology":
+        def f(p):
+            j = next(u for u in p.exec if u.kind == 1)
+            j.deps = [len(p.exec) - 1] + j.deps[1:]
+        plan = _mutated("matmul_p4_L2", f)
+    elif what == "coverage":
+        def f(p):  # keep one region of a repartition: the rest of the chunk stays unwritten
+            r = next(u for u in p.exec if u.kind == 2 and p.vertices[u.producer].name == "Z" and u.consumer >= 0)
+            r.deps = r.deps[:1]
+        plan = _mutated("chain8_pinned_L2", f)
+    elif what == "overlap":
+        def f(p):  # a refinement of a max-free map vertex listing a dep twice
+            r = next(u for u in p.exec if u.kind == 2 and p.vertices[u.producer].expr is not None
+                     and p.vertices[u.producer].expr.agg is None)
+            r.deps = r.deps + r.deps[:1]
+        plan = _mutated("mix_p4_L2", f)
+    else:
+        def f(p):
+            v = next(v for v in p.vertices if v.expr is not None)
+            v.d = [3] + v.d[1:]
+        plan = _mutated("matmul_p4_L2", f)
+    with pytest.raises(PlanError):
+        PreparedPlan(gpu_ctx, plan, precision="bf16")
+
+
+def test_missing_input_is_a_plan_error(gpu_ctx):
+    from paper_2410_02682_b200.executor import PlanError, PreparedPlan
+    plan = load_plan("matmul_p4_L2")
+    pp = PreparedPlan(gpu_ctx, plan, precision="bf16")
+    with pytest.raises(PlanError):
+        pp.upload({99: np.zeros(4)})
+    pp.close()
