@@ -249,12 +249,16 @@ __global__ void __launch_bounds__(128) softmax_kernel(const SoftmaxParams p) {
 #pragma unroll
       for (int e = 0; e < 4; ++e) mx = fmaxf(mx, v[4 * j + e]);
     }
+    if (jp.y) {
+      mx = static_cast<const float*>(jp.y)[row];  // the planned row max, computed upstream
+    } else {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if (lane == 0) red[warp] = mx;
-    __syncthreads();
-    mx = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
-    __syncthreads();
+      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      if (lane == 0) red[warp] = mx;
+      __syncthreads();
+      mx = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+      __syncthreads();
+    }
     float sum = 0.f;
 #pragma unroll
     for (int j = 0; j < NV; ++j) {

@@ -34,7 +34,7 @@ struct RowReduceParams {
 // Fused row softmax (max, sub, exp, sum, div of one row block in registers):
 // Y = exp(X - max_row) / sum_row exp(X - max_row), rows of `len` elements.
 struct SoftmaxParams {
-  const JoinPtrs* joins;  // x = the chain's input chunk, out/out16 = Y's chunk
+  const JoinPtrs* joins;  // x = the chain's input chunk, y = row maxima or null, out/out16 = Y's chunk
   int64_t rows;
   int len;
 };

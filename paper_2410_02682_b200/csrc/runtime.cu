@@ -402,6 +402,7 @@ struct ed_plan_h {
     int x;                                        // the chain's input vertex
     int64_t len;
     std::vector<std::pair<int, int>> pairs;       // (Y join, x chunk ref)
+    std::vector<int> m_refs;                      // row-max chunk refs when M stays unfused
   };
   struct Flash {                                  // T1 -> softmax -> O in one kernel
     int t1, y, o;
@@ -782,51 +783,63 @@ void ed_plan_h::build() {
       const int sv = V[e].inputs[0];
       if (!is(sv, OpKind::EWISE, 2, ED_JOIN_SUB) || memmap_[sv].y_mode != 2) continue;
       const int xv = V[sv].inputs[0], m = V[sv].inputs[1];
-      if (!is(m, OpKind::ROWREDUCE, 1, ED_AGG_MAX) || V[m].map != ED_MAP_IDENTITY || V[m].inputs[0] != xv) continue;
-      if (!sole_reader(m, sv) || !sole_reader(sv, e) || !sole_reader(sg, y) || is_output(e) ||
-          readers[e].size() != 2)
-        continue;
-      if (!all_local(m) || !all_local(sv) || !all_local(e) || !all_local(sg) || !all_local(y)) continue;
+      if (!sole_reader(sv, e) || !sole_reader(sg, y) || is_output(e) || readers[e].size() != 2) continue;
+      if (!all_local(sv) || !all_local(e) || !all_local(sg) || !all_local(y)) continue;
       const int64_t L = memmap_[sg].len;
-      if (memmap_[m].len != L || memmap_[sv].inner != L || memmap_[y].inner != L) continue;
+      if (memmap_[sv].inner != L || memmap_[y].inner != L) continue;
       if (L % 4 != 0 || L > 128 * 64 || f64) continue;  // the fused kernel keeps a row in registers
-      // every Y join must see one aligned row block: the same x chunk under M and S
-      bool ok = true;
-      std::vector<std::pair<int, int>> pairs;  // (y join, x buffer owner)
+      // M joins the chain when it is the row max of the same, aligned x chunks;
+      // otherwise (e.g. its label is split with a sibling fold) M is computed
+      // as planned and the chain reads the materialised row maxima
+      const bool m_fusable = is(m, OpKind::ROWREDUCE, 1, ED_AGG_MAX) && V[m].map == ED_MAP_IDENTITY &&
+                             V[m].inputs[0] == xv && sole_reader(m, sv) && all_local(m) && memmap_[m].len == L;
       auto join_at = [&](int ref, int w) {
         const int o = owner[ref];
         return (X[o].kind == ED_EXEC_JOIN && X[o].producer == w) ? o : -1;
       };
-      for (int yj : joins_of(y)) {
-        const int ej = join_at(X[yj].deps[0], e), sgj = join_at(X[yj].deps[1], sg);
-        const int sj = ej >= 0 ? join_at(X[ej].deps[0], sv) : -1;
-        const int mj = sj >= 0 ? join_at(X[sj].deps[1], m) : -1;
-        ok = ok && ej >= 0 && sgj >= 0 && sj >= 0 && mj >= 0 && owner[X[sgj].deps[0]] == ej &&
-             owner[X[mj].deps[0]] == owner[X[sj].deps[0]] && X[yj].sz == X[sj].sz && X[yj].sz % L == 0;
-        if (!ok) break;
-        pairs.push_back({yj, X[sj].deps[0]});
-      }
-      if (!ok || pairs.empty()) continue;
       Softmax sm;
+      bool ok = true, internal = m_fusable;
+      for (int attempt = 0; attempt < 2 && !sm.pairs.size(); ++attempt) {
+        ok = true;
+        sm.pairs.clear();
+        sm.m_refs.clear();
+        for (int yj : joins_of(y)) {
+          const int ej = join_at(X[yj].deps[0], e), sgj = join_at(X[yj].deps[1], sg);
+          const int sj = ej >= 0 ? join_at(X[ej].deps[0], sv) : -1;
+          ok = ok && ej >= 0 && sgj >= 0 && sj >= 0 && owner[X[sgj].deps[0]] == ej && X[yj].sz == X[sj].sz &&
+               X[yj].sz % L == 0;
+          if (ok && internal) {
+            const int mj = join_at(X[sj].deps[1], m);
+            ok = mj >= 0 && owner[X[mj].deps[0]] == owner[X[sj].deps[0]];
+          }
+          if (!ok) break;
+          sm.pairs.push_back({yj, X[sj].deps[0]});
+          if (!internal) sm.m_refs.push_back(X[sj].deps[1]);
+        }
+        if (!ok) {
+          sm.pairs.clear();
+          if (!internal) break;
+          internal = false;  // retry with the row maxima read from memory
+        }
+      }
+      if (!ok || sm.pairs.empty()) continue;
       sm.y = y;
       sm.x = xv;
       sm.len = L;
-      sm.pairs = pairs;
       softmax_[y] = sm;
-      for (int w : {m, sv, e, sg})
+      std::vector<int> gone = {sv, e, sg};
+      if (internal) gone.push_back(m);
+      for (int w : gone)
         for (int id = 0; id < ne; ++id)
           if (X[id].producer == w && X[id].kind != ED_EXEC_INPUT_CHUNK) virt[id] = 1;
-      memmap_.erase(m);
-      memmap_.erase(sv);
-      memmap_.erase(e);
-      memmap_.erase(sg);
+      for (int w : gone) memmap_.erase(w);
     }
     // (3) attention block: T1 = Q K^T (GEMM, maybe with a fused scale), the
     // softmax chain on T1 (or its scaled map), O = T3 V (GEMM, K = the row
     // label) -> one kernel; T1 and T3 are never materialised (bf16 only)
     for (auto& [yv, sm] : softmax_) {
       if (!bf16) break;
-      if (readers[yv].size() != 1 || is_output(yv)) continue;
+      if (readers[yv].size() != 1 || is_output(yv) || !sm.m_refs.empty()) continue;
       const int o = readers[yv][0];
       if (!gmap.count(o) || V[o].inputs[gmap[o].a_slot] != yv || !all_local(o)) continue;
       int t1 = sm.x;
@@ -888,8 +901,12 @@ void ed_plan_h::build() {
       continue;
     }
     if (u.kind == ED_EXEC_JOIN && softmax_.count(u.producer)) {
-      for (auto& [yj, xr] : softmax_[u.producer].pairs)
-        if (yj == id) buf[owner[xr]].need_main = true;
+      const Softmax& sm = softmax_[u.producer];
+      for (size_t k = 0; k < sm.pairs.size(); ++k)
+        if (sm.pairs[k].first == id) {
+          buf[owner[sm.pairs[k].second]].need_main = true;
+          if (!sm.m_refs.empty()) buf[owner[sm.m_refs[k]]].need_main = true;
+        }
       continue;
     }
     if (u.kind == ED_EXEC_INPUT_CHUNK) buf[owner[id]].need_main = true;
@@ -1431,9 +1448,11 @@ void ed_plan_h::allocate() {
       case OpKind::SOFTMAX: {
         const Softmax& sm = softmax_.at(X[id].producer);
         op.jptrs.clear();
-        for (auto& [yj, xr] : sm.pairs) {
+        for (size_t k = 0; k < sm.pairs.size(); ++k) {
+          const int yj = sm.pairs[k].first, xr = sm.pairs[k].second;
           JoinPtrs jp{};
           jp.x = buf[resolve(xr)].main;
+          jp.y = sm.m_refs.empty() ? nullptr : buf[resolve(sm.m_refs[k])].main;
           jp.out = buf[yj].main;
           jp.out16 = buf[yj].b16;
           op.jptrs.push_back(jp);
