@@ -148,6 +148,7 @@ struct GemmMap {
   int a_slot, b_slot;  // which einsum input feeds MMA-A / MMA-B
   Dim am, ak, ab, bn, bk, bb, cm, cn, cb;
   bool a_mn, b_mn;
+  labels lA, lB, Mc, Nc, Kc, Bc;  // operand label lists and the label classes
 };
 
 bool map_gemm(const Vtx& v, const shape& local_xy, bool bf16, GemmMap& g, std::string& why) {
@@ -193,6 +194,12 @@ bool map_gemm(const Vtx& v, const shape& local_xy, bool bf16, GemmMap& g, std::s
   const labels& Ncls = swap ? M : N;
   g.a_slot = swap ? 1 : 0;
   g.b_slot = swap ? 0 : 1;
+  g.lA = lA;
+  g.lB = lB;
+  g.Mc = Mcls;
+  g.Nc = Ncls;
+  g.Kc = K;
+  g.Bc = B;
   shape eA = extents(lA), eB = extents(lB), eZ = extents(v.lz);
   labels o1, o2, o3;
   bool ok = merge_dim(lA, eA, Mcls, g.am, o1) && merge_dim(v.lz, eZ, Mcls, g.cm, o2) && o1 == o2;
@@ -410,6 +417,17 @@ struct ed_plan_h {
     std::vector<std::array<int, 4>> regions;      // (Q ref, K ref, V ref, O region head)
   };
   std::map<int, Flash> flash_;                    // O vertex -> fused attention block
+  struct Seg {
+    int owner;                                    // source region buffer
+    int64_t k0, kext;                             // its range along the contraction label
+    Dim mn, k, b;                                 // its layout for the GEMM classes
+  };
+  struct KSeg {
+    int role = 0;                                 // 0: MMA-A operand segmented, 1: MMA-B
+    int64_t kseg = -1;
+    std::map<int, std::vector<Seg>> segs;         // join -> segments in K order
+  };
+  std::map<int, KSeg> kseg_;                      // GEMM einsum -> K-segmented operand
   std::set<int> flash_skip_;                      // einsums computed inside a Flash op
   std::map<int, Softmax> softmax_;                // Y vertex -> fused row-softmax chain
   std::map<int, std::pair<int, double>> epi_;     // GEMM einsum -> epilogue map (op, c)
@@ -890,6 +908,96 @@ void ed_plan_h::build() {
     }
   }
 
+  // ---- K-segmented operands: a GEMM operand that is a refinement pasting
+  // several producer regions along the contraction label is read straight
+  // from those regions (one pseudo-sibling per segment), never copied ----
+  kseg_.clear();
+  for (auto& [c, g] : gmap) {
+    if (flash_skip_.count(c)) continue;
+    bool c_local = true;
+    for (int id = 0; id < ne; ++id)
+      if (X[id].producer == c && !local[id]) c_local = false;
+    if (!c_local) continue;
+    std::vector<int> kl;
+    for (auto l : g.Kc) kl.push_back(l);
+    if (kl.size() != 1) continue;
+    for (int role = 0; role < 2 && !kseg_.count(c); ++role) {
+      const int slot = role == 0 ? g.a_slot : g.b_slot;
+      const labels& lop = slot == 0 ? V[c].lx : V[c].ly;
+      const int kd = int(std::find(lop.begin(), lop.end(), kl[0]) - lop.begin());
+      KSeg ks;
+      ks.role = role;
+      bool ok = true;
+      std::vector<int> refs;
+      int real_max = 1;
+      for (int jid = 0; jid < ne && ok; ++jid) {
+        if (X[jid].kind != ED_EXEC_JOIN || X[jid].producer != c) continue;
+        const int ref = X[jid].deps[slot];
+        const Ex& R = X[ref];
+        ok = R.kind == ED_EXEC_REFINEMENT && local[ref] && owner[ref] == ref && !virt[ref] && srcs[ref].size() >= 2;
+        if (!ok) break;
+        const shape& bound = V[R.producer].bound;
+        const shape dc = region_partition(ref);
+        std::vector<Seg> segs;
+        std::set<int64_t> starts;
+        for (auto& sr : srcs[ref]) {
+          for (size_t d = 0; d < bound.size() && ok; ++d) {
+            const int64_t c0 = R.key[d] * (bound[d] / dc[d]);
+            if (int(d) == kd) ok = sr.r0[d] >= c0 && sr.r0[d] + sr.ext[d] <= c0 + R.cb[d];
+            else ok = sr.r0[d] == c0 && sr.ext[d] == R.cb[d];
+          }
+          ok = ok && starts.insert(sr.r0[kd]).second && local[sr.id];
+          if (!ok) break;
+          Seg sg;
+          sg.owner = sr.id;
+          sg.k0 = sr.r0[kd] - R.key[kd] * (bound[kd] / dc[kd]);
+          sg.kext = sr.ext[kd];
+          labels o1;
+          const labels& mcls = role == 0 ? g.Mc : g.Nc;
+          ok = merge_dim(lop, sr.ext, mcls, sg.mn, o1) && merge_dim(lop, sr.ext, g.Kc, sg.k, o1) &&
+               merge_dim(lop, sr.ext, g.Bc, sg.b, o1);
+          segs.push_back(sg);
+        }
+        if (!ok) break;
+        std::sort(segs.begin(), segs.end(), [](const Seg& a, const Seg& b) { return a.k0 < b.k0; });
+        int64_t covered = 0;
+        for (auto& sg : segs) {
+          ok = ok && sg.kext == segs[0].kext && sg.k0 == covered;
+          covered += sg.kext;
+        }
+        ok = ok && covered == R.cb[kd];
+        if (!ok) break;
+        // the other operand is sliced along K: its segment starts must stay 16-byte aligned
+        const Dim& ok_dim = role == 0 ? g.bk : g.ak;
+        for (auto& sg : segs) ok = ok && (sg.k0 * ok_dim.stride * (bf16 ? 2 : 4)) % 16 == 0;
+        if (ks.kseg < 0) ks.kseg = segs[0].kext;
+        ok = ok && ks.kseg == segs[0].kext;
+        ks.segs[jid] = segs;
+        refs.push_back(ref);
+        const int real = fused_head[owner[jid]] ? int(region_sibs[owner[jid]].size()) : 1;
+        real_max = std::max(real_max, real);
+        ok = ok && real * int(segs.size()) * (x3 ? 3 : 1) <= kMaxSib;
+      }
+      if (!ok || refs.empty()) continue;
+      kseg_[c] = ks;
+      for (int ref : refs) virt[ref] = 1;
+    }
+  }
+
+  auto gemm_reads = [&](int jid) {
+    std::vector<int> r;
+    const int w = X[jid].producer;
+    for (int k = 0; k < int(X[jid].deps.size()); ++k) {
+      const int d = X[jid].deps[k];
+      if (kseg_.count(w) && k == (kseg_[w].role == 0 ? gmap[w].a_slot : gmap[w].b_slot)) {
+        for (auto& sg : kseg_[w].segs.at(jid)) r.push_back(sg.owner);
+      } else {
+        r.push_back(local[d] ? owner[d] : d);
+      }
+    }
+    return r;
+  };
+
   // ---- buffer needs ----
   for (int id = 0; id < ne; ++id) {
     if (!local[id] || virt[id] || virtual_join_src.count(id)) continue;
@@ -913,8 +1021,17 @@ void ed_plan_h::build() {
     if (u.kind == ED_EXEC_JOIN) {
       int w = u.producer;
       if (gmap.count(w)) {
-        for (int d : u.deps) {
-          int o = local[d] ? owner[d] : d;
+        std::vector<int> reads;
+        for (int k = 0; k < int(u.deps.size()); ++k) {
+          const int d = u.deps[k];
+          const bool segmented = kseg_.count(w) && k == (kseg_[w].role == 0 ? gmap[w].a_slot : gmap[w].b_slot);
+          if (segmented) {
+            for (auto& sg : kseg_[w].segs.at(id)) reads.push_back(sg.owner);
+          } else {
+            reads.push_back(local[d] ? owner[d] : d);
+          }
+        }
+        for (int o : reads) {
           if (bf16) buf[o].need_16 = true;
           else buf[o].need_main = true;
           if (x3) buf[o].need_lo = true;
@@ -1028,8 +1145,8 @@ void ed_plan_h::build() {
           for (int h = 0; h < ne; ++h) {
             if (!fused_head[h] || X[h].producer != u.producer) continue;
             for (int sidx : region_sibs[h])
-              for (int d : X[sidx].deps) {
-                const int o = local[d] ? owner[d] : d;
+              for (int o0 : gemm_reads(sidx)) {
+                const int o = o0;
                 if (X[o].kind == ED_EXEC_INPUT_CHUNK || !split_done.insert(o).second) continue;
                 Op sp{OpKind::SPLIT};
                 sp.name = "split_tf32";
@@ -1096,6 +1213,7 @@ void ed_plan_h::build() {
     ops.insert(ops.begin() + at, op);
   }
 
+  (void)0;
   // stash what allocate() needs
   this->srcs_.clear();
   for (int id = 0; id < ne; ++id)
@@ -1150,7 +1268,7 @@ void ed_plan_h::allocate() {
         p.bf16 = b16;
         p.M = int(g.am.ext);
         p.N = int(g.bn.ext);
-        p.K = int(g.ak.ext);
+        p.K = int(kseg_.count(u.producer) ? kseg_.at(u.producer).kseg : g.ak.ext);
         p.batch = int(g.ab.ext);
         p.a_mn = g.a_mn;
         p.b_mn = g.b_mn;
@@ -1174,24 +1292,52 @@ void ed_plan_h::allocate() {
           r.n_sib = int(sibs.size());
           r.map0 = int(op.maps.size());
           const bool x3 = opt.precision == ED_PREC_F32X3;
-          r.n_sib = int(sibs.size()) * (x3 ? 3 : 1);
-          for (int pseudo = 0; pseudo < int(sibs.size()) * (x3 ? 3 : 1); ++pseudo) {
-            const Ex& j = X[sibs[x3 ? pseudo / 3 : pseudo]];
+          const KSeg* ks = kseg_.count(u.producer) ? &kseg_.at(u.producer) : nullptr;
+          const int nseg = ks ? int(ks->segs.at(sibs[0]).size()) : 1;
+          const int per = nseg * (x3 ? 3 : 1);
+          r.n_sib = int(sibs.size()) * per;
+          // MN-major fp32 operands need the 32-byte-atom swizzle (see gemm_sm100.cu)
+          const CUtensorMapSwizzle mn_swz = b16 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
+          const int es_op = b16 ? 2 : 4;
+          for (int pseudo = 0; pseudo < r.n_sib; ++pseudo) {
+            const int sidx = sibs[pseudo / per];
+            const int seg = (pseudo % per) / (x3 ? 3 : 1);
+            const int part = x3 ? pseudo % 3 : 0;  // F32X3: hi*hi, hi*lo, lo*hi
+            const Ex& j = X[sidx];
             int da = resolve(j.deps[g.a_slot]), db = resolve(j.deps[g.b_slot]);
-            const void* pa = b16 ? buf[da].b16 : buf[da].main;
-            const void* pb = b16 ? buf[db].b16 : buf[db].main;
-            if (x3 && pseudo % 3 == 1) pb = buf[db].lo;  // hi * lo
-            if (x3 && pseudo % 3 == 2) pa = buf[da].lo;  // lo * hi
+            Dim am = g.am, ak = g.ak, ab = g.ab, bn = g.bn, bk = g.bk, bb = g.bb;
+            int64_t aoff = 0, boff = 0;
+            if (ks) {
+              const Seg& sg = ks->segs.at(sidx)[seg];
+              if (ks->role == 0) {
+                da = sg.owner;
+                am = sg.mn;
+                ak = sg.k;
+                ab = sg.b;
+                bk.ext = sg.kext;
+                boff = sg.k0 * g.bk.stride;
+              } else {
+                db = sg.owner;
+                bn = sg.mn;
+                bk = sg.k;
+                bb = sg.b;
+                ak.ext = sg.kext;
+                aoff = sg.k0 * g.ak.stride;
+              }
+            }
+            const char* pa = static_cast<const char*>(b16 ? buf[da].b16 : buf[da].main);
+            const char* pb = static_cast<const char*>(b16 ? buf[db].b16 : buf[db].main);
+            if (part == 1) pb = static_cast<const char*>(buf[db].lo);
+            if (part == 2) pa = static_cast<const char*>(buf[da].lo);
             if (!pa || !pb) throw ed_error(ED_ERR_PLAN, "GEMM operand buffer missing");
+            pa += aoff * es_op;
+            pb += boff * es_op;
             CUtensorMap ma, mb;
-            // MN-major fp32 operands need the 32-byte-atom swizzle (see gemm_sm100.cu)
-            const CUtensorMapSwizzle mn_swz = b16 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
-            if (!g.a_mn) make_map(&ma, pa, b16, g.ak.ext, g.am.ext, g.am.stride, g.ab.ext, g.ab.stride, BK, BM);
-            else make_map(&ma, pa, b16, g.am.ext, g.ak.ext, g.ak.stride, g.ab.ext, g.ab.stride, ATOM, BK, mn_swz);
+            if (!g.a_mn) make_map(&ma, pa, b16, ak.ext, am.ext, am.stride, ab.ext, ab.stride, BK, BM);
+            else make_map(&ma, pa, b16, am.ext, ak.ext, ak.stride, ab.ext, ab.stride, ATOM, BK, mn_swz);
             if (!g.b_mn)
-              make_map(&mb, pb, b16, g.bk.ext, g.bn.ext, g.bn.stride, g.bb.ext, g.bb.stride, BK,
-                       uint32_t(gemm_b_box(p.M)));
-            else make_map(&mb, pb, b16, g.bn.ext, g.bk.ext, g.bk.stride, g.bb.ext, g.bb.stride, ATOM, BK, mn_swz);
+              make_map(&mb, pb, b16, bk.ext, bn.ext, bn.stride, bb.ext, bb.stride, BK, uint32_t(gemm_b_box(p.M)));
+            else make_map(&mb, pb, b16, bn.ext, bk.ext, bk.stride, bb.ext, bb.stride, ATOM, BK, mn_swz);
             op.maps.push_back(ma);
             op.maps.push_back(mb);
             ++total_sib;
