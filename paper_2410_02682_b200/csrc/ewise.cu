@@ -236,12 +236,18 @@ __global__ void __launch_bounds__(128) softmax_kernel(const SoftmaxParams p) {
   const int t = threadIdx.x, lane = t % 32, warp = t / 32;
   for (int64_t row = blockIdx.x; row < p.rows; row += gridDim.x) {
     const float* xr = static_cast<const float*>(jp.x) + row * p.len;
+    const RowSeg* sg = p.segs ? p.segs + size_t(blockIdx.y) * p.n_seg : nullptr;
     float v[EPT];
     float mx = -INFINITY;
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
       const int i = (j * 128 + t) * 4;
-      float4 q = i < p.len ? __ldcs(reinterpret_cast<const float4*>(xr + i)) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+      const float* src = xr + i;
+      if (sg) {  // gather the row from its column segments in place
+        const RowSeg s = sg[i / p.seg_w];
+        src = s.ptr + (row + s.row0) * s.stride + (i % p.seg_w);
+      }
+      float4 q = i < p.len ? __ldcs(reinterpret_cast<const float4*>(src)) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
       v[4 * j] = q.x;
       v[4 * j + 1] = q.y;
       v[4 * j + 2] = q.z;

@@ -33,10 +33,20 @@ struct RowReduceParams {
 
 // Fused row softmax (max, sub, exp, sum, div of one row block in registers):
 // Y = exp(X - max_row) / sum_row exp(X - max_row), rows of `len` elements.
+// One column segment of a softmax input row read in place from a producer
+// region (the refinement that would paste it is elided).
+struct RowSeg {
+  const float* ptr;
+  int64_t row0;     // row of the consumer chunk's first row inside this region
+  int64_t stride;   // region row stride (elements)
+};
+
 struct SoftmaxParams {
   const JoinPtrs* joins;  // x = the chain's input chunk, y = row maxima or null, out/out16 = Y's chunk
   int64_t rows;
   int len;
+  const RowSeg* segs;     // nullable: n_seg segments per join, each seg_w columns
+  int n_seg, seg_w;
 };
 
 cudaError_t launch_softmax(const SoftmaxParams& p, int n_joins, cudaStream_t s);

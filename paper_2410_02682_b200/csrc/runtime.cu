@@ -284,6 +284,7 @@ struct Op {
   GemmLaunch gemm{};
   AttnLaunch attn{};
   std::vector<AttnRegion> aregions;
+  std::vector<RowSeg> rowsegs;         // SOFTMAX: x read in place from column segments
   std::vector<int> heads;              // GEMM: region heads (join ids), fold order
   std::vector<CUtensorMap> maps;       // GEMM: host copies, uploaded by allocate()
   std::vector<GemmRegion> regions;
@@ -410,6 +411,12 @@ struct ed_plan_h {
     int64_t len;
     std::vector<std::pair<int, int>> pairs;       // (Y join, x chunk ref)
     std::vector<int> m_refs;                      // row-max chunk refs when M stays unfused
+    struct XSeg {
+      int owner;
+      int64_t row0, stride;
+    };
+    std::vector<std::vector<XSeg>> xsegs;         // per pair: x read in place from column segments
+    int seg_w = 0;
   };
   struct Flash {                                  // T1 -> softmax -> O in one kernel
     int t1, y, o;
@@ -436,6 +443,7 @@ struct ed_plan_h {
   void* d_rects = nullptr;                        // RectGroup[] of fast refinements
   void* d_copy_desc = nullptr;                    // BlockCopy[] scratch for upload / download
   void* d_attn = nullptr;                         // tensor maps + regions of fused attention launches
+  void* d_rowsegs = nullptr;                      // RowSeg[] of softmax launches reading in place
   size_t copy_desc_bytes = 0;
 
   int rank_of(int id) const { return X[id].machine % ctx->world; }
@@ -984,6 +992,40 @@ void ed_plan_h::build() {
     }
   }
 
+  // softmax inputs that are a paste of column segments (rank 2) are read in place
+  for (auto& [y, sm] : softmax_) {
+    bool ok = true;
+    std::vector<std::vector<Softmax::XSeg>> all;
+    int w_all = 0;
+    for (auto& [yj, xr] : sm.pairs) {
+      const Ex& R = X[xr];
+      ok = R.kind == ED_EXEC_REFINEMENT && local[xr] && owner[xr] == xr && !virt[xr] && srcs[xr].size() >= 2 &&
+           R.cb.size() == 2 && R.cb[1] == sm.len;
+      if (!ok) break;
+      const shape& bound = V[R.producer].bound;
+      const shape dc = region_partition(xr);
+      const int64_t rs = R.key[0] * (bound[0] / dc[0]), cs = R.key[1] * (bound[1] / dc[1]);
+      std::vector<std::pair<int64_t, Softmax::XSeg>> segs;
+      for (auto& sr : srcs[xr]) {
+        ok = ok && local[sr.id] && sr.r0[0] <= rs && sr.r0[0] + sr.ext[0] >= rs + R.cb[0] && sr.ext[1] % 4 == 0;
+        segs.push_back({sr.r0[1] - cs, Softmax::XSeg{sr.id, rs - sr.r0[0], sr.ext[1]}});
+      }
+      std::sort(segs.begin(), segs.end(), [](auto& a, auto& b) { return a.first < b.first; });
+      const int64_t wdt = srcs[xr][0].ext[1];
+      for (size_t k = 0; k < segs.size() && ok; ++k) ok = segs[k].first == int64_t(k) * wdt && srcs[xr][k].ext[1] == wdt;
+      ok = ok && int64_t(segs.size()) * wdt == sm.len && (w_all == 0 || w_all == wdt);
+      if (!ok) break;
+      w_all = int(wdt);
+      std::vector<Softmax::XSeg> v;
+      for (auto& q : segs) v.push_back(q.second);
+      all.push_back(v);
+    }
+    if (!ok || all.empty()) continue;
+    sm.xsegs = all;
+    sm.seg_w = w_all;
+    for (auto& pr : sm.pairs) virt[pr.second] = 1;
+  }
+
   auto gemm_reads = [&](int jid) {
     std::vector<int> r;
     const int w = X[jid].producer;
@@ -1012,7 +1054,10 @@ void ed_plan_h::build() {
       const Softmax& sm = softmax_[u.producer];
       for (size_t k = 0; k < sm.pairs.size(); ++k)
         if (sm.pairs[k].first == id) {
-          buf[owner[sm.pairs[k].second]].need_main = true;
+          if (!sm.xsegs.empty())
+            for (auto& xs : sm.xsegs[k]) buf[xs.owner].need_main = true;
+          else
+            buf[owner[sm.pairs[k].second]].need_main = true;
           if (!sm.m_refs.empty()) buf[owner[sm.m_refs[k]]].need_main = true;
         }
       continue;
@@ -1256,7 +1301,7 @@ void ed_plan_h::allocate() {
 
   auto resolve = [&](int dep) { return local[dep] ? owner[dep] : dep; };
   size_t gemm_maps_total = 0, gemm_regions_total = 0, jptrs_total = 0, rect_total = 0;
-  size_t attn_maps_total = 0, attn_regions_total = 0;
+  size_t attn_maps_total = 0, attn_regions_total = 0, rowseg_total = 0;
   for (auto& op : ops) {
     const int id = int(reinterpret_cast<intptr_t>(op.ptr));
     switch (op.kind) {
@@ -1606,6 +1651,14 @@ void ed_plan_h::allocate() {
         }
         op.sm.rows = X[sm.pairs[0].first].sz / sm.len;
         op.sm.len = int(sm.len);
+        op.rowsegs.clear();
+        if (!sm.xsegs.empty()) {
+          op.sm.n_seg = int(sm.xsegs[0].size());
+          op.sm.seg_w = sm.seg_w;
+          for (auto& v : sm.xsegs)
+            for (auto& xs : v) op.rowsegs.push_back(RowSeg{static_cast<const float*>(buf[xs.owner].main), xs.row0, xs.stride});
+          rowseg_total += op.rowsegs.size();
+        }
         jptrs_total += op.jptrs.size();
         break;
       }
@@ -1652,6 +1705,17 @@ void ed_plan_h::allocate() {
         jptrs_total += op.jptrs.size();
         break;
       }
+    }
+  }
+  if (rowseg_total) {
+    CUDA_OK(cudaMalloc(&d_rowsegs, sizeof(RowSeg) * rowseg_total));
+    size_t o = 0;
+    for (auto& op : ops) {
+      if (op.rowsegs.empty()) continue;
+      RowSeg* d = static_cast<RowSeg*>(d_rowsegs) + o;
+      CUDA_OK(cudaMemcpy(d, op.rowsegs.data(), sizeof(RowSeg) * op.rowsegs.size(), cudaMemcpyHostToDevice));
+      op.sm.segs = d;
+      o += op.rowsegs.size();
     }
   }
   if (attn_maps_total) {
@@ -1777,6 +1841,7 @@ void ed_plan_h::destroy() {
   if (d_rects) cudaFree(d_rects);
   if (d_copy_desc) cudaFree(d_copy_desc);
   if (d_attn) cudaFree(d_attn);
+  if (d_rowsegs) cudaFree(d_rowsegs);
   if (d_regions) cudaFree(d_regions);
   if (d_ptrs) cudaFree(d_ptrs);
   if (d_err) cudaFree(d_err);
