@@ -112,8 +112,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         const Job J = job_of(p, jb);
         const AttnRegion R = p.regions[J.region];
         const CUtensorMap* mq = p.maps + R.q;
-        const CUtensorMap* mk = p.maps + R.k;
-        const CUtensorMap* mv = p.maps + R.v;
+        auto src_map = [&](const AttnSrc& a, int key, int dcol) {
+          return p.maps + a.base + (key / a.keys) * a.nd + dcol / a.dw;
+        };
         mbar_wait(q_empty, (local & 1) ^ 1);
         mbar_expect_tx(q_full, C_::Q_BYTES);
 #pragma unroll
@@ -125,9 +126,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           uint8_t* sv = sk + C_::K_BYTES;
           mbar_expect_tx(&kv_full[st], C_::STAGE);
 #pragma unroll
-          for (int c = 0; c < D / 64; ++c) tma_load_3d(sk + c * 16384, mk, &kv_full[st], c * 64, j * BKV, J.h);
+          for (int c = 0; c < D / 64; ++c)
+            tma_load_3d(sk + c * 16384, src_map(R.k, j * BKV, c * 64), &kv_full[st], (c * 64) % R.k.dw,
+                        (j * BKV) % R.k.keys, J.h + R.k.hoff);
 #pragma unroll
-          for (int a = 0; a < D / 64; ++a) tma_load_3d(sv + a * (BKV * 128), mv, &kv_full[st], a * 64, j * BKV, J.h);
+          for (int a = 0; a < D / 64; ++a)
+            tma_load_3d(sv + a * (BKV * 128), src_map(R.v, j * BKV, a * 64), &kv_full[st], (a * 64) % R.v.dw,
+                        (j * BKV) % R.v.keys, J.h + R.v.hoff);
         }
       }
     }

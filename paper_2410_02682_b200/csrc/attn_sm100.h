@@ -6,8 +6,17 @@
 namespace ed {
 
 // One output region: indices into AttnLaunch::maps.
+// K and V may be read in place from a regular grid of producer regions
+// (keys x head-dim) instead of a pasted chunk: map index for a 128-key block
+// j and 64-wide d slice c is base + (j*128 / keys) * nd + (c*64) / dw, at
+// coordinates {(c*64) % dw, (j*128) % keys, h + hoff}.
+struct AttnSrc {
+  int base, nd, keys, dw, hoff;
+};
+
 struct AttnRegion {
-  int q, k, v;      // Q [s,h,d], K [s2,h,d] (K-major, box {64, 128}); V [s2,h,d] (MN-major, box {64, 128})
+  int q;            // Q [s,h,d] (K-major, box {64, 128})
+  AttnSrc k, v;     // K [s2,h,d] (K-major), V [s2,h,d] (MN-major), boxes {64, 128}
   int o32, o16;     // O [s,h,d] store maps (box {32|64, 32}), -1 if that dtype is not needed
 };
 

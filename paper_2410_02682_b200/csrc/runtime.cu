@@ -20,6 +20,7 @@
 #include <array>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <numeric>
@@ -418,10 +419,18 @@ struct ed_plan_h {
     std::vector<std::vector<XSeg>> xsegs;         // per pair: x read in place from column segments
     int seg_w = 0;
   };
+  struct KVTiles {                                // K or V read in place from producer regions
+    bool tiled = false;
+    std::vector<int> owners;                      // grid (key block, d block), row-major
+    int nd = 1;
+    int64_t keys = 0, dw = 0, hoff = 0;
+    shape ext;                                    // source region extents (operand label order)
+  };
   struct Flash {                                  // T1 -> softmax -> O in one kernel
     int t1, y, o;
     float scale;
     std::vector<std::array<int, 4>> regions;      // (Q ref, K ref, V ref, O region head)
+    std::vector<KVTiles> ktiles, vtiles;          // per region
   };
   std::map<int, Flash> flash_;                    // O vertex -> fused attention block
   struct Seg {
@@ -904,6 +913,65 @@ void ed_plan_h::build() {
         f.regions.push_back({X[th].deps[gs.a_slot], X[th].deps[gs.b_slot], X[oh].deps[go.b_slot], oh});
       }
       if (!ok || f.regions.empty()) continue;
+      // K (T1's B) and V (O's B): read in place from their producers' regions
+      // when the pasting refinement is a regular grid over (keys, d)
+      auto tile = [&](int ref, const labels& lop, int keyl, int dl, int hl, KVTiles& t) {
+        const Ex& R = X[ref];
+        if (R.kind != ED_EXEC_REFINEMENT || !local[ref] || owner[ref] != ref || virt[ref] || srcs[ref].size() < 2 ||
+            lop.size() != 3)
+          return false;
+        const int kd = int(std::find(lop.begin(), lop.end(), keyl) - lop.begin());
+        const int dd = int(std::find(lop.begin(), lop.end(), dl) - lop.begin());
+        const int hd = int(std::find(lop.begin(), lop.end(), hl) - lop.begin());
+        if (kd > 2 || dd != 2 || hd > 2 || kd == hd) return false;  // d must be the contiguous label
+        const shape& bound = V[R.producer].bound;
+        const shape dc = region_partition(ref);
+        shape cs(3);
+        for (int i = 0; i < 3; ++i) cs[i] = R.key[i] * (bound[i] / dc[i]);
+        const auto& S = srcs[ref];
+        t.keys = S[0].ext[kd];
+        t.dw = S[0].ext[dd];
+        t.hoff = cs[hd] - S[0].r0[hd];
+        t.ext = S[0].ext;
+        if (t.keys % 128 || t.dw % 64 || R.cb[kd] % t.keys || R.cb[dd] % t.dw) return false;
+        const int nk = int(R.cb[kd] / t.keys);
+        t.nd = int(R.cb[dd] / t.dw);
+        t.owners.assign(size_t(nk) * t.nd, -1);
+        for (auto& sr : S) {
+          if (!local[sr.id] || sr.ext != t.ext || cs[hd] - sr.r0[hd] != t.hoff || sr.r0[hd] > cs[hd] ||
+              sr.r0[hd] + sr.ext[hd] < cs[hd] + R.cb[hd])
+            return false;
+          const int64_t ko = sr.r0[kd] - cs[kd], dof = sr.r0[dd] - cs[dd];
+          if (ko % t.keys || dof % t.dw || ko < 0 || dof < 0) return false;
+          int& cell = t.owners[size_t(ko / t.keys) * t.nd + size_t(dof / t.dw)];
+          if (cell >= 0) return false;
+          cell = sr.id;
+        }
+        for (int c : t.owners)
+          if (c < 0) return false;
+        t.tiled = true;
+        return true;
+      };
+      const labels& lk = gs.b_slot == 0 ? V[t1].lx : V[t1].ly;
+      const labels& lv = go.b_slot == 0 ? V[o].lx : V[o].ly;
+      bool kv_ok = true;
+      for (auto& r : f.regions) {
+        KVTiles kt, vt;
+        kv_ok = kv_ok && gs.Nc.size() == 1 && gs.Kc.size() == 1 && gs.Bc.size() == 1 && go.Kc.size() == 1 &&
+                go.Nc.size() == 1 && go.Bc.size() == 1 && tile(r[1], lk, gs.Nc[0], gs.Kc[0], gs.Bc[0], kt) &&
+                tile(r[2], lv, go.Kc[0], go.Nc[0], go.Bc[0], vt);
+        f.ktiles.push_back(kt);
+        f.vtiles.push_back(vt);
+      }
+      if (kv_ok) {
+        for (auto& r : f.regions) {
+          virt[r[1]] = 1;
+          virt[r[2]] = 1;
+        }
+      } else {
+        f.ktiles.assign(f.regions.size(), KVTiles{});
+        f.vtiles.assign(f.regions.size(), KVTiles{});
+      }
       flash_[o] = f;
       flash_skip_.insert(t1);
       flash_skip_.insert(yv);
@@ -1045,9 +1113,19 @@ void ed_plan_h::build() {
     if (!local[id] || virt[id] || virtual_join_src.count(id)) continue;
     const Ex& u = X[id];
     if (u.kind == ED_EXEC_JOIN && flash_.count(u.producer)) {
-      for (auto& r : flash_[u.producer].regions)
-        if (r[3] == id)
-          for (int k = 0; k < 3; ++k) buf[local[r[k]] ? owner[r[k]] : r[k]].need_16 = true;
+      const Flash& f = flash_[u.producer];
+      for (size_t q = 0; q < f.regions.size(); ++q) {
+        const auto& r = f.regions[q];
+        if (r[3] != id) continue;
+        buf[local[r[0]] ? owner[r[0]] : r[0]].need_16 = true;
+        for (int k = 1; k < 3; ++k) {
+          const KVTiles& t = k == 1 ? f.ktiles[q] : f.vtiles[q];
+          if (t.tiled)
+            for (int o2 : t.owners) buf[o2].need_16 = true;
+          else
+            buf[local[r[k]] ? owner[r[k]] : r[k]].need_16 = true;
+        }
+      }
       continue;
     }
     if (u.kind == ED_EXEC_JOIN && softmax_.count(u.producer)) {
@@ -1597,19 +1675,49 @@ void ed_plan_h::allocate() {
         for (auto& r : f.regions) {
           AttnRegion ar{};
           const void* q = buf[resolve(r[0])].b16;
-          const void* k = buf[resolve(r[1])].b16;
-          const void* v = buf[resolve(r[2])].b16;
-          if (!q || !k || !v) throw ed_error(ED_ERR_PLAN, "attention operand buffer missing");
+          const void* k = f.ktiles[size_t(&r - f.regions.data())].tiled ? nullptr : buf[resolve(r[1])].b16;
+          const void* v = f.vtiles[size_t(&r - f.regions.data())].tiled ? nullptr : buf[resolve(r[2])].b16;
+          if (!q) throw ed_error(ED_ERR_PLAN, "attention operand buffer missing");
           CUtensorMap m;
           make_map(&m, q, true, gs.ak.ext, gs.am.ext, gs.am.stride, gs.ab.ext, gs.ab.stride, 64, 128);
           ar.q = int(op.maps.size());
           op.maps.push_back(m);
-          make_map(&m, k, true, gs.bk.ext, gs.bn.ext, gs.bn.stride, gs.bb.ext, gs.bb.stride, 64, 128);
-          ar.k = int(op.maps.size());
-          op.maps.push_back(m);
-          make_map(&m, v, true, go.bn.ext, go.bk.ext, go.bk.stride, go.bb.ext, go.bb.stride, 64, 128);
-          ar.v = int(op.maps.size());
-          op.maps.push_back(m);
+          const size_t ri = size_t(&r - f.regions.data());
+          // K: {d, keys, h}; V: {d, keys, h} — from the pasted chunk, or from each
+          // source region of the grid with that region's own strides
+          auto kv_maps = [&](const KVTiles& t, const void* chunk, const Dim& dk, const Dim& keys, const Dim& hb,
+                             const labels& lop, int keyl, int hl, AttnSrc& out) {
+            out.base = int(op.maps.size());
+            if (!t.tiled) {
+              make_map(&m, chunk, true, dk.ext, keys.ext, keys.stride, hb.ext, hb.stride, 64, 128);
+              op.maps.push_back(m);
+              out.nd = 1;
+              out.keys = int(keys.ext);
+              out.dw = int(dk.ext);
+              out.hoff = 0;
+              return;
+            }
+            const int kd = int(std::find(lop.begin(), lop.end(), keyl) - lop.begin());
+            const int hd = int(std::find(lop.begin(), lop.end(), hl) - lop.begin());
+            shape st(3, 1);
+            for (int i = 1; i >= 0; --i) st[i] = st[i + 1] * t.ext[i + 1];
+            for (int o2 : t.owners) {
+              const void* b = buf[o2].b16;
+              if (!b) throw ed_error(ED_ERR_PLAN, "attention source buffer missing");
+              make_map(&m, b, true, t.ext[2], t.ext[kd], st[kd], t.ext[hd], st[hd], 64, 128);
+              op.maps.push_back(m);
+            }
+            out.nd = t.nd;
+            out.keys = int(t.keys);
+            out.dw = int(t.dw);
+            out.hoff = int(t.hoff);
+          };
+          const labels& lk = gs.b_slot == 0 ? V[f.t1].lx : V[f.t1].ly;
+          const labels& lv = go.b_slot == 0 ? V[f.o].lx : V[f.o].ly;
+          kv_maps(f.ktiles[ri], k, gs.bk, gs.bn, gs.bb, lk, gs.Nc.empty() ? -1 : gs.Nc[0], gs.Bc.empty() ? -1 : gs.Bc[0],
+                  ar.k);
+          kv_maps(f.vtiles[ri], v, go.bn, go.bk, go.bb, lv, go.Kc.empty() ? -1 : go.Kc[0], go.Bc.empty() ? -1 : go.Bc[0],
+                  ar.v);
           auto out_map = [&](void* base, bool o16) {
             const int oes = o16 ? 2 : 4;
             bool ok = base && (go.cm.ext == 1 || (go.cm.stride * oes) % 16 == 0) &&

@@ -145,6 +145,25 @@ def _vertex_tensor(pp, plan, w, torch):
             return out
         except Exception:
             continue
+    # no materialised refinement layer (consumers read the producer's regions
+    # in place): assemble from the region accumulators (region-head joins)
+    if v.expr is not None:
+        dls = v.expr.distinct_labels()
+        out = torch.empty(v.bound, dtype=torch.float64, device="cuda")
+        seen = torch.zeros(v.bound, dtype=torch.bool, device="cuda")
+        for u in plan.exec:
+            if u.kind != 1 or u.producer != w:
+                continue
+            try:
+                chunk = torch.from_numpy(pp.download_chunk(u.id)).cuda()
+            except Exception:
+                continue
+            key = [u.key[dls.index(l)] for l in v.expr.out]
+            sl = tuple(slice(k * c, (k + 1) * c) for k, c in zip(key, u.chunk_bound))
+            out[sl] = chunk
+            seen[sl] = True
+        if bool(seen.all()):
+            return out
     return None
 
 
