@@ -26,7 +26,14 @@ struct AttnLaunch {
   int n_regions;
   int H, S, T, D;              // heads, query rows, keys, head dim (per region)
   float scale;                 // scale of the fused T2 vertex (1 if none)
+  int n_pair_jobs, n_jobs;     // set by attn_schedule (launch_attn calls it)
+  long long* trace;            // debug event timestamps (ED_ATTN_TRACE), else null
 };
+
+// Split the (region, head, 128-row tile) space into tile-pair jobs and, for
+// the last wave, single-tile jobs, so that every CTA of the persistent grid
+// finishes at about the same time.
+void attn_schedule(AttnLaunch& p, int num_sms);
 
 bool attn_supported(int S, int T, int D);
 cudaError_t attn_prepare();

@@ -61,8 +61,16 @@ __device__ __forceinline__ TileCoord tile_coord(const GemmLaunch& p, int t, int 
   int r = t - c.region * per_region;
   c.b = r / per_batch;
   r -= c.b * per_batch;
-  c.m0 = (r / tiles_n) * TILE_M;
-  c.n0 = (r % tiles_n) * BN;
+  // grouped raster: kGroupM tile rows advance together along N, so one wave
+  // of ~74 cluster tiles touches ~8 A panels + ~9 B panels instead of
+  // 3 + tiles_n, and the panels it shares stay in L2 (hoc: 8192^2 tiles)
+  constexpr int kGroupM = 8;
+  const int g = r / (kGroupM * tiles_n);
+  const int gm0 = g * kGroupM;
+  const int gsz = tiles_m - gm0 < kGroupM ? tiles_m - gm0 : kGroupM;
+  const int rg = r - g * kGroupM * tiles_n;
+  c.m0 = (gm0 + rg % gsz) * TILE_M;
+  c.n0 = (rg / gsz) * BN;
   return c;
 }
 
