@@ -165,7 +165,7 @@ def run_reference(args, rank, world):
     v = statistics.median(vals)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOP/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["seconds"] * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference generate_inputs)",
             "config": {"workload": CONFIG_DESC.get(args.config, args.config), "graph": args.config,
                        "p": 8, "sample": cb["sample"]},
@@ -184,6 +184,9 @@ def main():
     ap.add_argument("--impl", default="ours")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--placement", default="gpu", choices=["gpu", "ref"],
+                    help="gpu: GPU-aware re-placement of memory-bound vertices (ed_gpu_placement); "
+                         "ref: the reference planner's machine_of")
     args = ap.parse_args()
     rank, world, local = dist_env()
     if args.impl == "reference":
@@ -209,6 +212,11 @@ def main():
 
     L = world
     plan = Plan.load(os.path.join(ROOT, "plans", f"{args.config}_p8_L{L}.json"))
+    est = None
+    if args.placement == "gpu" and L > 1:
+        from paper_2410_02682_b200.executor import gpu_placement
+        plan, b_ms, a_ms = gpu_placement(plan)
+        est = {"est_busiest_ms_ref": b_ms, "est_busiest_ms_gpu": a_ms}
     ins = synthetic_inputs(plan, 1234)
 
     def barrier():
@@ -304,9 +312,11 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": args.precision,
-                "data": "synthetic (integer [-4,4] like generate_inputs, numpy-seeded)",
+                "data": ("synthetic, numpy-seeded: " + ("integers in [-4,4]" if plan.integer_valued() else "U[-1,1)")
+                         + " like generate_inputs (runtime.cc:552-571)"),
                 "config": {"workload": CONFIG_DESC.get(args.config, args.config), "graph": args.config,
                            "p": 8, "L": L, "plan": f"plans/{args.config}_p8_L{L}.json",
+                           "placement": args.placement if L > 1 else "single GPU", "placement_estimate": est,
                            "l2": "inputs larger than L2 (1 GiB per input tensor); no flush needed",
                            "frac_of_peak": value / (pk * world)},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,

@@ -251,6 +251,28 @@ ED_API ed_status ed_download_chunk(struct ed_plan_h* h, int32_t exec_id, int32_t
 ED_API ed_status ed_plan_schedule(const ed_plan_c* plan, int32_t rank, int32_t world, ed_sched_op_c* out,
                                   int32_t cap, int32_t* n_out, char* err, size_t errlen);
 
+/* Device cost model for ed_gpu_placement (rates in units per second). */
+typedef struct {
+  double tensor_flops;       /* contraction rate per GPU (e.g. measured bf16 peak) */
+  double hbm_bytes;          /* memory-bound kernel rate per GPU (measured copy bandwidth) */
+  double link_bytes;         /* GPU-to-GPU rate per direction (NVLink 5) */
+  int32_t elem_bytes;        /* bytes per stored element (4: f32, 8: f64) */
+  int32_t max_passes;        /* local-search passes (0: default 4) */
+} ed_cost_model_c;
+
+/* Host-only (no GPU needed). GPU-aware re-placement:
+ * starting from the plan's machine_of (place_all, placement.cc:132-178),
+ * moves memory-bound exec vertices (non-contraction joins and refinements)
+ * between machines to minimise the estimated busiest-GPU time — compute at
+ * the cost model's rates plus whole-chunk transfers over the links — ties
+ * broken by transfer volume. Input chunks and mul/sum contraction joins keep
+ * their machines; the exec graph, keys and fold order are untouched, so the
+ * results are bitwise those of the original placement (acceptance.cc:241-250).
+ * machine_of: n_exec entries, written. est_ms (nullable, 2 entries): the
+ * estimated busiest-GPU milliseconds before and after. */
+ED_API ed_status ed_gpu_placement(const ed_plan_c* plan, const ed_cost_model_c* model, int32_t* machine_of,
+                                  double* est_ms, char* err, size_t errlen);
+
 /* Per-launch-class timings of the last profiled ed_run. */
 ED_API ed_status ed_kernel_stats(struct ed_plan_h* h, ed_kernel_stat_c* out, int32_t cap,
                           int32_t* n_out, char* err, size_t errlen);

@@ -47,6 +47,11 @@ def ref():
                                       C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_int,
                                       C.POINTER(C.c_void_p), C.POINTER(C.c_double),
                                       C.POINTER(C.c_int64), C.POINTER(C.c_int64)] + err
+        lib.edref_execute_placed.argtypes = [C.c_char_p, C.c_int64, C.c_int64, C.c_double, C.c_char_p,
+                                             C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_int,
+                                             C.POINTER(C.c_int32), C.c_int32,
+                                             C.POINTER(C.c_void_p), C.POINTER(C.c_double),
+                                             C.POINTER(C.c_int64), C.POINTER(C.c_int64)] + err
         lib.edref_eval_reference.argtypes = [C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)] + err
         lib.edref_eval_vertex.argtypes = [C.c_char_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p] + err
         _ref = lib
@@ -118,9 +123,10 @@ def ref_generate_input(graph_text: str, seed: int, vid: int, shape) -> np.ndarra
     return out.reshape(shape)
 
 
-def ref_execute(plan_doc: dict, inputs: dict, threaded=True, f32=False, corrupt=False):
+def ref_execute(plan_doc: dict, inputs: dict, threaded=True, f32=False, corrupt=False, machine_of=None):
     """Runs the reference run_end_to_end flow (planner re-run from the graph
     text, same p/L/alpha/pins, so the plan is identical). inputs: vid -> f64.
+    machine_of (optional) replaces the planner's placement_t::machine_of.
     Returns (outputs dict vid->array, execute seconds, counters, total)."""
     g = plan_doc["graph_text"]
     verts = plan_doc["vertices"]
@@ -135,9 +141,11 @@ def ref_execute(plan_doc: dict, inputs: dict, threaded=True, f32=False, corrupt=
     total = C.c_int64()
     err = C.create_string_buffer(1024)
     pj = json.dumps(plan_doc["pinned"]).encode() if plan_doc.get("pinned") else None
-    _check(ref().edref_execute(g.encode(), plan_doc["p"], L, plan_doc["alpha"], pj, ins,
-                               int(threaded), int(f32), int(corrupt), outs, C.byref(secs),
-                               counters, C.byref(total), err, 1024), err)
+    mo = (C.c_int32 * len(machine_of))(*machine_of) if machine_of is not None else None
+    _check(ref().edref_execute_placed(g.encode(), plan_doc["p"], L, plan_doc["alpha"], pj, ins,
+                                      int(threaded), int(f32), int(corrupt), mo,
+                                      len(machine_of) if machine_of is not None else 0, outs, C.byref(secs),
+                                      counters, C.byref(total), err, 1024), err)
     cnt = [(counters[3 * m], counters[3 * m + 1], counters[3 * m + 2]) for m in range(L)]
     return dict(zip(plan_doc["outputs"], outs_np)), secs.value, cnt, total.value
 

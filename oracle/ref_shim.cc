@@ -254,15 +254,25 @@ int edref_generate_input(const char* graph_text, uint64_t seed, int vid,
 // alone. inputs: one full row-major tensor per graph vertex (nullptr for
 // expression vertices). outputs: one buffer per graph output, in
 // graph.outputs order. counters: 3 per machine (fp, sent, received).
-int edref_execute(const char* graph_text, int64_t p, int64_t n_machines, double alpha,
-                  const char* pinned_json, const double* const* inputs,
-                  int threaded, int f32, int corrupt,
-                  double* const* outputs, double* exec_seconds,
-                  int64_t* counters, int64_t* total_transferred,
-                  char* err, size_t errlen) {
+// machine_of (nullable, one entry per exec vertex) overrides the planner's
+// placement_t::machine_of — e.g. a GPU-aware re-placement under test.
+int edref_execute_placed(const char* graph_text, int64_t p, int64_t n_machines, double alpha,
+                         const char* pinned_json, const double* const* inputs,
+                         int threaded, int f32, int corrupt, const int32_t* machine_of, int32_t n_machine_of,
+                         double* const* outputs, double* exec_seconds,
+                         int64_t* counters, int64_t* total_transferred,
+                         char* err, size_t errlen) {
   return guarded(err, errlen, [&] {
     auto g = parse_eingraph(graph_text);
     auto pipe = make_pipeline(g, p, n_machines, alpha, pinned_json);
+    if(machine_of) {
+      if(size_t(n_machine_of) != pipe.placement.machine_of.size()) {
+        throw std::runtime_error("machine_of size differs from the exec graph");
+      }
+      for(size_t i = 0; i != pipe.placement.machine_of.size(); ++i) {
+        pipe.placement.machine_of[i] = machine_of[i];
+      }
+    }
     auto ins = wrap_inputs(g, inputs);
     map<int, tensor_relation_t> chunked;
     for(auto const& [vid, t]: ins) {
@@ -295,6 +305,16 @@ int edref_execute(const char* graph_text, int64_t p, int64_t n_machines, double 
       *total_transferred = report.total_transferred;
     }
   });
+}
+
+int edref_execute(const char* graph_text, int64_t p, int64_t n_machines, double alpha,
+                  const char* pinned_json, const double* const* inputs,
+                  int threaded, int f32, int corrupt,
+                  double* const* outputs, double* exec_seconds,
+                  int64_t* counters, int64_t* total_transferred,
+                  char* err, size_t errlen) {
+  return edref_execute_placed(graph_text, p, n_machines, alpha, pinned_json, inputs, threaded, f32, corrupt,
+                              nullptr, 0, outputs, exec_seconds, counters, total_transferred, err, errlen);
 }
 
 // Dense oracle over the whole graph: outs has one buffer per graph vertex

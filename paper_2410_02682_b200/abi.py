@@ -130,11 +130,16 @@ class ed_sched_op_c(C.Structure):
 SCHED_COMPUTE, SCHED_SEND, SCHED_RECV = 0, 1, 2
 
 
+class ed_cost_model_c(C.Structure):
+    _fields_ = [("tensor_flops", C.c_double), ("hbm_bytes", C.c_double), ("link_bytes", C.c_double),
+                ("elem_bytes", C.c_int32), ("max_passes", C.c_int32)]
+
+
 # Every symbol include/ed_gpu.h declares (tests/test_abi.py checks exports).
 EXPORTED = [
     "ed_abi_version", "ed_nccl_unique_id", "ed_ctx_create", "ed_ctx_destroy",
     "ed_prepare", "ed_plan_destroy", "ed_upload", "ed_upload_tensors", "ed_run",
-    "ed_download", "ed_download_chunk", "ed_plan_schedule", "ed_kernel_stats",
+    "ed_download", "ed_download_chunk", "ed_plan_schedule", "ed_kernel_stats", "ed_gpu_placement",
 ]
 
 
@@ -159,6 +164,8 @@ def declare(lib):
     lib.ed_plan_schedule.argtypes = [C.POINTER(ed_plan_c), C.c_int32, C.c_int32, C.POINTER(ed_sched_op_c),
                                      C.c_int32, i32p] + err
     lib.ed_kernel_stats.argtypes = [P, C.POINTER(ed_kernel_stat_c), C.c_int32, i32p] + err
+    lib.ed_gpu_placement.argtypes = [C.POINTER(ed_plan_c), C.POINTER(ed_cost_model_c), i32p,
+                                     C.POINTER(C.c_double)] + err
     for name in EXPORTED[1:]:
         f = getattr(lib, name)
         if f.restype is C.c_int:  # default

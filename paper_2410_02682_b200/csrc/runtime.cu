@@ -1,14 +1,15 @@
 // libed_gpu: the B200 executor behind include/ed_gpu.h.
 //
 // Replaces execute() (runtime.cc:382-451). ed_prepare turns the placed
-// ExecGraph into a static schedule of kernel launches on one stream:
+// ExecGraph into a static schedule of kernel launches on a compute stream:
 //   * mul/sum joins of one output region -> ONE tcgen05 GEMM whose K loop
 //     runs over the region's aggregation siblings, so the sibling fold of the
 //     refinement (runtime.cc:242-261) happens in the TMEM accumulator;
 //   * every other join -> the exact generic inner-EinSum kernel;
 //   * refinements that are a single same-shape dependency -> aliases (no
 //     copy); all others -> the ordered gather/fold kernel;
-//   * remote dependencies (world > 1) -> NCCL send/recv on a comm stream.
+//   * remote dependencies (world > 1) -> NCCL send/recv groups on a comm
+//     stream that forks from / joins the compute stream (enqueue()).
 // The schedule is captured once into a CUDA graph and replayed by ed_run.
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -508,6 +509,8 @@ struct ed_plan_h {
   void allocate();
   void record();
   void launch_op(size_t i, cudaStream_t s);
+  void enqueue(cudaStream_t s);
+  std::vector<cudaEvent_t> comm_events;  // fork / join points of the comm stream
   void destroy();
 };
 
@@ -1916,6 +1919,57 @@ void ed_plan_h::launch_op(size_t i, cudaStream_t s) {
   }
 }
 
+// Every op in schedule order on the compute stream, except that each run of
+// consecutive transfers goes to the comm stream as ONE NCCL group (the
+// exchange of a repartition proceeds with all peers at once). The comm
+// stream forks from the compute stream before a run that sends (its
+// operands are produced by then) and the compute stream joins it right
+// after the run: transfers sit just before their data's first consumer, so
+// the sender keeps computing while its sends drain and a receiver's recvs
+// are posted as soon as the comm stream reaches them, ahead of its compute.
+// Buffers are never reused within a run (linear arena), so an early recv
+// cannot overwrite live data. Ranks enqueue the same transfers in the same
+// global order (transfers_by_consumer), so the groups match.
+void ed_plan_h::enqueue(cudaStream_t s) {
+  cudaStream_t cs = ctx->comm_stream;
+  size_t ev = 0;
+  auto next_event = [&]() {
+    if (ev == comm_events.size()) {
+      cudaEvent_t e;
+      CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      comm_events.push_back(e);
+    }
+    return comm_events[ev++];
+  };
+  auto is_comm = [&](size_t i) { return ops[i].kind == OpKind::SEND || ops[i].kind == OpKind::RECV; };
+  for (size_t i = 0; i < ops.size();) {
+    if (!is_comm(i)) {
+      if (opt.profile) CUDA_OK(cudaEventRecord(op_events[i], s));
+      launch_op(i, s);
+      ++i;
+      continue;
+    }
+    size_t j = i;
+    bool sends = false;
+    for (; j < ops.size() && is_comm(j); ++j) sends = sends || ops[j].kind == OpKind::SEND;
+    if (opt.profile)
+      for (size_t k = i; k < j; ++k) CUDA_OK(cudaEventRecord(op_events[k], s));
+    if (sends) {
+      cudaEvent_t fork = next_event();
+      CUDA_OK(cudaEventRecord(fork, s));
+      CUDA_OK(cudaStreamWaitEvent(cs, fork, 0));
+    }
+    NCCL_OK(ncclGroupStart());
+    for (size_t k = i; k < j; ++k) launch_op(k, cs);
+    NCCL_OK(ncclGroupEnd());
+    cudaEvent_t join = next_event();
+    CUDA_OK(cudaEventRecord(join, cs));
+    CUDA_OK(cudaStreamWaitEvent(s, join, 0));
+    i = j;
+  }
+  if (opt.profile) CUDA_OK(cudaEventRecord(op_events[ops.size()], s));
+}
+
 void ed_plan_h::record() {
   CUDA_OK(gemm_prepare());
   CUDA_OK(attn_prepare());
@@ -1925,7 +1979,7 @@ void ed_plan_h::record() {
   cudaStream_t s = ctx->stream;
   CUDA_OK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
   try {
-    for (size_t i = 0; i < ops.size(); ++i) launch_op(i, s);
+    enqueue(s);
   } catch (...) {
     cudaGraph_t g;
     cudaStreamEndCapture(s, &g);
@@ -1942,6 +1996,7 @@ void ed_plan_h::destroy() {
   if (ev0) cudaEventDestroy(ev0);
   if (ev1) cudaEventDestroy(ev1);
   for (auto e : op_events) cudaEventDestroy(e);
+  for (auto e : comm_events) cudaEventDestroy(e);
   if (arena) cudaFree(arena);
   if (d_deps) cudaFree(d_deps);
   if (d_maps) cudaFree(d_maps);
@@ -2239,15 +2294,8 @@ ed_status ed_run(ed_plan_h* h, ed_report_c* rep, char* err, size_t errlen) {
       for (auto& e : h->op_events) CUDA_OK(cudaEventCreate(&e));
     }
     CUDA_OK(cudaEventRecord(h->ev0, s));
-    if (h->gexec) {
-      CUDA_OK(cudaGraphLaunch(h->gexec, s));
-    } else {
-      for (size_t i = 0; i < h->ops.size(); ++i) {
-        if (h->opt.profile) CUDA_OK(cudaEventRecord(h->op_events[i], s));
-        h->launch_op(i, s);
-      }
-      if (h->opt.profile) CUDA_OK(cudaEventRecord(h->op_events[h->ops.size()], s));
-    }
+    if (h->gexec) CUDA_OK(cudaGraphLaunch(h->gexec, s));
+    else h->enqueue(s);
     CUDA_OK(cudaEventRecord(h->ev1, s));
     CUDA_OK(cudaEventSynchronize(h->ev1));
     int flag = 0;
@@ -2395,6 +2443,139 @@ ed_status ed_plan_schedule(const ed_plan_c* plan, int32_t rank, int32_t world, e
     }
     for (int i = 0; i < std::min<int>(cap, int(ops.size())); ++i) out[i] = ops[i];
     *n_out = int(ops.size());
+  });
+}
+
+namespace {
+
+// Estimated per-machine busy time of a placement (seconds): each vertex's
+// kernel time at the model's rates plus whole-chunk transfers, charged to
+// sender and receiver once per (chunk, destination machine) like pull()
+// (runtime.cc:157-172). Refinements the executor turns into aliases or
+// folds inside a region-fused GEMM (all deps local) cost nothing.
+struct SiteModel {
+  const ed_plan_h& h;
+  const ed_cost_model_c& cm;
+  std::vector<char> contraction;  // exec id is a mul/sum join
+  std::vector<char> fold_free;    // refinement free when co-located with all deps
+
+  SiteModel(const ed_plan_h& h_, const ed_cost_model_c& cm_) : h(h_), cm(cm_) {
+    const int ne = int(h.X.size());
+    contraction.assign(ne, 0);
+    fold_free.assign(ne, 0);
+    for (int id = 0; id < ne; ++id) {
+      const Ex& u = h.X[id];
+      if (u.kind == ED_EXEC_JOIN) {
+        const Vtx& w = h.V[u.producer];
+        contraction[id] = w.join == ED_JOIN_MUL && w.agg == ED_AGG_SUM;
+      }
+    }
+    for (int id = 0; id < ne; ++id) {
+      const Ex& u = h.X[id];
+      if (u.kind != ED_EXEC_REFINEMENT || u.deps.empty()) continue;
+      bool same = true;
+      for (int d : u.deps) same = same && h.X[d].sz == u.sz;
+      const bool identity = u.deps.size() == 1 && same;
+      bool siblings = same;
+      for (int d : u.deps) siblings = siblings && contraction[d] && h.X[d].producer == h.X[u.deps[0]].producer;
+      fold_free[id] = identity || siblings;
+    }
+  }
+
+  double comp(int id, const std::vector<int>& m) const {
+    const Ex& u = h.X[id];
+    const double es = cm.elem_bytes;
+    if (u.kind == ED_EXEC_INPUT_CHUNK) return 0.0;
+    if (u.kind == ED_EXEC_JOIN) {
+      if (contraction[id]) return 2.0 * double(u.fp) / cm.tensor_flops;
+      double el = double(u.sz);
+      for (int d : u.deps) el += double(h.X[d].sz);
+      return el * es / cm.hbm_bytes;
+    }
+    bool colocated = true;
+    for (int d : u.deps) colocated = colocated && m[d] == m[id];
+    if (fold_free[id] && colocated) return 0.0;
+    double el = double(u.sz);
+    for (int d : u.deps) el += double(std::min(h.X[d].sz, u.sz));
+    return el * es / cm.hbm_bytes;
+  }
+
+  // (busiest machine seconds, total transferred elements)
+  std::pair<double, double> eval(const std::vector<int>& m) const {
+    std::vector<double> site(size_t(h.n_machines), 0.0);
+    std::set<std::pair<int, int>> pulled;
+    double moved = 0.0;
+    for (int id = 0; id < int(h.X.size()); ++id) {
+      const Ex& u = h.X[id];
+      if (u.kind == ED_EXEC_INPUT_CHUNK) continue;
+      site[size_t(m[id])] += comp(id, m);
+      for (int d : u.deps)
+        if (m[d] != m[id] && pulled.insert({d, m[id]}).second) {
+          const double t = double(h.X[d].sz) * cm.elem_bytes / cm.link_bytes;
+          site[size_t(m[id])] += t;
+          site[size_t(m[d])] += t;
+          moved += double(h.X[d].sz);
+        }
+    }
+    return {*std::max_element(site.begin(), site.end()), moved};
+  }
+};
+
+}  // namespace
+
+ed_status ed_gpu_placement(const ed_plan_c* plan, const ed_cost_model_c* model, int32_t* machine_of, double* est_ms,
+                           char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!plan || !model || !machine_of) throw ed_error(ED_ERR_USAGE, "null argument");
+    if (!(model->tensor_flops > 0 && model->hbm_bytes > 0 && model->link_bytes > 0 && model->elem_bytes > 0))
+      throw ed_error(ED_ERR_USAGE, "cost model rates must be positive");
+    ed_ctx c;
+    c.world = std::max(1, plan->n_machines);
+    ed_plan_h h;
+    h.ctx = &c;
+    h.copy_plan(plan);
+    h.validate();
+    const int ne = int(h.X.size());
+    std::vector<int> m(static_cast<size_t>(ne));
+    for (int id = 0; id < ne; ++id) m[size_t(id)] = h.X[id].machine;
+    const SiteModel sm(h, *model);
+    auto cur = sm.eval(m);
+    const double before = cur.first;
+    auto better = [](std::pair<double, double> a, std::pair<double, double> b) {
+      const double tol = 1e-12 * std::max(1.0, b.first);
+      return a.first < b.first - tol || (std::abs(a.first - b.first) <= tol && a.second < b.second);
+    };
+    const int passes = model->max_passes > 0 ? model->max_passes : 4;
+    for (int pass = 0; pass < passes; ++pass) {
+      bool changed = false;
+      for (int id = 0; id < ne; ++id) {
+        const Ex& u = h.X[id];
+        if (u.kind == ED_EXEC_INPUT_CHUNK || sm.contraction[size_t(id)]) continue;
+        const int home = m[size_t(id)];
+        int best = home;
+        auto best_c = cur;
+        for (int l = 0; l < h.n_machines; ++l) {
+          if (l == home) continue;
+          m[size_t(id)] = l;
+          auto cl = sm.eval(m);
+          if (better(cl, best_c)) {
+            best_c = cl;
+            best = l;
+          }
+        }
+        m[size_t(id)] = best;
+        if (best != home) {
+          cur = best_c;
+          changed = true;
+        }
+      }
+      if (!changed) break;
+    }
+    for (int id = 0; id < ne; ++id) machine_of[id] = m[size_t(id)];
+    if (est_ms) {
+      est_ms[0] = before * 1e3;
+      est_ms[1] = cur.first * 1e3;
+    }
   });
 }
 

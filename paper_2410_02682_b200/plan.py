@@ -181,6 +181,15 @@ class Plan:
         return Plan(None, n_machines, alpha, verts, outputs, ex, taskgraph.get("predicted_cost", 0),
                     {"taskgraph": taskgraph, "execgraph": execgraph})
 
+    def with_machines(self, machine_of) -> "Plan":
+        """The same plan under another placement (placement_t::machine_of):
+        exec graph, keys and fold order unchanged."""
+        import dataclasses
+        if len(machine_of) != len(self.exec):
+            raise ValueError("machine_of needs one entry per exec vertex")
+        ex = [dataclasses.replace(u, deps=list(u.deps), machine=int(m)) for u, m in zip(self.exec, machine_of)]
+        return dataclasses.replace(self, exec=ex)
+
     @staticmethod
     def load(path) -> "Plan":
         with open(path) as f:

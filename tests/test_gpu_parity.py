@@ -231,3 +231,25 @@ def test_missing_input_is_a_plan_error(gpu_ctx):
     with pytest.raises(PlanError):
         pp.upload({99: np.zeros(4)})
     pp.close()
+
+
+REPLACED = ["attention_p8_L4_s1084", "mix_p4_L2_s41", "chain8_pinned_L4_s7", "ffnn_p4_L4_s1044",
+            "matmul_p8_L4_s1084"]
+
+
+@pytest.mark.parametrize("case", REPLACED)
+def test_gpu_placement_keeps_results(gpu_ctx, case):
+    """the GPU-aware re-placement runs to the reference's
+    outputs bit for bit (placement-independent, acceptance.cc:241-250), and
+    its counters are the reference accounting under the new machine_of (the
+    oracle, pinned to the reference in tests/test_placement.py)."""
+    from paper_2410_02682_b200.executor import gpu_placement
+    name, ins, o64, o32, orc, counters, total = load_golden(case)
+    plan = load_plan(name)
+    new, before, after = gpu_placement(plan)
+    assert after <= before
+    rep = _run(gpu_ctx, new, ins, "fp64")
+    for vid, a in o64.items():
+        _assert_matches(rep.outputs[vid], a, case, vid, "fp64", plan)
+    _, _, cnt, tot = B.oracle_execute(new, ins)
+    assert rep.machines == cnt and rep.total_transferred == tot

@@ -15,8 +15,17 @@ import pytest
 
 from conftest import ROOT, load_plan
 
+# "+gpu": the plan after the GPU-aware re-placement (ed_gpu_placement)
 CASES = [("chain8_pinned_L2", 2), ("ffnn_p4_L2", 2), ("attention_p8_L4", 4), ("attention_p8_L4", 2),
-         ("matmul8_pinned_L16", 4), ("mix_p4_L2", 2), ("softmax_p8_L4", 4)]
+         ("matmul8_pinned_L16", 4), ("mix_p4_L2", 2), ("softmax_p8_L4", 4), ("attention_p8_L4+gpu", 4),
+         ("ffnn_p8_L8+gpu", 4), ("mix_p4_L2+gpu", 2)]
+
+
+def _plan(name):
+    if name.endswith("+gpu"):
+        from paper_2410_02682_b200.executor import gpu_placement
+        return gpu_placement(load_plan(name[:-4]))[0]
+    return load_plan(name)
 
 
 def _free_port():
@@ -41,7 +50,7 @@ def _worker(rank, world, name, port, q):
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
         dist.init_process_group("gloo", rank=rank, world_size=world, timeout=timedelta(seconds=60))
-        plan = load_plan(name)
+        plan = _plan(name)
         ins = B.generate_inputs(plan, 5)
         _, want, _, total = B.oracle_execute(plan, ins, want_chunks=True)
         rank_of = lambda i: plan.exec[i].machine % world  # noqa: E731
@@ -96,7 +105,7 @@ def test_schedule_replay_over_gloo(name, world):
         p.join(timeout=60)
     for rank, status, sent, total in res:
         assert status == "ok", f"rank {rank}: {status}"
-    plan = load_plan(name)
+    plan = _plan(name)
     if world == plan.n_machines:
         # with one rank per machine the peer traffic is exactly the
         # reference's whole-chunk accounting (runtime.cc:119-172)
@@ -110,7 +119,7 @@ def test_schedule_is_a_global_order():
     build.build()
     from paper_2410_02682_b200.executor import plan_schedule
     for name, world in CASES:
-        plan = load_plan(name)
+        plan = _plan(name)
         per = [[(k, e, p) for k, e, p, _ in plan_schedule(plan, r, world) if k != "compute"] for r in range(world)]
         for a in range(world):
             for b in range(world):

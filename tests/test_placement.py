@@ -1,0 +1,75 @@
+"""GPU-aware re-placement (ed_gpu_placement), host-only.
+
+The re-placer may move memory-bound exec vertices between machines; it must
+never touch input chunks or contraction joins, never make the estimate worse,
+and — because results are placement-independent (acceptance.cc:241-250) —
+the re-placed plan must give bitwise the reference's outputs, while its
+transfer counters must equal what the UNMODIFIED reference execute()
+(runtime.cc:119-172) reports under the same machine_of.
+"""
+import numpy as np
+import pytest
+
+from conftest import load_plan
+from oracle import bridge as B
+from paper_2410_02682_b200 import build
+from paper_2410_02682_b200.executor import gpu_placement
+
+build.build()
+
+# small plans the re-placer actually changes (2-28 vertices moved)
+SMALL = ["attention_p8_L4", "mix_p4_L2", "chain8_pinned_L4", "ffnn_p8_L8", "attention_p8_L8", "ffnn_p4_L4",
+         "matmul_p8_L8"]
+BIG = ["ffnn_big_p8_L8", "attn_big_p8_L8", "attn_big_p8_L4", "bmm2_repart_p8_L8", "chain3_p8_L8", "hoc_p8_L8"]
+
+
+def _contraction(plan, u):
+    e = plan.vertices[u.producer].expr
+    return u.kind == 1 and e.join == "mul" and e.agg == "sum"
+
+
+@pytest.mark.parametrize("name", SMALL + BIG)
+def test_replacement_moves_only_memory_bound_vertices(name):
+    plan = load_plan(name)
+    new, before, after = gpu_placement(plan)
+    assert after <= before + 1e-12
+    for u, v in zip(plan.exec, new.exec):
+        assert (u.kind, u.key, u.deps, u.fp, u.sz) == (v.kind, v.key, v.deps, v.fp, v.sz)
+        assert 0 <= v.machine < plan.n_machines
+        if u.kind == 0 or _contraction(plan, u):
+            assert v.machine == u.machine, (name, u.id)
+
+
+def test_replacement_balances_the_ffnn_softmax():
+    """The reference piles FFNN's softmax vertices on GPUs 0-1;
+    the re-placer spreads them and cuts the estimated busiest-GPU time."""
+    plan = load_plan("ffnn_big_p8_L8")
+    new, before, after = gpu_placement(plan)
+    assert after < 0.85 * before
+    sm = plan.find("SM.max")
+    used = {new.exec[j].machine for j in plan.joins_of(sm)}
+    assert len(used) > 2
+
+
+def test_replacement_is_deterministic():
+    plan = load_plan("attn_big_p8_L8")
+    a = gpu_placement(plan)[0]
+    b = gpu_placement(plan)[0]
+    assert [u.machine for u in a.exec] == [u.machine for u in b.exec]
+
+
+@pytest.mark.skipif(not B.have_ref(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("name", SMALL)
+def test_replaced_plan_matches_reference(name):
+    plan = load_plan(name)
+    new, _, _ = gpu_placement(plan)
+    assert any(u.machine != v.machine for u, v in zip(plan.exec, new.exec))
+    ins = B.generate_inputs(plan, 11)
+    machines = [u.machine for u in new.exec]
+    want, _, ref_cnt, ref_total = B.ref_execute(plan.source, ins, threaded=False, machine_of=machines)
+    base, _, _, _ = B.ref_execute(plan.source, ins, threaded=False)
+    got, _, cnt, total = B.oracle_execute(new, ins)
+    for vid in plan.outputs:
+        assert np.array_equal(want[vid], base[vid]), "reference outputs depend on placement"
+        assert np.array_equal(got[vid], want[vid])
+    assert cnt == ref_cnt and total == ref_total
