@@ -8,9 +8,10 @@
 //
 // Label permutations are folded into 3-D TMA tensor maps {inner, outer,
 // batch} — K-major or MN-major per operand — so no transpose copy runs.
-// kCta = 2 pairs two SMs as one cluster (tcgen05 cta_group::2): a 256x256
+// kCta = 2 pairs two SMs as one cluster (tcgen05 cta_group::2): a 256xBN
 // tile per pair, each CTA loading half of A and half of B, so per-SM operand
-// traffic drops by a third and the smem ring gets six stages.
+// traffic drops by a third. BN = 256, or 128 for launches too small to
+// fill half the grid with 256-wide tiles (gemm_pick_bn).
 // Warp roles (192 threads, 1 CTA per SM):
 //   warp 0     TMA producer over a STAGES-deep smem ring (full/empty mbarriers)
 //   warp 1     TMEM allocator + single-thread tcgen05.mma issuer
@@ -28,11 +29,12 @@ namespace ed {
 namespace {
 
 constexpr int BM = 128;  // accumulator rows per CTA (TMEM lanes)
-constexpr int BN = 256;  // accumulator columns
+// accumulator columns per tile (BN): 256, or 128 for launches too small to
+// fill half the grid (gemm_pick_bn)
 constexpr int kThreads = 192;
 constexpr int kAccStages = 2;
 
-template <bool kBF16, int kCta>
+template <bool kBF16, int kCta, int BN>
 struct Cfg {
   static constexpr int ES = kBF16 ? 2 : 4;          // element bytes
   static constexpr int BK = 128 / ES;               // one 128-byte swizzle row of K
@@ -42,7 +44,7 @@ struct Cfg {
   static constexpr int A_BYTES = BM * 128;
   static constexpr int B_BYTES = B_ROWS * 128;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = kCta == 2 ? 6 : 4;
+  static constexpr int STAGES = BN == 256 ? (kCta == 2 ? 6 : 4) : (kCta == 2 ? 8 : 6);  // 192 KiB ring
   static constexpr int STORE_BYTES = 4 * 2 * 4096;  // 4 epilogue warps x 2 staging tiles of 32x128 B
   static constexpr int SMEM = STAGES * STAGE_BYTES + STORE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr int MN_ATOM = 128 / ES;          // MN elements per 128-byte atom
@@ -52,7 +54,7 @@ struct TileCoord {
   int region, b, m0, n0;
 };
 
-template <int TILE_M>
+template <int TILE_M, int BN>
 __device__ __forceinline__ TileCoord tile_coord(const GemmLaunch& p, int t, int tiles_m, int tiles_n) {
   TileCoord c;
   const int per_batch = tiles_m * tiles_n;
@@ -94,9 +96,9 @@ __device__ __forceinline__ void epi32(const GemmLaunch& p, uint32_t* r) {
   }
 }
 
-template <bool kBF16, int kCta>
+template <bool kBF16, int kCta, int BN>
 __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ GemmLaunch p) {
-  using C_ = Cfg<kBF16, kCta>;
+  using C_ = Cfg<kBF16, kCta, BN>;
   constexpr int STAGES = C_::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -139,7 +141,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     if (lane == 0) {
       int it = 0;
       for (int t = first; t < total; t += stride) {
-        const TileCoord tc = tile_coord<C_::TILE_M>(p, t, tiles_m, tiles_n);
+        const TileCoord tc = tile_coord<C_::TILE_M, BN>(p, t, tiles_m, tiles_n);
         const GemmRegion reg = p.regions[tc.region];
         const int am = tc.m0 + int(rank) * BM, bn = tc.n0 + int(rank) * C_::B_ROWS;
         for (int sib = 0; sib < reg.n_sib; ++sib) {
@@ -189,7 +191,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       const uint32_t a_sbo = a_lt == 1 ? 512u : 1024u, b_sbo = b_lt == 1 ? 512u : 1024u;
       int it = 0, local = 0;
       for (int t = first; t < total; t += stride, ++local) {
-        const TileCoord tc = tile_coord<C_::TILE_M>(p, t, tiles_m, tiles_n);
+        const TileCoord tc = tile_coord<C_::TILE_M, BN>(p, t, tiles_m, tiles_n);
         const int n_sib = p.regions[tc.region].n_sib;
         const int as = local & 1;
         const uint32_t aph = (local >> 1) & 1;
@@ -232,7 +234,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     int local = 0;
     uint32_t stage_ctr = 0;
     for (int t = first; t < total; t += stride, ++local) {
-      const TileCoord tc = tile_coord<C_::TILE_M>(p, t, tiles_m, tiles_n);
+      const TileCoord tc = tile_coord<C_::TILE_M, BN>(p, t, tiles_m, tiles_n);
       const GemmRegion reg = p.regions[tc.region];
       const int as = local & 1;
       const uint32_t aph = (local >> 1) & 1;
@@ -329,15 +331,15 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   }
 }
 
-template <bool kBF16, int kCta>
+template <bool kBF16, int kCta, int BN>
 cudaError_t prepare_t() {
-  return cudaFuncSetAttribute(gemm_kernel<kBF16, kCta>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              Cfg<kBF16, kCta>::SMEM);
+  return cudaFuncSetAttribute(gemm_kernel<kBF16, kCta, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              Cfg<kBF16, kCta, BN>::SMEM);
 }
 
-template <bool kBF16, int kCta>
+template <bool kBF16, int kCta, int BN>
 cudaError_t launch_t(const GemmLaunch& p, int num_sms, cudaStream_t stream) {
-  using C_ = Cfg<kBF16, kCta>;
+  using C_ = Cfg<kBF16, kCta, BN>;
   const long long tiles =
       (long long)((p.M + C_::TILE_M - 1) / C_::TILE_M) * ((p.N + BN - 1) / BN) * p.batch * p.n_regions;
   const int clusters = int(tiles < num_sms / kCta ? tiles : num_sms / kCta);
@@ -353,30 +355,50 @@ cudaError_t launch_t(const GemmLaunch& p, int num_sms, cudaStream_t stream) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, gemm_kernel<kBF16, kCta>, p);
+  return cudaLaunchKernelEx(&cfg, gemm_kernel<kBF16, kCta, BN>, p);
 }
 
 }  // namespace
 
 int gemm_bk(bool bf16) { return bf16 ? 64 : 32; }
-int gemm_bn(bool) { return BN; }
-bool gemm_paired(int M) { return M > BM; }
-int gemm_b_box(int M) { return gemm_paired(M) ? BN / 2 : BN; }
 int gemm_bm() { return BM; }
+bool gemm_paired(int M) { return M > BM; }
+int gemm_b_box(int M, int bn) { return gemm_paired(M) ? bn / 2 : bn; }
+
+int gemm_pick_bn(int M, int N, int batch, int n_regions, int num_sms) {
+  // 128-wide tiles need 1.5x the L2->SMEM bytes per flop of 256-wide ones,
+  // which a full grid cannot feed (measured on chain3: 0.094 -> 0.14 ms per
+  // GEMM), so they are used only when a single partial wave of 256-wide
+  // tiles would leave more than half of the SMs idle
+  const int cta = gemm_paired(M) ? 2 : 1;
+  const long long clusters = num_sms / cta;
+  const long long tiles256 =
+      (long long)((M + BM * cta - 1) / (BM * cta)) * ((N + 255) / 256) * batch * n_regions;
+  return 2 * tiles256 <= clusters && N > 128 ? 128 : 256;
+}
 
 cudaError_t gemm_prepare() {
   cudaError_t e;
-  if ((e = prepare_t<true, 1>()) != cudaSuccess) return e;
-  if ((e = prepare_t<false, 1>()) != cudaSuccess) return e;
-  if ((e = prepare_t<true, 2>()) != cudaSuccess) return e;
-  return prepare_t<false, 2>();
+  if ((e = prepare_t<true, 1, 256>()) != cudaSuccess) return e;
+  if ((e = prepare_t<false, 1, 256>()) != cudaSuccess) return e;
+  if ((e = prepare_t<true, 2, 256>()) != cudaSuccess) return e;
+  if ((e = prepare_t<false, 2, 256>()) != cudaSuccess) return e;
+  if ((e = prepare_t<true, 1, 128>()) != cudaSuccess) return e;
+  if ((e = prepare_t<false, 1, 128>()) != cudaSuccess) return e;
+  if ((e = prepare_t<true, 2, 128>()) != cudaSuccess) return e;
+  return prepare_t<false, 2, 128>();
 }
 
 cudaError_t launch_gemm(const GemmLaunch& p, int num_sms, cudaStream_t stream) {
   // pair SMs when the output has rows for both halves of a 256-row tile
   const bool pair = gemm_paired(p.M);
-  if (p.bf16) return pair ? launch_t<true, 2>(p, num_sms, stream) : launch_t<true, 1>(p, num_sms, stream);
-  return pair ? launch_t<false, 2>(p, num_sms, stream) : launch_t<false, 1>(p, num_sms, stream);
+  const bool narrow = p.bn == 128;
+  if (p.bf16) {
+    if (narrow) return pair ? launch_t<true, 2, 128>(p, num_sms, stream) : launch_t<true, 1, 128>(p, num_sms, stream);
+    return pair ? launch_t<true, 2, 256>(p, num_sms, stream) : launch_t<true, 1, 256>(p, num_sms, stream);
+  }
+  if (narrow) return pair ? launch_t<false, 2, 128>(p, num_sms, stream) : launch_t<false, 1, 128>(p, num_sms, stream);
+  return pair ? launch_t<false, 2, 256>(p, num_sms, stream) : launch_t<false, 1, 256>(p, num_sms, stream);
 }
 
 }  // namespace ed

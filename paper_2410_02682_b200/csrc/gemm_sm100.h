@@ -30,13 +30,15 @@ struct GemmLaunch {
   int bf16;                   // operand type: 1 bf16 (kind::f16), 0 fp32 (kind::tf32)
   int epi_map;                // fused map on the accumulator (ed_map_op) or -1
   float epi_c;                // scale constant of a fused scale map
+  int bn;                     // tile width: 256 or 128 (gemm_pick_bn)
 };
 
 int gemm_bk(bool bf16);
-int gemm_bn(bool bf16);
 int gemm_bm();
-bool gemm_paired(int M);  // 2-SM (cta_group::2) tiles for this M
-int gemm_b_box(int M);    // B rows (N) one CTA loads per K-major TMA box
+bool gemm_paired(int M);          // 2-SM (cta_group::2) tiles for this M
+int gemm_b_box(int M, int bn);    // B rows (N) one CTA loads per K-major TMA box
+// tile width: 128 when 256-wide tiles would leave over half the grid idle, else 256
+int gemm_pick_bn(int M, int N, int batch, int n_regions, int num_sms);
 constexpr int kStoreRows = 32;   // epilogue TMA-store box: 32 rows x 128 bytes
 cudaError_t gemm_prepare();  // sets the dynamic-smem attribute (call before capture)
 cudaError_t launch_gemm(const GemmLaunch& p, int num_sms, cudaStream_t stream);

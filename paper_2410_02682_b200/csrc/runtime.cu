@@ -1407,6 +1407,7 @@ void ed_plan_h::allocate() {
           p.epi_c = float(epi_.at(u.producer).second);
           op.name += "+map";
         }
+        p.bn = gemm_pick_bn(p.M, p.N, p.batch, int(op.heads.size()), ctx->num_sms);
         const uint32_t BK = uint32_t(gemm_bk(b16)), BM = uint32_t(gemm_bm());
         const uint32_t ATOM = 128u / (b16 ? 2u : 4u);
         op.maps.clear();
@@ -1462,7 +1463,7 @@ void ed_plan_h::allocate() {
             if (!g.a_mn) make_map(&ma, pa, b16, ak.ext, am.ext, am.stride, ab.ext, ab.stride, BK, BM);
             else make_map(&ma, pa, b16, am.ext, ak.ext, ak.stride, ab.ext, ab.stride, ATOM, BK, mn_swz);
             if (!g.b_mn)
-              make_map(&mb, pb, b16, bk.ext, bn.ext, bn.stride, bb.ext, bb.stride, BK, uint32_t(gemm_b_box(p.M)));
+              make_map(&mb, pb, b16, bk.ext, bn.ext, bn.stride, bb.ext, bb.stride, BK, uint32_t(gemm_b_box(p.M, p.bn)));
             else make_map(&mb, pb, b16, bn.ext, bk.ext, bk.stride, bb.ext, bb.stride, ATOM, BK, mn_swz);
             op.maps.push_back(ma);
             op.maps.push_back(mb);
