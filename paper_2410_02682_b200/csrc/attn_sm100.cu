@@ -20,12 +20,13 @@
 // fp32 range); the commit that signals S_t(j) also covers PV_t(j-1), so the
 // rescale never races an MMA. Epilogue: O / l -> swizzled smem -> TMA store.
 //
-// Warp roles (384 threads, three warpgroups): warps 0-3 softmax + epilogue
+// Warp roles (512 threads, four warpgroups): warps 0-3 softmax + epilogue
 // of tile 0, warps 4-7 of tile 1 (warp w owns TMEM lanes 32(w%4)..+32),
 // warp 8 TMA producer, warp 9 TMEM allocator + MMA issuer of tile 0, warp
-// 10 MMA issuer of tile 1, warp 11 idle. setmaxnreg moves registers from the
-// producer warpgroup to the softmax warpgroups, so a thread can hold its
-// whole 128-key S row.
+// 10 MMA issuer of tile 1, warp 11 idle, warps 12-15 the correction
+// warpgroup (O rescales, off the softmax's path). setmaxnreg moves
+// registers from the producer and correction warpgroups to the softmax
+// warpgroups, so a thread can hold its whole 128-key S row.
 // TMEM: S/P_0 [0,128) S/P_1 [128,256) O_0 [256,256+D) O_1 [256+D,256+2D).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -42,10 +43,11 @@ namespace {
 
 constexpr int BQ = 128;   // query rows per tile (TMEM lanes)
 constexpr int BKV = 128;  // keys per block
-constexpr int kThreads = 384;  // three warpgroups
+constexpr int kThreads = 512;  // four warpgroups
 constexpr int kTmaWarp = 8, kMmaWarp = 9;
-// register split (setmaxnreg): 2 x 128 x 224 + 128 x 56 <= 64K
-constexpr int kSoftmaxRegs = 224, kProducerRegs = 56;
+// register split (setmaxnreg): 2 x 128 x 200 + 128 x 48 + 128 x 56 <= 64K
+constexpr int kSoftmaxRegs = 200, kProducerRegs = 48, kCorrectionRegs = 56;
+constexpr int kCorrWarp0 = 12;  // warps 12-15: O rescale (correction) warpgroup
 // lazy rescale (log2 units): P = 2^(x - m) may reach 2^kRescale before O is
 // rescaled, and a rescale sets m = row max + kHeadroom. bf16 / fp32 keep full
 // relative precision over that span; O = sum P V keeps 2^64 / 4096 of headroom
@@ -61,7 +63,7 @@ struct ACfg {
   static constexpr int K_BYTES = BKV * D * 2;
   static constexpr int V_BYTES = BKV * D * 2;  // D/64 MN atoms of 128 key-rows x 128 B
   static constexpr int STG_BYTES = 4096;       // per softmax warp: 32 rows x 128 B
-  static constexpr int SMEM = 2 * Q_BYTES + 2 * K_BYTES + 2 * V_BYTES + 8 * STG_BYTES + 1024 + 256;
+  static constexpr int SMEM = 2 * Q_BYTES + 2 * K_BYTES + 2 * V_BYTES + 8 * STG_BYTES + 1024 + 256 + 1088;
   static constexpr int TMEM_COLS = 512;
   __host__ __device__ static constexpr int s_col(int t) { return t * BKV; }
   __host__ __device__ static constexpr int o_col(int t) { return 2 * BKV + t * D; }
@@ -182,6 +184,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
   uint64_t* p_half = bar + 20;   // [tile]: first 64 keys of P published
   uint64_t* t1_go = bar + 22;    // tile 1 starts half a step behind tile 0
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 23);
+  uint64_t* corr_req = bar + 24;   // [tile] softmax -> correction: factors posted
+  uint64_t* corr_done = bar + 26;  // [tile] correction -> MMA: O_t rescaled
+  float* fac = reinterpret_cast<float*>(bar + 32);      // [tile][row] rescale factor
+  int* fac_any = reinterpret_cast<int*>(fac + 2 * BQ);  // [tile][lane quarter] any row grew
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int nb = p.T / BKV;
@@ -201,6 +207,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
       if (i == 0) mbar_init(t1_go, 1);
       mbar_init(&o_full[i], 1);
       mbar_init(&o_empty[i], 4);
+      mbar_init(&corr_req[i], 4);
+      mbar_init(&corr_done[i], 4);
     }
     fence_mbar_init();
   }
@@ -210,7 +218,49 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp >= 8) {
+  if (warp >= kCorrWarp0) {
+    // ---------------- O rescale (correction) warpgroup ----------------
+    // Off the softmax's path: the softmax posts per-row factors right after
+    // its row max and goes on with exp2; this warp rescales its 32 rows of
+    // O_t in TMEM (only if one of them grew) and releases PV_t(j).
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kCorrectionRegs));
+    const int wq = warp & 3;
+    const uint32_t lane_base = uint32_t(wq * 32) << 16;
+    int cn0 = 0, cn1 = 0;
+    for (int jb = blockIdx.x; jb < jobs; jb += gridDim.x) {
+      const Job J = job_of(p, jb);
+      for (int j = 0; j < nb; ++j)
+        for (int t = 0; t <= J.two; ++t) {
+          int& cn = t ? cn1 : cn0;
+          mbar_wait(&corr_req[t], cn & 1);
+          ++cn;
+          if (fac_any[t * 4 + wq]) {
+            // PV_t(j-1) is complete: the softmax posted after S_t(j)'s commit
+            tc_fence_after();
+            const float f = fac[t * BQ + wq * 32 + lane];
+            const float2 f2 = make_float2(f, f);
+            const uint32_t o_addr = tmem + lane_base + uint32_t(C_::o_col(t));
+#pragma unroll 1
+            for (int c = 0; c < D / 32; ++c) {
+              uint32_t o[32];
+              tmem_ld_32x32b_x32(o_addr + uint32_t(c * 32), o);
+              tmem_ld_wait();
+#pragma unroll
+              for (int e = 0; e < 32; e += 2) {
+                const float2 r = fmul2(make_float2(__uint_as_float(o[e]), __uint_as_float(o[e + 1])), f2);
+                o[e] = __float_as_uint(r.x);
+                o[e + 1] = __float_as_uint(r.y);
+              }
+              tmem_st_32x32b_x32(o_addr + uint32_t(c * 32), o);
+            }
+            tmem_st_wait();
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&corr_done[t]);
+        }
+    }
+  } else if (warp >= 8) {
     // producer warpgroup: hand registers to the softmax warpgroups
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kProducerRegs));
     if (warp == kTmaWarp) {
@@ -304,6 +354,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             ++vc;
             const uint32_t va = smem_u32(sV + vst * C_::V_BYTES);
             mbar_wait(&p_half[t], pn & 1);
+            mbar_wait(&corr_done[t], pn & 1);
             ATTN_TRACE(3, t, j);
             if (j == 0) {  // the last job's epilogue has drained O_t
               mbar_wait(&o_empty[t], (on & 1) ^ 1);
@@ -405,13 +456,19 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           f = ex2(m - mn);
           m = mn;
         }
-        const bool wgrow = __any_sync(0xffffffffu, grow);
+        // post this row's factor to the correction warp of its lane quarter
+        {
+          const bool wgrow = __any_sync(0xffffffffu, grow);
+          fac[t * BQ + wq * 32 + lane] = f;
+          if (lane == 0) fac_any[t * 4 + wq] = wgrow;
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&corr_req[t]);
+        }
         // P = exp2(c log2e S - m), packed bf16, written over S in two halves
         // of 64 keys (the S values of a half are in registers before its
-        // P columns, which alias S columns [0, 64), are stored); without a
-        // rescale the first half is published at once so PV over it starts
-        // early. One pair in four is evaluated on the FMA pipe (exp2_poly2)
-        // to unload MUFU.
+        // P columns, which alias S columns [0, 64), are stored); the first
+        // half is published at once so PV over it starts early. One pair in
+        // four is evaluated on the FMA pipe (exp2_poly2) to unload MUFU.
         const float2 sc2v = make_float2(sc2, sc2), nm = make_float2(-m, -m);
         float2 acc0 = make_float2(0.f, 0.f), acc1 = acc0;
 #pragma unroll
@@ -433,36 +490,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             w[q] = pack_bf16(y.x, y.y);
           }
           tmem_st_32x32b_x32(s_addr + uint32_t(hh * 32), w);
-          if (hh == 1 && wgrow) {
-            // O_t rows *= f before any PV_t(j) (PV_t(j-1) is complete: its
-            // commit preceded S_t(j)'s); one TMEM round trip for all columns
-            uint32_t o[D];
-            const float2 f2 = make_float2(f, f);
-#pragma unroll
-            for (int c = 0; c < D / 32; ++c)
-              tmem_ld_32x32b_x32(o_addr + uint32_t(c * 32), *reinterpret_cast<uint32_t(*)[32]>(o + 32 * c));
-            tmem_ld_wait();
-#pragma unroll
-            for (int e = 0; e < D; e += 2) {
-              const float2 r = fmul2(make_float2(__uint_as_float(o[e]), __uint_as_float(o[e + 1])), f2);
-              o[e] = __float_as_uint(r.x);
-              o[e + 1] = __float_as_uint(r.y);
-            }
-#pragma unroll
-            for (int c = 0; c < D / 32; ++c)
-              tmem_st_32x32b_x32(o_addr + uint32_t(c * 32), *reinterpret_cast<const uint32_t(*)[32]>(o + 32 * c));
-          }
           if (lane == 0 && wq == 0 && hh == 0) ATTN_TRACE(8, t, j);
-          if (hh == 1 || !wgrow) {
-            tmem_st_wait();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) {
-              if (hh == 0 || wgrow) mbar_arrive(&p_half[t]);
-              if (hh == 1) mbar_arrive(&p_full[t]);
-            }
-            if (lane == 0 && wq == 0) ATTN_TRACE(1 + hh, t, j);
-          }
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(hh == 0 ? &p_half[t] : &p_full[t]);
+          if (lane == 0 && wq == 0) ATTN_TRACE(1 + hh, t, j);
         }
         acc0 = fadd2(acc0, acc1);
         l = l * f + (acc0.x + acc0.y);
