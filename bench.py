@@ -264,14 +264,23 @@ def main():
     g_n = sum(s["launches"] for s in gemm)
     step_ms = sum(s["ms"] for s in stats)
     traffic = None
+    tensor_active = None
     try:
-        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
-        traffic = prof.get(args.config, {}).get("dram_bytes_per_launch")
+        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json"))).get(args.config, {})
+        traffic = prof.get("dram_bytes_per_launch")
+        tensor_active = [l.get("tensor_active") for l in prof.get("launches", [])] or None
     except Exception:
         pass
+    # memory-bound launch classes: achieved algorithmic HBM GB/s against the
+    # measured copy bandwidth (the north star's shuffle / elementwise figure)
+    for st in stats:
+        if st["ms"] > 0 and not st["name"].startswith(("gemm", "attention")):
+            st["hbm_gbs"] = st["bytes"] / (st["ms"] / 1e3) / 1e9
+            st["hbm_frac"] = st["hbm_gbs"] / hbm
     achieved = g_fl / (g_ms / 1e3) / 1e12 if g_ms else 0.0
     roofline = {"bound": "tensor", "achieved": achieved, "peak": pk, "unit": "TFLOP/s",
                 "frac": achieved / pk if pk else None, "traffic": traffic,
+                "ncu_tensor_pipe_active": tensor_active,
                 "kernel": "tcgen05 GEMM (gemm_kernel)", "launches_per_step": g_n,
                 "share_of_step": g_ms / step_ms if step_ms else None,
                 "per_launch_tflop": g_fl / max(1, g_n) / 1e12, "peak_source": f"{peak_src} bf16 burst",

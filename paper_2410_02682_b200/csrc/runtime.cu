@@ -829,14 +829,26 @@ void ed_plan_h::build() {
       // M joins the chain when it is the row max of the same, aligned x chunks;
       // otherwise (e.g. its label is split with a sibling fold) M is computed
       // as planned and the chain reads the materialised row maxima
-      const bool m_fusable = is(m, OpKind::ROWREDUCE, 1, ED_AGG_MAX) && V[m].map == ED_MAP_IDENTITY &&
-                             V[m].inputs[0] == xv && sole_reader(m, sv) && all_local(m) && memmap_[m].len == L;
+      const bool m_max = is(m, OpKind::ROWREDUCE, 1, ED_AGG_MAX) && V[m].map == ED_MAP_IDENTITY &&
+                         V[m].inputs[0] == xv && sole_reader(m, sv) && all_local(m);
+      const bool m_fusable = m_max && memmap_[m].len == L;
+      // M's reduced labels split over siblings (a max fold in its refinement):
+      // when the chain's rows are whole rows of x, the row max the kernel
+      // takes in registers IS M's value (max is exact and order-free), so M's
+      // joins and fold are fused away too
+      bool m_full_rows = false;
+      if (m_max && !m_fusable) {
+        int64_t ext = 1;
+        for (size_t i = 0; i < V[m].lx.size(); ++i)
+          if (std::find(V[m].lz.begin(), V[m].lz.end(), V[m].lx[i]) == V[m].lz.end()) ext *= V[xv].bound[i];
+        m_full_rows = ext == L;
+      }
       auto join_at = [&](int ref, int w) {
         const int o = owner[ref];
         return (X[o].kind == ED_EXEC_JOIN && X[o].producer == w) ? o : -1;
       };
       Softmax sm;
-      bool ok = true, internal = m_fusable;
+      bool ok = true, internal = m_fusable || m_full_rows;
       for (int attempt = 0; attempt < 2 && !sm.pairs.size(); ++attempt) {
         ok = true;
         sm.pairs.clear();
@@ -846,7 +858,7 @@ void ed_plan_h::build() {
           const int sj = ej >= 0 ? join_at(X[ej].deps[0], sv) : -1;
           ok = ok && ej >= 0 && sgj >= 0 && sj >= 0 && owner[X[sgj].deps[0]] == ej && X[yj].sz == X[sj].sz &&
                X[yj].sz % L == 0;
-          if (ok && internal) {
+          if (ok && internal && !m_full_rows) {
             const int mj = join_at(X[sj].deps[1], m);
             ok = mj >= 0 && owner[X[mj].deps[0]] == owner[X[sj].deps[0]];
           }
