@@ -8,7 +8,10 @@ the reference planner's plan from plans/), inputs resident in HBM. `value`
 is contraction TFLOP/s = sum over mul/sum join kernels of 2*fp (SURVEY
 8(d)) / device time (CUDA events, max over ranks). `e2e` is the same metric
 through the C ABI with pinned host buffers: H2D of every input tensor,
-on-device chunking, ed_run, D2H of the assembled output, each step.
+on-device chunking, the run, D2H of the assembled output, every step, via
+ed_run_steps (the serving loop: step s+1's H2D overlaps step s's compute and
+D2H); `e2e.blocking_calls` is the same with one blocking
+ed_upload_tensors / ed_run / ed_download sequence per step.
 For N > 1 run under torchrun (one process per GPU).
 """
 import argparse
@@ -182,7 +185,7 @@ def main():
     ap.add_argument("--config", default="bmm2")
     ap.add_argument("--precision", default="bf16")
     ap.add_argument("--impl", default="ours")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--placement", default="gpu", choices=["gpu", "ref"],
                     help="gpu: GPU-aware re-placement of memory-bound vertices (ed_gpu_placement); "
@@ -297,20 +300,31 @@ def main():
     pp.upload(pins)
     pp.run()
     pp.download(into=outs_np)
+    # (a) blocking calls per step: ed_upload_tensors, ed_run, ed_download
     barrier()
     t0 = time.perf_counter()
     for _ in range(args.e2e_steps):
         pp.upload(pins)
         pp.run()
         pp.download(into=outs_np)
+    seq_s = time.perf_counter() - t0
+    # (b) the serving loop in one call, ed_run_steps: step s+1's H2D overlaps
+    # step s's compute and D2H (copy streams, double-buffered staging)
+    pp.run_steps([pins] * 2, [outs_np] * 2)
+    barrier()
+    t0 = time.perf_counter()
+    pp.run_steps([pins] * args.e2e_steps, [outs_np] * args.e2e_steps)
     e2e_s = time.perf_counter() - t0
     if world > 1:
-        t = torch.tensor([e2e_s], dtype=torch.float64)
+        t = torch.tensor([e2e_s, seq_s], dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_s = float(t.item())
+        e2e_s, seq_s = float(t[0].item()), float(t[1].item())
     pp.close()
     e2e = {"value": flops * args.e2e_steps / e2e_s / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d,
-           "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s / args.e2e_steps * 1e3}
+           "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s / args.e2e_steps * 1e3, "api": "ed_run_steps",
+           "blocking_calls": {"value": flops * args.e2e_steps / seq_s / 1e12,
+                              "ms_per_step": seq_s / args.e2e_steps * 1e3,
+                              "api": "ed_upload_tensors + ed_run + ed_download per step"}}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -238,6 +238,18 @@ ED_API ed_status ed_run(struct ed_plan_h* h, ed_report_c* report, char* err, siz
 ED_API ed_status ed_download(struct ed_plan_h* h, ed_output_c* outputs, int32_t n,
                       char* err, size_t errlen);
 
+/* n_steps end-to-end steps of a serving loop in one call: for step s, upload
+ * inputs[s*n_in .. s*n_in+n_in) (chunked on the device), run, and assemble and
+ * copy outputs[s*n_out .. s*n_out+n_out) to the host. The host-to-device copies
+ * of step s+1 run on a copy stream while step s computes and its outputs
+ * travel device-to-host on another (double-buffered staging), so a step costs
+ * about max(H2D, D2H) + compute instead of their sum. Host buffers should be
+ * pinned for the copies to overlap. Blocks until every output is written;
+ * report (nullable) as ed_run, device_ms spanning all steps. With world > 1
+ * this is the plain upload / run / collective-download sequence per step. */
+ED_API ed_status ed_run_steps(struct ed_plan_h* h, int32_t n_steps, const ed_tensor_in_c* inputs, int32_t n_in,
+                              ed_output_c* outputs, int32_t n_out, ed_report_c* report, char* err, size_t errlen);
+
 /* Copy one exec vertex's produced chunk D2H (per-vertex parity tests).
  * Returns ED_ERR_USAGE if the chunk is not resident on this rank. */
 ED_API ed_status ed_download_chunk(struct ed_plan_h* h, int32_t exec_id, int32_t dtype,

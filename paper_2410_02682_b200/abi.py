@@ -140,6 +140,7 @@ EXPORTED = [
     "ed_abi_version", "ed_nccl_unique_id", "ed_ctx_create", "ed_ctx_destroy",
     "ed_prepare", "ed_plan_destroy", "ed_upload", "ed_upload_tensors", "ed_run",
     "ed_download", "ed_download_chunk", "ed_plan_schedule", "ed_kernel_stats", "ed_gpu_placement",
+    "ed_run_steps",
 ]
 
 
@@ -164,6 +165,8 @@ def declare(lib):
     lib.ed_plan_schedule.argtypes = [C.POINTER(ed_plan_c), C.c_int32, C.c_int32, C.POINTER(ed_sched_op_c),
                                      C.c_int32, i32p] + err
     lib.ed_kernel_stats.argtypes = [P, C.POINTER(ed_kernel_stat_c), C.c_int32, i32p] + err
+    lib.ed_run_steps.argtypes = [P, C.c_int32, C.POINTER(ed_tensor_in_c), C.c_int32, C.POINTER(ed_output_c),
+                                 C.c_int32, C.POINTER(ed_report_c)] + err
     lib.ed_gpu_placement.argtypes = [C.POINTER(ed_plan_c), C.POINTER(ed_cost_model_c), i32p,
                                      C.POINTER(C.c_double)] + err
     for name in EXPORTED[1:]:

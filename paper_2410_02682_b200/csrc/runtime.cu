@@ -28,6 +28,7 @@
 #include <set>
 #include <stdexcept>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "ed_gpu.h"
@@ -393,6 +394,18 @@ struct ed_plan_h {
   int* d_err = nullptr;
   void* staging = nullptr;
   size_t staging_bytes = 0;
+  // ed_run_steps: copy streams, double-buffered staging, cached copy descriptors
+  struct CopyPlan {
+    void* d = nullptr;  // BlockCopy[] on the device
+    int n = 0, rank = 0;
+    int64_t max_rows = 1;
+  };
+  std::map<std::tuple<int, int, const void*, int>, CopyPlan> copy_cache;
+  cudaStream_t cs_in = nullptr, cs_out = nullptr;
+  void* stg_in[2] = {nullptr, nullptr};
+  void* stg_out[2] = {nullptr, nullptr};
+  size_t stg_in_bytes = 0, stg_out_bytes = 0;
+  cudaEvent_t ev_pipe[8] = {};  // in_full[2], in_free[2], out_full[2], out_free[2]
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t gexec = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -2022,6 +2035,16 @@ void ed_plan_h::destroy() {
   if (d_ptrs) cudaFree(d_ptrs);
   if (d_err) cudaFree(d_err);
   if (staging) cudaFree(staging);
+  for (auto& [k, c] : copy_cache)
+    if (c.d) cudaFree(c.d);
+  for (void* b : stg_in)
+    if (b) cudaFree(b);
+  for (void* b : stg_out)
+    if (b) cudaFree(b);
+  for (auto e : ev_pipe)
+    if (e) cudaEventDestroy(e);
+  if (cs_in) cudaStreamDestroy(cs_in);
+  if (cs_out) cudaStreamDestroy(cs_out);
 }
 
 namespace {
@@ -2044,9 +2067,9 @@ DT dt_of(int dtype) { return dtype == ED_DTYPE_F64 ? DT::F64 : DT::F32; }
 
 // chunk <-> whole-tensor rectangle copies (BlockCopy) for graph vertex w over
 // partition `part`; to_chunks: whole (staging) -> chunk buffers, else back.
-void block_copies(ed_plan_h* h, int w, const shape& part, const std::vector<int>& ids, bool to_chunks,
-                  const void* whole_src, void* whole_dst, DT whole_dt, cudaStream_t s,
-                  const std::vector<void*>* remote = nullptr) {
+std::vector<BlockCopy> copy_groups(ed_plan_h* h, int w, const shape& part, const std::vector<int>& ids,
+                                   bool to_chunks, const void* whole_src, void* whole_dst,
+                                   const std::vector<void*>* remote, int64_t& max_rows) {
   const shape& bound = h->V[w].bound;
   const int rank = int(bound.size());
   if (rank == 0) throw ed_error(ED_ERR_UNSUPPORTED, "rank-0 tensors");
@@ -2060,7 +2083,7 @@ void block_copies(ed_plan_h* h, int w, const shape& part, const std::vector<int>
     b *= cb[i];
   }
   std::vector<BlockCopy> groups;
-  int64_t max_rows = 1;
+  max_rows = 1;
   for (size_t n = 0; n < ids.size(); ++n) {
     const int id = ids[n];
     void* chunk = (remote && (*remote)[n]) ? (*remote)[n] : (h->local[id] ? h->buf[h->owner[id]].main : nullptr);
@@ -2096,6 +2119,15 @@ void block_copies(ed_plan_h* h, int w, const shape& part, const std::vector<int>
     }
     groups.push_back(g);
   }
+  return groups;
+}
+
+void block_copies(ed_plan_h* h, int w, const shape& part, const std::vector<int>& ids, bool to_chunks,
+                  const void* whole_src, void* whole_dst, DT whole_dt, cudaStream_t s,
+                  const std::vector<void*>* remote = nullptr) {
+  int64_t max_rows = 1;
+  const std::vector<BlockCopy> groups = copy_groups(h, w, part, ids, to_chunks, whole_src, whole_dst, remote, max_rows);
+  const int rank = int(h->V[w].bound.size());
   if (groups.empty()) return;
   const size_t need = sizeof(BlockCopy) * groups.size();
   if (h->copy_desc_bytes < need) {
@@ -2405,6 +2437,176 @@ ed_status ed_download(ed_plan_h* h, ed_output_c* outs, int32_t n, char* err, siz
       for (void* r : remote)
         if (r) CUDA_OK(cudaFreeAsync(r, s));
       CUDA_OK(cudaStreamSynchronize(s));
+    }
+  });
+}
+
+namespace {
+
+// exec ids holding graph vertex w's chunks for upload (input chunks) or
+// download (its final refinement layer), runtime.cc:432-448
+std::vector<int> io_chunks(const ed_plan_h* h, int w, bool input) {
+  std::vector<int> ids;
+  for (int id = 0; id < int(h->X.size()); ++id) {
+    const Ex& u = h->X[id];
+    const bool mine = input ? (u.kind == ED_EXEC_INPUT_CHUNK && u.producer == w)
+                            : (h->V[w].arity == 0 ? (u.kind == ED_EXEC_INPUT_CHUNK && u.producer == w)
+                                                  : (u.kind == ED_EXEC_REFINEMENT && u.producer == w && u.consumer < 0));
+    if (mine) ids.push_back(id);
+  }
+  return ids;
+}
+
+// whole tensor <-> chunks through a staging buffer with descriptors built
+// once and kept on the device (no host->device copy inside the pipeline)
+void cached_copy(ed_plan_h* h, int w, bool to_chunks, void* whole, int dtype, cudaStream_t s) {
+  const auto key = std::make_tuple(w, int(to_chunks), static_cast<const void*>(whole), dtype);
+  auto it = h->copy_cache.find(key);
+  if (it == h->copy_cache.end()) {
+    ed_plan_h::CopyPlan c;
+    const shape part = (h->V[w].arity == 0 || to_chunks) ? h->V[w].d : h->out_partition(w);
+    const std::vector<int> ids = io_chunks(h, w, to_chunks);
+    const std::vector<BlockCopy> g =
+        copy_groups(h, w, part, ids, to_chunks, to_chunks ? whole : nullptr, to_chunks ? nullptr : whole, nullptr,
+                    c.max_rows);
+    c.n = int(g.size());
+    c.rank = int(h->V[w].bound.size());
+    if (c.n) {
+      CUDA_OK(cudaMalloc(&c.d, sizeof(BlockCopy) * g.size()));
+      CUDA_OK(cudaMemcpy(c.d, g.data(), sizeof(BlockCopy) * g.size(), cudaMemcpyHostToDevice));
+    }
+    it = h->copy_cache.emplace(key, c).first;
+  }
+  const ed_plan_h::CopyPlan& c = it->second;
+  if (!c.n) return;
+  BlockCopyParams p{};
+  p.rank = c.rank;
+  p.in_dt = int(to_chunks ? dt_of(dtype) : h->store);
+  p.out_dt = int(to_chunks ? h->store : dt_of(dtype));
+  p.groups = static_cast<const BlockCopy*>(c.d);
+  CUDA_OK(launch_blockcopy(p, c.n, c.max_rows, s));
+}
+
+void throw_status(ed_status st, const char* msg) {
+  if (st != ED_OK) throw ed_error(st, msg);
+}
+
+}  // namespace
+
+ed_status ed_run_steps(ed_plan_h* h, int32_t n_steps, const ed_tensor_in_c* ins, int32_t n_in, ed_output_c* outs,
+                       int32_t n_out, ed_report_c* rep, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!h || n_steps < 0 || n_in < 0 || n_out < 0 || (n_in && !ins) || (n_out && !outs))
+      throw ed_error(ED_ERR_USAGE, "null argument");
+    if (h->ctx->world > 1) {  // collective download: the plain sequence, step by step
+      char e2[512];
+      for (int st = 0; st < n_steps; ++st) {
+        throw_status(ed_upload_tensors(h, ins + size_t(st) * n_in, n_in, e2, sizeof e2), e2);
+        throw_status(ed_run(h, rep, e2, sizeof e2), e2);
+        throw_status(ed_download(h, outs + size_t(st) * n_out, n_out, e2, sizeof e2), e2);
+      }
+      return;
+    }
+    CUDA_OK(cudaSetDevice(h->ctx->device));
+    size_t in_b = 0, out_b = 0;
+    for (int64_t i = 0; i < int64_t(n_steps) * n_in; ++i) {
+      const ed_tensor_in_c& t = ins[i];
+      if (t.vertex_id < 0 || t.vertex_id >= int(h->V.size()) || h->V[t.vertex_id].arity != 0)
+        throw ed_error(ED_ERR_PLAN, "execute: no relation supplied for an input");
+      if (t.n != prod(h->V[t.vertex_id].bound)) throw ed_error(ED_ERR_PLAN, "ed_run_steps: input size mismatch");
+      in_b = std::max(in_b, size_t(t.n) * dt_size(t.dtype));
+    }
+    for (int64_t i = 0; i < int64_t(n_steps) * n_out; ++i) {
+      const ed_output_c& o = outs[i];
+      if (o.vertex_id < 0 || o.vertex_id >= int(h->V.size())) throw ed_error(ED_ERR_USAGE, "output vertex out of range");
+      if (o.n != prod(h->V[o.vertex_id].bound)) throw ed_error(ED_ERR_USAGE, "output size mismatch");
+      if (io_chunks(h, o.vertex_id, false).empty()) throw ed_error(ED_ERR_PLAN, "no final refinement layer for output");
+      out_b = std::max(out_b, size_t(o.n) * dt_size(o.dtype));
+    }
+    if (!h->cs_in) {
+      CUDA_OK(cudaStreamCreateWithFlags(&h->cs_in, cudaStreamNonBlocking));
+      CUDA_OK(cudaStreamCreateWithFlags(&h->cs_out, cudaStreamNonBlocking));
+      for (auto& e : h->ev_pipe) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    auto grow = [&](void* (&b)[2], size_t& have, size_t need) {
+      if (have >= need) return;
+      CUDA_OK(cudaDeviceSynchronize());
+      for (void*& x : b) {
+        if (x) CUDA_OK(cudaFree(x));
+        CUDA_OK(cudaMalloc(&x, need));
+      }
+      have = need;
+      // descriptors point into the old buffers
+      for (auto& [k, c] : h->copy_cache)
+        if (c.d) cudaFree(c.d);
+      h->copy_cache.clear();
+    };
+    grow(h->stg_in, h->stg_in_bytes, in_b);
+    grow(h->stg_out, h->stg_out_bytes, out_b);
+    cudaEvent_t* in_full = h->ev_pipe;
+    cudaEvent_t* in_free = h->ev_pipe + 2;
+    cudaEvent_t* out_full = h->ev_pipe + 4;
+    cudaEvent_t* out_free = h->ev_pipe + 6;
+    cudaStream_t s = h->ctx->stream;
+    CUDA_OK(cudaMemsetAsync(h->d_err, 0, sizeof(int), s));
+    CUDA_OK(cudaEventRecord(h->ev0, s));
+    int bi = 0, bo = 0;
+    for (int st = 0; st < n_steps; ++st) {
+      // inputs: H2D on the copy-in stream, chunk() on the compute stream
+      // (after the previous step's run has read the input chunks)
+      for (int k = 0; k < n_in; ++k) {
+        const ed_tensor_in_c& t = ins[size_t(st) * n_in + k];
+        const int b = bi++ & 1;
+        const size_t bytes = size_t(t.n) * dt_size(t.dtype);
+        CUDA_OK(cudaStreamWaitEvent(h->cs_in, in_free[b], 0));
+        CUDA_OK(cudaMemcpyAsync(h->stg_in[b], t.data, bytes, cudaMemcpyHostToDevice, h->cs_in));
+        CUDA_OK(cudaEventRecord(in_full[b], h->cs_in));
+        CUDA_OK(cudaStreamWaitEvent(s, in_full[b], 0));
+        cached_copy(h, t.vertex_id, true, h->stg_in[b], t.dtype, s);
+        for (int id : io_chunks(h, t.vertex_id, true))
+          if (h->local[id] && h->buf[id].lo)
+            CUDA_OK(launch_split_lo(static_cast<const float*>(h->buf[id].main), static_cast<float*>(h->buf[id].lo),
+                                    h->X[id].sz, s));
+        CUDA_OK(cudaEventRecord(in_free[b], s));
+      }
+      if (h->gexec) CUDA_OK(cudaGraphLaunch(h->gexec, s));
+      else h->enqueue(s);
+      // outputs: assemble on the compute stream, D2H on the copy-out stream,
+      // overlapping the next step's uploads
+      for (int k = 0; k < n_out; ++k) {
+        const ed_output_c& o = outs[size_t(st) * n_out + k];
+        const int b = bo++ & 1;
+        CUDA_OK(cudaStreamWaitEvent(s, out_free[b], 0));
+        cached_copy(h, o.vertex_id, false, h->stg_out[b], o.dtype, s);
+        CUDA_OK(cudaEventRecord(out_full[b], s));
+        CUDA_OK(cudaStreamWaitEvent(h->cs_out, out_full[b], 0));
+        CUDA_OK(cudaMemcpyAsync(o.data, h->stg_out[b], size_t(o.n) * dt_size(o.dtype), cudaMemcpyDeviceToHost,
+                                h->cs_out));
+        CUDA_OK(cudaEventRecord(out_free[b], h->cs_out));
+      }
+    }
+    CUDA_OK(cudaEventRecord(h->ev1, s));
+    CUDA_OK(cudaStreamSynchronize(h->cs_out));
+    CUDA_OK(cudaStreamSynchronize(s));
+    CUDA_OK(cudaStreamSynchronize(h->cs_in));
+    int flag = 0;
+    CUDA_OK(cudaMemcpy(&flag, h->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+    if (flag) throw ed_error(ED_ERR_EVAL, "division by zero");
+    if (rep) {
+      if (rep->machines)
+        for (int m = 0; m < std::min(rep->n_machines, h->n_machines); ++m) rep->machines[m] = h->counters[m];
+      rep->total_transferred = h->total_transferred;
+      rep->wall_steps = int64_t(h->X.size());
+      rep->max_site_cost = h->max_site_cost;
+      float ms = 0;
+      CUDA_OK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+      rep->device_ms = ms;
+      rep->peer_bytes = 0;
+      rep->contraction_flops = h->contraction_flops;
+      int launches = 0;
+      for (auto& op : h->ops)
+        if (op.kind != OpKind::SEND && op.kind != OpKind::RECV) ++launches;
+      rep->gpu_launches = launches;
     }
   });
 }

@@ -192,6 +192,39 @@ class PreparedPlan:
             _check(library().ed_download(self.h, arr, len(descs), err, n), err)
         return outs
 
+    def run_steps(self, inputs: list, outputs: list) -> RunReport:
+        """ed_run_steps: len(inputs) end-to-end steps (upload inputs[s], run,
+        download into outputs[s]) with step s+1's H2D overlapping step s's
+        compute and D2H. inputs[s]: vid -> whole tensor; outputs[s]: vid ->
+        preallocated array (pinned host memory for the copies to overlap)."""
+        if len(inputs) != len(outputs):
+            raise ValueError("one output dict per input dict")
+        n_steps = len(inputs)
+        n_in = len(inputs[0]) if n_steps else 0
+        n_out = len(outputs[0]) if n_steps else 0
+        tin = (abi.ed_tensor_in_c * max(1, n_steps * n_in))()
+        tout = (abi.ed_output_c * max(1, n_steps * n_out))()
+        keep = []
+        for st in range(n_steps):
+            if len(inputs[st]) != n_in or len(outputs[st]) != n_out:
+                raise ValueError("every step needs the same inputs and outputs")
+            for k, (vid, val) in enumerate(inputs[st].items()):
+                a = _host(val)
+                keep.append(a)
+                tin[st * n_in + k] = abi.ed_tensor_in_c(vid, _dt(a), a.ctypes.data, a.size)
+            for k, (vid, a) in enumerate(outputs[st].items()):
+                tout[st * n_out + k] = abi.ed_output_c(vid, _dt(a), a.ctypes.data, a.size)
+        L = self.plan.n_machines
+        machines = (abi.ed_machine_c * L)()
+        rep = abi.ed_report_c()
+        rep.n_machines = L
+        rep.machines = C.cast(machines, C.POINTER(abi.ed_machine_c))
+        err, n = _err()
+        _check(library().ed_run_steps(self.h, n_steps, tin, n_in, tout, n_out, C.byref(rep), err, n), err)
+        return RunReport([(m.fp, m.sent, m.received) for m in machines], rep.total_transferred,
+                         rep.wall_steps, rep.max_site_cost, {}, rep.device_ms, rep.peer_bytes,
+                         rep.contraction_flops, rep.gpu_launches)
+
     def download_chunk(self, exec_id: int, dtype=np.float64) -> np.ndarray:
         u = self.plan.exec[exec_id]
         a = np.empty(u.chunk_bound, dtype=dtype)

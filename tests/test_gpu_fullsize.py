@@ -256,3 +256,25 @@ def test_attention_block_runs_fused(gpu_ctx, name):
     with pytest.raises(EdError):
         pp.download_chunk(ref)
     pp.close()
+
+
+@pytest.mark.parametrize("name", ["bmm2_s_p8_L1", "ffnn_s_p8_L1", "matmul_p8_L1"])
+def test_run_steps_pipeline_matches_blocking_calls(gpu_ctx, name):
+    """ed_run_steps (pipelined serving loop) gives, step for step, the outputs
+    of the blocking upload / run / download sequence on the same inputs."""
+    from paper_2410_02682_b200.executor import PreparedPlan
+    plan = load_plan(name)
+    steps = [_inputs(plan, seed=s) for s in (1, 2, 3)]
+    pp = PreparedPlan(gpu_ctx, plan, precision="bf16")
+    want = []
+    for ins in steps:
+        pp.upload(ins)
+        pp.run()
+        want.append(pp.download(dtype=np.float32))
+    got = [{vid: np.empty(plan.vertices[vid].bound, dtype=np.float32) for vid in plan.outputs} for _ in steps]
+    rep = pp.run_steps(steps, got)
+    pp.close()
+    assert rep.device_ms > 0
+    for w, g in zip(want, got):
+        for vid in plan.outputs:
+            assert np.array_equal(w[vid], g[vid])
