@@ -56,6 +56,12 @@ constexpr float kRescale = 64.0f, kHeadroom = 48.0f;
 // exp2 pairs q with bit q % 8 set run on the FMA pipe (measured: 2 of 8 is
 // ~2% faster than MUFU only; more is slower, the kernel is not MUFU-bound)
 constexpr int kPolyPairs = 0x88;
+// 1: the two MMA threads take turns (PV_t(j) + S_t(j+1) groups alternate on
+// the tensor pipe), so the tiles' softmaxes run in anti-phase
+#ifndef ED_ATTN_ALT
+#define ED_ATTN_ALT 1
+#endif
+constexpr bool kAlternate = ED_ATTN_ALT;
 
 template <int D>
 struct ACfg {
@@ -186,6 +192,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 23);
   uint64_t* corr_req = bar + 24;   // [tile] softmax -> correction: factors posted
   uint64_t* corr_done = bar + 26;  // [tile] correction -> MMA: O_t rescaled
+  uint64_t* turn = bar + 28;       // [tile] the tensor pipe alternates PV+S groups between tiles
   float* fac = reinterpret_cast<float*>(bar + 32);      // [tile][row] rescale factor
   int* fac_any = reinterpret_cast<int*>(fac + 2 * BQ);  // [tile][lane quarter] any row grew
 
@@ -209,6 +216,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
       mbar_init(&o_empty[i], 4);
       mbar_init(&corr_req[i], 4);
       mbar_init(&corr_done[i], 4);
+      mbar_init(&turn[i], 1);
     }
     fence_mbar_init();
   }
@@ -313,7 +321,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         const uint32_t idesc_s = umma_idesc(1u, BQ, BKV, 0u, 0u);  // Q, K both K-major (d)
         const uint32_t idesc_o = umma_idesc(1u, BQ, D, 0u, 1u);    // P from TMEM (keys), V MN-major (d)
         const uint32_t qa = smem_u32(sQ + t * C_::Q_BYTES);
-        int kc = 0, vc = 0, qn = 0, pn = 0, on = 0, gn = 0;
+        int kc = 0, vc = 0, qn = 0, pn = 0, on = 0, gn = 0, tn = 0;
         auto issue_s = [&](int kst) {
           const uint32_t ka = smem_u32(sK + kst * C_::K_BYTES);
 #pragma unroll
@@ -355,6 +363,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             const uint32_t va = smem_u32(sV + vst * C_::V_BYTES);
             mbar_wait(&p_half[t], pn & 1);
             mbar_wait(&corr_done[t], pn & 1);
+            if (kAlternate && J.two) {  // tile 0 holds the first turn
+              mbar_wait(&turn[t], (tn & 1) ^ (t == 0 ? 1 : 0));
+              ++tn;
+            }
             ATTN_TRACE(3, t, j);
             if (j == 0) {  // the last job's epilogue has drained O_t
               mbar_wait(&o_empty[t], (on & 1) ^ 1);
@@ -379,6 +391,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             if (j == nb - 1) mma_commit(&o_full[t]);
             if (j + 1 < nb) {
               kst = kc & 1;
+              ATTN_TRACE(9, t, j + 1);
               mbar_wait(&k_full[kst], (kc >> 1) & 1);
               ++kc;
               tc_fence_after();
@@ -387,6 +400,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
               if (j + 1 == nb - 1) mma_commit(&q_empty[t]);
               for (int r = 0; r < rel; ++r) mma_commit(&k_empty[kst]);
             }
+            if (kAlternate && J.two) mbar_arrive(&turn[t ^ 1]);
           }
         }
       }
@@ -585,8 +599,8 @@ cudaError_t launch_d(const AttnLaunch& p0, int num_sms, cudaStream_t s) {
     cudaMemcpy(h, p.trace, sizeof(h), cudaMemcpyDeviceToHost);
     cudaFree(p.trace);
     const long long t0 = h[5 * 128];
-    const char* names[9] = {"s_ready", "p_half", "p_full", "mma_got_half", "mma_got_full", "s_issued", "s_loaded", "max_done", "half0_stored"};
-    for (int ev = 0; ev < 9; ++ev)
+    const char* names[10] = {"s_ready", "p_half", "p_full", "mma_got_half", "mma_got_full", "s_issued", "s_loaded", "max_done", "half0_stored", "pvb_issued"};
+    for (int ev = 0; ev < 10; ++ev)
       for (int t = 0; t < 2; ++t) {
         std::fprintf(stderr, "attn_trace %-13s t%d:", names[ev], t);
         for (int j = 0; j < 33; ++j) std::fprintf(stderr, " %lld", h[(ev * 2 + t) * 64 + j] ? h[(ev * 2 + t) * 64 + j] - t0 : -1);
