@@ -57,9 +57,12 @@ constexpr float kRescale = 64.0f, kHeadroom = 48.0f;
 // ~2% faster than MUFU only; more is slower, the kernel is not MUFU-bound)
 constexpr int kPolyPairs = 0x88;
 // 1: the two MMA threads take turns (PV_t(j) + S_t(j+1) groups alternate on
-// the tensor pipe), so the tiles' softmaxes run in anti-phase
+// the tensor pipe), so the tiles' softmaxes run in anti-phase. Measured
+// slower (0.346 vs 0.32 ms on attn_big): each group then waits a whole
+// softmax for its turn, and the TS-form PV MMAs still slow down under the
+// other tile's TMEM stores (profiles/r01b_micro_tcgen05.md). Off by default.
 #ifndef ED_ATTN_ALT
-#define ED_ATTN_ALT 1
+#define ED_ATTN_ALT 0
 #endif
 constexpr bool kAlternate = ED_ATTN_ALT;
 
