@@ -228,6 +228,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  griddep_wait();  // the prologue above overlapped the previous kernel (PDL)
 
   if (warp >= kCorrWarp0) {
     // ---------------- O rescale (correction) warpgroup ----------------
@@ -279,6 +280,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
       if (lane == 0) {
         int kc = 0, vc = 0, qn0 = 0, qn1 = 0;
         for (int jb = blockIdx.x; jb < jobs; jb += gridDim.x) {
+          if (jb + int(gridDim.x) >= jobs) griddep_launch();  // last job: the next kernel may launch
           const Job J = job_of(p, jb);
           const AttnRegion R = p.regions[J.region];
           const CUtensorMap* mq = p.maps + R.q;
@@ -594,8 +596,17 @@ cudaError_t launch_d(const AttnLaunch& p0, int num_sms, cudaStream_t s) {
     cudaMalloc(&p.trace, 10 * 2 * 64 * sizeof(long long));
     cudaMemsetAsync(p.trace, 0, 10 * 2 * 64 * sizeof(long long), s);
   }
-  attn_kernel<D, kPolyPairs><<<p.n_jobs < num_sms ? p.n_jobs : num_sms, kThreads, ACfg<D>::SMEM, s>>>(p);
-  cudaError_t e = cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(p.n_jobs < num_sms ? p.n_jobs : num_sms);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = ACfg<D>::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute pdl[1];
+  pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  pdl[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = pdl;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, attn_kernel<D, kPolyPairs>, p);
   if (p.trace) {
     long long h[10 * 2 * 64];
     cudaStreamSynchronize(s);

@@ -135,12 +135,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // everything above overlaps the previous kernel's tail (PDL); operands and
+  // outputs are touched only after it has completed
+  griddep_wait();
 
   if (warp == 0) {
     // ---- TMA producer (both CTAs of a pair load their halves) ----
     if (lane == 0) {
       int it = 0;
       for (int t = first; t < total; t += stride) {
+        if (t + stride >= total) griddep_launch();  // last tile: the next kernel may launch
         const TileCoord tc = tile_coord<C_::TILE_M, BN>(p, t, tiles_m, tiles_n);
         const GemmRegion reg = p.regions[tc.region];
         const int am = tc.m0 + int(rank) * BM, bn = tc.n0 + int(rank) * C_::B_ROWS;
@@ -348,13 +352,15 @@ cudaError_t launch_t(const GemmLaunch& p, int num_sms, cudaStream_t stream) {
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = C_::SMEM;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = kCta;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, gemm_kernel<kBF16, kCta, BN>, p);
 }
 

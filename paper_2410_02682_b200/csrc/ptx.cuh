@@ -45,6 +45,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// ---- programmatic dependent launch ---------------------------------------
+// wait until the preceding grid of the stream has completed and its memory
+// is visible (no-op when this grid was launched without the PDL attribute)
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// let the next grid of the stream start launching (its CTAs run their
+// prologue on free SMs, then block in griddep_wait)
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---- clusters ----------------------------------------------------------------
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
