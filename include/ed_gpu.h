@@ -135,8 +135,18 @@ typedef struct {
   int32_t corrupt;          /* exec_options_t::corrupt test hook: +1 on one join output */
   int32_t profile;          /* 1: time every launch with CUDA events (ed_kernel_stats) */
   int32_t no_graph;         /* 1: launch eagerly instead of replaying a CUDA graph */
-  int32_t reserved[4];
+  int32_t transport;        /* ed_transport: how remote dependencies move (world > 1) */
+  int32_t reserved[3];
 } ed_options_c;
+
+/* ED_TRANSPORT_NCCL: ncclSend / ncclRecv groups on a comm stream (needs the
+ *   context's NCCL communicator).
+ * ED_TRANSPORT_PEER: the consumer copies the producer's chunk straight out of
+ *   the producer's HBM (CUDA IPC mapping; NVLink between GPUs) once a ready
+ *   flag in the producer's memory carries this run's epoch. Needs
+ *   ed_peer_export / ed_peer_import before the first ed_run; works with several
+ *   ranks on one GPU too (tests). */
+typedef enum { ED_TRANSPORT_NCCL = 0, ED_TRANSPORT_PEER = 1 } ed_transport;
 
 /* One input chunk (tensor_relation_t::chunks entry, relation.h:13-19),
  * row-major over exec vertex exec_id's chunk_bound. */
@@ -206,7 +216,8 @@ struct ed_plan_h;
 ED_API int32_t ed_abi_version(void);
 
 /* NCCL bootstrap id (128 bytes) for world > 1, made on rank 0 and
- * broadcast by the caller. */
+ * broadcast by the caller. ed_ctx_create takes nccl_id = NULL for a world
+ * that only uses the peer transport. */
 ED_API ed_status ed_nccl_unique_id(void* out, size_t len, char* err, size_t errlen);
 
 ED_API ed_status ed_ctx_create(int32_t device, int32_t rank, int32_t world,
@@ -284,6 +295,17 @@ typedef struct {
  * estimated busiest-GPU milliseconds before and after. */
 ED_API ed_status ed_gpu_placement(const ed_plan_c* plan, const ed_cost_model_c* model, int32_t* machine_of,
                                   double* est_ms, char* err, size_t errlen);
+
+/* Peer transport bootstrap (ED_TRANSPORT_PEER, world > 1). ed_peer_export
+ * writes this rank's blob (IPC handles of its chunk arena and flag words, and
+ * the arena offset of every chunk it holds) into out (capacity cap, *len set;
+ * call with out = NULL to get the size). The caller all-gathers the blobs
+ * (any bootstrap: torch.distributed, MPI, files) and hands every rank the
+ * world's blobs in rank order: ed_peer_import maps the peers' memory and
+ * records the CUDA graph. */
+ED_API ed_status ed_peer_export(struct ed_plan_h* h, void* out, size_t cap, size_t* len, char* err, size_t errlen);
+ED_API ed_status ed_peer_import(struct ed_plan_h* h, const void* blobs, size_t blob_len, int32_t n, char* err,
+                                size_t errlen);
 
 /* Per-launch-class timings of the last profiled ed_run. */
 ED_API ed_status ed_kernel_stats(struct ed_plan_h* h, ed_kernel_stat_c* out, int32_t cap,

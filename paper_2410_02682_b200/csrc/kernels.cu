@@ -336,6 +336,55 @@ cudaError_t launch_split_lo(const float* x, float* lo, int64_t n, cudaStream_t s
   return cudaGetLastError();
 }
 
+namespace {
+__global__ void peer_tick_kernel(int* epoch) { *epoch += 1; }
+__global__ void peer_signal_kernel(int* flag, const int* epoch) {
+  const int e = *epoch;
+  __threadfence_system();
+  asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(flag), "r"(e) : "memory");
+}
+struct PeerFlags {
+  int* f[16];
+};
+__global__ void peer_wait_kernel(PeerFlags fl, int n, const int* epoch, int delta, int* err, int tag) {
+  const int want = *epoch + delta;
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (int i = 0; i < n; ++i) {
+    int v;
+    for (;;) {
+      asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(fl.f[i]) : "memory");
+      if (v >= want) break;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 20000000000ull) {  // 20 s: report instead of hanging the stream
+        if (err) atomicExch(err, 1 + tag * 64 + i);
+        return;
+      }
+      __nanosleep(64);
+    }
+  }
+}
+}  // namespace
+
+cudaError_t launch_peer_tick(int* epoch, cudaStream_t s) {
+  peer_tick_kernel<<<1, 1, 0, s>>>(epoch);
+  return cudaGetLastError();
+}
+cudaError_t launch_peer_signal(int* flag, const int* epoch, cudaStream_t s) {
+  peer_signal_kernel<<<1, 1, 0, s>>>(flag, epoch);
+  return cudaGetLastError();
+}
+cudaError_t launch_peer_wait(int* const* flags, int n, const int* epoch, int delta, cudaStream_t s, int* err,
+                             int tag) {
+  PeerFlags fl{};
+  for (int done = 0; done < n; done += 16) {  // 16 flags per launch
+    const int k = n - done < 16 ? n - done : 16;
+    for (int i = 0; i < k; ++i) fl.f[i] = flags[done + i];
+    peer_wait_kernel<<<1, 1, 0, s>>>(fl, k, epoch, delta, err, tag);
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t launch_add_one(void* p, DT dt, cudaStream_t s) {
   add_one_kernel<<<1, 1, 0, s>>>(p, int(dt));
   return cudaGetLastError();

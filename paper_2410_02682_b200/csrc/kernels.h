@@ -109,4 +109,12 @@ cudaError_t launch_split_lo(const float* x, float* lo, int64_t n, cudaStream_t s
 cudaError_t launch_convert(const void* src, DT in, void* dst, DT out, int64_t n, cudaStream_t s);
 cudaError_t launch_add_one(void* p, DT dt, cudaStream_t s);  // exec_options_t::corrupt hook
 
+// Peer-memory transport (CUDA IPC / NVLink): run epochs and ready flags.
+cudaError_t launch_peer_tick(int* epoch, cudaStream_t s);                     // epoch += 1
+cudaError_t launch_peer_signal(int* flag, const int* epoch, cudaStream_t s);  // flag = epoch (release, system scope)
+// spin until every flags[i] >= epoch + delta (acquire, system scope); after
+// 20 s give up and set *err = 1 + tag * 64 + i (the stream then continues)
+cudaError_t launch_peer_wait(int* const* flags, int n, const int* epoch, int delta, cudaStream_t s, int* err = nullptr,
+                             int tag = -1);
+
 }  // namespace ed

@@ -305,6 +305,7 @@ struct Op {
   DT dt = DT::F32;
   int peer = -1;
   size_t count = 0;
+  int exec = -1;      // SEND / RECV: the chunk's exec id
 };
 
 struct Buffer {
@@ -502,17 +503,45 @@ struct ed_plan_h {
   void* main_of(int id) { return buf[owner[id]].main; }
   void* b16_of(int id) { return buf[owner[id]].b16; }
 
-  // remote dependencies per consumer: (dep, destination rank), placed before
-  // the dep's first consumer on that rank, in exec-id order on every rank
+  // Remote dependencies: (dep, destination rank), placed before the dep's
+  // first consumer on that rank — where the consumer is LAUNCHED: the joins
+  // of one einsum run as one grouped launch at the position of its first
+  // join, so a transfer feeding any of them goes before that position. The
+  // positions depend on the plan only, so every rank derives the same
+  // global transfer order.
   std::vector<std::vector<std::pair<int, int>>> transfers_by_consumer() const {
     const int ne = int(X.size());
+    std::map<int, int> first_join;  // einsum -> its lowest join id
+    for (int id = 0; id < ne; ++id)
+      if (X[id].kind == ED_EXEC_JOIN) first_join.emplace(X[id].producer, id);
     std::vector<std::vector<std::pair<int, int>>> at(ne);
+    std::map<std::pair<int, int>, int> pos;  // (dep, dst) -> launch position of its first consumer
+    for (int id = 0; id < ne; ++id) {
+      if (X[id].kind == ED_EXEC_INPUT_CHUNK) continue;
+      const int dst = rank_of(id);
+      const int lp = X[id].kind == ED_EXEC_JOIN ? first_join.at(X[id].producer) : id;
+      for (int d : X[id].deps) {
+        if (rank_of(d) == dst) continue;
+        auto it = pos.find({d, dst});
+        if (it == pos.end()) pos.emplace(std::make_pair(d, dst), lp);
+        else it->second = std::min(it->second, lp);
+      }
+    }
+    // within one position, transfers keep the consumers' exec-id order
+    std::vector<std::tuple<int, int, int, int>> order;  // (position, first consumer, dep, dst)
     std::set<std::pair<int, int>> seen;
     for (int id = 0; id < ne; ++id) {
       if (X[id].kind == ED_EXEC_INPUT_CHUNK) continue;
-      int dst = rank_of(id);
+      const int dst = rank_of(id);
       for (int d : X[id].deps)
-        if (rank_of(d) != dst && seen.insert({d, dst}).second) at[id].push_back({d, dst});
+        if (rank_of(d) != dst && seen.insert({d, dst}).second) order.emplace_back(pos.at({d, dst}), id, d, dst);
+    }
+    std::stable_sort(order.begin(), order.end(),
+                     [](const auto& a, const auto& b) { return std::get<0>(a) < std::get<0>(b); });
+    for (auto& [p, c, d, dst] : order) {
+      (void)c;
+      if (d >= p) throw ed_error(ED_ERR_PLAN, "transfer scheduled before its chunk is produced");
+      at[p].push_back({d, dst});
     }
     return at;
   }
@@ -524,6 +553,33 @@ struct ed_plan_h {
   void launch_op(size_t i, cudaStream_t s);
   void enqueue(cudaStream_t s);
   std::vector<cudaEvent_t> comm_events;  // fork / join points of the comm stream
+  // peer transport (ED_TRANSPORT_PEER): run epoch, exported flag words
+  // [0] run done, [1] outputs downloaded, [2 + id] chunk id ready; the peers'
+  // arenas, flags and chunk offsets as mapped by ed_peer_import
+  bool peer = false, peer_ready = false;
+  int* d_epoch = nullptr;
+  int* d_pflags = nullptr;
+  int* d_perr = nullptr;  // a peer wait that timed out: 1 + tag * 64 + flag
+  void check_peer_error() {
+    if (!d_perr) return;
+    int e = 0;
+    CUDA_OK(cudaMemcpy(&e, d_perr, sizeof(int), cudaMemcpyDeviceToHost));
+    if (!e) return;
+    CUDA_OK(cudaMemset(d_perr, 0, sizeof(int)));
+    const int tag = (e - 1) / 64, i = (e - 1) % 64, ne = int(X.size());
+    std::string what = tag < ne   ? "chunk " + std::to_string(tag) + " from rank " + std::to_string(rank_of(tag))
+                       : tag == ne ? "the run-start barrier (rank " + std::to_string(i) + ")"
+                       : tag == ne + 1 ? "rank " + std::to_string(i) + " finishing the run (download)"
+                                       : "rank 0's download";
+    throw ed_error(ED_ERR_CUDA, "peer transport: timed out waiting for " + what);
+  }
+  std::vector<char*> peer_arena;
+  std::vector<int*> peer_flags;
+  std::vector<std::vector<int64_t>> peer_off;
+  int64_t arena_offset(int id) const {
+    const Buffer& b = buf[owner[id]];
+    return b.main ? int64_t(static_cast<char*>(b.main) - static_cast<char*>(arena)) : -1;
+  }
   void destroy();
 };
 
@@ -1235,6 +1291,7 @@ void ed_plan_h::build() {
       if (rank_of(d) == me) {
         Op op{OpKind::SEND};
         op.name = "nccl_send";
+        op.exec = d;
         op.peer = dst;
         op.ptr = reinterpret_cast<void*>(d);  // resolved after allocation
         op.count = size_t(X[d].sz);
@@ -1243,6 +1300,7 @@ void ed_plan_h::build() {
       } else if (dst == me) {
         Op op{OpKind::RECV};
         op.name = "nccl_recv";
+        op.exec = d;
         op.peer = rank_of(d);
         op.ptr = reinterpret_cast<void*>(d);
         op.count = size_t(X[d].sz);
@@ -1912,6 +1970,14 @@ void ed_plan_h::allocate() {
       ro += op.regions.size();
     }
   }
+  if (peer) {
+    CUDA_OK(cudaMalloc(&d_epoch, sizeof(int)));
+    CUDA_OK(cudaMemset(d_epoch, 0, sizeof(int)));
+    CUDA_OK(cudaMalloc(&d_pflags, sizeof(int) * (X.size() + 2)));
+    CUDA_OK(cudaMemset(d_pflags, 0, sizeof(int) * (X.size() + 2)));
+    CUDA_OK(cudaMalloc(&d_perr, sizeof(int)));
+    CUDA_OK(cudaMemset(d_perr, 0, sizeof(int)));
+  }
 }
 
 void ed_plan_h::launch_op(size_t i, cudaStream_t s) {
@@ -1937,10 +2003,19 @@ void ed_plan_h::launch_op(size_t i, cudaStream_t s) {
       break;
     case OpKind::CONVERT: CUDA_OK(launch_convert(op.gen.x, store, op.gen.out16, DT::BF16, op.gen.n_out, s)); break;
     case OpKind::SEND:
-      NCCL_OK(ncclSend(op.ptr, op.count, f64 ? ncclFloat64 : ncclFloat32, op.peer, ctx->comm, s));
+      if (peer) CUDA_OK(launch_peer_signal(d_pflags + 2 + op.exec, d_epoch, s));  // chunk ready for the peer
+      else NCCL_OK(ncclSend(op.ptr, op.count, f64 ? ncclFloat64 : ncclFloat32, op.peer, ctx->comm, s));
       break;
     case OpKind::RECV:
-      NCCL_OK(ncclRecv(op.ptr, op.count, f64 ? ncclFloat64 : ncclFloat32, op.peer, ctx->comm, s));
+      if (peer) {
+        int* f = peer_flags[size_t(op.peer)] + 2 + op.exec;
+        CUDA_OK(launch_peer_wait(&f, 1, d_epoch, 0, s, d_perr, op.exec));
+        const int64_t off = peer_off[size_t(op.peer)][size_t(op.exec)];
+        if (off < 0) throw ed_error(ED_ERR_PLAN, "peer transport: chunk not resident on its producer rank");
+        CUDA_OK(cudaMemcpyAsync(op.ptr, peer_arena[size_t(op.peer)] + off, op.count * es, cudaMemcpyDeviceToDevice, s));
+      } else {
+        NCCL_OK(ncclRecv(op.ptr, op.count, f64 ? ncclFloat64 : ncclFloat32, op.peer, ctx->comm, s));
+      }
       break;
   }
 }
@@ -1948,9 +2023,9 @@ void ed_plan_h::launch_op(size_t i, cudaStream_t s) {
 // Every op in schedule order on the compute stream, except that each run of
 // consecutive transfers goes to the comm stream as ONE NCCL group (the
 // exchange of a repartition proceeds with all peers at once). The comm
-// stream forks from the compute stream before a run that sends (its
-// operands are produced by then) and the compute stream joins it right
-// after the run: transfers sit just before their data's first consumer, so
+// stream forks from the compute stream before every run (a send's operand
+// is produced by then, and the fork keeps the comm stream inside the CUDA
+// graph capture) and the compute stream joins it right after the run: transfers sit just before their data's first consumer, so
 // the sender keeps computing while its sends drain and a receiver's recvs
 // are posted as soon as the comm stream reaches them, ahead of its compute.
 // Buffers are never reused within a run (linear arena), so an early recv
@@ -1959,6 +2034,14 @@ void ed_plan_h::launch_op(size_t i, cudaStream_t s) {
 void ed_plan_h::enqueue(cudaStream_t s) {
   cudaStream_t cs = ctx->comm_stream;
   size_t ev = 0;
+  if (peer) {
+    // new run: advance the epoch, then wait until every rank has finished its
+    // previous run (its receives from our chunks are complete: write-after-read)
+    CUDA_OK(launch_peer_tick(d_epoch, s));
+    std::vector<int*> done(peer_flags.size());
+    for (size_t r = 0; r < done.size(); ++r) done[r] = peer_flags[r];
+    CUDA_OK(launch_peer_wait(done.data(), int(done.size()), d_epoch, -1, s, d_perr, int(X.size())));
+  }
   auto next_event = [&]() {
     if (ev == comm_events.size()) {
       cudaEvent_t e;
@@ -1976,32 +2059,34 @@ void ed_plan_h::enqueue(cudaStream_t s) {
       continue;
     }
     size_t j = i;
-    bool sends = false;
-    for (; j < ops.size() && is_comm(j); ++j) sends = sends || ops[j].kind == OpKind::SEND;
+    while (j < ops.size() && is_comm(j)) ++j;
     if (opt.profile)
       for (size_t k = i; k < j; ++k) CUDA_OK(cudaEventRecord(op_events[k], s));
-    if (sends) {
+    {
+      // every run forks from the compute stream: a send's chunk is produced by
+      // then, and a receive must follow the run's start (epoch, graph capture)
       cudaEvent_t fork = next_event();
       CUDA_OK(cudaEventRecord(fork, s));
       CUDA_OK(cudaStreamWaitEvent(cs, fork, 0));
     }
-    NCCL_OK(ncclGroupStart());
+    if (!peer) NCCL_OK(ncclGroupStart());
     for (size_t k = i; k < j; ++k) launch_op(k, cs);
-    NCCL_OK(ncclGroupEnd());
+    if (!peer) NCCL_OK(ncclGroupEnd());
     cudaEvent_t join = next_event();
     CUDA_OK(cudaEventRecord(join, cs));
     CUDA_OK(cudaStreamWaitEvent(s, join, 0));
     i = j;
   }
   if (opt.profile) CUDA_OK(cudaEventRecord(op_events[ops.size()], s));
+  if (peer) CUDA_OK(launch_peer_signal(d_pflags, d_epoch, s));  // this run is done on this rank
 }
 
 void ed_plan_h::record() {
   CUDA_OK(gemm_prepare());
   CUDA_OK(attn_prepare());
-  CUDA_OK(cudaEventCreate(&ev0));
-  CUDA_OK(cudaEventCreate(&ev1));
-  if (opt.no_graph || opt.profile) return;
+  if (!ev0) CUDA_OK(cudaEventCreate(&ev0));
+  if (!ev1) CUDA_OK(cudaEventCreate(&ev1));
+  if (opt.no_graph || opt.profile || (peer && !peer_ready)) return;  // peer: recorded by ed_peer_import
   cudaStream_t s = ctx->stream;
   CUDA_OK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
   try {
@@ -2023,6 +2108,14 @@ void ed_plan_h::destroy() {
   if (ev1) cudaEventDestroy(ev1);
   for (auto e : op_events) cudaEventDestroy(e);
   for (auto e : comm_events) cudaEventDestroy(e);
+  for (size_t r = 0; r < peer_arena.size(); ++r)
+    if (int(r) != ctx->rank) {
+      if (peer_arena[r]) cudaIpcCloseMemHandle(peer_arena[r]);
+      if (peer_flags[r]) cudaIpcCloseMemHandle(peer_flags[r]);
+    }
+  if (d_epoch) cudaFree(d_epoch);
+  if (d_perr) cudaFree(d_perr);
+  if (d_pflags) cudaFree(d_pflags);
   if (arena) cudaFree(arena);
   if (d_deps) cudaFree(d_deps);
   if (d_maps) cudaFree(d_maps);
@@ -2213,8 +2306,8 @@ ed_status ed_ctx_create(int32_t device, int32_t rank, int32_t world, const void*
     try {
       CUDA_OK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
       CUDA_OK(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
-      if (world > 1) {
-        if (!nccl_id || nccl_id_len < sizeof(ncclUniqueId)) throw ed_error(ED_ERR_USAGE, "world > 1 needs an NCCL id");
+      if (world > 1 && nccl_id) {
+        if (nccl_id_len < sizeof(ncclUniqueId)) throw ed_error(ED_ERR_USAGE, "NCCL id too short");
         ncclUniqueId id;
         std::memcpy(&id, nccl_id, sizeof(id));
         NCCL_OK(ncclCommInitRank(&c->comm, world, id, rank));
@@ -2247,6 +2340,11 @@ ed_status ed_prepare(ed_ctx* ctx, const ed_plan_c* plan, const ed_options_c* opt
     if (h->opt.precision < 0 || h->opt.precision > 4) {
       delete h;
       throw ed_error(ED_ERR_USAGE, "unknown precision");
+    }
+    h->peer = ctx->world > 1 && h->opt.transport == ED_TRANSPORT_PEER;
+    if (ctx->world > 1 && !h->peer && !ctx->comm) {
+      delete h;
+      throw ed_error(ED_ERR_USAGE, "world > 1 without an NCCL communicator needs ED_TRANSPORT_PEER");
     }
     h->f64 = h->opt.precision == ED_PREC_FP64;
     h->store = h->f64 ? DT::F64 : DT::F32;
@@ -2330,6 +2428,7 @@ ed_status ed_upload_tensors(ed_plan_h* h, const ed_tensor_in_c* ts, int32_t n, c
 ed_status ed_run(ed_plan_h* h, ed_report_c* rep, char* err, size_t errlen) {
   return guarded(err, errlen, [&] {
     if (!h) throw ed_error(ED_ERR_USAGE, "null plan");
+    if (h->peer && !h->peer_ready) throw ed_error(ED_ERR_USAGE, "ED_TRANSPORT_PEER: call ed_peer_import first");
     CUDA_OK(cudaSetDevice(h->ctx->device));
     cudaStream_t s = h->ctx->stream;
     CUDA_OK(cudaMemsetAsync(h->d_err, 0, sizeof(int), s));
@@ -2343,6 +2442,7 @@ ed_status ed_run(ed_plan_h* h, ed_report_c* rep, char* err, size_t errlen) {
     else h->enqueue(s);
     CUDA_OK(cudaEventRecord(h->ev1, s));
     CUDA_OK(cudaEventSynchronize(h->ev1));
+    h->check_peer_error();
     int flag = 0;
     CUDA_OK(cudaMemcpy(&flag, h->d_err, sizeof(int), cudaMemcpyDeviceToHost));
     float ms = 0;
@@ -2409,7 +2509,21 @@ ed_status ed_download(ed_plan_h* h, ed_output_c* outs, int32_t n, char* err, siz
       if (ids.empty()) throw ed_error(ED_ERR_PLAN, "no final refinement layer for output");
       // world > 1: every rank calls; chunks held elsewhere travel to rank 0
       std::vector<void*> remote(ids.size(), nullptr);
-      if (world > 1) {
+      if (world > 1 && h->peer) {
+        if (me != 0) continue;  // rank 0 reads our chunks; we wait for it below
+        // once every rank has finished the run, copy its chunks out of its HBM
+        std::vector<int*> done(h->peer_flags.begin(), h->peer_flags.end());
+        CUDA_OK(launch_peer_wait(done.data(), int(done.size()), h->d_epoch, 0, s, h->d_perr, int(h->X.size()) + 1));
+        for (size_t k = 0; k < ids.size(); ++k) {
+          const int id = ids[k], src = h->rank_of(id);
+          if (src == 0) continue;
+          const int64_t off = h->peer_off[size_t(src)][size_t(id)];
+          if (off < 0) throw ed_error(ED_ERR_PLAN, "peer transport: output chunk not resident on its rank");
+          CUDA_OK(cudaMallocAsync(&remote[k], size_t(h->X[id].sz) * h->es, s));
+          CUDA_OK(cudaMemcpyAsync(remote[k], h->peer_arena[size_t(src)] + off, size_t(h->X[id].sz) * h->es,
+                                  cudaMemcpyDeviceToDevice, s));
+        }
+      } else if (world > 1) {
         NCCL_OK(ncclGroupStart());
         for (size_t k = 0; k < ids.size(); ++k) {
           int id = ids[k], src = h->rank_of(id);
@@ -2437,6 +2551,17 @@ ed_status ed_download(ed_plan_h* h, ed_output_c* outs, int32_t n, char* err, siz
       for (void* r : remote)
         if (r) CUDA_OK(cudaFreeAsync(r, s));
       CUDA_OK(cudaStreamSynchronize(s));
+    }
+    if (world > 1 && h->peer) {
+      // rank 0 has copied every remote output chunk once its flag [1] carries
+      // this run's epoch; until then the other ranks must not start a new run
+      if (me == 0) CUDA_OK(launch_peer_signal(h->d_pflags + 1, h->d_epoch, s));
+      else {
+        int* f = h->peer_flags[0] + 1;
+        CUDA_OK(launch_peer_wait(&f, 1, h->d_epoch, 0, s, h->d_perr, int(h->X.size()) + 2));
+      }
+      CUDA_OK(cudaStreamSynchronize(s));
+      h->check_peer_error();
     }
   });
 }
@@ -2791,6 +2916,75 @@ ed_status ed_gpu_placement(const ed_plan_c* plan, const ed_cost_model_c* model, 
       est_ms[0] = before * 1e3;
       est_ms[1] = cur.first * 1e3;
     }
+  });
+}
+
+namespace {
+
+struct PeerBlobHead {
+  int32_t magic, rank, world, n_exec;
+  cudaIpcMemHandle_t arena, flags;
+};
+constexpr int32_t kPeerMagic = 0x45445031;  // "EDP1"
+
+size_t peer_blob_len(const ed_plan_h* h) { return sizeof(PeerBlobHead) + sizeof(int64_t) * h->X.size(); }
+
+}  // namespace
+
+ed_status ed_peer_export(ed_plan_h* h, void* out, size_t cap, size_t* len, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!h || !len) throw ed_error(ED_ERR_USAGE, "null argument");
+    if (!h->peer) throw ed_error(ED_ERR_USAGE, "plan was not prepared with ED_TRANSPORT_PEER in a world > 1");
+    *len = peer_blob_len(h);
+    if (!out) return;
+    if (cap < *len) throw ed_error(ED_ERR_USAGE, "ed_peer_export: buffer too small");
+    CUDA_OK(cudaSetDevice(h->ctx->device));
+    PeerBlobHead hd{};
+    hd.magic = kPeerMagic;
+    hd.rank = h->ctx->rank;
+    hd.world = h->ctx->world;
+    hd.n_exec = int32_t(h->X.size());
+    CUDA_OK(cudaIpcGetMemHandle(&hd.arena, h->arena));
+    CUDA_OK(cudaIpcGetMemHandle(&hd.flags, h->d_pflags));
+    std::memcpy(out, &hd, sizeof hd);
+    auto* off = reinterpret_cast<int64_t*>(static_cast<char*>(out) + sizeof hd);
+    for (int id = 0; id < int(h->X.size()); ++id) off[id] = h->local[id] ? h->arena_offset(id) : -1;
+  });
+}
+
+ed_status ed_peer_import(ed_plan_h* h, const void* blobs, size_t blob_len, int32_t n, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!h || !blobs) throw ed_error(ED_ERR_USAGE, "null argument");
+    if (!h->peer) throw ed_error(ED_ERR_USAGE, "plan was not prepared with ED_TRANSPORT_PEER in a world > 1");
+    if (h->peer_ready) throw ed_error(ED_ERR_USAGE, "ed_peer_import: already imported");
+    if (n != h->ctx->world || blob_len != peer_blob_len(h)) throw ed_error(ED_ERR_USAGE, "ed_peer_import: need one blob per rank");
+    CUDA_OK(cudaSetDevice(h->ctx->device));
+    const int world = h->ctx->world, me = h->ctx->rank;
+    h->peer_arena.assign(size_t(world), nullptr);
+    h->peer_flags.assign(size_t(world), nullptr);
+    h->peer_off.assign(size_t(world), {});
+    for (int r = 0; r < world; ++r) {
+      const char* b = static_cast<const char*>(blobs) + size_t(r) * blob_len;
+      PeerBlobHead hd;
+      std::memcpy(&hd, b, sizeof hd);
+      if (hd.magic != kPeerMagic || hd.rank != r || hd.world != world || hd.n_exec != int32_t(h->X.size()))
+        throw ed_error(ED_ERR_USAGE, "ed_peer_import: blob " + std::to_string(r) + " does not belong to this plan");
+      h->peer_off[size_t(r)].resize(h->X.size());
+      std::memcpy(h->peer_off[size_t(r)].data(), b + sizeof hd, sizeof(int64_t) * h->X.size());
+      if (r == me) {
+        h->peer_arena[size_t(r)] = static_cast<char*>(h->arena);
+        h->peer_flags[size_t(r)] = h->d_pflags;
+        continue;
+      }
+      void* a = nullptr;
+      void* f = nullptr;
+      CUDA_OK(cudaIpcOpenMemHandle(&a, hd.arena, cudaIpcMemLazyEnablePeerAccess));
+      CUDA_OK(cudaIpcOpenMemHandle(&f, hd.flags, cudaIpcMemLazyEnablePeerAccess));
+      h->peer_arena[size_t(r)] = static_cast<char*>(a);
+      h->peer_flags[size_t(r)] = static_cast<int*>(f);
+    }
+    h->peer_ready = true;
+    h->record();
   });
 }
 

@@ -118,7 +118,8 @@ class PreparedPlan:
     """A plan resident on the GPU: buffers allocated, kernels chosen, CUDA graph
     recorded (ed_prepare). Upload, run and download may be repeated."""
 
-    def __init__(self, ctx: Context, plan: Plan, precision="bf16", corrupt=False, profile=False, graph=True):
+    def __init__(self, ctx: Context, plan: Plan, precision="bf16", corrupt=False, profile=False, graph=True,
+                 transport="nccl"):
         self.ctx, self.plan = ctx, plan
         self._pc, self._keep = plan.to_c()
         opt = abi.ed_options_c()
@@ -126,6 +127,7 @@ class PreparedPlan:
         opt.corrupt = int(bool(corrupt))
         opt.profile = int(bool(profile))
         opt.no_graph = int(not graph)
+        opt.transport = abi.TRANSPORT[transport]
         h = C.c_void_p()
         err, n = _err()
         _check(library().ed_prepare(ctx.h, C.byref(self._pc), C.byref(opt), C.byref(h), err, n), err)
@@ -191,6 +193,25 @@ class PreparedPlan:
             err, n = _err()
             _check(library().ed_download(self.h, arr, len(descs), err, n), err)
         return outs
+
+    # ---- peer transport bootstrap (ED_TRANSPORT_PEER) -------------------------
+    def peer_export(self) -> bytes:
+        """This rank's blob (IPC handles + chunk offsets) for ed_peer_import."""
+        n = C.c_size_t()
+        err, en = _err()
+        _check(library().ed_peer_export(self.h, None, 0, C.byref(n), err, en), err)
+        buf = C.create_string_buffer(n.value)
+        _check(library().ed_peer_export(self.h, buf, n.value, C.byref(n), err, en), err)
+        return buf.raw[:n.value]
+
+    def peer_import(self, blobs: list):
+        """Every rank's blob, in rank order (e.g. from all_gather_object)."""
+        if not blobs or any(len(b) != len(blobs[0]) for b in blobs):
+            raise ValueError("one equally sized blob per rank")
+        joined = b"".join(blobs)
+        buf = C.create_string_buffer(joined, len(joined))
+        err, en = _err()
+        _check(library().ed_peer_import(self.h, buf, len(blobs[0]), len(blobs), err, en), err)
 
     def run_steps(self, inputs: list, outputs: list) -> RunReport:
         """ed_run_steps: len(inputs) end-to-end steps (upload inputs[s], run,

@@ -1,0 +1,113 @@
+"""Multi-rank execution with real device-to-device transfers on ONE GPU.
+
+World 2 / 4: one process per rank, all on cuda:0 (NCCL refuses two ranks on
+one device, so these runs use the peer transport: a consumer copies the
+producer's chunk straight out of the producer's HBM through a CUDA IPC
+mapping once the producer's ready flag carries the run's epoch — on an 8-GPU
+box the same copies travel over NVLink). Each rank runs its share of the
+placed ExecGraph through the C ABI, rank 0 assembles the outputs (collective
+ed_download), and they must equal the reference executor's outputs bit for bit
+(FP64) with the reference's transfer counters; two consecutive runs exercise
+the epoch / write-after-read barriers.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, load_golden, load_plan
+
+pytestmark = pytest.mark.gpu
+
+CASES = [("attention_p8_L4_s1084", 4), ("attention_p8_L4_s1084", 2), ("ffnn_p4_L2_s23", 2),
+         ("chain8_pinned_L4_s7", 4), ("mix_p4_L2_s41", 2), ("softmax_p8_L4_s1084", 4)]
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, case, port, q, precision, replaced):
+    import sys
+    from datetime import timedelta
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    try:
+        import torch.distributed as dist
+        from paper_2410_02682_b200.executor import Context, PreparedPlan, gpu_placement
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world, timeout=timedelta(seconds=120))
+        name, ins, o64, o32, orc, counters, total = load_golden(case)
+        plan = load_plan(name)
+        if replaced:
+            plan = gpu_placement(plan)[0]
+        ctx = Context(0, rank, world, None)
+        pp = PreparedPlan(ctx, plan, precision=precision, transport="peer")
+        blobs = [None] * world
+        dist.all_gather_object(blobs, pp.peer_export())
+        pp.peer_import(blobs)
+        pp.upload(ins)
+        results = []
+        for _ in range(2):
+            rep = pp.run()
+            outs = pp.download()
+            results.append((rep.machines, rep.total_transferred, outs if rank == 0 else None))
+        pp.close()
+        ctx.close()
+        dist.barrier()
+        q.put((rank, "ok", results if rank == 0 else None))
+        dist.destroy_process_group()
+    except Exception as e:  # surface the failure to the parent
+        import traceback
+        q.put((rank, f"{type(e).__name__}: {e}\n{traceback.format_exc()[-1500:]}", None))
+
+
+def _run(case, world, precision="fp64", replaced=False):
+    import torch.multiprocessing as mp
+    from paper_2410_02682_b200 import build
+    build.build()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, case, port, q, precision, replaced)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=280) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, status, _ in res:
+        assert status == "ok", f"rank {rank}: {status}"
+    return next(r for rank, s, r in res if rank == 0)
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("case,world", CASES)
+def test_peer_transport_fp64_bitexact(case, world):
+    from oracle import bridge as B
+    name, ins, o64, o32, orc, counters, total = load_golden(case)
+    plan = load_plan(name)
+    has_exp = any(v.expr is not None and v.expr.map == "exp" for v in plan.vertices)
+    for machines, tt, outs in _run(case, world):
+        for vid, want in o64.items():
+            got = outs[vid]
+            if not np.array_equal(got, want):
+                # device exp vs host libm (tests/test_gpu_parity.py: EXP_ULP)
+                assert has_exp and B.max_rel_err(got, want) <= 1e-14, (case, vid)
+        assert tt == total and [tuple(m) for m in machines] == [tuple(c) for c in counters]
+
+
+@pytest.mark.timeout(300)
+def test_peer_transport_replaced_plan_bf16():
+    """The GPU-aware re-placement run on 4 ranks in the tensor-core mode."""
+    case = "attention_p8_L4_s1084"
+    name, ins, o64, o32, orc, counters, total = load_golden(case)
+    from oracle import bridge as B
+    for machines, tt, outs in _run(case, 4, precision="bf16", replaced=True):
+        for vid, want in o64.items():
+            assert B.max_rel_err(outs[vid], want) <= 3e-2
