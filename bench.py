@@ -187,11 +187,15 @@ def main():
     ap.add_argument("--impl", default="ours")
     ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "peer"],
+                    help="N > 1: remote chunks over NCCL send/recv, or read from the producer's HBM (CUDA IPC)")
     ap.add_argument("--placement", default="gpu", choices=["gpu", "ref"],
                     help="gpu: GPU-aware re-placement of memory-bound vertices (ed_gpu_placement); "
                          "ref: the reference planner's machine_of")
     args = ap.parse_args()
     rank, world, local = dist_env()
+    if os.environ.get("ED_SAME_DEVICE"):  # functional check of N ranks on one GPU (peer transport only)
+        local = 0
     if args.impl == "reference":
         return run_reference(args, rank, world)
 
@@ -209,7 +213,7 @@ def main():
         if rank == 0:
             idt = torch.tensor(list(Context.nccl_unique_id()), dtype=torch.uint8)
         dist.broadcast(idt, 0)
-        ctx = Context(local, rank, world, bytes(idt.tolist()))
+        ctx = Context(local, rank, world, bytes(idt.tolist()) if args.transport == "nccl" else None)
     else:
         ctx = Context(local)
 
@@ -226,8 +230,16 @@ def main():
         if world > 1:
             torch.distributed.barrier()
 
+    def prepared(**kw):
+        pp = PreparedPlan(ctx, plan, precision=args.precision, transport=args.transport, **kw)
+        if world > 1 and args.transport == "peer":
+            blobs = [None] * world
+            torch.distributed.all_gather_object(blobs, pp.peer_export())
+            pp.peer_import(blobs)
+        return pp
+
     # ---- device-resident throughput --------------------------------------
-    pp = PreparedPlan(ctx, plan, precision=args.precision)
+    pp = prepared()
     pp.upload(ins)
     with Clocks(local) as clk:
         time.sleep(0.5)  # let the sampler start before the timed region
@@ -255,7 +267,7 @@ def main():
 
     # ---- kernel shares / roofline (one profiled run) -----------------------
     pk, pk_sus, hbm, peak_src = peaks()
-    pp = PreparedPlan(ctx, plan, precision=args.precision, profile=True)
+    pp = prepared(profile=True)
     pp.upload(ins)
     pp.run()
     pp.run()
@@ -294,7 +306,7 @@ def main():
     pins = {vid: t.numpy() for vid, t in pin.items()}
     outs = {vid: torch.empty(plan.vertices[vid].bound, dtype=torch.float32).pin_memory() for vid in plan.outputs}
     outs_np = {vid: t.numpy() for vid, t in outs.items()}
-    pp = PreparedPlan(ctx, plan, precision=args.precision)
+    pp = prepared()
     h2d = sum(a.nbytes for a in pins.values())
     d2h = sum(a.nbytes for a in outs_np.values())
     pp.upload(pins)
@@ -340,6 +352,7 @@ def main():
                 "config": {"workload": CONFIG_DESC.get(args.config, args.config), "graph": args.config,
                            "p": 8, "L": L, "plan": f"plans/{args.config}_p8_L{L}.json",
                            "placement": args.placement if L > 1 else "single GPU", "placement_estimate": est,
+                           "transport": args.transport if L > 1 else None,
                            "l2": "inputs larger than L2 (1 GiB per input tensor); no flush needed",
                            "frac_of_peak": value / (pk * world)},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
