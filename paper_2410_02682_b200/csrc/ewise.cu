@@ -225,15 +225,31 @@ __global__ void __launch_bounds__(128) rowreduce_seq_kernel(const RowReduceParam
   }
 }
 
-// One 128-thread block per row; the row lives in registers (EPT per thread),
-// so X is read once and Y written once (the five unfused vertices move the
-// row eight times).
-template <int EPT>
-__global__ void __launch_bounds__(128) softmax_kernel(const SoftmaxParams p) {
+// One block of NT threads per row; the row lives in registers (EPT per
+// thread), so X is read once and Y written once (the five unfused vertices
+// move the row eight times). Long rows use 256 threads so a thread holds at
+// most 32 values and more rows are in flight per SM.
+template <int EPT, int NT>
+__global__ void __launch_bounds__(NT) softmax_kernel(const SoftmaxParams p) {
   constexpr int NV = EPT / 4;
-  __shared__ float red[4];
+  constexpr int NW = NT / 32;
+  __shared__ float red[NW];
   const JoinPtrs jp = p.joins[blockIdx.y];
   const int t = threadIdx.x, lane = t % 32, warp = t / 32;
+  auto block_reduce = [&](float v, bool is_max) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float w = __shfl_xor_sync(0xffffffffu, v, o);
+      v = is_max ? fmaxf(v, w) : v + w;
+    }
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    float r = red[0];
+#pragma unroll
+    for (int i = 1; i < NW; ++i) r = is_max ? fmaxf(r, red[i]) : r + red[i];
+    __syncthreads();
+    return r;
+  };
   for (int64_t row = blockIdx.x; row < p.rows; row += gridDim.x) {
     const float* xr = static_cast<const float*>(jp.x) + row * p.len;
     const RowSeg* sg = p.segs ? p.segs + size_t(blockIdx.y) * p.n_seg : nullptr;
@@ -241,7 +257,7 @@ __global__ void __launch_bounds__(128) softmax_kernel(const SoftmaxParams p) {
     float mx = -INFINITY;
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
-      const int i = (j * 128 + t) * 4;
+      const int i = (j * NT + t) * 4;
       const float* src = xr + i;
       if (sg) {  // gather the row from its column segments in place
         const RowSeg s = sg[i / p.seg_w];
@@ -255,38 +271,25 @@ __global__ void __launch_bounds__(128) softmax_kernel(const SoftmaxParams p) {
 #pragma unroll
       for (int e = 0; e < 4; ++e) mx = fmaxf(mx, v[4 * j + e]);
     }
-    if (jp.y) {
-      mx = static_cast<const float*>(jp.y)[row];  // the planned row max, computed upstream
-    } else {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      if (lane == 0) red[warp] = mx;
-      __syncthreads();
-      mx = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
-      __syncthreads();
-    }
+    if (jp.y) mx = static_cast<const float*>(jp.y)[row];  // the planned row max, computed upstream
+    else mx = block_reduce(mx, true);
     float sum = 0.f;
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
-      const int i = (j * 128 + t) * 4;
+      const int i = (j * NT + t) * 4;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        v[4 * j + e] = i < p.len ? expf(v[4 * j + e] - mx) : 0.f;
+        v[4 * j + e] = i < p.len ? __expf(v[4 * j + e] - mx) : 0.f;
         sum += v[4 * j + e];
       }
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    if (lane == 0) red[warp] = sum;
-    __syncthreads();
-    sum = (red[0] + red[1]) + (red[2] + red[3]);
-    __syncthreads();
+    sum = block_reduce(sum, false);
     const float inv = __frcp_rn(sum);
     float* yo = jp.out ? static_cast<float*>(jp.out) + row * p.len : nullptr;
     __nv_bfloat16* y16 = jp.out16 ? static_cast<__nv_bfloat16*>(jp.out16) + row * p.len : nullptr;
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
-      const int i = (j * 128 + t) * 4;
+      const int i = (j * NT + t) * 4;
       if (i >= p.len) continue;
       const float a = v[4 * j] * inv, b = v[4 * j + 1] * inv, c = v[4 * j + 2] * inv, d = v[4 * j + 3] * inv;
       if (yo) __stcs(reinterpret_cast<float4*>(yo + i), make_float4(a, b, c, d));
@@ -320,10 +323,10 @@ cudaError_t launch_ewise(const EwiseParams& p, int n_joins, bool f64, bool exact
 cudaError_t launch_softmax(const SoftmaxParams& p, int n_joins, cudaStream_t s) {
   const unsigned rows = unsigned(p.rows < 65535 * 8 ? p.rows : 65535 * 8);
   dim3 grid(rows, n_joins);
-  if (p.len <= 128 * 8) softmax_kernel<8><<<grid, 128, 0, s>>>(p);
-  else if (p.len <= 128 * 16) softmax_kernel<16><<<grid, 128, 0, s>>>(p);
-  else if (p.len <= 128 * 32) softmax_kernel<32><<<grid, 128, 0, s>>>(p);
-  else if (p.len <= 128 * 64) softmax_kernel<64><<<grid, 128, 0, s>>>(p);
+  if (p.len <= 128 * 8) softmax_kernel<8, 128><<<grid, 128, 0, s>>>(p);
+  else if (p.len <= 128 * 16) softmax_kernel<16, 128><<<grid, 128, 0, s>>>(p);
+  else if (p.len <= 128 * 32) softmax_kernel<32, 128><<<grid, 128, 0, s>>>(p);
+  else if (p.len <= 256 * 32) softmax_kernel<32, 256><<<grid, 256, 0, s>>>(p);
   else return cudaErrorInvalidValue;
   return cudaGetLastError();
 }
