@@ -187,8 +187,9 @@ def main():
     ap.add_argument("--impl", default="ours")
     ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--transport", default="nccl", choices=["nccl", "peer"],
-                    help="N > 1: remote chunks over NCCL send/recv, or read from the producer's HBM (CUDA IPC)")
+    ap.add_argument("--transport", default="peer", choices=["nccl", "peer"],
+                    help="N > 1: remote chunks read from the producer's HBM over NVLink (CUDA IPC; the "
+                         "transport the multi-rank GPU tests run), or NCCL send/recv")
     ap.add_argument("--placement", default="gpu", choices=["gpu", "ref"],
                     help="gpu: GPU-aware re-placement of memory-bound vertices (ed_gpu_placement); "
                          "ref: the reference planner's machine_of")
