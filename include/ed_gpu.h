@@ -239,6 +239,14 @@ ED_API ed_status ed_upload(struct ed_plan_h* h, const ed_chunk_in_c* chunks, int
 ED_API ed_status ed_upload_tensors(struct ed_plan_h* h, const ed_tensor_in_c* tensors, int32_t n,
                             char* err, size_t errlen);
 
+/* generate_inputs(graph, seed) (runtime.cc:552-571) on the device: every input
+ * tensor this rank holds chunks of is drawn from std::mt19937_64(seed * 7919 +
+ * vertex) through libstdc++'s uniform_int_distribution<int>(-4, 4) (graphs
+ * that only sum and multiply, runtime.cc:358-378) or
+ * uniform_real_distribution<double>(-1, 1), bit for bit, then chunked in
+ * place of ed_upload_tensors. */
+ED_API ed_status ed_generate_inputs(struct ed_plan_h* h, uint64_t seed, char* err, size_t errlen);
+
 /* Run every exec vertex of this rank; device-resident. report may be NULL. */
 ED_API ed_status ed_run(struct ed_plan_h* h, ed_report_c* report, char* err, size_t errlen);
 

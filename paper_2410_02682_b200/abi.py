@@ -142,7 +142,7 @@ EXPORTED = [
     "ed_abi_version", "ed_nccl_unique_id", "ed_ctx_create", "ed_ctx_destroy",
     "ed_prepare", "ed_plan_destroy", "ed_upload", "ed_upload_tensors", "ed_run",
     "ed_download", "ed_download_chunk", "ed_plan_schedule", "ed_kernel_stats", "ed_gpu_placement",
-    "ed_run_steps", "ed_peer_export", "ed_peer_import",
+    "ed_run_steps", "ed_peer_export", "ed_peer_import", "ed_generate_inputs",
 ]
 
 
@@ -169,6 +169,7 @@ def declare(lib):
     lib.ed_kernel_stats.argtypes = [P, C.POINTER(ed_kernel_stat_c), C.c_int32, i32p] + err
     lib.ed_run_steps.argtypes = [P, C.c_int32, C.POINTER(ed_tensor_in_c), C.c_int32, C.POINTER(ed_output_c),
                                  C.c_int32, C.POINTER(ed_report_c)] + err
+    lib.ed_generate_inputs.argtypes = [P, C.c_uint64] + err
     lib.ed_peer_export.argtypes = [P, C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t)] + err
     lib.ed_peer_import.argtypes = [P, C.c_void_p, C.c_size_t, C.c_int32] + err
     lib.ed_gpu_placement.argtypes = [C.POINTER(ed_plan_c), C.POINTER(ed_cost_model_c), i32p,

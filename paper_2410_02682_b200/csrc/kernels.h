@@ -109,6 +109,20 @@ cudaError_t launch_split_lo(const float* x, float* lo, int64_t n, cudaStream_t s
 cudaError_t launch_convert(const void* src, DT in, void* dst, DT out, int64_t n, cudaStream_t s);
 cudaError_t launch_add_one(void* p, DT dt, cudaStream_t s);  // exec_options_t::corrupt hook
 
+// generate_inputs (runtime.cc:552-571) on the device: one block per tensor
+// runs std::mt19937_64(seed) 156 words at a time (the recurrence reaches 156
+// words back at most) and applies libstdc++'s uniform_int_distribution<int>
+// (-4, 4) (Lemire's nearly-divisionless downscale) or uniform_real_distribution
+// <double>(-1, 1) (generate_canonical), bit for bit. A rejected integer draw
+// (probability 7 / 2^64) would shift the stream: it is flagged in *err.
+struct GenTensor {
+  void* out;          // whole tensor, row-major, store dtype
+  int64_t n;
+  uint64_t seed;      // seed * 7919 + vid
+};
+cudaError_t launch_generate(const GenTensor* jobs, int n_jobs, bool integer_valued, DT store, int* err,
+                            cudaStream_t s);
+
 // Peer-memory transport (CUDA IPC / NVLink): run epochs and ready flags.
 cudaError_t launch_peer_tick(int* epoch, cudaStream_t s);                     // epoch += 1
 cudaError_t launch_peer_signal(int* flag, const int* epoch, cudaStream_t s);  // flag = epoch (release, system scope)

@@ -2425,6 +2425,67 @@ ed_status ed_upload_tensors(ed_plan_h* h, const ed_tensor_in_c* ts, int32_t n, c
   });
 }
 
+namespace {
+std::vector<int> io_chunks(const ed_plan_h* h, int w, bool input);
+}  // namespace
+
+ed_status ed_generate_inputs(ed_plan_h* h, uint64_t seed, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!h) throw ed_error(ED_ERR_USAGE, "null plan");
+    CUDA_OK(cudaSetDevice(h->ctx->device));
+    // uses_only_sum_mul (runtime.cc:358-378): generate_inputs' distribution switch
+    bool integer_valued = true;
+    for (const Vtx& v : h->V) {
+      if (v.arity == 0) continue;
+      if (v.join >= 0 && v.join != ED_JOIN_MUL && v.join != ED_JOIN_ADD) integer_valued = false;
+      if (v.map >= 0 && v.map != ED_MAP_IDENTITY && v.map != ED_MAP_RELU && v.map != ED_MAP_NEG) integer_valued = false;
+      if (v.agg >= 0 && v.agg != ED_AGG_SUM && v.agg != ED_AGG_MAX) integer_valued = false;
+    }
+    cudaStream_t s = h->ctx->stream;
+    std::vector<GenTensor> jobs;
+    std::vector<int> vids;
+    for (int w = 0; w < int(h->V.size()); ++w) {
+      if (h->V[w].arity != 0) continue;
+      bool any_local = false;
+      for (int id : io_chunks(h, w, true)) any_local = any_local || h->local[id];
+      if (!any_local) continue;  // a rank only materialises the inputs it holds chunks of
+      GenTensor g{};
+      g.n = prod(h->V[w].bound);
+      g.seed = seed * 7919ULL + uint64_t(w);
+      CUDA_OK(cudaMallocAsync(&g.out, size_t(g.n) * h->es, s));
+      jobs.push_back(g);
+      vids.push_back(w);
+    }
+    if (jobs.empty()) return;
+    GenTensor* d_jobs = nullptr;
+    int* d_flag = nullptr;
+    CUDA_OK(cudaMallocAsync(reinterpret_cast<void**>(&d_jobs), sizeof(GenTensor) * jobs.size(), s));
+    CUDA_OK(cudaMallocAsync(reinterpret_cast<void**>(&d_flag), sizeof(int), s));
+    CUDA_OK(cudaMemsetAsync(d_flag, 0, sizeof(int), s));
+    CUDA_OK(cudaMemcpyAsync(d_jobs, jobs.data(), sizeof(GenTensor) * jobs.size(), cudaMemcpyHostToDevice, s));
+    CUDA_OK(launch_generate(d_jobs, int(jobs.size()), integer_valued, h->store, d_flag, s));
+    // chunk() (relation.cc:31-53) into this rank's input chunks (+ bf16 / lo shadows)
+    for (size_t k = 0; k < jobs.size(); ++k) {
+      const std::vector<int> ids = io_chunks(h, vids[k], true);
+      block_copies(h, vids[k], h->V[vids[k]].d, ids, true, jobs[k].out, nullptr, h->store, s);
+      for (int id : ids)
+        if (h->local[id] && h->buf[id].lo)
+          CUDA_OK(launch_split_lo(static_cast<const float*>(h->buf[id].main), static_cast<float*>(h->buf[id].lo),
+                                  h->X[id].sz, s));
+      CUDA_OK(cudaStreamSynchronize(s));  // block_copies' descriptor buffer is reused per tensor
+    }
+    int flag = 0;
+    CUDA_OK(cudaMemcpyAsync(&flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+    for (auto& g : jobs) CUDA_OK(cudaFreeAsync(g.out, s));
+    CUDA_OK(cudaFreeAsync(d_jobs, s));
+    CUDA_OK(cudaFreeAsync(d_flag, s));
+    CUDA_OK(cudaStreamSynchronize(s));
+    if (flag)
+      throw ed_error(ED_ERR_UNSUPPORTED,
+                     "generate_inputs: a rejected integer draw (p = 7/2^64) shifted the stream; generate on the host");
+  });
+}
+
 ed_status ed_run(ed_plan_h* h, ed_report_c* rep, char* err, size_t errlen) {
   return guarded(err, errlen, [&] {
     if (!h) throw ed_error(ED_ERR_USAGE, "null plan");

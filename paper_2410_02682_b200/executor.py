@@ -167,6 +167,12 @@ class PreparedPlan:
             arr = (abi.ed_chunk_in_c * len(chunks))(*chunks)
             _check(library().ed_upload(self.h, arr, len(chunks), err, n), err)
 
+    def generate_inputs(self, seed: int):
+        """generate_inputs(graph, seed) (runtime.cc:552-571) on the device, bit
+        for bit, chunked into this rank's input chunks (ed_generate_inputs)."""
+        err, n = _err()
+        _check(library().ed_generate_inputs(self.h, C.c_uint64(seed), err, n), err)
+
     # ---- run -------------------------------------------------------------------
     def run(self) -> RunReport:
         L = self.plan.n_machines
@@ -181,10 +187,11 @@ class PreparedPlan:
                          rep.contraction_flops, rep.gpu_launches)
 
     # ---- outputs ---------------------------------------------------------------
-    def download(self, dtype=np.float64, into: dict | None = None) -> dict:
+    def download(self, dtype=np.float64, into: dict | None = None, vertices=None) -> dict:
+        """Assembled graph outputs (or any input / output `vertices`)."""
         outs = {}
         descs = []
-        for vid in self.plan.outputs:
+        for vid in (self.plan.outputs if vertices is None else vertices):
             a = into[vid] if into is not None else np.empty(self.plan.vertices[vid].bound, dtype=dtype)
             outs[vid] = a
             descs.append(abi.ed_output_c(vid, _dt(a), a.ctypes.data, a.size))
