@@ -341,13 +341,38 @@ constexpr int kMtN = 312, kMtM = 156;
 
 // std::mt19937_64 (MT19937-64): x[k+312] = x[k+156] ^ ((x[k] & UM | x[k+1] & LM) >> 1) ^ (x[k+1] & 1 ? A : 0);
 // output k = temper(x[312 + k]). The 312-word window lives in shared memory;
-// each step makes the next 156 words in parallel (156 threads).
-__global__ void __launch_bounds__(kMtM) generate_kernel(const GenTensor* jobs, int integer_valued, int store,
-                                                        int* err) {
+// each step, threads 0-155 make the next 156 words while threads 156-311
+// temper, transform and store the 156 words made in the step before (they
+// sit in the half of the window the current step does not overwrite).
+__device__ __forceinline__ void gen_emit(const GenTensor& J, int64_t k, uint64_t y, int integer_valued, int store,
+                                         int* err) {
+  if (k >= J.n) return;
+  y ^= (y >> 29) & 0x5555555555555555ULL;
+  y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
+  y ^= (y << 37) & 0xFFF7EEE000000000ULL;
+  y ^= y >> 43;
+  double v;
+  if (integer_valued) {
+    // _S_nd<unsigned __int128>(g, 9): product = g() * 9, reject if low < (-9) % 9 = 7
+    if (y * 9ULL < 7ULL) atomicExch(err, 1);
+    v = double(int64_t(__umul64hi(y, 9ULL)) - 4);
+  } else {
+    // generate_canonical<double, 53>: double(g()) / 2^64, clamped below 1; then u * (b - a) + a
+    double u = __dmul_rn(__ull2double_rn(y), 0x1p-64);
+    if (u >= 1.0) u = 0x1.fffffffffffffp-1;
+    v = __dadd_rn(__dmul_rn(u, 2.0), -1.0);
+  }
+  if (store == int(DT::F64)) static_cast<double*>(J.out)[k] = v;
+  else static_cast<float*>(J.out)[k] = __double2float_rn(v);
+}
+
+__global__ void __launch_bounds__(2 * kMtM) generate_kernel(const GenTensor* jobs, int integer_valued, int store,
+                                                            int* err) {
   __shared__ uint64_t w[kMtN];
   const GenTensor J = jobs[blockIdx.x];
-  const int i = threadIdx.x;
-  if (i == 0) {  // init_genrand64: seeding is sequential
+  const bool maker = threadIdx.x < kMtM;
+  const int i = maker ? threadIdx.x : threadIdx.x - kMtM;
+  if (threadIdx.x == 0) {  // init_genrand64: seeding is sequential
     uint64_t x = J.seed;
     w[0] = x;
     for (int k = 1; k < kMtN; ++k) {
@@ -357,37 +382,22 @@ __global__ void __launch_bounds__(kMtM) generate_kernel(const GenTensor* jobs, i
   }
   __syncthreads();
   int b = 0;  // w[b .. b+155] holds x[t .. t+155], w[b^156 ..] holds x[t+156 .. t+311]
-  for (int64_t base = 0; base < J.n; base += kMtM) {
-    const uint64_t a = w[b + i];
-    const uint64_t a1 = i + 1 < kMtM ? w[b + i + 1] : w[(b ^ kMtM)];
-    const uint64_t m = w[(b ^ kMtM) + i];
-    const uint64_t x = (a & 0xFFFFFFFF80000000ULL) | (a1 & 0x7FFFFFFFULL);
-    const uint64_t nx = m ^ (x >> 1) ^ ((a1 & 1ULL) ? 0xB5026F5AA96619E9ULL : 0ULL);
+  for (int64_t base = 0; base < J.n + kMtM; base += kMtM) {
+    uint64_t nx = 0;
+    if (maker) {
+      const uint64_t a = w[b + i];
+      const uint64_t a1 = i + 1 < kMtM ? w[b + i + 1] : w[(b ^ kMtM)];
+      const uint64_t m = w[(b ^ kMtM) + i];
+      const uint64_t x = (a & 0xFFFFFFFF80000000ULL) | (a1 & 0x7FFFFFFFULL);
+      nx = m ^ (x >> 1) ^ ((a1 & 1ULL) ? 0xB5026F5AA96619E9ULL : 0ULL);
+    } else if (base > 0) {
+      // outputs base - 156 + i = x[t + 156 + i], made by the previous step
+      gen_emit(J, base - kMtM + i, w[(b ^ kMtM) + i], integer_valued, store, err);
+    }
     __syncthreads();
-    w[b + i] = nx;  // x[t+i] is dead once every thread has read it
+    if (maker) w[b + i] = nx;  // x[t+i] is dead once every thread has read it
     __syncthreads();
     b ^= kMtM;
-    const int64_t k = base + i;
-    if (k < J.n) {
-      uint64_t y = nx;
-      y ^= (y >> 29) & 0x5555555555555555ULL;
-      y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
-      y ^= (y << 37) & 0xFFF7EEE000000000ULL;
-      y ^= y >> 43;
-      double v;
-      if (integer_valued) {
-        // _S_nd<unsigned __int128>(g, 9): product = g() * 9, reject if low < (-9) % 9 = 7
-        if (y * 9ULL < 7ULL) atomicExch(err, 1);
-        v = double(int64_t(__umul64hi(y, 9ULL)) - 4);
-      } else {
-        // generate_canonical<double, 53>: double(g()) / 2^64, clamped below 1; then u * (b - a) + a
-        double u = __dmul_rn(__ull2double_rn(y), 0x1p-64);
-        if (u >= 1.0) u = 0x1.fffffffffffffp-1;
-        v = __dadd_rn(__dmul_rn(u, 2.0), -1.0);
-      }
-      if (store == int(DT::F64)) static_cast<double*>(J.out)[k] = v;
-      else static_cast<float*>(J.out)[k] = __double2float_rn(v);
-    }
   }
 }
 
@@ -422,7 +432,7 @@ __global__ void peer_wait_kernel(PeerFlags fl, int n, const int* epoch, int delt
 
 cudaError_t launch_generate(const GenTensor* jobs, int n_jobs, bool integer_valued, DT store, int* err,
                             cudaStream_t s) {
-  generate_kernel<<<n_jobs, kMtM, 0, s>>>(jobs, int(integer_valued), int(store), err);
+  generate_kernel<<<n_jobs, 2 * kMtM, 0, s>>>(jobs, int(integer_valued), int(store), err);
   return cudaGetLastError();
 }
 
