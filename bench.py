@@ -264,6 +264,14 @@ def main():
     flops = plan.contraction_flops()
     value = flops * args.steps / (tot_ms / 1e3) / 1e12
     launches = rep.gpu_launches
+    # chunk bytes this rank sent to peers per step (NCCL or peer transport)
+    sent = rep.peer_bytes
+    if world > 1:
+        t = torch.tensor([float(sent)], dtype=torch.float64)
+        torch.distributed.all_reduce(t)
+        sent = float(t.item())
+    transfers = {"bytes_per_step": sent, "gbs": sent / (tot_ms / args.steps / 1e3) / 1e9 if tot_ms else 0.0,
+                 "note": "all ranks' peer bytes / step time (one step moves them concurrently)"}
     pp.close()
 
     # ---- kernel shares / roofline (one profiled run) -----------------------
@@ -357,7 +365,7 @@ def main():
                            "l2": "inputs larger than L2 (1 GiB per input tensor); no flush needed",
                            "frac_of_peak": value / (pk * world)},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": launches * args.steps, "clocks": clk.summary()}
+                "gpu_launches": launches * args.steps, "clocks": clk.summary(), "transfers": transfers}
         print(json.dumps(line), flush=True)
     ctx.close()
 
