@@ -95,6 +95,10 @@ class Clocks:
         # lags by up to one period, so allow 50 ms of slack)
         t0, t1 = getattr(self, "t0", 0.0), getattr(self, "t1", 1e18)
         inside = [s for t, s in self.samples if t0 <= t <= t1 + 0.05]
+        window = "timed region"
+        if not inside:  # a region shorter than the sampling period: take the samples right around it
+            inside = [s for t, s in self.samples if t0 - 0.15 <= t <= t1 + 0.15]
+            window = "timed region +-150 ms"
         if not inside:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
         sm = [float(s[1]) for s in inside if s[1].replace(".", "").isdigit()]
@@ -103,7 +107,8 @@ class Clocks:
         reasons = sorted({names[i] for s in inside for i in range(4) if s[5 + i].lower().startswith("active")})
         pw = [float(s[3]) for s in inside if s[3].replace(".", "").isdigit()]
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(inside), "power_w_max": max(pw) if pw else None}
+                "reasons": reasons, "samples": len(inside), "power_w_max": max(pw) if pw else None,
+                "window": window}
 
 
 def dist_env():
