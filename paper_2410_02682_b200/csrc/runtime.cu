@@ -306,6 +306,7 @@ struct Op {
   int peer = -1;
   size_t count = 0;
   int exec = -1;      // SEND / RECV: the chunk's exec id
+  int einsum = -1;    // GEMM: the graph vertex it computes
 };
 
 struct Buffer {
@@ -553,6 +554,25 @@ struct ed_plan_h {
   void launch_op(size_t i, cudaStream_t s);
   void enqueue(cudaStream_t s);
   std::vector<cudaEvent_t> comm_events;  // fork / join points of the comm stream
+  cudaStream_t aux[2] = {nullptr, nullptr};  // independent GEMMs run as parallel graph branches
+  // graph vertex a is an ancestor of b (data flows from a to b)
+  bool ancestor(int a, int b) const {
+    std::vector<int> todo{b};
+    std::vector<char> seen(V.size(), 0);
+    while (!todo.empty()) {
+      const int w = todo.back();
+      todo.pop_back();
+      for (int k = 0; k < V[w].arity; ++k) {
+        const int in = V[w].inputs[k];
+        if (in == a) return true;
+        if (in >= 0 && !seen[size_t(in)]) {
+          seen[size_t(in)] = 1;
+          todo.push_back(in);
+        }
+      }
+    }
+    return false;
+  }
   // peer transport (ED_TRANSPORT_PEER): run epoch, exported flag words
   // [0] run done, [1] outputs downloaded, [2 + id] chunk id ready; the peers'
   // arenas, flags and chunk offsets as mapped by ed_peer_import
@@ -1368,6 +1388,7 @@ void ed_plan_h::build() {
         // one persistent launch for every region of this einsum on this rank
         Op op{OpKind::GEMM};
         op.bf16 = bf16;
+        op.einsum = u.producer;
         op.name = std::string(bf16 ? "gemm_bf16:" : "gemm_tf32:") + w.name;
         op.ptr = reinterpret_cast<void*>(id);
         for (int h = 0; h < ne; ++h)
@@ -2052,6 +2073,38 @@ void ed_plan_h::enqueue(cudaStream_t s) {
   };
   auto is_comm = [&](size_t i) { return ops[i].kind == OpKind::SEND || ops[i].kind == OpKind::RECV; };
   for (size_t i = 0; i < ops.size();) {
+    // consecutive GEMMs of mutually independent einsums (e.g. attention's Q, K, V
+    // projections) run as parallel branches: each persistent grid's last,
+    // partial wave leaves SMs the next one fills
+    size_t g = i;
+    if (!opt.profile) {
+      while (g < ops.size() && ops[g].kind == OpKind::GEMM && g - i < 3) {
+        bool indep = true;
+        for (size_t a = i; a < g && indep; ++a) indep = !ancestor(ops[a].einsum, ops[g].einsum);
+        if (!indep) break;
+        ++g;
+      }
+    }
+    if (g - i >= 2) {
+      cudaEvent_t fork = next_event();
+      CUDA_OK(cudaEventRecord(fork, s));
+      std::vector<cudaEvent_t> joins;
+      for (size_t k = i + 1; k < g; ++k) {
+        cudaStream_t a = aux[k - i - 1];
+        if (!a) {
+          CUDA_OK(cudaStreamCreateWithFlags(&aux[k - i - 1], cudaStreamNonBlocking));
+          a = aux[k - i - 1];
+        }
+        CUDA_OK(cudaStreamWaitEvent(a, fork, 0));
+        launch_op(k, a);
+        joins.push_back(next_event());
+        CUDA_OK(cudaEventRecord(joins.back(), a));
+      }
+      launch_op(i, s);
+      for (cudaEvent_t e : joins) CUDA_OK(cudaStreamWaitEvent(s, e, 0));
+      i = g;
+      continue;
+    }
     if (!is_comm(i)) {
       if (opt.profile) CUDA_OK(cudaEventRecord(op_events[i], s));
       launch_op(i, s);
@@ -2108,6 +2161,8 @@ void ed_plan_h::destroy() {
   if (ev1) cudaEventDestroy(ev1);
   for (auto e : op_events) cudaEventDestroy(e);
   for (auto e : comm_events) cudaEventDestroy(e);
+  for (auto a : aux)
+    if (a) cudaStreamDestroy(a);
   for (size_t r = 0; r < peer_arena.size(); ++r)
     if (int(r) != ctx->rank) {
       if (peer_arena[r]) cudaIpcCloseMemHandle(peer_arena[r]);
