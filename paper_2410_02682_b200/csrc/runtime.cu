@@ -863,15 +863,35 @@ void ed_plan_h::build() {
     for (int w = 0; w < nv; ++w)
       for (int k = 0; k < V[w].arity; ++k) readers[V[w].inputs[k]].push_back(w);
     auto is_output = [&](int w) { return std::find(outputs.begin(), outputs.end(), w) != outputs.end(); };
+    // Fusions are decided per rank: a vertex can be fused on this rank when it
+    // has work here and none of the chunks it makes here is read by another
+    // rank (what other ranks need is never fused away). With one rank this is
+    // "all of its exec vertices are local".
+    std::vector<char> remote_read(ne, 0);
+    for (int id = 0; id < ne; ++id)
+      if (!local[id])
+        for (int d : X[id].deps) remote_read[d] = 1;
+    // fused away on this rank: has work here, and no chunk it makes here is
+    // read by another rank
     auto all_local = [&](int w) {
-      for (int id = 0; id < ne; ++id)
-        if (X[id].producer == w && !local[id]) return false;
-      return true;
+      bool any = false;
+      for (int id = 0; id < ne; ++id) {
+        if (X[id].producer != w || X[id].kind == ED_EXEC_INPUT_CHUNK || !local[id]) continue;
+        if (remote_read[id]) return false;
+        any = true;
+      }
+      return any;
     };
-    auto joins_of = [&](int w) {
+    // computed inside a fused kernel but still materialised: work here suffices
+    auto has_local = [&](int w) {
+      for (int id = 0; id < ne; ++id)
+        if (X[id].producer == w && X[id].kind == ED_EXEC_JOIN && local[id]) return true;
+      return false;
+    };
+    auto joins_of = [&](int w) {  // this rank's joins of w
       std::vector<int> r;
       for (int id = 0; id < ne; ++id)
-        if (X[id].kind == ED_EXEC_JOIN && X[id].producer == w) r.push_back(id);
+        if (X[id].kind == ED_EXEC_JOIN && X[id].producer == w && local[id]) r.push_back(id);
       return r;
     };
     auto sole_reader = [&](int w, int r) {
@@ -881,7 +901,7 @@ void ed_plan_h::build() {
     for (int v = 0; v < nv; ++v) {
       if (!memmap_.count(v) || memmap_[v].kind != OpKind::EWISE || V[v].arity != 1) continue;
       const int u = V[v].inputs[0];
-      if (!gmap.count(u) || !sole_reader(u, v) || !all_local(u) || !all_local(v)) continue;
+      if (!gmap.count(u) || !sole_reader(u, v) || !all_local(u) || !has_local(v)) continue;
       if (V[v].map == ED_MAP_EXP) continue;  // only cheap maps go into the epilogue
       bool ok = true;
       for (int j : joins_of(v)) {
@@ -893,7 +913,7 @@ void ed_plan_h::build() {
       for (int j : joins_of(v)) virtual_join_src[j] = 0;
       // u's own values never exist: its chunks hold map(u)
       for (int id = 0; id < ne; ++id)
-        if (X[id].producer == u && X[id].kind != ED_EXEC_INPUT_CHUNK) opaque_[id] = 1;
+        if (X[id].producer == u && X[id].kind != ED_EXEC_INPUT_CHUNK && local[id]) opaque_[id] = 1;
       memmap_.erase(v);
     }
     alias_pass(virtual_join_src);
@@ -911,7 +931,7 @@ void ed_plan_h::build() {
       if (!is(sv, OpKind::EWISE, 2, ED_JOIN_SUB) || memmap_[sv].y_mode != 2) continue;
       const int xv = V[sv].inputs[0], m = V[sv].inputs[1];
       if (!sole_reader(sv, e) || !sole_reader(sg, y) || is_output(e) || readers[e].size() != 2) continue;
-      if (!all_local(sv) || !all_local(e) || !all_local(sg) || !all_local(y)) continue;
+      if (!all_local(sv) || !all_local(e) || !all_local(sg) || !has_local(y)) continue;
       const int64_t L = memmap_[sg].len;
       if (memmap_[sv].inner != L || memmap_[y].inner != L) continue;
       if (L % 4 != 0 || L > 128 * 64 || f64) continue;  // the fused kernel keeps a row in registers
@@ -934,7 +954,7 @@ void ed_plan_h::build() {
       }
       auto join_at = [&](int ref, int w) {
         const int o = owner[ref];
-        return (X[o].kind == ED_EXEC_JOIN && X[o].producer == w) ? o : -1;
+        return (X[o].kind == ED_EXEC_JOIN && X[o].producer == w && local[o]) ? o : -1;
       };
       Softmax sm;
       bool ok = true, internal = m_fusable || m_full_rows;
@@ -976,29 +996,36 @@ void ed_plan_h::build() {
     // (3) attention block: T1 = Q K^T (GEMM, maybe with a fused scale), the
     // softmax chain on T1 (or its scaled map), O = T3 V (GEMM, K = the row
     // label) -> one kernel; T1 and T3 are never materialised (bf16 only)
+    static const bool ftrace = std::getenv("ED_FUSE_TRACE") != nullptr;
+#define REJECT(k)                                                                            \
+  {                                                                                          \
+    if (ftrace) std::fprintf(stderr, "[ed] rank %d: attention block at %s not fused (%d)\n", me, \
+                             V[yv].name.c_str(), k);                                         \
+    continue;                                                                                \
+  }
     for (auto& [yv, sm] : softmax_) {
       if (!bf16) break;
-      if (readers[yv].size() != 1 || is_output(yv) || !sm.m_refs.empty()) continue;
+      if (readers[yv].size() != 1 || is_output(yv) || !sm.m_refs.empty()) REJECT(1)
       const int o = readers[yv][0];
-      if (!gmap.count(o) || V[o].inputs[gmap[o].a_slot] != yv || !all_local(o)) continue;
+      if (!gmap.count(o) || V[o].inputs[gmap[o].a_slot] != yv || !has_local(o) || !all_local(yv)) REJECT(2)
       int t1 = sm.x;
       float scale = 1.0f;
       if (!gmap.count(t1)) {
         // x is a map vertex fused into its GEMM's epilogue (T2 = scale(T1))
         const int u = V[t1].arity == 1 ? V[t1].inputs[0] : -1;
-        if (u < 0 || !epi.count(u) || epi[u].first != ED_MAP_SCALE) continue;
+        if (u < 0 || !epi.count(u) || epi[u].first != ED_MAP_SCALE || !all_local(t1)) REJECT(3)
         scale = float(epi[u].second);
         t1 = u;
       } else if (epi.count(t1)) {
-        continue;
+        REJECT(4)
       }
-      if (!gmap.count(t1) || !all_local(t1)) continue;
+      if (!gmap.count(t1) || !all_local(t1)) REJECT(5)
       const GemmMap& gs = gmap[t1];
       const GemmMap& go = gmap[o];
       const int64_t H = gs.ab.ext, S = gs.am.ext, T = gs.bn.ext, Dd = gs.ak.ext;
       if (gs.a_mn || gs.b_mn || !go.b_mn || go.a_mn || go.ab.ext != H || go.am.ext != S || go.ak.ext != T ||
           go.bn.ext != Dd || T != sm.len || !attn_supported(int(S), int(T), int(Dd)))
-        continue;
+        REJECT(6)
       // region correspondence: O region <- T3 chunk <- T1 region (single siblings)
       std::map<int, int> t1_of_y;
       for (auto& [yj, xr] : sm.pairs) t1_of_y[yj] = owner[xr];
@@ -1013,10 +1040,12 @@ void ed_plan_h::build() {
         if (!ok) break;
         const int th = it->second;
         ok = fused_head[th] && X[th].producer == t1 && region_sibs[th].size() == 1;
+        if (!ok && ftrace) std::fprintf(stderr, "[ed] rank %d: O region %d <- T1 join %d (head %d, sibs %zu)\n", me, oh, th, int(fused_head[th]), region_sibs[th].size());
         if (!ok) break;
         f.regions.push_back({X[th].deps[gs.a_slot], X[th].deps[gs.b_slot], X[oh].deps[go.b_slot], oh});
       }
-      if (!ok || f.regions.empty()) continue;
+      if (!ok || f.regions.empty()) REJECT(8)
+#undef REJECT
       // K (T1's B) and V (O's B): read in place from their producers' regions
       // when the pasting refinement is a regular grid over (keys, d)
       auto tile = [&](int ref, const labels& lop, int keyl, int dl, int hl, KVTiles& t) {
