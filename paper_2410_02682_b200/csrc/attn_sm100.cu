@@ -462,6 +462,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           }
         }
         if (lane == 0 && wq == 0) ATTN_TRACE(7, t, j);
+        if (lane == 0 && wq != 0) ATTN_TRACE(12 + wq, t, j);
         // reference max with hysteresis: when a row's max passes m + kRescale
         // the new reference is max + kHeadroom, so P spans [2^-kHeadroom,
         // 2^kRescale] at the row max and rescales stay rare
@@ -515,6 +516,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           __syncwarp();
           if (lane == 0) mbar_arrive(hh == 0 ? &p_half[t] : &p_full[t]);
           if (lane == 0 && wq == 0) ATTN_TRACE(1 + hh, t, j);
+          if (lane == 0 && wq != 0 && hh == 1) ATTN_TRACE(9 + wq, t, j);
         }
         acc0 = fadd2(acc0, acc1);
         l = l * f + (acc0.x + acc0.y);
@@ -593,8 +595,8 @@ cudaError_t launch_d(const AttnLaunch& p0, int num_sms, cudaStream_t s) {
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(s, &cs);
   if (trace && cs == cudaStreamCaptureStatusNone) {
-    cudaMalloc(&p.trace, 10 * 2 * 64 * sizeof(long long));
-    cudaMemsetAsync(p.trace, 0, 10 * 2 * 64 * sizeof(long long), s);
+    cudaMalloc(&p.trace, 16 * 2 * 64 * sizeof(long long));
+    cudaMemsetAsync(p.trace, 0, 16 * 2 * 64 * sizeof(long long), s);
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(p.n_jobs < num_sms ? p.n_jobs : num_sms);
@@ -608,13 +610,13 @@ cudaError_t launch_d(const AttnLaunch& p0, int num_sms, cudaStream_t s) {
   cfg.numAttrs = 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, attn_kernel<D, kPolyPairs>, p);
   if (p.trace) {
-    long long h[10 * 2 * 64];
+    long long h[16 * 2 * 64];
     cudaStreamSynchronize(s);
     cudaMemcpy(h, p.trace, sizeof(h), cudaMemcpyDeviceToHost);
     cudaFree(p.trace);
     const long long t0 = h[5 * 128];
-    const char* names[10] = {"s_ready", "p_half", "p_full", "mma_got_half", "mma_got_full", "s_issued", "s_loaded", "max_done", "half0_stored", "pvb_issued"};
-    for (int ev = 0; ev < 10; ++ev)
+    const char* names[16] = {"s_ready", "p_half", "p_full", "mma_got_half", "mma_got_full", "s_issued", "s_loaded", "max_done", "half0_stored", "pvb_issued", "p_full_w1", "p_full_w2", "p_full_w3", "max_w1", "max_w2", "max_w3"};
+    for (int ev = 0; ev < 16; ++ev)
       for (int t = 0; t < 2; ++t) {
         std::fprintf(stderr, "attn_trace %-13s t%d:", names[ev], t);
         for (int j = 0; j < 33; ++j) std::fprintf(stderr, " %lld", h[(ev * 2 + t) * 64 + j] ? h[(ev * 2 + t) * 64 + j] - t0 : -1);
