@@ -289,6 +289,9 @@ typedef struct {
   double link_bytes;         /* GPU-to-GPU rate per direction (NVLink 5) */
   int32_t elem_bytes;        /* bytes per stored element (4: f32, 8: f64) */
   int32_t max_passes;        /* local-search passes (0: default 4) */
+  int32_t fuse_chains;       /* 1: keep each region of a fusable chain (attention block, row softmax,
+                                map epilogue) on one GPU so the executor can fuse it per rank */
+  int32_t reserved;
 } ed_cost_model_c;
 
 /* Host-only (no GPU needed). GPU-aware re-placement:

@@ -134,7 +134,8 @@ TRANSPORT = {"nccl": 0, "peer": 1}
 
 class ed_cost_model_c(C.Structure):
     _fields_ = [("tensor_flops", C.c_double), ("hbm_bytes", C.c_double), ("link_bytes", C.c_double),
-                ("elem_bytes", C.c_int32), ("max_passes", C.c_int32)]
+                ("elem_bytes", C.c_int32), ("max_passes", C.c_int32), ("fuse_chains", C.c_int32),
+                ("reserved", C.c_int32)]
 
 
 # Every symbol include/ed_gpu.h declares (tests/test_abi.py checks exports).

@@ -294,13 +294,15 @@ def plan_schedule(plan: Plan, rank: int, world: int):
     return [(names[arr[i].kind], arr[i].exec_id, arr[i].peer, arr[i].elems) for i in range(n.value)]
 
 
-def gpu_placement(plan: Plan, tensor_tflops=1652.1, hbm_gbs=6548.8, link_gbs=900.0, elem_bytes=4, passes=0):
+def gpu_placement(plan: Plan, tensor_tflops=1652.1, hbm_gbs=6548.8, link_gbs=900.0, elem_bytes=4, passes=0,
+                  fuse_chains=True):
     """GPU-aware re-placement (ed_gpu_placement; host-only): returns
     (plan with the new machine_of, estimated busiest-GPU ms before, after).
     Defaults: MEASURED_PEAKS.json bf16 / HBM copy rates, NVLink 5 per
-    direction."""
+    direction. fuse_chains keeps each region of a fusable chain on one GPU."""
     pc, keep = plan.to_c()
-    model = abi.ed_cost_model_c(tensor_tflops * 1e12, hbm_gbs * 1e9, link_gbs * 1e9, elem_bytes, passes)
+    model = abi.ed_cost_model_c(tensor_tflops * 1e12, hbm_gbs * 1e9, link_gbs * 1e9, elem_bytes, passes,
+                                int(fuse_chains), 0)
     m = (C.c_int32 * max(1, len(plan.exec)))()
     est = (C.c_double * 2)()
     err, en = _err()

@@ -132,13 +132,16 @@ def test_peer_transport_replaced_plan_bf16():
 
 
 @pytest.mark.timeout(300)
-@pytest.mark.parametrize("name,fused", [("attn_s_p8_L2", "attention_fused"), ("ffnn_s_p8_L2", "softmax_rows")])
-def test_peer_transport_fuses_per_rank(name, fused):
-    """Cross-vertex fusions are decided per rank: with the reduced twins on two
-    ranks every rank still runs the fused kernel for its co-located regions,
-    and the outputs agree with the single-rank run."""
-    got = _run(name + ".plan", 2, precision="bf16", want_kernels=True)
-    for rank in (0, 1):
+@pytest.mark.parametrize("name,fused,world,replaced", [
+    ("attn_s_p8_L2", "attention_fused", 2, False), ("ffnn_s_p8_L2", "softmax_rows", 2, False),
+    ("attn_s_p8_L4", "attention_fused", 4, True), ("ffnn_s_p8_L4", "softmax_rows", 4, True)])
+def test_peer_transport_fuses_per_rank(name, fused, world, replaced):
+    """Cross-vertex fusions are decided per rank: with the reduced twins on
+    2 / 4 ranks (the 4-rank plans re-placed with fuse_chains, which keeps each
+    chain region on one GPU) every rank runs the fused kernel for its
+    co-located regions, and the outputs agree with the single-rank run."""
+    got = _run(name + ".plan", world, precision="bf16", replaced=replaced, want_kernels=True)
+    for rank in range(world):
         assert any(k.startswith(fused) for k in got[rank][1]), (rank, got[rank][1])
     results = got[0][0]
     single = results[-1]
