@@ -23,7 +23,8 @@ from . import abi
 from .plan import Plan
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libed_gpu.so")
+# ED_LIB_PATH: a variant build of the same library (development experiments)
+LIB_PATH = os.environ.get("ED_LIB_PATH") or os.path.join(HERE, "libed_gpu.so")
 
 _lib = None
 
