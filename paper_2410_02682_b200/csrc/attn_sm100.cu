@@ -47,6 +47,11 @@ constexpr int kThreads = 512;  // four warpgroups
 constexpr int kTmaWarp = 8, kMmaWarp = 9;
 // register split (setmaxnreg): 2 x 128 x 200 + 128 x 48 + 128 x 56 <= 64K
 constexpr int kSoftmaxRegs = 200, kProducerRegs = 48, kCorrectionRegs = 56;
+// the softmax warpgroups can only take what the others give back from the
+// launch allocation (65536 / threads per thread), or setmaxnreg.inc never returns
+constexpr int kLaunchRegs = (65536 / kThreads) & ~7;
+static_assert(2 * (kSoftmaxRegs - kLaunchRegs) <= (kLaunchRegs - kProducerRegs) + (kLaunchRegs - kCorrectionRegs),
+              "setmaxnreg split exceeds the launch allocation");
 constexpr int kCorrWarp0 = 12;  // warps 12-15: O rescale (correction) warpgroup
 // lazy rescale (log2 units): P = 2^(x - m) may reach 2^kRescale before O is
 // rescaled, and a rescale sets m = row max + kHeadroom. bf16 / fp32 keep full
