@@ -1,0 +1,84 @@
+"""Randomised parity: 40 random EinSum graphs (oracle/gen_fuzz.py) planned,
+placed and executed by the unmodified reference — contractions over mul, add,
+sqdiff, absdiff with sum or max, broadcast joins, maps, reductions, p in
+{1,2,4,8}, L in {1,2,4}. The CPU oracle and the B200 executor (through the C
+ABI) must reproduce the reference's f64 outputs bit for bit (the f32 mode's
+too) and its transfer counters; tensor-core modes stay within the stated
+bound relative to the output's scale.
+"""
+import glob
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+from oracle import bridge as B
+
+FUZZ = os.path.join(GOLDEN, "fuzz")
+CASES = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(FUZZ, "*.npz")))
+TOL = {"tf32": 1e-2, "bf16": 3e-2, "fp32x3": 1e-5}
+
+
+def _load(case):
+    from paper_2410_02682_b200.plan import Plan
+    name = case.rsplit("_s", 1)[0]
+    with open(os.path.join(FUZZ, name + ".json")) as f:
+        plan = Plan.from_json(json.load(f))
+    z = np.load(os.path.join(FUZZ, case + ".npz"))
+    ins = {int(k[3:]): z[k] for k in z.files if k.startswith("in_")}
+    o64 = {int(k[6:]): z[k] for k in z.files if k.startswith("out64_")}
+    o32 = {int(k[6:]): z[k] for k in z.files if k.startswith("out32_")}
+    return plan, ins, o64, o32, [tuple(int(x) for x in r) for r in z["counters"]], int(z["total"])
+
+
+def _has_exp(plan):
+    return any(v.expr is not None and v.expr.map == "exp" for v in plan.vertices)
+
+
+def _same(got, want, plan, ulp):
+    if np.array_equal(got, want):
+        return True
+    # exp: device / host libm may differ in the last bit (tests/test_gpu_parity.py)
+    return _has_exp(plan) and B.max_rel_err(got, want) <= ulp
+
+
+def test_fuzz_cases_present():
+    assert len(CASES) >= 40
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_fuzz_oracle_matches_reference(case):
+    plan, ins, o64, o32, counters, total = _load(case)
+    got, _, cnt, tot = B.oracle_execute(plan, ins)
+    for vid, want in o64.items():
+        assert _same(got[vid], want, plan, 1e-14), (case, vid)
+    assert [tuple(c) for c in cnt] == counters and tot == total
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", CASES)
+def test_fuzz_gpu_fp64_fp32_bitexact(gpu_ctx, case):
+    from paper_2410_02682_b200.executor import execute
+    plan, ins, o64, o32, counters, total = _load(case)
+    rep = execute(plan, ins, precision="fp64", ctx=gpu_ctx)
+    for vid, want in o64.items():
+        assert _same(rep.outputs[vid], want, plan, 1e-14), (case, vid, B.max_rel_err(rep.outputs[vid], want))
+    assert rep.machines == counters and rep.total_transferred == total
+    rep = execute(plan, ins, precision="fp32", ctx=gpu_ctx)
+    for vid, want in o32.items():
+        assert _same(rep.outputs[vid], want, plan, 1e-6), (case, vid, B.max_rel_err(rep.outputs[vid], want))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("prec", ["tf32", "bf16", "fp32x3"])
+@pytest.mark.parametrize("case", CASES)
+def test_fuzz_gpu_tensor_core_modes(gpu_ctx, case, prec):
+    from paper_2410_02682_b200.executor import execute
+    plan, ins, o64, o32, counters, total = _load(case)
+    rep = execute(plan, ins, precision=prec, ctx=gpu_ctx)
+    for vid, want in o64.items():
+        scale = max(1.0, float(np.max(np.abs(want)))) if want.size else 1.0
+        err = float(np.max(np.abs(rep.outputs[vid] - want))) / scale if want.size else 0.0
+        assert err <= TOL[prec], (case, vid, err)
