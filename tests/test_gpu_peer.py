@@ -43,7 +43,10 @@ def _worker(rank, world, case, port, q, precision, replaced, want_kernels=False)
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
         dist.init_process_group("gloo", rank=rank, world_size=world, timeout=timedelta(seconds=120))
-        if case.endswith(".plan"):  # a plan without a golden fixture: seeded host inputs
+        if case.startswith("fuzz:"):  # a randomised fixture (tests/test_gpu_fuzz.py)
+            from test_gpu_fuzz import _load
+            plan, ins, o64, o32, counters, total = _load(case[5:])
+        elif case.endswith(".plan"):  # a plan without a golden fixture: seeded host inputs
             from oracle import bridge as B
             name = case[:-5]
             plan = load_plan(name)
@@ -150,3 +153,27 @@ def test_peer_transport_fuses_per_rank(name, fused, world, replaced):
             # both runs round to bf16, with different sibling fold orders:
             # compare relative to the output's scale
             assert np.max(np.abs(outs[vid] - want)) <= 1e-2 * np.max(np.abs(want)), vid
+
+
+def _fuzz_multirank():
+    import glob
+    from test_gpu_fuzz import CASES
+    out = []
+    for c in CASES:
+        L = int(c.split("_L")[1].split("_")[0])
+        if L > 1:
+            out.append((c, L))
+    return out[:8]
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("case,world", _fuzz_multirank())
+def test_peer_transport_fuzz_fp64_bitexact(case, world):
+    """Random graphs (tests/test_gpu_fuzz.py) on L ranks of one GPU through
+    the peer transport: bit-exact f64 and the reference's counters."""
+    from test_gpu_fuzz import _load, _same
+    plan, ins, o64, o32, counters, total = _load(case)
+    for machines, tt, outs in _run("fuzz:" + case, world):
+        for vid, want in o64.items():
+            assert _same(outs[vid], want, plan, 1e-14), (case, vid)
+        assert tt == total and [tuple(m) for m in machines] == [tuple(c) for c in counters]
