@@ -1,0 +1,93 @@
+"""Randomised fusion parity: attention- and FFNN-shaped graphs with random
+sizes, scales and partitions (the reference planner's choice for random p and
+L), run in the tensor-core modes where the executor fuses the epilogue maps,
+the row softmax and the attention block. Reference outputs come from the
+unmodified reference executor (oracle/_ref, built in-tree) on the same inputs
+at test time, on inputs scaled to keep the logits O(1); the bar is the bf16 /
+tf32 tolerance relative to each output's scale, and the row softmax must have
+fused.
+"""
+import random
+
+import numpy as np
+import pytest
+
+from oracle import bridge as B
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not B.have_ref(), reason="oracle/_ref not built")]
+
+TOL = {"bf16": 3e-2, "tf32": 1e-2}
+
+
+def attention_text(rng):
+    s, a = rng.choice([128, 256]), rng.choice([128, 256])
+    h, d = rng.choice([1, 2, 4]), rng.choice([64, 128])
+    c = rng.choice([0.0625, 0.125, 0.5])
+    return (f"input Q:[{s},{a}]\ninput K:[{s},{a}]\ninput V:[{s},{a}]\n"
+            f"input WQ:[{a},{h},{d}]\ninput WK:[{a},{h},{d}]\ninput WV:[{a},{h},{d}]\ninput WO:[{a},{h},{d}]\n"
+            "QH[s,h,d] = sum[a] mul(Q[s,a], WQ[a,h,d])\n"
+            "KH[s2,h,d] = sum[a] mul(K[s2,a], WK[a,h,d])\n"
+            "VH[s2,h,d] = sum[a] mul(V[s2,a], WV[a,h,d])\n"
+            "T1[h,s,s2] = sum[d] mul(QH[s,h,d], KH[s2,h,d])\n"
+            f"T2[h,s,s2] = map scale({c})(T1[h,s,s2])\n"
+            "SM.max[h,s] = max[s2] map identity(T2[h,s,s2])\n"
+            "SM.sub[h,s,s2] = sub(T2[h,s,s2], SM.max[h,s])\n"
+            "SM.exp[h,s,s2] = map exp(SM.sub[h,s,s2])\n"
+            "SM.sum[h,s] = sum[s2] map identity(SM.exp[h,s,s2])\n"
+            "T3[h,s,s2] = div(SM.exp[h,s,s2], SM.sum[h,s])\n"
+            "O[s,h,d] = sum[s2] mul(T3[h,s,s2], VH[s2,h,d])\n"
+            "Y[s,a] = sum[h,d] mul(O[s,h,d], WO[a,h,d])\n"
+            "output Y\n"), "attention_fused"
+
+
+def ffnn_text(rng):
+    b, n, m, k = rng.choice([128, 256, 512]), rng.choice([128, 256]), rng.choice([128, 256]), rng.choice([128, 256, 512])
+    return (f"input X:[{b},{n}]\ninput W1:[{n},{m}]\ninput W2:[{m},{k}]\n"
+            "A[i,j] = sum[l] mul(X[i,l], W1[l,j])\n"
+            "B[i,j] = map relu(A[i,j])\n"
+            "C[i,k] = sum[j] mul(B[i,j], W2[j,k])\n"
+            "SM.max[i] = max[k] map identity(C[i,k])\n"
+            "SM.sub[i,k] = sub(C[i,k], SM.max[i])\n"
+            "SM.exp[i,k] = map exp(SM.sub[i,k])\n"
+            "SM.sum[i] = sum[k] map identity(SM.exp[i,k])\n"
+            "Y[i,k] = div(SM.exp[i,k], SM.sum[i])\n"
+            "output Y\n"), "softmax_rows"
+
+
+CASES = []
+_rng = random.Random(7)
+for i in range(16):
+    CASES.append((i, "attention" if i % 2 == 0 else "ffnn", _rng.choice([1, 2, 4, 8]), _rng.choice([1, 2])))
+
+
+@pytest.mark.parametrize("prec", ["bf16", "tf32"])
+@pytest.mark.parametrize("i,kind,p,L", CASES)
+def test_fusion_fuzz(gpu_ctx, i, kind, p, L, prec):
+    from paper_2410_02682_b200.executor import PreparedPlan
+    from paper_2410_02682_b200.plan import Plan
+    rng = random.Random(1000 + i)
+    text, fused = attention_text(rng) if kind == "attention" else ffnn_text(rng)
+    doc = B.ref_plan_json(text, p, L)
+    plan = Plan.from_json(doc)
+    # inputs scaled so the logits stay O(1): the bar is then about fusion
+    # (layout, region correspondence, fold order), not bf16's logit rounding
+    ins = {vid: a * 0.25 for vid, a in B.generate_inputs(plan, 50 + i).items()}
+    want, _, cnt, tot = B.ref_execute(doc, ins, threaded=False)
+    pp = PreparedPlan(gpu_ctx, plan, precision=prec, profile=True)
+    try:
+        pp.upload(ins)
+        rep = pp.run()
+        got = pp.download()
+        names = [k["name"] for k in pp.kernel_stats()]
+    finally:
+        pp.close()
+    for vid, w in want.items():
+        scale = max(1.0, float(np.max(np.abs(w))))
+        err = float(np.max(np.abs(got[vid] - w))) / scale
+        assert err <= TOL[prec], (text, p, L, vid, err, names)
+    assert rep.total_transferred == tot and [tuple(m) for m in rep.machines] == [tuple(c) for c in cnt]
+    if prec == "bf16" and (kind == "ffnn" or p <= 2):
+        # the row softmax fuses whenever its chain's joins line up (every FFNN
+        # plan here); the attention block whenever the softmax label is not
+        # split (the planner splits it at p = 8 for these sizes)
+        assert any(n.startswith(fused) for n in names), names
