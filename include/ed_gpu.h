@@ -300,8 +300,12 @@ typedef struct {
  * between machines to minimise the estimated busiest-GPU time — compute at
  * the cost model's rates plus whole-chunk transfers over the links — ties
  * broken by transfer volume. Input chunks and mul/sum contraction joins keep
- * their machines; the exec graph, keys and fold order are untouched, so the
- * results are bitwise those of the original placement (acceptance.cc:241-250).
+ * their machines (with fuse_chains, the QK^T joins of an attention block move
+ * with the block: each region of a fusable chain is kept on one GPU so the
+ * executor can fuse it there, and the chain's memory-bound work is credited
+ * while it stays together); the exec graph, keys and fold order are untouched,
+ * so the results are bitwise those of the original placement
+ * (acceptance.cc:241-250).
  * machine_of: n_exec entries, written. est_ms (nullable, 2 entries): the
  * estimated busiest-GPU milliseconds before and after. */
 ED_API ed_status ed_gpu_placement(const ed_plan_c* plan, const ed_cost_model_c* model, int32_t* machine_of,
