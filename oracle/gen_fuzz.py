@@ -29,8 +29,8 @@ OUT = os.path.join(ROOT, "tests", "golden", "fuzz")
 LABELS = "ijklmn"
 
 
-def rand_graph(rng: random.Random) -> str:
-    size = {l: rng.choice([8, 16, 32]) for l in LABELS}
+def rand_graph(rng: random.Random, sizes=(8, 16, 32), max_elems=4096) -> str:
+    size = {l: rng.choice(list(sizes)) for l in LABELS}
     tensors = []  # (name, labels, is_input)
     lines = []
 
@@ -43,7 +43,7 @@ def rand_graph(rng: random.Random) -> str:
     def pick_labels(k):
         while True:
             ls = rng.sample(LABELS, k)
-            if elems(ls) <= 4096:
+            if elems(ls) <= max_elems:
                 return ls
 
     for n in range(rng.randint(2, 3)):
@@ -69,7 +69,7 @@ def rand_graph(rng: random.Random) -> str:
                 continue
             agg = [l for l in shared if rng.random() < 0.8] or shared[:1]
             out = [l for l in union if l not in agg]
-            if not out or elems(out) > 4096:
+            if not out or elems(out) > max_elems:
                 continue
             rng.shuffle(out)
             aggop, join = rng.choice([("sum", "mul"), ("sum", "mul"), ("sum", "add"), ("sum", "sqdiff"),

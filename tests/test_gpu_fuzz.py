@@ -82,3 +82,41 @@ def test_fuzz_gpu_tensor_core_modes(gpu_ctx, case, prec):
         scale = max(1.0, float(np.max(np.abs(want)))) if want.size else 1.0
         err = float(np.max(np.abs(rep.outputs[vid] - want))) / scale if want.size else 0.0
         assert err <= TOL[prec], (case, vid, err)
+
+
+# live cases: more random graphs, larger labels (16-64), reference run at test time;
+# f64 bit-exact, bf16 within its bound
+LIVE = list(range(60))
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not B.have_ref(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("k", LIVE)
+def test_fuzz_live_gpu(gpu_ctx, k):
+    import random
+    from oracle.gen_fuzz import rand_graph
+    from paper_2410_02682_b200.executor import execute
+    from paper_2410_02682_b200.plan import Plan
+    rng = random.Random(777 + k)
+    text = None
+    while text is None:
+        text = rand_graph(rng, sizes=(16, 32, 64), max_elems=32768)
+    p, L = rng.choice([1, 2, 4, 8]), rng.choice([1, 2, 4, 8])
+    try:
+        doc = B.ref_plan_json(text, p, L)
+    except Exception as e:  # the planner rejects some (graph, p) pairs
+        pytest.skip(f"planner: {e}")
+    plan = Plan.from_json(doc)
+    ins = B.generate_inputs(plan, 900 + k)
+    want, _, cnt, tot = B.ref_execute(doc, ins, threaded=False)
+    if any(not np.all(np.isfinite(a)) for a in want.values()):
+        pytest.skip("non-finite reference output")
+    rep = execute(plan, ins, precision="fp64", ctx=gpu_ctx)
+    for vid, w in want.items():
+        assert _same(rep.outputs[vid], w, plan, 1e-14), (text, p, L, vid, B.max_rel_err(rep.outputs[vid], w))
+    assert rep.machines == [tuple(c) for c in cnt] and rep.total_transferred == tot
+    rep = execute(plan, ins, precision="bf16", ctx=gpu_ctx)
+    for vid, w in want.items():
+        scale = max(1.0, float(np.max(np.abs(w)))) if w.size else 1.0
+        err = float(np.max(np.abs(rep.outputs[vid] - w))) / scale if w.size else 0.0
+        assert err <= TOL["bf16"], (text, p, L, vid, err)
