@@ -23,7 +23,7 @@ OUT = os.path.join(ROOT, "plans")
 
 # config graphs (graphs/*.eg); p = 8 throughout
 CONFIGS = ["chain3", "bmm2", "ffnn_big", "attn_big", "hoc"]
-TWINS = ["chain3_s", "bmm2_s", "ffnn_s", "attn_s", "hoc_s"]
+TWINS = ["chain3_s", "bmm2_s", "ffnn_s", "attn_s", "hoc_s", "hoc_m"]  # hoc_m: bench.py's CPU-baseline sample
 # C2's repartition variant: batch-sharded Z1 feeding row-sharded Z2
 # (pinning precedent test_runtime.cc:58-72)
 BMM2_REPART = {"Z1": [8, 1, 1, 8, 1, 1], "Z2": [1, 8, 1, 1, 1, 1]}

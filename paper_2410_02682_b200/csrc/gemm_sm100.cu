@@ -34,7 +34,7 @@ constexpr int BM = 128;  // accumulator rows per CTA (TMEM lanes)
 constexpr int kThreads = 192;
 constexpr int kAccStages = 2;
 
-template <bool kBF16, int kCta, int BN>
+template <bool kBF16, int kCta, int BN, bool kX3 = false>
 struct Cfg {
   static constexpr int ES = kBF16 ? 2 : 4;          // element bytes
   static constexpr int BK = 128 / ES;               // one 128-byte swizzle row of K
@@ -43,11 +43,17 @@ struct Cfg {
   static constexpr int B_ROWS = BN / kCta;          // B rows (N) loaded per CTA
   static constexpr int A_BYTES = BM * 128;
   static constexpr int B_BYTES = B_ROWS * 128;
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = BN == 256 ? (kCta == 2 ? 6 : 4) : (kCta == 2 ? 8 : 6);  // 192 KiB ring
+  // kX3 (fp32-accurate 3xTF32): a stage holds A_hi | B_hi | A_lo | B_lo and
+  // feeds three products hi*hi + hi*lo + lo*hi into the same accumulator
+  static constexpr int LO_OFF = A_BYTES + B_BYTES;  // offset of the lo copies in a stage
+  static constexpr int NPROD = kX3 ? 3 : 1;
+  static constexpr int NMAP = kX3 ? 4 : 2;          // tensor maps per sibling
+  static constexpr int STAGE_BYTES = (kX3 ? 2 : 1) * (A_BYTES + B_BYTES);
+  static constexpr int STAGES = 196608 / STAGE_BYTES > 8 ? 8 : 196608 / STAGE_BYTES;  // 192 KiB ring
   static constexpr int STORE_BYTES = 4 * 2 * 4096;  // 4 epilogue warps x 2 staging tiles of 32x128 B
   static constexpr int SMEM = STAGES * STAGE_BYTES + STORE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr int MN_ATOM = 128 / ES;          // MN elements per 128-byte atom
+  static_assert(SMEM <= 232448, "shared memory");
 };
 
 struct TileCoord {
@@ -66,7 +72,7 @@ __device__ __forceinline__ TileCoord tile_coord(const GemmLaunch& p, int t, int 
   // grouped raster: kGroupM tile rows advance together along N, so one wave
   // of ~74 cluster tiles touches ~8 A panels + ~9 B panels instead of
   // 3 + tiles_n, and the panels it shares stay in L2 (hoc: 8192^2 tiles)
-  constexpr int kGroupM = 8;
+  const int kGroupM = p.group_m;
   const int g = r / (kGroupM * tiles_n);
   const int gm0 = g * kGroupM;
   const int gsz = tiles_m - gm0 < kGroupM ? tiles_m - gm0 : kGroupM;
@@ -96,9 +102,9 @@ __device__ __forceinline__ void epi32(const GemmLaunch& p, uint32_t* r) {
   }
 }
 
-template <bool kBF16, int kCta, int BN>
+template <bool kBF16, int kCta, int BN, bool kX3>
 __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ GemmLaunch p) {
-  using C_ = Cfg<kBF16, kCta, BN>;
+  using C_ = Cfg<kBF16, kCta, BN, kX3>;
   constexpr int STAGES = C_::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -149,7 +155,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         const GemmRegion reg = p.regions[tc.region];
         const int am = tc.m0 + int(rank) * BM, bn = tc.n0 + int(rank) * C_::B_ROWS;
         for (int sib = 0; sib < reg.n_sib; ++sib) {
-          const CUtensorMap* ma = p.maps + reg.map0 + 2 * sib;
+          const CUtensorMap* ma = p.maps + reg.map0 + C_::NMAP * sib;
           const CUtensorMap* mb = ma + 1;
           for (int kb = 0; kb < kblocks; ++kb, ++it) {
             const int s = it % STAGES;
@@ -163,18 +169,25 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
               if (kCta == 2) tma_load_3d_2sm(dst, m, &full_bar[s], c0, c1, tc.b);
               else tma_load_3d(dst, m, &full_bar[s], c0, c1, tc.b);
             };
-            if (!p.a_mn) {
-              load(sa, ma, k0, am);
-            } else {
 #pragma unroll
-              for (int i = 0; i < BM / C_::MN_ATOM; ++i) load(sa + i * C_::BK * 128, ma, am + i * C_::MN_ATOM, k0);
-            }
-            if (!p.b_mn) {
-              load(sb, mb, k0, bn);
-            } else {
+            for (int part = 0; part < (kX3 ? 2 : 1); ++part) {  // hi, then (kX3) lo copies
+              uint8_t* pa = sa + part * C_::LO_OFF;
+              uint8_t* pb = sb + part * C_::LO_OFF;
+              const CUtensorMap* pma = ma + 2 * part;
+              const CUtensorMap* pmb = mb + 2 * part;
+              if (!p.a_mn) {
+                load(pa, pma, k0, am);
+              } else {
 #pragma unroll
-              for (int i = 0; i < C_::B_ROWS / C_::MN_ATOM; ++i)
-                load(sb + i * C_::BK * 128, mb, bn + i * C_::MN_ATOM, k0);
+                for (int i = 0; i < BM / C_::MN_ATOM; ++i) load(pa + i * C_::BK * 128, pma, am + i * C_::MN_ATOM, k0);
+              }
+              if (!p.b_mn) {
+                load(pb, pmb, k0, bn);
+              } else {
+#pragma unroll
+                for (int i = 0; i < C_::B_ROWS / C_::MN_ATOM; ++i)
+                  load(pb + i * C_::BK * 128, pmb, bn + i * C_::MN_ATOM, k0);
+              }
             }
           }
         }
@@ -212,9 +225,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           const uint32_t sa = smem_u32(smem + s * C_::STAGE_BYTES);
           const uint32_t sb = sa + C_::A_BYTES;
 #pragma unroll
-          for (int k = 0; k < C_::BK / C_::UMMA_K; ++k) {
-            const uint64_t ad = umma_desc_sw128(sa + k * a_step, a_lbo, a_sbo, a_lt);
-            const uint64_t bd = umma_desc_sw128(sb + k * b_step, b_lbo, b_sbo, b_lt);
+          for (int k = 0; k < C_::NPROD * (C_::BK / C_::UMMA_K); ++k) {
+            // kX3: k-steps of hi*hi, then hi*lo, then lo*hi over the same stage
+            const int prod = k / (C_::BK / C_::UMMA_K), kk = k % (C_::BK / C_::UMMA_K);
+            const uint32_t oa = prod == 2 ? uint32_t(C_::LO_OFF) : 0u, ob = prod == 1 ? uint32_t(C_::LO_OFF) : 0u;
+            const uint64_t ad = umma_desc_sw128(sa + oa + kk * a_step, a_lbo, a_sbo, a_lt);
+            const uint64_t bd = umma_desc_sw128(sb + ob + kk * b_step, b_lbo, b_sbo, b_lt);
             const uint32_t acc = (i | k) != 0;
             if (kCta == 2) {
               if (kBF16) mma_f16_2sm(d_tmem, ad, bd, idesc, acc);
@@ -335,15 +351,15 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   }
 }
 
-template <bool kBF16, int kCta, int BN>
+template <bool kBF16, int kCta, int BN, bool kX3 = false>
 cudaError_t prepare_t() {
-  return cudaFuncSetAttribute(gemm_kernel<kBF16, kCta, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              Cfg<kBF16, kCta, BN>::SMEM);
+  return cudaFuncSetAttribute(gemm_kernel<kBF16, kCta, BN, kX3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              Cfg<kBF16, kCta, BN, kX3>::SMEM);
 }
 
-template <bool kBF16, int kCta, int BN>
+template <bool kBF16, int kCta, int BN, bool kX3 = false>
 cudaError_t launch_t(const GemmLaunch& p, int num_sms, cudaStream_t stream) {
-  using C_ = Cfg<kBF16, kCta, BN>;
+  using C_ = Cfg<kBF16, kCta, BN, kX3>;
   const long long tiles =
       (long long)((p.M + C_::TILE_M - 1) / C_::TILE_M) * ((p.N + BN - 1) / BN) * p.batch * p.n_regions;
   const int clusters = int(tiles < num_sms / kCta ? tiles : num_sms / kCta);
@@ -361,7 +377,7 @@ cudaError_t launch_t(const GemmLaunch& p, int num_sms, cudaStream_t stream) {
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, gemm_kernel<kBF16, kCta, BN>, p);
+  return cudaLaunchKernelEx(&cfg, gemm_kernel<kBF16, kCta, BN, kX3>, p);
 }
 
 }  // namespace
@@ -392,7 +408,11 @@ cudaError_t gemm_prepare() {
   if ((e = prepare_t<true, 1, 128>()) != cudaSuccess) return e;
   if ((e = prepare_t<false, 1, 128>()) != cudaSuccess) return e;
   if ((e = prepare_t<true, 2, 128>()) != cudaSuccess) return e;
-  return prepare_t<false, 2, 128>();
+  if ((e = prepare_t<false, 2, 128>()) != cudaSuccess) return e;
+  if ((e = prepare_t<false, 1, 256, true>()) != cudaSuccess) return e;
+  if ((e = prepare_t<false, 2, 256, true>()) != cudaSuccess) return e;
+  if ((e = prepare_t<false, 1, 128, true>()) != cudaSuccess) return e;
+  return prepare_t<false, 2, 128, true>();
 }
 
 cudaError_t launch_gemm(const GemmLaunch& p, int num_sms, cudaStream_t stream) {
@@ -402,6 +422,11 @@ cudaError_t launch_gemm(const GemmLaunch& p, int num_sms, cudaStream_t stream) {
   if (p.bf16) {
     if (narrow) return pair ? launch_t<true, 2, 128>(p, num_sms, stream) : launch_t<true, 1, 128>(p, num_sms, stream);
     return pair ? launch_t<true, 2, 256>(p, num_sms, stream) : launch_t<true, 1, 256>(p, num_sms, stream);
+  }
+  if (p.x3) {
+    if (narrow)
+      return pair ? launch_t<false, 2, 128, true>(p, num_sms, stream) : launch_t<false, 1, 128, true>(p, num_sms, stream);
+    return pair ? launch_t<false, 2, 256, true>(p, num_sms, stream) : launch_t<false, 1, 256, true>(p, num_sms, stream);
   }
   if (narrow) return pair ? launch_t<false, 2, 128>(p, num_sms, stream) : launch_t<false, 1, 128>(p, num_sms, stream);
   return pair ? launch_t<false, 2, 256>(p, num_sms, stream) : launch_t<false, 1, 256>(p, num_sms, stream);

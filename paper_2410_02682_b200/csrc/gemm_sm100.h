@@ -11,7 +11,8 @@ constexpr int kMaxSib = 8;  // aggregation siblings folded in one accumulator
 // A_s * B_s (K-concatenated), written to c32 and/or its bf16 shadow c16.
 struct GemmRegion {
   int n_sib;
-  int map0;        // maps[map0 + 2*s] = A_s, maps[map0 + 2*s + 1] = B_s
+  int map0;        // maps[map0 + 2*s] = A_s, maps[map0 + 2*s + 1] = B_s; with x3
+                   // four per sibling: A_s, B_s, A_s lo, B_s lo
   int cmap32;      // output tensor map for TMA stores (-1: direct stores)
   int cmap16;
   float* c32;
@@ -31,6 +32,9 @@ struct GemmLaunch {
   int epi_map;                // fused map on the accumulator (ed_map_op) or -1
   float epi_c;                // scale constant of a fused scale map
   int bn;                     // tile width: 256 or 128 (gemm_pick_bn)
+  int group_m;                // grouped raster: tile rows that advance together along N
+  int x3;                     // fp32-accurate 3xTF32: each stage carries hi and lo operand copies
+                              // and feeds hi*hi + hi*lo + lo*hi into one accumulator
 };
 
 int gemm_bk(bool bf16);

@@ -1542,6 +1542,9 @@ void ed_plan_h::allocate() {
           op.name += "+map";
         }
         p.bn = gemm_pick_bn(p.M, p.N, p.batch, int(op.heads.size()), ctx->num_sms);
+        p.x3 = opt.precision == ED_PREC_F32X3;
+        p.group_m = 8;
+        if (const char* gm = std::getenv("ED_GEMM_GROUP_M")) p.group_m = std::max(1, std::atoi(gm));  // experiments
         const uint32_t BK = uint32_t(gemm_bk(b16)), BM = uint32_t(gemm_bm());
         const uint32_t ATOM = 128u / (b16 ? 2u : 4u);
         op.maps.clear();
@@ -1555,15 +1558,13 @@ void ed_plan_h::allocate() {
           const bool x3 = opt.precision == ED_PREC_F32X3;
           const KSeg* ks = kseg_.count(u.producer) ? &kseg_.at(u.producer) : nullptr;
           const int nseg = ks ? int(ks->segs.at(sibs[0]).size()) : 1;
-          const int per = nseg * (x3 ? 3 : 1);
-          r.n_sib = int(sibs.size()) * per;
+          r.n_sib = int(sibs.size()) * nseg;
           // MN-major fp32 operands need the 32-byte-atom swizzle (see gemm_sm100.cu)
           const CUtensorMapSwizzle mn_swz = b16 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
           const int es_op = b16 ? 2 : 4;
           for (int pseudo = 0; pseudo < r.n_sib; ++pseudo) {
-            const int sidx = sibs[pseudo / per];
-            const int seg = (pseudo % per) / (x3 ? 3 : 1);
-            const int part = x3 ? pseudo % 3 : 0;  // F32X3: hi*hi, hi*lo, lo*hi
+            const int sidx = sibs[pseudo / nseg];
+            const int seg = pseudo % nseg;
             const Ex& j = X[sidx];
             int da = resolve(j.deps[g.a_slot]), db = resolve(j.deps[g.b_slot]);
             Dim am = g.am, ak = g.ak, ab = g.ab, bn = g.bn, bk = g.bk, bb = g.bb;
@@ -1586,22 +1587,24 @@ void ed_plan_h::allocate() {
                 aoff = sg.k0 * g.ak.stride;
               }
             }
-            const char* pa = static_cast<const char*>(b16 ? buf[da].b16 : buf[da].main);
-            const char* pb = static_cast<const char*>(b16 ? buf[db].b16 : buf[db].main);
-            if (part == 1) pb = static_cast<const char*>(buf[db].lo);
-            if (part == 2) pa = static_cast<const char*>(buf[da].lo);
-            if (!pa || !pb) throw ed_error(ED_ERR_PLAN, "GEMM operand buffer missing");
-            pa += aoff * es_op;
-            pb += boff * es_op;
-            CUtensorMap ma, mb;
-            if (!g.a_mn) make_map(&ma, pa, b16, ak.ext, am.ext, am.stride, ab.ext, ab.stride, BK, BM);
-            else make_map(&ma, pa, b16, am.ext, ak.ext, ak.stride, ab.ext, ab.stride, ATOM, BK, mn_swz);
-            if (!g.b_mn)
-              make_map(&mb, pb, b16, bk.ext, bn.ext, bn.stride, bb.ext, bb.stride, BK, uint32_t(gemm_b_box(p.M, p.bn)));
-            else make_map(&mb, pb, b16, bn.ext, bk.ext, bk.stride, bb.ext, bb.stride, ATOM, BK, mn_swz);
-            op.maps.push_back(ma);
-            op.maps.push_back(mb);
-            ++total_sib;
+            // F32X3: A, B, then their lo copies (x - tf32(x)); the kernel feeds
+            // hi*hi + hi*lo + lo*hi from one stage into the accumulator
+            for (int part = 0; part < (x3 ? 2 : 1); ++part) {
+              const char* pa = static_cast<const char*>(b16 ? buf[da].b16 : part ? buf[da].lo : buf[da].main);
+              const char* pb = static_cast<const char*>(b16 ? buf[db].b16 : part ? buf[db].lo : buf[db].main);
+              if (!pa || !pb) throw ed_error(ED_ERR_PLAN, "GEMM operand buffer missing");
+              pa += aoff * es_op;
+              pb += boff * es_op;
+              CUtensorMap ma, mb;
+              if (!g.a_mn) make_map(&ma, pa, b16, ak.ext, am.ext, am.stride, ab.ext, ab.stride, BK, BM);
+              else make_map(&ma, pa, b16, am.ext, ak.ext, ak.stride, ab.ext, ab.stride, ATOM, BK, mn_swz);
+              if (!g.b_mn)
+                make_map(&mb, pb, b16, bk.ext, bn.ext, bn.stride, bb.ext, bb.stride, BK, uint32_t(gemm_b_box(p.M, p.bn)));
+              else make_map(&mb, pb, b16, bn.ext, bk.ext, bk.stride, bb.ext, bb.stride, ATOM, BK, mn_swz);
+              op.maps.push_back(ma);
+              op.maps.push_back(mb);
+            }
+            total_sib += x3 ? 2 : 1;
           }
           r.c32 = static_cast<float*>(buf[head].main);
           r.c16 = buf[head].b16;

@@ -194,6 +194,7 @@ class PreparedPlan:
         descs = []
         for vid in (self.plan.outputs if vertices is None else vertices):
             a = into[vid] if into is not None else np.empty(self.plan.vertices[vid].bound, dtype=dtype)
+            _out_ok(a, int(np.prod(self.plan.vertices[vid].bound)))
             outs[vid] = a
             descs.append(abi.ed_output_c(vid, _dt(a), a.ctypes.data, a.size))
         if descs:
@@ -242,6 +243,7 @@ class PreparedPlan:
                 keep.append(a)
                 tin[st * n_in + k] = abi.ed_tensor_in_c(vid, _dt(a), a.ctypes.data, a.size)
             for k, (vid, a) in enumerate(outputs[st].items()):
+                _out_ok(a, int(np.prod(self.plan.vertices[vid].bound)))
                 tout[st * n_out + k] = abi.ed_output_c(vid, _dt(a), a.ctypes.data, a.size)
         L = self.plan.n_machines
         machines = (abi.ed_machine_c * L)()
@@ -257,6 +259,7 @@ class PreparedPlan:
     def download_chunk(self, exec_id: int, dtype=np.float64) -> np.ndarray:
         u = self.plan.exec[exec_id]
         a = np.empty(u.chunk_bound, dtype=dtype)
+        _out_ok(a, int(np.prod(u.chunk_bound)))
         err, n = _err()
         _check(library().ed_download_chunk(self.h, exec_id, _dt(a), a.ctypes.data, a.size, err, n), err)
         return a
@@ -279,7 +282,23 @@ def _host(a):
 
 
 def _dt(a):
-    return abi.DTYPE_F64 if a.dtype == np.float64 else abi.DTYPE_F32
+    if a.dtype == np.float64:
+        return abi.DTYPE_F64
+    if a.dtype == np.float32:
+        return abi.DTYPE_F32
+    raise ValueError(f"unsupported dtype {a.dtype}: the library reads and writes float32 / float64 only")
+
+
+def _out_ok(a, n):
+    """An output buffer the library writes n elements into through a raw
+    pointer: float32 / float64, C-contiguous, writeable, exactly n elements."""
+    if not isinstance(a, np.ndarray):
+        raise ValueError("output buffers must be numpy arrays")
+    _dt(a)
+    if not a.flags.c_contiguous or not a.flags.writeable:
+        raise ValueError("output buffers must be C-contiguous and writeable")
+    if a.size != n:
+        raise ValueError(f"output buffer has {a.size} elements, the tensor {n}")
 
 
 def plan_schedule(plan: Plan, rank: int, world: int):

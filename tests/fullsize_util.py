@@ -1,0 +1,160 @@
+"""Checkers for the full-size parity tests (test infrastructure only).
+
+* `op_fp64`: one vertex of eval_expr (reference.cc:3-60) restated with
+  torch in fp64 on the GPU — fast enough for 10^12-flop vertices;
+* `ref_slice`: the reference's OWN eval_expr (oracle/_ref, the unmodified
+  sources) on a row slice of one vertex, fed the same inputs — pins the
+  torch restatement to the reference where the reference can afford it;
+* `max_rel_err`: tensor.cc:9-19, the reference's parity metric.
+"""
+import numpy as np
+
+from oracle import bridge as B
+
+U32 = 2.0 ** -24   # fp32 unit roundoff
+U16 = 2.0 ** -9    # bf16 unit roundoff (8 significant bits)
+
+
+def letters(e):
+    m = {}
+    for ls in e.ins + [e.out]:
+        for l in ls:
+            m.setdefault(l, chr(ord("a") + len(m)))
+    return m
+
+
+def op_fp64(v, args, torch, absolute=False):
+    """eval_expr of graph vertex v on fp64 torch tensors. absolute=True gives
+    sum |x|*|y| for a mul/sum contraction (the magnitude every partial sum
+    is bounded by, whatever the summation order)."""
+    e = v.expr
+    lt = letters(e)
+    si = ["".join(lt[l] for l in ls) for ls in e.ins]
+    so = "".join(lt[l] for l in e.out)
+    x = args[0]
+    y = args[1] if e.is_binary else None
+    if e.join == "mul" and e.agg == "sum":
+        if absolute:
+            x, y = x.abs(), y.abs()
+        return torch.einsum(f"{si[0]},{si[1]}->{so}", x, y)
+    if e.is_binary:
+        shape = [x.shape[si[0].index(c)] if c in si[1] else 1 for c in si[0]]
+        yb = y.permute(*[si[1].index(c) for c in si[0] if c in si[1]]).reshape(shape)
+        r = {"sub": x - yb, "div": x / yb, "add": x + yb, "mul": x * yb}[e.join]
+        if e.agg is None:
+            return r
+        red = [si[0].index(c) for c in si[0] if c not in so]
+        return r.amax(dim=red) if e.agg == "max" else r.sum(dim=red)
+    m = {"relu": torch.relu, "exp": torch.exp, "neg": torch.neg, "identity": lambda t: t,
+         "scale": lambda t: t * e.scale_c}[e.map](x)
+    if e.agg is None:
+        return m
+    red = [si[0].index(c) for c in si[0] if c not in so]
+    return m.amax(dim=red) if e.agg == "max" else m.sum(dim=red)
+
+
+def contraction_k(plan, v):
+    """Length of each dot product of a mul/sum vertex (product of the
+    aggregated labels' extents)."""
+    e = v.expr
+    ext = {}
+    for ls, b in zip(e.ins, [plan.vertices[w].bound for w in v.inputs]):
+        for l, n in zip(ls, b):
+            ext[l] = n
+    k = 1
+    for l in e.agg_labels():
+        k *= ext[l]
+    return k
+
+
+def max_rel_err(got, want, torch):
+    """tensor.cc:9-19: max |got - want| / max(1, |want|)."""
+    return float(((got - want).abs() / want.abs().clamp(min=1.0)).max().item())
+
+
+def normwise(got, want):
+    return float(((got - want).abs().max() / want.abs().max().clamp(min=1e-300)).item())
+
+
+def vertex_tensor(pp, plan, w, torch):
+    """The GPU's value of graph vertex w (fp64 on the GPU), assembled from a
+    materialised refinement layer of w, or from its region accumulators
+    (region-head joins); None if w was fused into a consumer's kernel."""
+    layers = {}
+    for u in plan.exec:
+        if u.kind == 2 and u.producer == w:
+            layers.setdefault((u.consumer, u.slot), []).append(u)
+    v = plan.vertices[w]
+    for lay in layers.values():
+        out = torch.empty(v.bound, dtype=torch.float64, device="cuda")
+        try:
+            for u in lay:
+                sl = tuple(slice(k * c, (k + 1) * c) for k, c in zip(u.key, u.chunk_bound))
+                out[sl] = torch.from_numpy(pp.download_chunk(u.id)).cuda()
+            return out
+        except Exception:
+            continue
+    if v.expr is not None:
+        dls = v.expr.distinct_labels()
+        out = torch.empty(v.bound, dtype=torch.float64, device="cuda")
+        seen = torch.zeros(v.bound, dtype=torch.bool, device="cuda")
+        for u in plan.exec:
+            if u.kind != 1 or u.producer != w:
+                continue
+            try:
+                chunk = torch.from_numpy(pp.download_chunk(u.id)).cuda()
+            except Exception:
+                continue
+            key = [u.key[dls.index(l)] for l in v.expr.out]
+            sl = tuple(slice(k * c, (k + 1) * c) for k, c in zip(key, u.chunk_bound))
+            out[sl] = chunk
+            seen[sl] = True
+        if bool(seen.all()):
+            return out
+    return None
+
+
+def slice_label(v):
+    """The output label a row slice cuts: the largest-extent output label of
+    the first operand (2 of its values leave every vertex of the configs at
+    <= 1.4e8 scalar products for the reference's interpretive eval_expr)."""
+    e = v.expr
+    best, ext = None, 0
+    for l, n in zip(e.out, v.bound):
+        if l in e.ins[0] and n > ext:
+            best, ext = l, n
+    return best
+
+
+def _vertex_line(graph_text, name):
+    for line in graph_text.splitlines():
+        s = line.strip()
+        if s.startswith(name + "[") and "=" in s:
+            return s
+    raise KeyError(name)
+
+
+def ref_slice(plan, graph_text, v, args, r0, rows, torch):
+    """The reference's eval_expr (reference.cc:3-60, through oracle/_ref's
+    edref_eval_vertex) on rows [r0, r0+rows) of v's slice label: a one-vertex
+    graph whose inputs are the given tensors cut to those rows. Returns
+    (reference slice, index tuple of that slice in v's output)."""
+    e = v.expr
+    lab = slice_label(v)
+    decl, arrs = [], []
+    for ls, w, a in zip(e.ins, v.inputs, args):
+        idx = tuple(slice(r0, r0 + rows) if l == lab else slice(None) for l in ls)
+        t = a[idx]
+        arrs.append(np.ascontiguousarray(t.cpu().numpy(), dtype=np.float64))
+        decl.append(f"input {plan.vertices[w].name}:[{','.join(str(n) for n in t.shape)}]")
+    if len(set(v.inputs)) != len(v.inputs):
+        raise ValueError("a vertex reading one tensor twice")
+    text = "\n".join(decl + [_vertex_line(graph_text, v.name), f"output {v.name}"]) + "\n"
+    oshape = [rows if l == lab else n for l, n in zip(e.out, v.bound)]
+    out = np.empty(oshape, dtype=np.float64)
+    err = B.C.create_string_buffer(1024)
+    vid = len(decl)  # the expression vertex follows its input declarations
+    y = arrs[1] if len(arrs) > 1 else None
+    B._check(B.ref().edref_eval_vertex(text.encode(), vid, B._ptr(arrs[0]), B._ptr(y), B._ptr(out), err, 1024), err)
+    oidx = tuple(slice(r0, r0 + rows) if l == lab else slice(None) for l in e.out)
+    return torch.from_numpy(out).to(args[0].device), oidx

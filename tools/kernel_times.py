@@ -1,6 +1,6 @@
 """Per-launch-class device times of a plan on one GPU (profile mode).
 
-usage: python tools/kernel_times.py PLAN [runs]   (ED_LIB_PATH selects a variant build)
+usage: python tools/kernel_times.py PLAN [runs] [precision]   (ED_LIB_PATH selects a variant build)
 """
 import os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -12,7 +12,8 @@ name = sys.argv[1]
 runs = int(sys.argv[2]) if len(sys.argv) > 2 else 10
 ctx = Context(0)
 plan = load_plan(name)
-pp = PreparedPlan(ctx, plan, precision="bf16", profile=True)
+prec = sys.argv[3] if len(sys.argv) > 3 else "bf16"
+pp = PreparedPlan(ctx, plan, precision=prec, profile=True)
 pp.generate_inputs(1)
 for _ in range(3):
     pp.run()
