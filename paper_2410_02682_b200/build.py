@@ -10,8 +10,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libed_gpu.so")
-SOURCES = ["runtime.cu", "gemm_sm100.cu", "kernels.cu", "ewise.cu", "attn_sm100.cu"]
-HEADERS = ["ptx.cuh", "gemm_sm100.h", "kernels.h", "ewise.h", "attn_sm100.h"]
+SOURCES = ["api.cu", "plan.cu", "build.cu", "alloc.cu", "exec.cu", "io.cu", "placement.cu", "gemm_sm100.cu",
+           "kernels.cu", "ewise.cu", "attn_sm100.cu"]
+HEADERS = ["runtime.h", "ptx.cuh", "gemm_sm100.h", "kernels.h", "ewise.h", "attn_sm100.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # The toolchain's libstdc++.so link is missing (only the .a resolves); a static
 # libstdc++ inside a dlopen'ed .so clashes with the host's, so link the system

@@ -1,0 +1,171 @@
+// Contexts and plan lifetime (ed_ctx_create, ed_prepare, ed_plan_destroy) and
+// the peer transport's bootstrap (ed_peer_export / ed_peer_import).
+#include "runtime.h"
+
+namespace {
+
+struct PeerBlobHead {
+  int32_t magic, rank, world, n_exec;
+  cudaIpcMemHandle_t arena, flags;
+};
+constexpr int32_t kPeerMagic = 0x45445031;  // "EDP1"
+
+size_t peer_blob_len(const ed_plan_h* h) { return sizeof(PeerBlobHead) + sizeof(int64_t) * h->X.size(); }
+
+}  // namespace
+
+extern "C" {
+
+int32_t ed_abi_version(void) { return ED_ABI_VERSION; }
+
+ed_status ed_nccl_unique_id(void* out, size_t len, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!out || len < sizeof(ncclUniqueId)) throw ed_error(ED_ERR_USAGE, "buffer too small for ncclUniqueId");
+    ncclUniqueId id;
+    NCCL_OK(ncclGetUniqueId(&id));
+    std::memcpy(out, &id, sizeof(id));
+  });
+}
+
+ed_status ed_ctx_create(int32_t device, int32_t rank, int32_t world, const void* nccl_id, size_t nccl_id_len,
+                        ed_ctx** out, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!out || world < 1 || rank < 0 || rank >= world) throw ed_error(ED_ERR_USAGE, "bad rank/world");
+    int n = 0;
+    CUDA_OK(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n) throw ed_error(ED_ERR_USAGE, "no such CUDA device");
+    CUDA_OK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CUDA_OK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) throw ed_error(ED_ERR_UNSUPPORTED, "libed_gpu is built for sm_100a (B200)");
+    auto* c = new ed_ctx;
+    c->device = device;
+    c->num_sms = prop.multiProcessorCount;
+    c->rank = rank;
+    c->world = world;
+    try {
+      CUDA_OK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      CUDA_OK(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+      if (world > 1 && nccl_id) {
+        if (nccl_id_len < sizeof(ncclUniqueId)) throw ed_error(ED_ERR_USAGE, "NCCL id too short");
+        ncclUniqueId id;
+        std::memcpy(&id, nccl_id, sizeof(id));
+        NCCL_OK(ncclCommInitRank(&c->comm, world, id, rank));
+      }
+    } catch (...) {
+      ed_ctx_destroy(c);
+      throw;
+    }
+    *out = c;
+  });
+}
+
+void ed_ctx_destroy(ed_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->comm) ncclCommDestroy(c->comm);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+  delete c;
+}
+
+ed_status ed_prepare(ed_ctx* ctx, const ed_plan_c* plan, const ed_options_c* options, ed_plan_h** out,
+                     char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!ctx || !out) throw ed_error(ED_ERR_USAGE, "null context or output");
+    CUDA_OK(cudaSetDevice(ctx->device));
+    auto* h = new ed_plan_h;
+    h->ctx = ctx;
+    if (options) h->opt = *options;
+    if (h->opt.precision < 0 || h->opt.precision > 4) {
+      delete h;
+      throw ed_error(ED_ERR_USAGE, "unknown precision");
+    }
+    h->peer = ctx->world > 1 && h->opt.transport == ED_TRANSPORT_PEER;
+    if (ctx->world > 1 && !h->peer && !ctx->comm) {
+      delete h;
+      throw ed_error(ED_ERR_USAGE, "world > 1 without an NCCL communicator needs ED_TRANSPORT_PEER");
+    }
+    h->f64 = h->opt.precision == ED_PREC_FP64;
+    h->store = h->f64 ? DT::F64 : DT::F32;
+    h->es = h->f64 ? 8 : 4;
+    try {
+      h->copy_plan(plan);
+      h->validate();
+      h->build();
+      h->allocate();
+      h->record();
+    } catch (...) {
+      h->destroy();
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+void ed_plan_destroy(ed_plan_h* h) {
+  if (!h) return;
+  cudaSetDevice(h->ctx->device);
+  h->destroy();
+  delete h;
+}
+
+ed_status ed_peer_export(ed_plan_h* h, void* out, size_t cap, size_t* len, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!h || !len) throw ed_error(ED_ERR_USAGE, "null argument");
+    if (!h->peer) throw ed_error(ED_ERR_USAGE, "plan was not prepared with ED_TRANSPORT_PEER in a world > 1");
+    *len = peer_blob_len(h);
+    if (!out) return;
+    if (cap < *len) throw ed_error(ED_ERR_USAGE, "ed_peer_export: buffer too small");
+    CUDA_OK(cudaSetDevice(h->ctx->device));
+    PeerBlobHead hd{};
+    hd.magic = kPeerMagic;
+    hd.rank = h->ctx->rank;
+    hd.world = h->ctx->world;
+    hd.n_exec = int32_t(h->X.size());
+    CUDA_OK(cudaIpcGetMemHandle(&hd.arena, h->arena));
+    CUDA_OK(cudaIpcGetMemHandle(&hd.flags, h->d_pflags));
+    std::memcpy(out, &hd, sizeof hd);
+    auto* off = reinterpret_cast<int64_t*>(static_cast<char*>(out) + sizeof hd);
+    for (int id = 0; id < int(h->X.size()); ++id) off[id] = h->local[id] ? h->arena_offset(id) : -1;
+  });
+}
+
+ed_status ed_peer_import(ed_plan_h* h, const void* blobs, size_t blob_len, int32_t n, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!h || !blobs) throw ed_error(ED_ERR_USAGE, "null argument");
+    if (!h->peer) throw ed_error(ED_ERR_USAGE, "plan was not prepared with ED_TRANSPORT_PEER in a world > 1");
+    if (h->peer_ready) throw ed_error(ED_ERR_USAGE, "ed_peer_import: already imported");
+    if (n != h->ctx->world || blob_len != peer_blob_len(h)) throw ed_error(ED_ERR_USAGE, "ed_peer_import: need one blob per rank");
+    CUDA_OK(cudaSetDevice(h->ctx->device));
+    const int world = h->ctx->world, me = h->ctx->rank;
+    h->peer_arena.assign(size_t(world), nullptr);
+    h->peer_flags.assign(size_t(world), nullptr);
+    h->peer_off.assign(size_t(world), {});
+    for (int r = 0; r < world; ++r) {
+      const char* b = static_cast<const char*>(blobs) + size_t(r) * blob_len;
+      PeerBlobHead hd;
+      std::memcpy(&hd, b, sizeof hd);
+      if (hd.magic != kPeerMagic || hd.rank != r || hd.world != world || hd.n_exec != int32_t(h->X.size()))
+        throw ed_error(ED_ERR_USAGE, "ed_peer_import: blob " + std::to_string(r) + " does not belong to this plan");
+      h->peer_off[size_t(r)].resize(h->X.size());
+      std::memcpy(h->peer_off[size_t(r)].data(), b + sizeof hd, sizeof(int64_t) * h->X.size());
+      if (r == me) {
+        h->peer_arena[size_t(r)] = static_cast<char*>(h->arena);
+        h->peer_flags[size_t(r)] = h->d_pflags;
+        continue;
+      }
+      void* a = nullptr;
+      void* f = nullptr;
+      CUDA_OK(cudaIpcOpenMemHandle(&a, hd.arena, cudaIpcMemLazyEnablePeerAccess));
+      CUDA_OK(cudaIpcOpenMemHandle(&f, hd.flags, cudaIpcMemLazyEnablePeerAccess));
+      h->peer_arena[size_t(r)] = static_cast<char*>(a);
+      h->peer_flags[size_t(r)] = static_cast<int*>(f);
+    }
+    h->peer_ready = true;
+    h->record();
+  });
+}
+
+}  // extern "C"

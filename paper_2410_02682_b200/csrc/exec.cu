@@ -1,0 +1,276 @@
+// Running a prepared plan: one launch per op on the compute stream, transfer
+// runs on the comm stream, independent GEMMs as parallel branches, all
+// captured once into a CUDA graph (record) and replayed by ed_run.
+#include "runtime.h"
+
+void ed_plan_h::launch_op(size_t i, cudaStream_t s) {
+  Op& op = ops[i];
+  switch (op.kind) {
+    case OpKind::GEMM: CUDA_OK(launch_gemm(op.gemm, ctx->num_sms, s)); break;
+    case OpKind::GENERIC: CUDA_OK(launch_generic(op.gen, f64, s)); break;
+    case OpKind::REFINE:
+      if (!op.groups.empty()) CUDA_OK(launch_rect(op.rect, int(op.groups.size()), op.max_rows, f64, s));
+      else CUDA_OK(launch_refine(op.ref, f64, s));
+      break;
+    case OpKind::CORRUPT: CUDA_OK(launch_add_one(op.ptr, op.dt, s)); break;
+    case OpKind::EWISE:
+      CUDA_OK(launch_ewise(op.ew, int(op.jptrs.size()), f64, opt.precision == ED_PREC_FP32, s));
+      break;
+    case OpKind::FLASH: CUDA_OK(launch_attn(op.attn, ctx->num_sms, s)); break;
+    case OpKind::SPLIT:
+      CUDA_OK(launch_split_lo(static_cast<const float*>(op.gen.x), static_cast<float*>(op.gen.out), op.gen.n_out, s));
+      break;
+    case OpKind::SOFTMAX: CUDA_OK(launch_softmax(op.sm, int(op.jptrs.size()), s)); break;
+    case OpKind::ROWREDUCE:
+      CUDA_OK(launch_rowreduce(op.rr, int(op.jptrs.size()), f64, opt.precision == ED_PREC_FP32, s));
+      break;
+    case OpKind::CONVERT: CUDA_OK(launch_convert(op.gen.x, store, op.gen.out16, DT::BF16, op.gen.n_out, s)); break;
+    case OpKind::SEND:
+      if (peer) CUDA_OK(launch_peer_signal(d_pflags + 2 + op.exec, d_epoch, s));  // chunk ready for the peer
+      else NCCL_OK(ncclSend(op.ptr, op.count, f64 ? ncclFloat64 : ncclFloat32, op.peer, ctx->comm, s));
+      break;
+    case OpKind::RECV:
+      if (peer) {
+        int* f = peer_flags[size_t(op.peer)] + 2 + op.exec;
+        CUDA_OK(launch_peer_wait(&f, 1, d_epoch, 0, s, d_perr, op.exec));
+        const int64_t off = peer_off[size_t(op.peer)][size_t(op.exec)];
+        if (off < 0) throw ed_error(ED_ERR_PLAN, "peer transport: chunk not resident on its producer rank");
+        CUDA_OK(cudaMemcpyAsync(op.ptr, peer_arena[size_t(op.peer)] + off, op.count * es, cudaMemcpyDeviceToDevice, s));
+      } else {
+        NCCL_OK(ncclRecv(op.ptr, op.count, f64 ? ncclFloat64 : ncclFloat32, op.peer, ctx->comm, s));
+      }
+      break;
+  }
+}
+
+// Every op in schedule order on the compute stream, except that each run of
+// consecutive transfers goes to the comm stream as ONE NCCL group (the
+// exchange of a repartition proceeds with all peers at once). The comm
+// stream forks from the compute stream before every run (a send's operand
+// is produced by then, and the fork keeps the comm stream inside the CUDA
+// graph capture) and the compute stream joins it right after the run: transfers sit just before their data's first consumer, so
+// the sender keeps computing while its sends drain and a receiver's recvs
+// are posted as soon as the comm stream reaches them, ahead of its compute.
+// Buffers are never reused within a run (linear arena), so an early recv
+// cannot overwrite live data. Ranks enqueue the same transfers in the same
+// global order (transfers_by_consumer), so the groups match.
+void ed_plan_h::enqueue(cudaStream_t s) {
+  cudaStream_t cs = ctx->comm_stream;
+  size_t ev = 0;
+  if (peer) {
+    // new run: advance the epoch, then wait until every rank has finished its
+    // previous run (its receives from our chunks are complete: write-after-read)
+    CUDA_OK(launch_peer_tick(d_epoch, s));
+    std::vector<int*> done(peer_flags.size());
+    for (size_t r = 0; r < done.size(); ++r) done[r] = peer_flags[r];
+    CUDA_OK(launch_peer_wait(done.data(), int(done.size()), d_epoch, -1, s, d_perr, int(X.size())));
+  }
+  auto next_event = [&]() {
+    if (ev == comm_events.size()) {
+      cudaEvent_t e;
+      CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      comm_events.push_back(e);
+    }
+    return comm_events[ev++];
+  };
+  auto is_comm = [&](size_t i) { return ops[i].kind == OpKind::SEND || ops[i].kind == OpKind::RECV; };
+  for (size_t i = 0; i < ops.size();) {
+    // consecutive GEMMs of mutually independent einsums (e.g. attention's Q, K, V
+    // projections) run as parallel branches: each persistent grid's last,
+    // partial wave leaves SMs the next one fills
+    size_t g = i;
+    if (!opt.profile) {
+      while (g < ops.size() && ops[g].kind == OpKind::GEMM && g - i < 3) {
+        bool indep = true;
+        for (size_t a = i; a < g && indep; ++a) indep = !ancestor(ops[a].einsum, ops[g].einsum);
+        if (!indep) break;
+        ++g;
+      }
+    }
+    if (g - i >= 2) {
+      cudaEvent_t fork = next_event();
+      CUDA_OK(cudaEventRecord(fork, s));
+      std::vector<cudaEvent_t> joins;
+      for (size_t k = i + 1; k < g; ++k) {
+        cudaStream_t a = aux[k - i - 1];
+        if (!a) {
+          CUDA_OK(cudaStreamCreateWithFlags(&aux[k - i - 1], cudaStreamNonBlocking));
+          a = aux[k - i - 1];
+        }
+        CUDA_OK(cudaStreamWaitEvent(a, fork, 0));
+        launch_op(k, a);
+        joins.push_back(next_event());
+        CUDA_OK(cudaEventRecord(joins.back(), a));
+      }
+      launch_op(i, s);
+      for (cudaEvent_t e : joins) CUDA_OK(cudaStreamWaitEvent(s, e, 0));
+      i = g;
+      continue;
+    }
+    if (!is_comm(i)) {
+      if (opt.profile) CUDA_OK(cudaEventRecord(op_events[i], s));
+      launch_op(i, s);
+      ++i;
+      continue;
+    }
+    size_t j = i;
+    while (j < ops.size() && is_comm(j)) ++j;
+    if (opt.profile)
+      for (size_t k = i; k < j; ++k) CUDA_OK(cudaEventRecord(op_events[k], s));
+    {
+      // every run forks from the compute stream: a send's chunk is produced by
+      // then, and a receive must follow the run's start (epoch, graph capture)
+      cudaEvent_t fork = next_event();
+      CUDA_OK(cudaEventRecord(fork, s));
+      CUDA_OK(cudaStreamWaitEvent(cs, fork, 0));
+    }
+    if (!peer) NCCL_OK(ncclGroupStart());
+    for (size_t k = i; k < j; ++k) launch_op(k, cs);
+    if (!peer) NCCL_OK(ncclGroupEnd());
+    cudaEvent_t join = next_event();
+    CUDA_OK(cudaEventRecord(join, cs));
+    CUDA_OK(cudaStreamWaitEvent(s, join, 0));
+    i = j;
+  }
+  if (opt.profile) CUDA_OK(cudaEventRecord(op_events[ops.size()], s));
+  if (peer) CUDA_OK(launch_peer_signal(d_pflags, d_epoch, s));  // this run is done on this rank
+}
+
+void ed_plan_h::record() {
+  CUDA_OK(gemm_prepare());
+  CUDA_OK(attn_prepare());
+  if (!ev0) CUDA_OK(cudaEventCreate(&ev0));
+  if (!ev1) CUDA_OK(cudaEventCreate(&ev1));
+  if (opt.no_graph || opt.profile || (peer && !peer_ready)) return;  // peer: recorded by ed_peer_import
+  cudaStream_t s = ctx->stream;
+  CUDA_OK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  try {
+    enqueue(s);
+  } catch (...) {
+    cudaGraph_t g;
+    cudaStreamEndCapture(s, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  CUDA_OK(cudaStreamEndCapture(s, &graph));
+  CUDA_OK(cudaGraphInstantiate(&gexec, graph, 0));
+}
+
+void ed_plan_h::destroy() {
+  if (gexec) cudaGraphExecDestroy(gexec);
+  if (graph) cudaGraphDestroy(graph);
+  if (ev0) cudaEventDestroy(ev0);
+  if (ev1) cudaEventDestroy(ev1);
+  for (auto e : op_events) cudaEventDestroy(e);
+  for (auto e : comm_events) cudaEventDestroy(e);
+  for (auto a : aux)
+    if (a) cudaStreamDestroy(a);
+  for (size_t r = 0; r < peer_arena.size(); ++r)
+    if (int(r) != ctx->rank) {
+      if (peer_arena[r]) cudaIpcCloseMemHandle(peer_arena[r]);
+      if (peer_flags[r]) cudaIpcCloseMemHandle(peer_flags[r]);
+    }
+  if (d_epoch) cudaFree(d_epoch);
+  if (d_perr) cudaFree(d_perr);
+  if (d_pflags) cudaFree(d_pflags);
+  if (arena) cudaFree(arena);
+  if (d_deps) cudaFree(d_deps);
+  if (d_maps) cudaFree(d_maps);
+  if (d_joinptrs) cudaFree(d_joinptrs);
+  if (d_rects) cudaFree(d_rects);
+  if (d_copy_desc) cudaFree(d_copy_desc);
+  if (d_attn) cudaFree(d_attn);
+  if (d_rowsegs) cudaFree(d_rowsegs);
+  if (d_regions) cudaFree(d_regions);
+  if (d_ptrs) cudaFree(d_ptrs);
+  if (d_err) cudaFree(d_err);
+  if (staging) cudaFree(staging);
+  for (auto& [k, c] : copy_cache)
+    if (c.d) cudaFree(c.d);
+  for (void* b : stg_in)
+    if (b) cudaFree(b);
+  for (void* b : stg_out)
+    if (b) cudaFree(b);
+  for (auto e : ev_pipe)
+    if (e) cudaEventDestroy(e);
+  if (cs_in) cudaStreamDestroy(cs_in);
+  if (cs_out) cudaStreamDestroy(cs_out);
+}
+
+extern "C" {
+
+ed_status ed_run(ed_plan_h* h, ed_report_c* rep, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!h) throw ed_error(ED_ERR_USAGE, "null plan");
+    if (h->peer && !h->peer_ready) throw ed_error(ED_ERR_USAGE, "ED_TRANSPORT_PEER: call ed_peer_import first");
+    CUDA_OK(cudaSetDevice(h->ctx->device));
+    cudaStream_t s = h->ctx->stream;
+    CUDA_OK(cudaMemsetAsync(h->d_err, 0, sizeof(int), s));
+    if (h->opt.profile && h->op_events.size() != h->ops.size() + 1) {
+      for (auto e : h->op_events) cudaEventDestroy(e);
+      h->op_events.assign(h->ops.size() + 1, nullptr);
+      for (auto& e : h->op_events) CUDA_OK(cudaEventCreate(&e));
+    }
+    CUDA_OK(cudaEventRecord(h->ev0, s));
+    if (h->gexec) CUDA_OK(cudaGraphLaunch(h->gexec, s));
+    else h->enqueue(s);
+    CUDA_OK(cudaEventRecord(h->ev1, s));
+    CUDA_OK(cudaEventSynchronize(h->ev1));
+    h->check_peer_error();
+    int flag = 0;
+    CUDA_OK(cudaMemcpy(&flag, h->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+    float ms = 0;
+    CUDA_OK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+    if (h->opt.profile) {
+      std::map<std::string, size_t> idx;
+      h->stats.clear();
+      for (size_t i = 0; i < h->ops.size(); ++i) {
+        float t = 0;
+        CUDA_OK(cudaEventElapsedTime(&t, h->op_events[i], h->op_events[i + 1]));
+        const Op& op = h->ops[i];
+        auto it = idx.find(op.name);
+        if (it == idx.end()) {
+          ed_kernel_stat_c st{};
+          std::snprintf(st.name, sizeof(st.name), "%s", op.name.c_str());
+          it = idx.emplace(op.name, h->stats.size()).first;
+          h->stats.push_back(st);
+        }
+        auto& st = h->stats[it->second];
+        st.launches += 1;
+        st.ms += t;
+        st.flops += op.flops;
+        st.bytes += op.bytes;
+      }
+    }
+    if (flag) throw ed_error(ED_ERR_EVAL, "division by zero");
+    if (rep) {
+      if (rep->machines)
+        for (int m = 0; m < std::min(rep->n_machines, h->n_machines); ++m) rep->machines[m] = h->counters[m];
+      rep->total_transferred = h->total_transferred;
+      rep->wall_steps = int64_t(h->X.size());
+      rep->max_site_cost = h->max_site_cost;
+      rep->device_ms = ms;
+      int64_t pb = 0;
+      int launches = 0;
+      for (auto& op : h->ops) {
+        if (op.kind == OpKind::SEND) pb += int64_t(op.count) * int64_t(h->es);
+        if (op.kind != OpKind::SEND && op.kind != OpKind::RECV) ++launches;
+      }
+      rep->peer_bytes = pb;
+      rep->contraction_flops = h->contraction_flops;
+      rep->gpu_launches = launches;
+    }
+  });
+}
+
+ed_status ed_kernel_stats(ed_plan_h* h, ed_kernel_stat_c* out, int32_t cap, int32_t* n_out, char* err,
+                          size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!h || !n_out) throw ed_error(ED_ERR_USAGE, "null argument");
+    int k = std::min<int>(cap, int(h->stats.size()));
+    for (int i = 0; i < k; ++i) out[i] = h->stats[i];
+    *n_out = int(h->stats.size());
+  });
+}
+
+}  // extern "C"

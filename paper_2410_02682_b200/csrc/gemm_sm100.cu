@@ -21,6 +21,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "gemm_sm100.h"
 #include "ptx.cuh"
 
@@ -102,9 +104,14 @@ __device__ __forceinline__ void epi32(const GemmLaunch& p, uint32_t* r) {
   }
 }
 
-template <bool kBF16, int kCta, int BN, bool kX3>
+// kMc = 2: two 2-SM pairs form one 4-CTA cluster over a 256 x 2BN tile; they
+// share the A panel, each pair loading half of every A box and multicasting it
+// to both pairs, so each A byte leaves L2 once per cluster instead of twice.
+template <bool kBF16, int kCta, int BN, bool kX3, int kMc>
 __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ GemmLaunch p) {
   using C_ = Cfg<kBF16, kCta, BN, kX3>;
+  static_assert(kMc == 1 || kCta == 2, "A multicast pairs 2-SM tiles");
+  constexpr int kClu = kCta * kMc;  // CTAs per cluster
   constexpr int STAGES = C_::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -117,17 +124,24 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  const uint32_t rank = kCta == 2 ? cluster_ctarank() : 0;
+  const uint32_t crank = kClu > 1 ? cluster_ctarank() : 0;
+  const uint32_t rank = kCta == 2 ? (crank & 1u) : 0u;  // CTA within its MMA pair
+  const uint32_t q = kCta == 2 ? (crank >> 1) : 0u;     // pair within the cluster (kMc)
   const int tiles_m = (p.M + C_::TILE_M - 1) / C_::TILE_M;
-  const int tiles_n = (p.N + BN - 1) / BN;
+  const int tiles_n = (p.N + BN * kMc - 1) / (BN * kMc);  // cluster tiles along N
   const int total = tiles_m * tiles_n * p.batch * p.n_regions;
   const int kblocks = (p.K + C_::BK - 1) / C_::BK;
-  const int first = blockIdx.x / kCta, stride = gridDim.x / kCta;
+  const int first = blockIdx.x / kClu, stride = gridDim.x / kClu;
+  auto coord = [&](int t) {
+    TileCoord c = tile_coord<C_::TILE_M, BN * kMc>(p, t, tiles_m, tiles_n);
+    c.n0 += int(q) * BN;
+    return c;
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
+      mbar_init(&empty_bar[s], kMc);  // one MMA commit per pair reading this stage
     }
     for (int s = 0; s < kAccStages; ++s) {
       mbar_init(&acc_full[s], 1);
@@ -137,7 +151,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   }
   if (warp == 1) tmem_alloc<kAccStages * BN, kCta>(tmem_slot);
   tc_fence_before();
-  if (kCta == 2) cluster_sync();
+  if (kClu > 1) cluster_sync();
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
@@ -151,9 +165,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       int it = 0;
       for (int t = first; t < total; t += stride) {
         if (t + stride >= total) griddep_launch();  // last tile: the next kernel may launch
-        const TileCoord tc = tile_coord<C_::TILE_M, BN>(p, t, tiles_m, tiles_n);
+        const TileCoord tc = coord(t);
         const GemmRegion reg = p.regions[tc.region];
         const int am = tc.m0 + int(rank) * BM, bn = tc.n0 + int(rank) * C_::B_ROWS;
+        // kMc: CTAs with the same rank in both pairs hold the same A rows
+        const uint16_t a_mask = uint16_t((1u << rank) | (1u << (2 + rank)));
         for (int sib = 0; sib < reg.n_sib; ++sib) {
           const CUtensorMap* ma = p.maps + reg.map0 + C_::NMAP * sib;
           const CUtensorMap* mb = ma + 1;
@@ -175,7 +191,20 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
               uint8_t* pb = sb + part * C_::LO_OFF;
               const CUtensorMap* pma = ma + 2 * part;
               const CUtensorMap* pmb = mb + 2 * part;
-              if (!p.a_mn) {
+              if (kMc == 2) {
+                // this pair's half of the A box, multicast to both pairs (K-major:
+                // 64 of the 128 rows; MN-major: half of the 128-byte MN atoms)
+                if (!p.a_mn) {
+                  tma_load_3d_2sm_mc(pa + q * (BM / 2) * 128, pma, &full_bar[s], k0, am + int(q) * (BM / 2), tc.b,
+                                     a_mask);
+                } else {
+                  constexpr int NA = BM / C_::MN_ATOM;
+#pragma unroll
+                  for (int i = int(q) * NA / 2; i < (int(q) + 1) * NA / 2; ++i)
+                    tma_load_3d_2sm_mc(pa + i * C_::BK * 128, pma, &full_bar[s], am + i * C_::MN_ATOM, k0, tc.b,
+                                       a_mask);
+                }
+              } else if (!p.a_mn) {
                 load(pa, pma, k0, am);
               } else {
 #pragma unroll
@@ -208,7 +237,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       const uint32_t a_sbo = a_lt == 1 ? 512u : 1024u, b_sbo = b_lt == 1 ? 512u : 1024u;
       int it = 0, local = 0;
       for (int t = first; t < total; t += stride, ++local) {
-        const TileCoord tc = tile_coord<C_::TILE_M, BN>(p, t, tiles_m, tiles_n);
+        const TileCoord tc = coord(t);
         const int n_sib = p.regions[tc.region].n_sib;
         const int as = local & 1;
         const uint32_t aph = (local >> 1) & 1;
@@ -240,21 +269,22 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
               else mma_tf32(d_tmem, ad, bd, idesc, acc);
             }
           }
-          if (kCta == 2) mma_commit_2sm(&empty_bar[s]);
+          // the stage is free once every pair that reads it has consumed it
+          if (kCta == 2) mma_commit_2sm(&empty_bar[s], kMc == 2 ? 0xF : 0x3);
           else mma_commit(&empty_bar[s]);
         }
-        if (kCta == 2) mma_commit_2sm(&acc_full[as]);
+        if (kCta == 2) mma_commit_2sm(&acc_full[as], uint16_t(0x3u << (2 * q)));
         else mma_commit(&acc_full[as]);
       }
     }
   } else {
     // ---- epilogue: TMEM -> registers -> HBM (each CTA its 128 rows) ----
     const int wq = warp & 3;  // TMEM lane quarter this warp may access
-    const uint32_t empty_leader = kCta == 2 ? mapa(smem_u32(acc_empty), 0) : 0;
+    const uint32_t empty_leader = kCta == 2 ? mapa(smem_u32(acc_empty), 2 * q) : 0;
     int local = 0;
     uint32_t stage_ctr = 0;
     for (int t = first; t < total; t += stride, ++local) {
-      const TileCoord tc = tile_coord<C_::TILE_M, BN>(p, t, tiles_m, tiles_n);
+      const TileCoord tc = coord(t);
       const GemmRegion reg = p.regions[tc.region];
       const int as = local & 1;
       const uint32_t aph = (local >> 1) & 1;
@@ -343,7 +373,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   }
 
   tc_fence_before();
-  if (kCta == 2) cluster_sync();
+  if (kClu > 1) cluster_sync();
   else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
@@ -351,33 +381,62 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   }
 }
 
-template <bool kBF16, int kCta, int BN, bool kX3 = false>
-cudaError_t prepare_t() {
-  return cudaFuncSetAttribute(gemm_kernel<kBF16, kCta, BN, kX3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              Cfg<kBF16, kCta, BN, kX3>::SMEM);
+// co-resident clusters per kernel variant (clusters never span a GPC, so
+// 4-CTA clusters may leave SMs idle): measured once by the occupancy API
+template <bool kBF16, int kCta, int BN, bool kX3, int kMc>
+int& max_clusters() {
+  static int n = 0;
+  return n;
 }
 
-template <bool kBF16, int kCta, int BN, bool kX3 = false>
+template <bool kBF16, int kCta, int BN, bool kX3 = false, int kMc = 1>
+cudaError_t prepare_t() {
+  using C_ = Cfg<kBF16, kCta, BN, kX3>;
+  auto kern = gemm_kernel<kBF16, kCta, BN, kX3, kMc>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM);
+  if (e != cudaSuccess || kMc == 1) return e;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(kCta * kMc);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = C_::SMEM;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kCta * kMc;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  e = cudaOccupancyMaxActiveClusters(&n, kern, &cfg);
+  max_clusters<kBF16, kCta, BN, kX3, kMc>() = n;
+  return e;
+}
+
+template <bool kBF16, int kCta, int BN, bool kX3 = false, int kMc = 1>
 cudaError_t launch_t(const GemmLaunch& p, int num_sms, cudaStream_t stream) {
   using C_ = Cfg<kBF16, kCta, BN, kX3>;
-  const long long tiles =
-      (long long)((p.M + C_::TILE_M - 1) / C_::TILE_M) * ((p.N + BN - 1) / BN) * p.batch * p.n_regions;
-  const int clusters = int(tiles < num_sms / kCta ? tiles : num_sms / kCta);
+  constexpr int kClu = kCta * kMc;
+  const long long tiles = (long long)((p.M + C_::TILE_M - 1) / C_::TILE_M) * ((p.N + BN * kMc - 1) / (BN * kMc)) *
+                          p.batch * p.n_regions;
+  int cap = num_sms / kClu;
+  const int resident = max_clusters<kBF16, kCta, BN, kX3, kMc>();
+  if (kMc > 1 && resident > 0 && resident < cap) cap = resident;
+  const int clusters = int(tiles < cap ? tiles : cap);
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(clusters * kCta);
+  cfg.gridDim = dim3(clusters * kClu);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = C_::SMEM;
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = kCta;
+  attr[0].val.clusterDim.x = kClu;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, gemm_kernel<kBF16, kCta, BN, kX3>, p);
+  return cudaLaunchKernelEx(&cfg, gemm_kernel<kBF16, kCta, BN, kX3, kMc>, p);
 }
 
 }  // namespace
@@ -386,6 +445,17 @@ int gemm_bk(bool bf16) { return bf16 ? 64 : 32; }
 int gemm_bm() { return BM; }
 bool gemm_paired(int M) { return M > BM; }
 int gemm_b_box(int M, int bn) { return gemm_paired(M) ? bn / 2 : bn; }
+
+bool gemm_use_mc(int M, int N, int bn) {
+  // A multicast over two 2-SM pairs: 256-row tiles, 256-wide, and at least
+  // two N tiles so the second pair has work of its own
+  static const int env = [] {
+    const char* e = std::getenv("ED_GEMM_MC");
+    return e ? std::atoi(e) : 1;
+  }();
+  return env != 0 && gemm_paired(M) && bn == 256 && N > 256;
+}
+int gemm_a_box_rows(bool mc) { return mc ? BM / 2 : BM; }
 
 int gemm_pick_bn(int M, int N, int batch, int n_regions, int num_sms) {
   // 128-wide tiles need 1.5x the L2->SMEM bytes per flop of 256-wide ones,
@@ -412,13 +482,21 @@ cudaError_t gemm_prepare() {
   if ((e = prepare_t<false, 1, 256, true>()) != cudaSuccess) return e;
   if ((e = prepare_t<false, 2, 256, true>()) != cudaSuccess) return e;
   if ((e = prepare_t<false, 1, 128, true>()) != cudaSuccess) return e;
-  return prepare_t<false, 2, 128, true>();
+  if ((e = prepare_t<false, 2, 128, true>()) != cudaSuccess) return e;
+  if ((e = prepare_t<true, 2, 256, false, 2>()) != cudaSuccess) return e;
+  if ((e = prepare_t<false, 2, 256, false, 2>()) != cudaSuccess) return e;
+  return prepare_t<false, 2, 256, true, 2>();
 }
 
 cudaError_t launch_gemm(const GemmLaunch& p, int num_sms, cudaStream_t stream) {
   // pair SMs when the output has rows for both halves of a 256-row tile
   const bool pair = gemm_paired(p.M);
   const bool narrow = p.bn == 128;
+  if (p.mc && pair && !narrow) {  // 4-CTA clusters sharing A (gemm_use_mc)
+    if (p.bf16) return launch_t<true, 2, 256, false, 2>(p, num_sms, stream);
+    if (p.x3) return launch_t<false, 2, 256, true, 2>(p, num_sms, stream);
+    return launch_t<false, 2, 256, false, 2>(p, num_sms, stream);
+  }
   if (p.bf16) {
     if (narrow) return pair ? launch_t<true, 2, 128>(p, num_sms, stream) : launch_t<true, 1, 128>(p, num_sms, stream);
     return pair ? launch_t<true, 2, 256>(p, num_sms, stream) : launch_t<true, 1, 256>(p, num_sms, stream);

@@ -32,6 +32,7 @@ struct GemmLaunch {
   int epi_map;                // fused map on the accumulator (ed_map_op) or -1
   float epi_c;                // scale constant of a fused scale map
   int bn;                     // tile width: 256 or 128 (gemm_pick_bn)
+  int mc;                     // 1: 4-CTA clusters, two 2-SM pairs sharing (multicasting) the A panel
   int group_m;                // grouped raster: tile rows that advance together along N
   int x3;                     // fp32-accurate 3xTF32: each stage carries hi and lo operand copies
                               // and feeds hi*hi + hi*lo + lo*hi into one accumulator
@@ -43,6 +44,8 @@ bool gemm_paired(int M);          // 2-SM (cta_group::2) tiles for this M
 int gemm_b_box(int M, int bn);    // B rows (N) one CTA loads per K-major TMA box
 // tile width: 128 when 256-wide tiles would leave over half the grid idle, else 256
 int gemm_pick_bn(int M, int N, int batch, int n_regions, int num_sms);
+bool gemm_use_mc(int M, int N, int bn);  // A multicast across two 2-SM pairs for this launch
+int gemm_a_box_rows(bool mc);            // A rows per K-major TMA box (half a pair's rows with multicast)
 constexpr int kStoreRows = 32;   // epilogue TMA-store box: 32 rows x 128 bytes
 cudaError_t gemm_prepare();  // sets the dynamic-smem attribute (call before capture)
 cudaError_t launch_gemm(const GemmLaunch& p, int num_sms, cudaStream_t stream);

@@ -118,6 +118,17 @@ __device__ __forceinline__ void tma_load_3d_2sm(void* dst, const CUtensorMap* m,
       : "memory");
 }
 
+// Paired-CTA load multicast to every CTA in `mask` (same smem offset in
+// each); each destination's bytes are counted on its pair leader's barrier.
+__device__ __forceinline__ void tma_load_3d_2sm_mc(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1,
+                                                   int c2, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1), "r"(c2), "h"(mask)
+      : "memory");
+}
+
 // the same loads with an L2 eviction-priority policy (createpolicy)
 __device__ __forceinline__ void tma_load_3d_hint(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1,
                                                  int c2, uint64_t policy) {
@@ -244,12 +255,13 @@ __device__ __forceinline__ void mma_f16_2sm(uint32_t d_tmem, uint64_t a_desc, ui
       "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
-// Paired commit: arrive on the barrier at this offset in both CTAs.
-__device__ __forceinline__ void mma_commit_2sm(uint64_t* bar) {
+// Paired commit: arrive on the barrier at this offset in every CTA of
+// `mask` (default: both CTAs of the first pair).
+__device__ __forceinline__ void mma_commit_2sm(uint64_t* bar, uint16_t mask = 3) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
           smem_u32(bar)),
-      "h"(uint16_t(3))
+      "h"(mask)
       : "memory");
 }
 // Arrive on an mbarrier once all previously issued MMAs of this thread finish.
