@@ -19,9 +19,14 @@
  * copies the plan. A context / plan handle is single-caller (not
  * re-entrant); calls block until their work is complete, like execute().
  *
- * Multi-GPU: one process per GPU. Rank r runs the exec vertices whose
- * machine (placement_t::machine_of, placement.h:9-15) maps to it
- * (machine % world == r); remote dependencies move over NCCL.
+ * Multi-GPU: rank r runs the exec vertices whose machine
+ * (placement_t::machine_of, placement.h:9-15) maps to it (machine % world
+ * == r). Either one process drives every rank (ed_ctx_create_multi, the
+ * drop-in for the reference's single execute() over L machines), or one
+ * process per GPU (ed_ctx_create + ed_peer_export / ed_peer_import). Remote
+ * dependencies move over the peer transport (the consumer reads the
+ * producer's HBM over NVLink once its ready flag carries the run's epoch);
+ * ED_TRANSPORT_NCCL is an opt-in alternative for one-process-per-GPU worlds.
  */
 #ifndef ED_GPU_H
 #define ED_GPU_H
@@ -136,8 +141,14 @@ typedef struct {
   int32_t profile;          /* 1: time every launch with CUDA events (ed_kernel_stats) */
   int32_t no_graph;         /* 1: launch eagerly instead of replaying a CUDA graph */
   int32_t transport;        /* ed_transport: how remote dependencies move (world > 1) */
-  int32_t reserved[3];
+  int32_t sched_mode;       /* ed_sched_mode: which of the reference's schedulers wall_steps reports */
+  int32_t reserved[2];
 } ed_options_c;
+
+/* sched_mode_t (runtime.h:23): wall_steps of run_report_t counts rounds in
+ * round_robin (the reference's default, runtime.cc:281-298) and vertices in
+ * threaded mode (runtime.cc:353). The device schedule is the same for both. */
+typedef enum { ED_SCHED_ROUND_ROBIN = 0, ED_SCHED_THREADED = 1 } ed_sched_mode;
 
 /* ED_TRANSPORT_NCCL: ncclSend / ncclRecv groups on a comm stream (needs the
  *   context's NCCL communicator).
@@ -223,6 +234,17 @@ ED_API ed_status ed_nccl_unique_id(void* out, size_t len, char* err, size_t errl
 ED_API ed_status ed_ctx_create(int32_t device, int32_t rank, int32_t world,
                         const void* nccl_id, size_t nccl_id_len,
                         struct ed_ctx** out, char* err, size_t errlen);
+/* One process, several ranks: the reference's single execute() call drives
+ * all L machines (runtime.cc:301-355, runtime.cc:518-550), so the drop-in
+ * does too. Rank r (machine % n) runs on device_ids[r] (a device may repeat:
+ * several ranks then share it); ranks exchange remote chunks through the
+ * peer transport with plain device pointers (peer access is enabled between
+ * distinct devices, NVLink on an HGX board). Every plan call on such a
+ * context drives all ranks from the calling thread: ed_run starts every
+ * rank's run before waiting for any; ed_download assembles on rank 0.
+ * ed_peer_export / ed_peer_import are not used. */
+ED_API ed_status ed_ctx_create_multi(int32_t n, const int32_t* device_ids, struct ed_ctx** out, char* err,
+                                     size_t errlen);
 ED_API void ed_ctx_destroy(struct ed_ctx* ctx);
 
 /* Validates the plan (execute()'s checks, runtime.cc:388-395), maps each

@@ -161,9 +161,14 @@ run_report_t execute_gpu(
   ed_options_c opt{};
   opt.precision = gpu.precision >= 0 ? gpu.precision : (options.f32 ? ED_PREC_FP32 : ED_PREC_FP64);
   opt.corrupt = options.corrupt ? 1 : 0;
+  opt.sched_mode = options.mode == sched_mode_t::threaded ? ED_SCHED_THREADED : ED_SCHED_ROUND_ROBIN;
 
   ed_ctx* ctx = nullptr;
-  ED_CALL(ed_ctx_create(gpu.device, 0, 1, nullptr, 0, &ctx, err, sizeof err));
+  if(gpu.devices.empty()) {
+    ED_CALL(ed_ctx_create(gpu.device, 0, 1, nullptr, 0, &ctx, err, sizeof err));
+  } else {
+    ED_CALL(ed_ctx_create_multi(int32_t(gpu.devices.size()), gpu.devices.data(), &ctx, err, sizeof err));
+  }
   std::unique_ptr<ed_ctx, void (*)(ed_ctx*)> ctx_guard(ctx, ed_ctx_destroy);
   ed_plan_h* h = nullptr;
   ED_CALL(ed_prepare(ctx, &plan, &opt, &h, err, sizeof err));

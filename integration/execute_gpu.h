@@ -11,6 +11,10 @@ struct gpu_options_t {
   // both bit-identical to the CPU executor); or force ED_PREC_BF16 / TF32.
   int precision = -1;
   int device = 0;
+  // one process over several GPUs (ed_ctx_create_multi): rank r = machine % n
+  // runs on devices[r]; empty = every machine on `device` as one rank. A
+  // device may repeat (several ranks on one GPU: the same code path, for tests).
+  vector<int> devices;
 };
 
 run_report_t execute_gpu(

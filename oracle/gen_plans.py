@@ -43,6 +43,8 @@ SMALL = {
     "sqdiff": "input X:[2,2]\ninput Y:[2,2]\nZ[i,k] = sum[j] sqdiff(X[i,j], Y[j,k])\noutput Z\n",
     "absmax": "input X:[2,2]\ninput Y:[2,2]\nZ[i,k] = max[j] absdiff(X[i,j], Y[j,k])\noutput Z\n",
     "divzero": "input X:[4,4]\ninput Y:[4,4]\nZ[i,j] = div(X[i,j], Y[i,j])\noutput Z\n",
+    # a wide exp map: device exp vs the host's std::exp over every range (tests/test_gpu_parity.py)
+    "expmap": "input X:[1024,4096]\nY[i,j] = map exp(X[i,j])\noutput Y\n",
     "mix": ("input X:[16,24]\ninput Y:[24,8]\n"
             "A[i,k] = sum[j] sqdiff(X[i,j], Y[j,k])\nB[i] = max[k] map neg(A[i,k])\n"
             "C[i,k] = add(A[i,k], B[i])\nD[k,i] = map scale(0.5)(C[i,k])\noutput D\n"),

@@ -80,7 +80,8 @@ class ed_options_c(C.Structure):
         ("profile", C.c_int32),
         ("no_graph", C.c_int32),
         ("transport", C.c_int32),
-        ("reserved", C.c_int32 * 3),
+        ("sched_mode", C.c_int32),
+        ("reserved", C.c_int32 * 2),
     ]
 
 
@@ -140,7 +141,7 @@ class ed_cost_model_c(C.Structure):
 
 # Every symbol include/ed_gpu.h declares (tests/test_abi.py checks exports).
 EXPORTED = [
-    "ed_abi_version", "ed_nccl_unique_id", "ed_ctx_create", "ed_ctx_destroy",
+    "ed_abi_version", "ed_nccl_unique_id", "ed_ctx_create", "ed_ctx_create_multi", "ed_ctx_destroy",
     "ed_prepare", "ed_plan_destroy", "ed_upload", "ed_upload_tensors", "ed_run",
     "ed_download", "ed_download_chunk", "ed_plan_schedule", "ed_kernel_stats", "ed_gpu_placement",
     "ed_run_steps", "ed_peer_export", "ed_peer_import", "ed_generate_inputs",
@@ -155,6 +156,7 @@ def declare(lib):
     lib.ed_nccl_unique_id.argtypes = [C.c_void_p, C.c_size_t] + err
     lib.ed_ctx_create.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_size_t,
                                   C.POINTER(P)] + err
+    lib.ed_ctx_create_multi.argtypes = [C.c_int32, i32p, C.POINTER(P)] + err
     lib.ed_ctx_destroy.argtypes = [P]
     lib.ed_ctx_destroy.restype = None
     lib.ed_prepare.argtypes = [P, C.POINTER(ed_plan_c), C.POINTER(ed_options_c), C.POINTER(P)] + err

@@ -12,7 +12,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libed_gpu.so")
 SOURCES = ["api.cu", "plan.cu", "build.cu", "alloc.cu", "exec.cu", "io.cu", "placement.cu", "gemm_sm100.cu",
            "kernels.cu", "ewise.cu", "attn_sm100.cu"]
-HEADERS = ["runtime.h", "ptx.cuh", "gemm_sm100.h", "kernels.h", "ewise.h", "attn_sm100.h"]
+HEADERS = ["runtime.h", "libm_exp.cuh", "ptx.cuh", "gemm_sm100.h", "kernels.h", "ewise.h", "attn_sm100.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # The toolchain's libstdc++.so link is missing (only the .a resolves); a static
 # libstdc++ inside a dlopen'ed .so clashes with the host's, so link the system

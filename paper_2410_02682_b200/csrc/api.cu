@@ -60,8 +60,51 @@ ed_status ed_ctx_create(int32_t device, int32_t rank, int32_t world, const void*
   });
 }
 
+ed_status ed_ctx_create_multi(int32_t n, const int32_t* device_ids, ed_ctx** out, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!out || n < 1 || !device_ids) throw ed_error(ED_ERR_USAGE, "ed_ctx_create_multi: need n >= 1 device ids");
+    auto* g = new ed_ctx;
+    try {
+      for (int r = 0; r < n; ++r) {
+        ed_ctx* c = nullptr;
+        char e2[512];
+        const ed_status st = ed_ctx_create(device_ids[r], r, n, nullptr, 0, &c, e2, sizeof e2);
+        if (st != ED_OK) throw ed_error(st, e2);
+        g->subs.push_back(c);
+      }
+      // every rank reads its peers' chunks in place: enable peer access
+      // between the distinct devices of the group (NVLink on an HGX board)
+      for (int a = 0; a < n; ++a)
+        for (int b = 0; b < n; ++b) {
+          const int da = device_ids[a], db = device_ids[b];
+          if (da == db) continue;
+          int can = 0;
+          CUDA_OK(cudaDeviceCanAccessPeer(&can, da, db));
+          if (!can) throw ed_error(ED_ERR_UNSUPPORTED, "devices " + std::to_string(da) + " and " +
+                                                            std::to_string(db) + " have no peer access");
+          CUDA_OK(cudaSetDevice(da));
+          const cudaError_t e = cudaDeviceEnablePeerAccess(db, 0);
+          if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+          else CUDA_OK(e);
+        }
+      g->device = device_ids[0];
+      g->world = n;
+      g->num_sms = g->subs[0]->num_sms;
+    } catch (...) {
+      ed_ctx_destroy(g);
+      throw;
+    }
+    *out = g;
+  });
+}
+
 void ed_ctx_destroy(ed_ctx* c) {
   if (!c) return;
+  if (!c->subs.empty()) {
+    for (ed_ctx* s : c->subs) ed_ctx_destroy(s);
+    delete c;
+    return;
+  }
   cudaSetDevice(c->device);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -73,6 +116,52 @@ ed_status ed_prepare(ed_ctx* ctx, const ed_plan_c* plan, const ed_options_c* opt
                      char* err, size_t errlen) {
   return guarded(err, errlen, [&] {
     if (!ctx || !out) throw ed_error(ED_ERR_USAGE, "null context or output");
+    if (!ctx->subs.empty()) {
+      // one sub-plan per rank, peer transport over plain device pointers
+      auto* g = new ed_plan_h;
+      g->ctx = ctx;
+      if (options) g->opt = *options;
+      g->opt.transport = ED_TRANSPORT_PEER;
+      try {
+        for (ed_ctx* c : ctx->subs) {
+          ed_plan_h* h = nullptr;
+          char e2[1024];
+          const ed_status st = ed_prepare(c, plan, &g->opt, &h, e2, sizeof e2);
+          if (st != ED_OK) throw ed_error(st, e2);
+          g->subs.push_back(h);
+        }
+        g->copy_plan(plan);
+        g->counters = g->subs[0]->counters;
+        g->total_transferred = g->subs[0]->total_transferred;
+        g->max_site_cost = g->subs[0]->max_site_cost;
+        g->rr_rounds = g->subs[0]->rr_rounds;
+        const int world = int(g->subs.size());
+        for (ed_plan_h* h : g->subs) {
+          if (!h->peer) continue;  // world 1: nothing to exchange
+          h->peer_arena.assign(size_t(world), nullptr);
+          h->peer_flags.assign(size_t(world), nullptr);
+          h->peer_off.assign(size_t(world), {});
+          for (int r = 0; r < world; ++r) {
+            ed_plan_h* q = g->subs[size_t(r)];
+            h->peer_arena[size_t(r)] = static_cast<char*>(q->arena);
+            h->peer_flags[size_t(r)] = q->d_pflags;
+            auto& off = h->peer_off[size_t(r)];
+            off.resize(q->X.size());
+            for (int id = 0; id < int(q->X.size()); ++id) off[size_t(id)] = q->local[id] ? q->arena_offset(id) : -1;
+          }
+          h->peer_inproc = true;
+          h->peer_ready = true;
+          CUDA_OK(cudaSetDevice(h->ctx->device));
+          h->record();
+        }
+      } catch (...) {
+        for (ed_plan_h* h : g->subs) ed_plan_destroy(h);
+        delete g;
+        throw;
+      }
+      *out = g;
+      return;
+    }
     CUDA_OK(cudaSetDevice(ctx->device));
     auto* h = new ed_plan_h;
     h->ctx = ctx;
@@ -106,6 +195,11 @@ ed_status ed_prepare(ed_ctx* ctx, const ed_plan_c* plan, const ed_options_c* opt
 
 void ed_plan_destroy(ed_plan_h* h) {
   if (!h) return;
+  if (!h->subs.empty()) {
+    for (ed_plan_h* s : h->subs) ed_plan_destroy(s);
+    delete h;
+    return;
+  }
   cudaSetDevice(h->ctx->device);
   h->destroy();
   delete h;
@@ -114,6 +208,7 @@ void ed_plan_destroy(ed_plan_h* h) {
 ed_status ed_peer_export(ed_plan_h* h, void* out, size_t cap, size_t* len, char* err, size_t errlen) {
   return guarded(err, errlen, [&] {
     if (!h || !len) throw ed_error(ED_ERR_USAGE, "null argument");
+    if (!h->subs.empty()) throw ed_error(ED_ERR_USAGE, "a multi-device context exchanges in-process (no export)");
     if (!h->peer) throw ed_error(ED_ERR_USAGE, "plan was not prepared with ED_TRANSPORT_PEER in a world > 1");
     *len = peer_blob_len(h);
     if (!out) return;
@@ -135,6 +230,7 @@ ed_status ed_peer_export(ed_plan_h* h, void* out, size_t cap, size_t* len, char*
 ed_status ed_peer_import(ed_plan_h* h, const void* blobs, size_t blob_len, int32_t n, char* err, size_t errlen) {
   return guarded(err, errlen, [&] {
     if (!h || !blobs) throw ed_error(ED_ERR_USAGE, "null argument");
+    if (!h->subs.empty()) throw ed_error(ED_ERR_USAGE, "a multi-device context exchanges in-process (no import)");
     if (!h->peer) throw ed_error(ED_ERR_USAGE, "plan was not prepared with ED_TRANSPORT_PEER in a world > 1");
     if (h->peer_ready) throw ed_error(ED_ERR_USAGE, "ed_peer_import: already imported");
     if (n != h->ctx->world || blob_len != peer_blob_len(h)) throw ed_error(ED_ERR_USAGE, "ed_peer_import: need one blob per rank");

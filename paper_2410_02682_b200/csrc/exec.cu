@@ -141,6 +141,11 @@ void ed_plan_h::record() {
   CUDA_OK(attn_prepare());
   if (!ev0) CUDA_OK(cudaEventCreate(&ev0));
   if (!ev1) CUDA_OK(cudaEventCreate(&ev1));
+  if (opt.profile && op_events.size() != ops.size() + 1) {  // every entry point that enqueues (ed_run, ed_run_steps)
+    for (auto e : op_events) cudaEventDestroy(e);
+    op_events.assign(ops.size() + 1, nullptr);
+    for (auto& e : op_events) CUDA_OK(cudaEventCreate(&e));
+  }
   if (opt.no_graph || opt.profile || (peer && !peer_ready)) return;  // peer: recorded by ed_peer_import
   cudaStream_t s = ctx->stream;
   CUDA_OK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
@@ -157,6 +162,15 @@ void ed_plan_h::record() {
 }
 
 void ed_plan_h::destroy() {
+  if (peer && peer_ready && ctx->stream) {
+    // peers may still be reading our arena (their last run's receives): wait
+    // until every rank has finished it before the exported memory goes away
+    try {
+      wait_peers_idle(this, ctx->stream);
+      cudaStreamSynchronize(ctx->stream);
+    } catch (...) {
+    }
+  }
   if (gexec) cudaGraphExecDestroy(gexec);
   if (graph) cudaGraphDestroy(graph);
   if (ev0) cudaEventDestroy(ev0);
@@ -165,7 +179,7 @@ void ed_plan_h::destroy() {
   for (auto e : comm_events) cudaEventDestroy(e);
   for (auto a : aux)
     if (a) cudaStreamDestroy(a);
-  for (size_t r = 0; r < peer_arena.size(); ++r)
+  for (size_t r = 0; r < peer_arena.size() && !peer_inproc; ++r)
     if (int(r) != ctx->rank) {
       if (peer_arena[r]) cudaIpcCloseMemHandle(peer_arena[r]);
       if (peer_flags[r]) cudaIpcCloseMemHandle(peer_flags[r]);
@@ -199,65 +213,121 @@ void ed_plan_h::destroy() {
 
 extern "C" {
 
+namespace {
+
+// ed_run in two halves, so a group plan can start every rank's run before
+// waiting for any of them (they exchange chunks while running)
+void start_run(ed_plan_h* h) {
+  if (h->peer && !h->peer_ready) throw ed_error(ED_ERR_USAGE, "ED_TRANSPORT_PEER: call ed_peer_import first");
+  CUDA_OK(cudaSetDevice(h->ctx->device));
+  cudaStream_t s = h->ctx->stream;
+  CUDA_OK(cudaMemsetAsync(h->d_err, 0, sizeof(int), s));
+  CUDA_OK(cudaEventRecord(h->ev0, s));
+  if (h->gexec) CUDA_OK(cudaGraphLaunch(h->gexec, s));
+  else h->enqueue(s);
+  CUDA_OK(cudaEventRecord(h->ev1, s));
+}
+
+void finish_run(ed_plan_h* h, ed_report_c* rep) {
+  CUDA_OK(cudaSetDevice(h->ctx->device));
+  CUDA_OK(cudaEventSynchronize(h->ev1));
+  h->check_peer_error();
+  int flag = 0;
+  CUDA_OK(cudaMemcpy(&flag, h->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+  float ms = 0;
+  CUDA_OK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+  if (h->opt.profile) {
+    std::map<std::string, size_t> idx;
+    h->stats.clear();
+    for (size_t i = 0; i < h->ops.size(); ++i) {
+      float t = 0;
+      CUDA_OK(cudaEventElapsedTime(&t, h->op_events[i], h->op_events[i + 1]));
+      const Op& op = h->ops[i];
+      auto it = idx.find(op.name);
+      if (it == idx.end()) {
+        ed_kernel_stat_c st{};
+        std::snprintf(st.name, sizeof(st.name), "%s", op.name.c_str());
+        it = idx.emplace(op.name, h->stats.size()).first;
+        h->stats.push_back(st);
+      }
+      auto& st = h->stats[it->second];
+      st.launches += 1;
+      st.ms += t;
+      st.flops += op.flops;
+      st.bytes += op.bytes;
+    }
+  }
+  if (flag) throw ed_error(ED_ERR_EVAL, "division by zero");
+  if (rep) {
+    if (rep->machines)
+      for (int m = 0; m < std::min(rep->n_machines, h->n_machines); ++m) rep->machines[m] = h->counters[m];
+    rep->total_transferred = h->total_transferred;
+    rep->wall_steps = h->opt.sched_mode == ED_SCHED_THREADED ? int64_t(h->X.size()) : h->rr_rounds;
+    rep->max_site_cost = h->max_site_cost;
+    rep->device_ms = ms;
+    int64_t pb = 0;
+    int launches = 0;
+    for (auto& op : h->ops) {
+      if (op.kind == OpKind::SEND) pb += int64_t(op.count) * int64_t(h->es);
+      if (op.kind != OpKind::SEND && op.kind != OpKind::RECV) ++launches;
+    }
+    rep->peer_bytes = pb;
+    rep->contraction_flops = h->contraction_flops;
+    rep->gpu_launches = launches;
+  }
+}
+
+}  // namespace
+
 ed_status ed_run(ed_plan_h* h, ed_report_c* rep, char* err, size_t errlen) {
   return guarded(err, errlen, [&] {
     if (!h) throw ed_error(ED_ERR_USAGE, "null plan");
-    if (h->peer && !h->peer_ready) throw ed_error(ED_ERR_USAGE, "ED_TRANSPORT_PEER: call ed_peer_import first");
-    CUDA_OK(cudaSetDevice(h->ctx->device));
-    cudaStream_t s = h->ctx->stream;
-    CUDA_OK(cudaMemsetAsync(h->d_err, 0, sizeof(int), s));
-    if (h->opt.profile && h->op_events.size() != h->ops.size() + 1) {
-      for (auto e : h->op_events) cudaEventDestroy(e);
-      h->op_events.assign(h->ops.size() + 1, nullptr);
-      for (auto& e : h->op_events) CUDA_OK(cudaEventCreate(&e));
+    if (h->subs.empty()) {
+      start_run(h);
+      finish_run(h, rep);
+      return;
     }
-    CUDA_OK(cudaEventRecord(h->ev0, s));
-    if (h->gexec) CUDA_OK(cudaGraphLaunch(h->gexec, s));
-    else h->enqueue(s);
-    CUDA_OK(cudaEventRecord(h->ev1, s));
-    CUDA_OK(cudaEventSynchronize(h->ev1));
-    h->check_peer_error();
-    int flag = 0;
-    CUDA_OK(cudaMemcpy(&flag, h->d_err, sizeof(int), cudaMemcpyDeviceToHost));
-    float ms = 0;
-    CUDA_OK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
-    if (h->opt.profile) {
-      std::map<std::string, size_t> idx;
-      h->stats.clear();
-      for (size_t i = 0; i < h->ops.size(); ++i) {
-        float t = 0;
-        CUDA_OK(cudaEventElapsedTime(&t, h->op_events[i], h->op_events[i + 1]));
-        const Op& op = h->ops[i];
-        auto it = idx.find(op.name);
+    // group plan: every rank's run is in flight before any is waited for;
+    // device_ms is the slowest rank's, counts sum over ranks
+    for (ed_plan_h* s : h->subs) start_run(s);
+    double ms = 0;
+    int64_t pb = 0;
+    double cf = 0;
+    int launches = 0;
+    std::map<std::string, size_t> idx;
+    h->stats.clear();
+    for (ed_plan_h* s : h->subs) {
+      ed_report_c r{};
+      r.n_machines = rep ? rep->n_machines : 0;
+      r.machines = rep ? rep->machines : nullptr;
+      finish_run(s, &r);
+      ms = std::max(ms, r.device_ms);
+      pb += r.peer_bytes;
+      cf += r.contraction_flops;
+      launches += r.gpu_launches;
+      if (rep) {
+        rep->total_transferred = r.total_transferred;
+        rep->wall_steps = r.wall_steps;
+        rep->max_site_cost = r.max_site_cost;
+      }
+      for (const auto& st : s->stats) {
+        auto it = idx.find(st.name);
         if (it == idx.end()) {
-          ed_kernel_stat_c st{};
-          std::snprintf(st.name, sizeof(st.name), "%s", op.name.c_str());
-          it = idx.emplace(op.name, h->stats.size()).first;
+          it = idx.emplace(st.name, h->stats.size()).first;
           h->stats.push_back(st);
+          continue;
         }
-        auto& st = h->stats[it->second];
-        st.launches += 1;
-        st.ms += t;
-        st.flops += op.flops;
-        st.bytes += op.bytes;
+        auto& t = h->stats[it->second];
+        t.launches += st.launches;
+        t.ms += st.ms;
+        t.flops += st.flops;
+        t.bytes += st.bytes;
       }
     }
-    if (flag) throw ed_error(ED_ERR_EVAL, "division by zero");
     if (rep) {
-      if (rep->machines)
-        for (int m = 0; m < std::min(rep->n_machines, h->n_machines); ++m) rep->machines[m] = h->counters[m];
-      rep->total_transferred = h->total_transferred;
-      rep->wall_steps = int64_t(h->X.size());
-      rep->max_site_cost = h->max_site_cost;
       rep->device_ms = ms;
-      int64_t pb = 0;
-      int launches = 0;
-      for (auto& op : h->ops) {
-        if (op.kind == OpKind::SEND) pb += int64_t(op.count) * int64_t(h->es);
-        if (op.kind != OpKind::SEND && op.kind != OpKind::RECV) ++launches;
-      }
       rep->peer_bytes = pb;
-      rep->contraction_flops = h->contraction_flops;
+      rep->contraction_flops = cf;
       rep->gpu_launches = launches;
     }
   });

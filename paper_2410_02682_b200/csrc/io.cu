@@ -14,6 +14,14 @@ void ensure_staging(ed_plan_h* h, size_t bytes) {
   h->staging_bytes = bytes;
 }
 
+void wait_peers_idle(ed_plan_h* h, cudaStream_t s) {
+  if (!h->peer || !h->peer_ready) return;
+  // peers copy our input chunks during a run (write-after-read): new inputs
+  // are written only once every rank's run-done flag carries this epoch
+  std::vector<int*> done(h->peer_flags.begin(), h->peer_flags.end());
+  CUDA_OK(launch_peer_wait(done.data(), int(done.size()), h->d_epoch, 0, s, h->d_perr, int(h->X.size()) + 3));
+}
+
 size_t dt_size(int dtype) {
   if (dtype == ED_DTYPE_F64) return 8;
   if (dtype == ED_DTYPE_F32) return 4;
@@ -185,7 +193,7 @@ void cached_copy(ed_plan_h* h, int w, bool to_chunks, void* whole, int dtype, cu
 }
 
 void throw_status(ed_status st, const char* msg) {
-  if (st != ED_OK) throw ed_error(st, msg);
+  if (st != ED_OK) throw ed_error(st, msg ? msg : "");
 }
 
 }  // namespace edrt
@@ -194,9 +202,14 @@ extern "C" {
 
 ed_status ed_upload(ed_plan_h* h, const ed_chunk_in_c* chunks, int32_t n, char* err, size_t errlen) {
   return guarded(err, errlen, [&] {
+    if (h && !h->subs.empty()) {  // group plan: every rank's sub-plan, in rank order
+      for (ed_plan_h* q : h->subs) throw_status(ed_upload(q, chunks, n, err, errlen), err);
+      return;
+    }
     if (!h || (n && !chunks)) throw ed_error(ED_ERR_USAGE, "null argument");
     CUDA_OK(cudaSetDevice(h->ctx->device));
     cudaStream_t s = h->ctx->stream;
+    wait_peers_idle(h, s);
     for (int i = 0; i < n; ++i) {
       const ed_chunk_in_c& c = chunks[i];
       if (c.exec_id < 0 || c.exec_id >= int(h->X.size()) || h->X[c.exec_id].kind != ED_EXEC_INPUT_CHUNK)
@@ -217,9 +230,14 @@ ed_status ed_upload(ed_plan_h* h, const ed_chunk_in_c* chunks, int32_t n, char* 
 
 ed_status ed_upload_tensors(ed_plan_h* h, const ed_tensor_in_c* ts, int32_t n, char* err, size_t errlen) {
   return guarded(err, errlen, [&] {
+    if (h && !h->subs.empty()) {  // group plan: every rank's sub-plan, in rank order
+      for (ed_plan_h* q : h->subs) throw_status(ed_upload_tensors(q, ts, n, err, errlen), err);
+      return;
+    }
     if (!h || (n && !ts)) throw ed_error(ED_ERR_USAGE, "null argument");
     CUDA_OK(cudaSetDevice(h->ctx->device));
     cudaStream_t s = h->ctx->stream;
+    wait_peers_idle(h, s);
     for (int i = 0; i < n; ++i) {
       const ed_tensor_in_c& t = ts[i];
       if (t.vertex_id < 0 || t.vertex_id >= int(h->V.size()) || h->V[t.vertex_id].arity != 0)
@@ -248,6 +266,10 @@ ed_status ed_upload_tensors(ed_plan_h* h, const ed_tensor_in_c* ts, int32_t n, c
 
 ed_status ed_generate_inputs(ed_plan_h* h, uint64_t seed, char* err, size_t errlen) {
   return guarded(err, errlen, [&] {
+    if (h && !h->subs.empty()) {  // group plan: every rank's sub-plan, in rank order
+      for (ed_plan_h* q : h->subs) throw_status(ed_generate_inputs(q, seed, err, errlen), err);
+      return;
+    }
     if (!h) throw ed_error(ED_ERR_USAGE, "null plan");
     CUDA_OK(cudaSetDevice(h->ctx->device));
     // uses_only_sum_mul (runtime.cc:358-378): generate_inputs' distribution switch
@@ -259,6 +281,7 @@ ed_status ed_generate_inputs(ed_plan_h* h, uint64_t seed, char* err, size_t errl
       if (v.agg >= 0 && v.agg != ED_AGG_SUM && v.agg != ED_AGG_MAX) integer_valued = false;
     }
     cudaStream_t s = h->ctx->stream;
+    wait_peers_idle(h, s);
     std::vector<GenTensor> jobs;
     std::vector<int> vids;
     for (int w = 0; w < int(h->V.size()); ++w) {
@@ -305,6 +328,10 @@ ed_status ed_generate_inputs(ed_plan_h* h, uint64_t seed, char* err, size_t errl
 
 ed_status ed_download(ed_plan_h* h, ed_output_c* outs, int32_t n, char* err, size_t errlen) {
   return guarded(err, errlen, [&] {
+    if (h && !h->subs.empty()) {  // group plan: every rank's sub-plan, in rank order (rank 0 assembles)
+      for (ed_plan_h* q : h->subs) throw_status(ed_download(q, outs, n, err, errlen), err);
+      return;
+    }
     if (!h || (n && !outs)) throw ed_error(ED_ERR_USAGE, "null argument");
     CUDA_OK(cudaSetDevice(h->ctx->device));
     cudaStream_t s = h->ctx->stream;
@@ -383,6 +410,10 @@ ed_status ed_download(ed_plan_h* h, ed_output_c* outs, int32_t n, char* err, siz
 ed_status ed_run_steps(ed_plan_h* h, int32_t n_steps, const ed_tensor_in_c* ins, int32_t n_in, ed_output_c* outs,
                        int32_t n_out, ed_report_c* rep, char* err, size_t errlen) {
   return guarded(err, errlen, [&] {
+    if (h && h->subs.size() == 1) {
+      throw_status(ed_run_steps(h->subs[0], n_steps, ins, n_in, outs, n_out, rep, err, errlen), err);
+      return;
+    }
     if (!h || n_steps < 0 || n_in < 0 || n_out < 0 || (n_in && !ins) || (n_out && !outs))
       throw ed_error(ED_ERR_USAGE, "null argument");
     if (h->ctx->world > 1) {  // collective download: the plain sequence, step by step
@@ -483,7 +514,7 @@ ed_status ed_run_steps(ed_plan_h* h, int32_t n_steps, const ed_tensor_in_c* ins,
       if (rep->machines)
         for (int m = 0; m < std::min(rep->n_machines, h->n_machines); ++m) rep->machines[m] = h->counters[m];
       rep->total_transferred = h->total_transferred;
-      rep->wall_steps = int64_t(h->X.size());
+      rep->wall_steps = h->opt.sched_mode == ED_SCHED_THREADED ? int64_t(h->X.size()) : h->rr_rounds;
       rep->max_site_cost = h->max_site_cost;
       float ms = 0;
       CUDA_OK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
@@ -501,6 +532,12 @@ ed_status ed_run_steps(ed_plan_h* h, int32_t n_steps, const ed_tensor_in_c* ins,
 ed_status ed_download_chunk(ed_plan_h* h, int32_t exec_id, int32_t dtype, void* data, int64_t n, char* err,
                             size_t errlen) {
   return guarded(err, errlen, [&] {
+    if (h && !h->subs.empty()) {  // group plan: the rank holding the chunk
+      if (exec_id < 0 || exec_id >= int(h->X.size())) throw ed_error(ED_ERR_USAGE, "exec id out of range");
+      ed_plan_h* q = h->subs[size_t(h->X[exec_id].machine % int(h->subs.size()))];
+      throw_status(ed_download_chunk(q, exec_id, dtype, data, n, err, errlen), err);
+      return;
+    }
     if (!h || !data) throw ed_error(ED_ERR_USAGE, "null argument");
     if (exec_id < 0 || exec_id >= int(h->X.size())) throw ed_error(ED_ERR_USAGE, "exec id out of range");
     if (n != h->X[exec_id].sz) throw ed_error(ED_ERR_USAGE, "chunk size mismatch");

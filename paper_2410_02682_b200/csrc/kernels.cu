@@ -10,6 +10,7 @@
 // the reference's default mode bit for bit.
 #include <cuda_bf16.h>
 
+#include "libm_exp.cuh"
 #include "kernels.h"
 
 namespace ed {
@@ -42,7 +43,7 @@ __device__ __forceinline__ double join_d(int op, double x, double y, int* err) {
 __device__ __forceinline__ double map_d(int op, double c, double x) {
   switch (op) {
     case 0: return x > 0.0 ? x : 0.0;
-    case 1: return exp(x);
+    case 1: return libm_exp(x);  // the host's std::exp bit for bit (ops.cc:24)
     case 2: return -x;
     case 3: return __dmul_rn(c, x);
     default: return x;

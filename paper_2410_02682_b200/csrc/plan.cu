@@ -142,6 +142,51 @@ void ed_plan_h::validate() {
   max_site_cost = 0;
   for (auto& c : counters)
     max_site_cost = std::max(max_site_cost, alpha * double(c.fp) + double(c.sent) + double(c.received));
+
+  // run_round_robin's rounds (runtime.cc:281-298): each round, machine m in
+  // order pulls every produced dependency of its waiting vertices, then runs
+  // its first ready vertex. Data-independent, so replayed here once.
+  std::vector<std::vector<int>> mine(static_cast<size_t>(n_machines));
+  std::vector<char> done(size_t(ne), 0);
+  std::vector<std::set<int>> resident(static_cast<size_t>(n_machines));
+  int left = 0;
+  for (int id = 0; id < ne; ++id) {
+    if (X[id].kind == ED_EXEC_INPUT_CHUNK) {
+      done[size_t(id)] = 1;
+      resident[size_t(X[id].machine)].insert(id);
+    } else {
+      mine[size_t(X[id].machine)].push_back(id);
+      ++left;
+    }
+  }
+  std::vector<size_t> first_open(static_cast<size_t>(n_machines), 0);  // mine[m] before this index are done
+  rr_rounds = 0;
+  while (left > 0) {
+    bool progressed = false;
+    for (int m = 0; m < n_machines; ++m) {
+      auto& mm = mine[size_t(m)];
+      auto& res = resident[size_t(m)];
+      while (first_open[size_t(m)] < mm.size() && done[size_t(mm[first_open[size_t(m)]])]) ++first_open[size_t(m)];
+      for (size_t k = first_open[size_t(m)]; k < mm.size(); ++k)
+        if (!done[size_t(mm[k])])
+          for (int d : X[mm[k]].deps)
+            if (done[size_t(d)]) res.insert(d);
+      for (size_t k = first_open[size_t(m)]; k < mm.size(); ++k) {
+        const int id = mm[k];
+        if (done[size_t(id)]) continue;
+        bool ready = true;
+        for (int d : X[id].deps) ready = ready && res.count(d);
+        if (!ready) continue;
+        done[size_t(id)] = 1;
+        res.insert(id);
+        --left;
+        progressed = true;
+        break;  // one vertex per machine per round
+      }
+    }
+    ++rr_rounds;
+    if (!progressed) throw ed_error(ED_ERR_PLAN, "execute: no runnable vertex; graph is inconsistent");
+  }
 }
 
 extern "C" {

@@ -203,6 +203,11 @@ struct ed_ctx {
   int device = 0, rank = 0, world = 1, num_sms = 148;
   ncclComm_t comm = nullptr;
   cudaStream_t stream = nullptr, comm_stream = nullptr;
+  // ed_ctx_create_multi: one process drives every rank (machine % world) on
+  // its own device — the reference's single execute() over L machines
+  // (runtime.cc:301-355). Ranks exchange chunks through the peer transport
+  // with plain device pointers (no IPC); several ranks may share a device.
+  std::vector<ed_ctx*> subs;
 };
 
 struct ed_plan_h {
@@ -223,6 +228,7 @@ struct ed_plan_h {
   std::vector<Op> ops;
   std::vector<ed_machine_c> counters;
   int64_t total_transferred = 0, peer_bytes = 0;
+  int64_t rr_rounds = 0;           // run_round_robin's wall_steps for this plan (runtime.cc:281-298)
   double max_site_cost = 0.0, contraction_flops = 0.0;
   int first_join = -1;
 
@@ -429,6 +435,7 @@ struct ed_plan_h {
     std::string what = tag < ne   ? "chunk " + std::to_string(tag) + " from rank " + std::to_string(rank_of(tag))
                        : tag == ne ? "the run-start barrier (rank " + std::to_string(i) + ")"
                        : tag == ne + 1 ? "rank " + std::to_string(i) + " finishing the run (download)"
+                       : tag == ne + 3 ? "rank " + std::to_string(i) + " finishing the run (new inputs / teardown)"
                                        : "rank 0's download";
     throw ed_error(ED_ERR_CUDA, "peer transport: timed out waiting for " + what);
   }
@@ -440,6 +447,11 @@ struct ed_plan_h {
     return b.main ? int64_t(static_cast<char*>(b.main) - static_cast<char*>(arena)) : -1;
   }
   void destroy();
+  // group plan (prepared on an ed_ctx_create_multi context): one sub-plan per
+  // rank; entry points dispatch to them. peer_inproc: peer pointers are the
+  // sibling sub-plans' own allocations, not IPC mappings.
+  std::vector<ed_plan_h*> subs;
+  bool peer_inproc = false;
 };
 
 namespace edrt {
@@ -448,4 +460,9 @@ size_t dt_size(int dtype);
 DT dt_of(int dtype);
 void ensure_staging(ed_plan_h* h, size_t bytes);
 std::vector<int> io_chunks(const ed_plan_h* h, int w, bool input);
+// peer transport: block the stream until every rank has finished the current
+// run, so this rank's exported chunks may be overwritten or freed
+void wait_peers_idle(ed_plan_h* h, cudaStream_t s);
+// rethrow a nested entry point's status (group plans forward to sub-plans)
+void throw_status(ed_status st, const char* msg);
 }  // namespace edrt

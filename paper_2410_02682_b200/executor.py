@@ -96,6 +96,20 @@ class Context:
         _check(lib.ed_ctx_create(device, rank, world, idbuf, len(nccl_id) if nccl_id else 0, C.byref(h), err, n), err)
         self.h = h
 
+    @classmethod
+    def multi(cls, device_ids) -> "Context":
+        """One process driving len(device_ids) ranks (ed_ctx_create_multi):
+        rank r on device_ids[r]; devices may repeat (ranks then share one)."""
+        self = cls.__new__(cls)
+        lib = library()
+        self.rank, self.world = 0, len(device_ids)
+        ids = (C.c_int32 * len(device_ids))(*device_ids)
+        h = C.c_void_p()
+        err, n = _err()
+        _check(lib.ed_ctx_create_multi(len(device_ids), ids, C.byref(h), err, n), err)
+        self.h = h
+        return self
+
     @staticmethod
     def nccl_unique_id() -> bytes:
         buf = C.create_string_buffer(128)

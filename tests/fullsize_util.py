@@ -114,16 +114,32 @@ def vertex_tensor(pp, plan, w, torch):
     return None
 
 
-def slice_label(v):
-    """The output label a row slice cuts: the largest-extent output label of
-    the first operand (2 of its values leave every vertex of the configs at
-    <= 1.4e8 scalar products for the reference's interpretive eval_expr)."""
+def slice_picks(plan, v, which, budget=3e7):
+    """Which rows of v's output a reference slice evaluates: output labels,
+    largest extent first, are cut to 2 values (at the start for which = 0,
+    5/7 of the way in for which = 1) until the slice's scalar products
+    (output elements x aggregated extent) fit the budget — about a second of
+    the reference's interpretive eval_expr. Returns {label: (start, count)}."""
     e = v.expr
-    best, ext = None, 0
-    for l, n in zip(e.out, v.bound):
-        if l in e.ins[0] and n > ext:
-            best, ext = l, n
-    return best
+    ext = {}
+    for ls, w in zip(e.ins, v.inputs):
+        for l, n in zip(ls, plan.vertices[w].bound):
+            ext[l] = n
+    k = 1
+    for l in e.agg_labels():
+        k *= ext[l]
+    picks = {}
+    size = 1
+    for l in e.out:
+        size *= ext[l]
+    for l in sorted(e.out, key=lambda l: -ext[l]):
+        if size * k <= budget:
+            break
+        n = ext[l]
+        cnt = min(2, n)
+        picks[l] = (0 if which == 0 else (n * 5) // 7 // cnt * cnt, cnt)
+        size = size // n * cnt
+    return picks
 
 
 def _vertex_line(graph_text, name):
@@ -134,27 +150,28 @@ def _vertex_line(graph_text, name):
     raise KeyError(name)
 
 
-def ref_slice(plan, graph_text, v, args, r0, rows, torch):
+def ref_slice(plan, graph_text, v, args, picks, torch):
     """The reference's eval_expr (reference.cc:3-60, through oracle/_ref's
-    edref_eval_vertex) on rows [r0, r0+rows) of v's slice label: a one-vertex
-    graph whose inputs are the given tensors cut to those rows. Returns
-    (reference slice, index tuple of that slice in v's output)."""
+    edref_eval_vertex) on a slice of v (picks: {label: (start, count)}): a
+    one-vertex graph whose inputs are the given tensors cut to those ranges.
+    Returns (reference slice, index tuple of that slice in v's output)."""
     e = v.expr
-    lab = slice_label(v)
     decl, arrs = [], []
-    for ls, w, a in zip(e.ins, v.inputs, args):
-        idx = tuple(slice(r0, r0 + rows) if l == lab else slice(None) for l in ls)
-        t = a[idx]
-        arrs.append(np.ascontiguousarray(t.cpu().numpy(), dtype=np.float64))
-        decl.append(f"input {plan.vertices[w].name}:[{','.join(str(n) for n in t.shape)}]")
     if len(set(v.inputs)) != len(v.inputs):
         raise ValueError("a vertex reading one tensor twice")
+
+    def cut(ls):
+        return tuple(slice(picks[l][0], picks[l][0] + picks[l][1]) if l in picks else slice(None) for l in ls)
+
+    for ls, w, a in zip(e.ins, v.inputs, args):
+        t = a[cut(ls)]
+        arrs.append(np.ascontiguousarray(t.cpu().numpy(), dtype=np.float64))
+        decl.append(f"input {plan.vertices[w].name}:[{','.join(str(n) for n in t.shape)}]")
     text = "\n".join(decl + [_vertex_line(graph_text, v.name), f"output {v.name}"]) + "\n"
-    oshape = [rows if l == lab else n for l, n in zip(e.out, v.bound)]
+    oshape = [picks[l][1] if l in picks else n for l, n in zip(e.out, v.bound)]
     out = np.empty(oshape, dtype=np.float64)
     err = B.C.create_string_buffer(1024)
     vid = len(decl)  # the expression vertex follows its input declarations
     y = arrs[1] if len(arrs) > 1 else None
     B._check(B.ref().edref_eval_vertex(text.encode(), vid, B._ptr(arrs[0]), B._ptr(y), B._ptr(out), err, 1024), err)
-    oidx = tuple(slice(r0, r0 + rows) if l == lab else slice(None) for l in e.out)
-    return torch.from_numpy(out).to(args[0].device), oidx
+    return torch.from_numpy(out).to(args[0].device), cut(e.out)

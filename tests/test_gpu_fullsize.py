@@ -61,11 +61,10 @@ def _exact_values(plan, ins, torch):
 def _ref_slice_agrees(plan, doc, v, args, want, torch, tol=1e-12):
     """The reference's own eval_expr on two sampled row slices of v equals the
     fp64 checker there (exactly on integers; to 1e-12 relative otherwise)."""
-    lab = U.slice_label(v)
-    n = v.bound[v.expr.out.index(lab)]
-    for r0 in (0, (n * 5) // 7):
-        ref, idx = U.ref_slice(plan, doc["graph_text"], v, args, r0, 2, torch)
-        assert U.max_rel_err(want[idx], ref, torch) <= tol, (v.name, r0)
+    for which in (0, 1):
+        picks = U.slice_picks(plan, v, which)
+        ref, idx = U.ref_slice(plan, doc["graph_text"], v, args, picks, torch)
+        assert U.max_rel_err(want[idx], ref, torch) <= tol, (v.name, picks)
 
 
 @pytest.mark.parametrize("name", INTEGER)

@@ -31,17 +31,14 @@ def _has_exp(plan):
     return any(v.expr is not None and v.expr.map == "exp" for v in plan.vertices)
 
 
-# The reference computes exp with the host libm (std::exp, ops.cc:25); the
-# device's exp may differ from it in the last bit, so graphs containing an
-# exp vertex are held to last-bit bounds instead of bit equality.
-EXP_ULP = {"fp64": 1e-14, "fp32": 1e-6}
-
-
+# exp runs the reference's own libm algorithm on the device (csrc/libm_exp.cuh,
+# glibc's __exp_fma restated op for op), so exp-bearing graphs are held to bit
+# equality like every other graph.
 def _assert_matches(got, want, case, vid, prec, plan):
     if np.array_equal(got, want):
         return
     err = B.max_rel_err(got, want)
-    assert _has_exp(plan) and err <= EXP_ULP[prec], f"{case}: vertex {vid} differs (max_rel_err {err:.3e})"
+    raise AssertionError(f"{case}: vertex {vid} differs in {prec} (max_rel_err {err:.3e})")
 
 
 def _run(ctx, plan, ins, prec, **kw):
@@ -167,7 +164,9 @@ def test_reference_flow_with_gpu_executor(gpu_ctx, tmp_path):
     """The reference's own run_end_to_end flow (build_pipeline, generate_inputs,
     chunk) with execute() and the C++ adapter execute_gpu() side by side
     (integration/ed_check.cc): bit-identical outputs in f64 and f32 mode
-    (exp-bearing graphs within last-bit bounds), identical machine counters,
+    (round-robin) and f64 threaded
+    (exp-bearing graphs within last-bit bounds), identical machine counters and
+    wall_steps in both scheduler modes,
     and an audit within the cost-model bounds, over the acceptance matrix."""
     import json
     import os
@@ -181,7 +180,7 @@ def test_reference_flow_with_gpu_executor(gpu_ctx, tmp_path):
         (tmp_path / f"{g}.eg").write_text(doc["graph_text"])
     r = subprocess.run([exe, str(tmp_path)], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
-    assert "72/72 passed" in r.stdout
+    assert "180/180 passed" in r.stdout  # 108 single-rank + 72 with L ranks in one process
 
 
 def _mutated(name, fn):
@@ -253,3 +252,27 @@ def test_gpu_placement_keeps_results(gpu_ctx, case):
         _assert_matches(rep.outputs[vid], a, case, vid, "fp64", plan)
     _, _, cnt, tot = B.oracle_execute(new, ins)
     assert rep.machines == cnt and rep.total_transferred == tot
+
+
+def test_device_exp_is_host_libm_exp(gpu_ctx):
+    """map exp on the device equals the reference's eval_expr (std::exp,
+    ops.cc:24) bit for bit on 4M doubles spanning underflow, the normal range,
+    subnormal results and overflow, in fp64 and fp32 mode."""
+    from conftest import load_doc
+    import fullsize_util as U
+    torch = pytest.importorskip("torch")
+    plan = load_plan("expmap_p1_L1")
+    doc = load_doc("expmap_p1_L1")
+    rng = np.random.default_rng(11)
+    x = np.concatenate([rng.uniform(-750, 720, 2 ** 21), rng.uniform(-40, 40, 2 ** 20), rng.uniform(-1, 1, 2 ** 20)])
+    x[:8] = [0.0, -0.0, 709.782712893384, -708.4, -745.2, 1024.0, np.inf, -np.inf]
+    x = x.reshape(1024, 4096)
+    v = plan.vertices[plan.outputs[0]]
+    want, idx = U.ref_slice(plan, doc["graph_text"], v, [torch.from_numpy(x)], {}, torch)
+    want = want.numpy()
+    got = _run(gpu_ctx, plan, {plan.find("X"): x}, "fp64").outputs[plan.outputs[0]]
+    assert np.array_equal(got, want)
+    x32 = x.astype(np.float32).astype(np.float64)
+    want32, _ = U.ref_slice(plan, doc["graph_text"], v, [torch.from_numpy(x32)], {}, torch)
+    got32 = _run(gpu_ctx, plan, {plan.find("X"): x32}, "fp32").outputs[plan.outputs[0]]
+    assert np.array_equal(got32, want32.numpy().astype(np.float32).astype(np.float64))

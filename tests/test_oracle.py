@@ -8,7 +8,7 @@ import os
 import numpy as np
 import pytest
 
-from conftest import GOLDEN, golden_cases, load_golden, load_plan
+from conftest import GOLDEN, ROOT, golden_cases, load_golden, load_plan
 from oracle import bridge as B
 from paper_2410_02682_b200 import abi
 
@@ -164,3 +164,16 @@ def test_oracle_matches_live_reference_on_pinned_plans():
         oo, _, ocnt, otot = B.oracle_execute(plan, ins)
         assert all(np.array_equal(ro[k], oo[k]) for k in ro)
         assert cnt == ocnt and tot == otot
+
+
+def test_device_exp_restatement_matches_host_libm(tmp_path):
+    """csrc/libm_exp.cuh (the device's map exp) compiled for the host equals
+    the host's std::exp (ops.cc:24) bit for bit on 8M random doubles over
+    every range and on the overflow / underflow / subnormal edges."""
+    import subprocess
+    exe = tmp_path / "exp_check"
+    subprocess.run(["g++", "-O2", "-ffp-contract=off", os.path.join(ROOT, "oracle", "exp_check.cc"), "-o", str(exe)],
+                   check=True)
+    r = subprocess.run([str(exe), "2000000"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout[-2000:]
+    assert r.stdout.strip().endswith("0 / 8000022 differ")
