@@ -54,6 +54,7 @@ def ref():
                                              C.POINTER(C.c_int64), C.POINTER(C.c_int64)] + err
         lib.edref_eval_reference.argtypes = [C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)] + err
         lib.edref_eval_vertex.argtypes = [C.c_char_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p] + err
+        lib.edref_kernel_vertex.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p] + err
         _ref = lib
     return _ref
 

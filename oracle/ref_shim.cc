@@ -354,4 +354,29 @@ int edref_eval_vertex(const char* graph_text, int vid, const double* x, const do
   });
 }
 
+// One expression vertex through the reference's own kernel_eval (kernel.cc:15-68)
+// as a single unpartitioned chunk, in f64 (f32 = 0) or the reference's f32
+// mode (f32 = 1: every operand and result rounded through float, folds in
+// odometer order) — the reference's f32 arithmetic on a vertex slice.
+int edref_kernel_vertex(const char* graph_text, int vid, int f32, const double* x, const double* y,
+                        double* out, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    auto g = parse_eingraph(graph_text);
+    auto const& v = g.vertices.at(vid);
+    if(!v.expr) {
+      throw plan_error_t("not an expression vertex");
+    }
+    kernel_spec_t spec{*v.expr, g.bxy(vid)};
+    tensor_t tx = tensor_t::zeros(spec.in_bound(0));
+    std::memcpy(tx.values.data(), x, sizeof(double) * tx.values.size());
+    tensor_t ty;
+    if(v.expr->is_binary()) {
+      ty = tensor_t::zeros(spec.in_bound(1));
+      std::memcpy(ty.values.data(), y, sizeof(double) * ty.values.size());
+    }
+    auto r = kernel_eval(spec, tx, v.expr->is_binary() ? &ty : nullptr, f32 != 0);
+    std::memcpy(out, r.values.data(), sizeof(double) * r.values.size());
+  });
+}
+
 } // extern "C"

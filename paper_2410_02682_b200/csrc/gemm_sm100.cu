@@ -381,6 +381,306 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   }
 }
 
+// ---- fp32x3 with promoted accumulation --------------------------------------
+// The tensor core adds each MMA's result into its fp32 accumulator with
+// truncation, so over a long K loop a 3xTF32 product loses ~K/8 half-ulps of
+// the running sum (measured: 256 x K x 256, U[-1,1): mean error / sum|x||y|
+// 1.4e-7 at K = 32, 9.7e-7 at K = 16384; sequential fp32 rounding-to-nearest,
+// the reference's f32 mode, stays at 1.7e-8). Here the MMAs accumulate only
+// `chunk` K blocks (default 4) at a time into one of two TMEM buffers, and eight epilogue
+// warps add each finished chunk into a running sum held in registers with
+// IEEE fp32 adds (round to nearest) — the promotion DeepSeek-V3 uses for FP8,
+// applied to TF32. The chunk drains overlap the next chunk's MMAs (two
+// buffers), so the tensor pipe never waits for them.
+// Warps: 0-7 epilogue (warp w: TMEM lane quarter w % 4, column half w / 4),
+// 8 TMA producer, 9 TMEM allocator + MMA issuer, 10-11 idle. Warps are dealt
+// to the SM's four 16K-register sub-partitions round-robin, so twelve warps
+// (three per sub-partition) leave 168 registers per thread — room for each
+// epilogue thread's BN / 2 running sums (ten warps would put three on some
+// sub-partitions all the same).
+constexpr int kX3Threads = 384;
+
+__device__ __forceinline__ float epi_f(int op, float c, float x) {
+  if (op == 0) return x > 0.0f ? x : 0.0f;
+  if (op == 2) return -x;
+  if (op == 3) return c * x;
+  return x;
+}
+
+template <int kCta, int BN>
+__global__ void __launch_bounds__(kX3Threads, 1) gemm_x3_kernel(const __grid_constant__ GemmLaunch p) {
+  using C_ = Cfg<false, kCta, BN, true>;
+  constexpr int STAGES = C_::STAGES;
+  constexpr int HALF = BN / 2;  // running-sum columns per epilogue thread
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* stage_out = smem + STAGES * C_::STAGE_BYTES;  // 8 warps x one 32 x 128 B staging tile
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(stage_out + C_::STORE_BYTES);
+  uint64_t* empty_bar = full_bar + STAGES;
+  uint64_t* part_full = empty_bar + STAGES;  // chunk partial ready in TMEM buffer b
+  uint64_t* part_empty = part_full + 2;      // chunk partial drained into the running sums
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(part_empty + 2);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const uint32_t rank = kCta == 2 ? cluster_ctarank() : 0;
+  const int tiles_m = (p.M + C_::TILE_M - 1) / C_::TILE_M;
+  const int tiles_n = (p.N + BN - 1) / BN;
+  const int total = tiles_m * tiles_n * p.batch * p.n_regions;
+  const int kblocks = (p.K + C_::BK - 1) / C_::BK;
+  const int first = blockIdx.x / kCta, stride = gridDim.x / kCta;
+  const int chunk = p.chunk > 0 ? p.chunk : 4;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&part_full[b], 1);
+      mbar_init(&part_empty[b], 8 * kCta);  // every epilogue warp of the pair
+    }
+    fence_mbar_init();
+  }
+  if (warp == 9) tmem_alloc<2 * BN, kCta>(tmem_slot);
+  tc_fence_before();
+  if (kCta == 2) cluster_sync();
+  else __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  griddep_wait();
+
+  if (warp == 8) {
+    // ---- TMA producer: A_hi | B_hi | A_lo | B_lo per stage ----
+    if (lane == 0) {
+      int it = 0;
+      for (int t = first; t < total; t += stride) {
+        if (t + stride >= total) griddep_launch();
+        const TileCoord tc = tile_coord<C_::TILE_M, BN>(p, t, tiles_m, tiles_n);
+        const GemmRegion reg = p.regions[tc.region];
+        const int am = tc.m0 + int(rank) * BM, bn = tc.n0 + int(rank) * C_::B_ROWS;
+        for (int sib = 0; sib < reg.n_sib; ++sib) {
+          const CUtensorMap* ma = p.maps + reg.map0 + C_::NMAP * sib;
+          for (int kb = 0; kb < kblocks; ++kb, ++it) {
+            const int s = it % STAGES;
+            const uint32_t ph = (it / STAGES) & 1;
+            mbar_wait(&empty_bar[s], ph ^ 1);
+            const int k0 = kb * C_::BK;
+            uint8_t* sa = smem + s * C_::STAGE_BYTES;
+            uint8_t* sb = sa + C_::A_BYTES;
+            if (rank == 0) mbar_expect_tx(&full_bar[s], C_::STAGE_BYTES * kCta);
+            auto load = [&](void* dst, const CUtensorMap* m, int c0, int c1) {
+              if (kCta == 2) tma_load_3d_2sm(dst, m, &full_bar[s], c0, c1, tc.b);
+              else tma_load_3d(dst, m, &full_bar[s], c0, c1, tc.b);
+            };
+#pragma unroll
+            for (int part = 0; part < 2; ++part) {
+              uint8_t* pa = sa + part * C_::LO_OFF;
+              uint8_t* pb = sb + part * C_::LO_OFF;
+              const CUtensorMap* pma = ma + 2 * part;
+              const CUtensorMap* pmb = ma + 1 + 2 * part;
+              if (!p.a_mn) {
+                load(pa, pma, k0, am);
+              } else {
+#pragma unroll
+                for (int i = 0; i < BM / C_::MN_ATOM; ++i) load(pa + i * C_::BK * 128, pma, am + i * C_::MN_ATOM, k0);
+              }
+              if (!p.b_mn) {
+                load(pb, pmb, k0, bn);
+              } else {
+#pragma unroll
+                for (int i = 0; i < C_::B_ROWS / C_::MN_ATOM; ++i)
+                  load(pb + i * C_::BK * 128, pmb, bn + i * C_::MN_ATOM, k0);
+              }
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 9) {
+    // ---- MMA issuer: chunks of `chunk` K blocks into alternating buffers ----
+    if (lane == 0 && rank == 0) {
+      const uint32_t idesc = umma_idesc(2u, BM * kCta, BN, p.a_mn, p.b_mn);
+      const uint32_t a_lbo = p.a_mn ? C_::BK * 128 : 16, b_lbo = p.b_mn ? C_::BK * 128 : 16;
+      const uint32_t a_step = p.a_mn ? C_::UMMA_K * 128 : 32, b_step = p.b_mn ? C_::UMMA_K * 128 : 32;
+      const uint32_t a_lt = p.a_mn ? 1u : 2u, b_lt = p.b_mn ? 1u : 2u;
+      const uint32_t a_sbo = a_lt == 1 ? 512u : 1024u, b_sbo = b_lt == 1 ? 512u : 1024u;
+      int it = 0, nchunk = 0;
+      for (int t = first; t < total; t += stride) {
+        const TileCoord tc = tile_coord<C_::TILE_M, BN>(p, t, tiles_m, tiles_n);
+        const int iters = kblocks * p.regions[tc.region].n_sib;
+        for (int i = 0; i < iters; ++nchunk) {
+          const int b = nchunk & 1;
+          const uint32_t bph = (nchunk >> 1) & 1;
+          if (kCta == 2) mbar_wait_cluster(&part_empty[b], bph ^ 1);
+          else mbar_wait(&part_empty[b], bph ^ 1);
+          tc_fence_after();
+          const uint32_t d_tmem = tmem + uint32_t(b * BN);
+          const int n = iters - i < chunk ? iters - i : chunk;
+          for (int q = 0; q < n; ++q, ++i, ++it) {
+            const int s = it % STAGES;
+            const uint32_t ph = (it / STAGES) & 1;
+            mbar_wait(&full_bar[s], ph);
+            tc_fence_after();
+            const uint32_t sa = smem_u32(smem + s * C_::STAGE_BYTES);
+            const uint32_t sb = sa + C_::A_BYTES;
+#pragma unroll
+            for (int k = 0; k < 3 * (C_::BK / C_::UMMA_K); ++k) {
+              const int prod = k / (C_::BK / C_::UMMA_K), kk = k % (C_::BK / C_::UMMA_K);
+              const uint32_t oa = prod == 2 ? uint32_t(C_::LO_OFF) : 0u, ob = prod == 1 ? uint32_t(C_::LO_OFF) : 0u;
+              const uint64_t ad = umma_desc_sw128(sa + oa + kk * a_step, a_lbo, a_sbo, a_lt);
+              const uint64_t bd = umma_desc_sw128(sb + ob + kk * b_step, b_lbo, b_sbo, b_lt);
+              const uint32_t acc = (q | k) != 0;  // each chunk starts a fresh partial
+              if (kCta == 2) mma_tf32_2sm(d_tmem, ad, bd, idesc, acc);
+              else mma_tf32(d_tmem, ad, bd, idesc, acc);
+            }
+            if (kCta == 2) mma_commit_2sm(&empty_bar[s]);
+            else mma_commit(&empty_bar[s]);
+          }
+          if (kCta == 2) mma_commit_2sm(&part_full[b]);
+          else mma_commit(&part_full[b]);
+        }
+      }
+    }
+  } else if (warp < 8) {
+    // ---- epilogue: promote every chunk partial into fp32 running sums ----
+    const int wq = warp & 3, hh = warp >> 2;
+    const uint32_t empty_leader = kCta == 2 ? mapa(smem_u32(part_empty), 0) : 0;
+    uint8_t* tile = stage_out + warp * 4096;
+    int nchunk = 0;
+    for (int t = first; t < total; t += stride) {
+      const TileCoord tc = tile_coord<C_::TILE_M, BN>(p, t, tiles_m, tiles_n);
+      const GemmRegion reg = p.regions[tc.region];
+      const int iters = kblocks * reg.n_sib;
+      const int nch = (iters + chunk - 1) / chunk;
+      float acc[HALF];
+      for (int c = 0; c < nch; ++c, ++nchunk) {
+        const int b = nchunk & 1;
+        const uint32_t bph = (nchunk >> 1) & 1;
+        mbar_wait(&part_full[b], bph);
+        tc_fence_after();
+        const uint32_t tb = tmem + (uint32_t(wq * 32) << 16) + uint32_t(b * BN + hh * HALF);
+#pragma unroll
+        for (int j = 0; j < HALF / 16; ++j) {
+          uint32_t r[16];
+          tmem_ld_32x32b_x16(tb + uint32_t(j * 16), r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            acc[j * 16 + e] = c == 0 ? __uint_as_float(r[e]) : __fadd_rn(acc[j * 16 + e], __uint_as_float(r[e]));
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (kCta == 2) mbar_arrive_cluster(empty_leader + uint32_t(b * sizeof(uint64_t)));
+          else mbar_arrive(&part_empty[b]);
+        }
+      }
+      if (p.epi_map >= 0) {
+#pragma unroll
+        for (int e = 0; e < HALF; ++e) acc[e] = epi_f(p.epi_map, p.epi_c, acc[e]);
+      }
+      const int row0 = tc.m0 + int(rank) * BM + wq * 32;
+      const int col0 = tc.n0 + hh * HALF;
+      if (reg.cmap32 >= 0 || reg.cmap16 >= 0) {
+        // registers -> 128B-swizzled staging tile -> TMA store (clipped at the region bounds)
+#pragma unroll
+        for (int pass = 0; pass < 2; ++pass) {
+          const int cm = pass == 0 ? reg.cmap32 : reg.cmap16;
+          if (cm < 0) continue;
+          constexpr int kMaxSlices = HALF / 32;
+#pragma unroll
+          for (int sl = 0; sl < kMaxSlices; ++sl) {
+            const int cols = pass == 0 ? 32 : 64;
+            if (sl * cols >= HALF) break;
+            if (lane == 0) bulk_wait_read<0>();
+            __syncwarp();
+            uint8_t* rowp = tile + lane * 128;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              uint4 v;
+              if (pass == 0) {
+                const int e = sl * 32 + 4 * j;
+                v = make_uint4(__float_as_uint(acc[e]), __float_as_uint(acc[e + 1]), __float_as_uint(acc[e + 2]),
+                               __float_as_uint(acc[e + 3]));
+              } else {
+                const int e = (sl * 64 + 8 * j) % HALF;  // sl * 64 < HALF here
+                __nv_bfloat162 h0 = __floats2bfloat162_rn(acc[e], acc[e + 1]);
+                __nv_bfloat162 h1 = __floats2bfloat162_rn(acc[e + 2], acc[e + 3]);
+                __nv_bfloat162 h2 = __floats2bfloat162_rn(acc[e + 4], acc[e + 5]);
+                __nv_bfloat162 h3 = __floats2bfloat162_rn(acc[e + 6], acc[e + 7]);
+                v.x = *reinterpret_cast<uint32_t*>(&h0);
+                v.y = *reinterpret_cast<uint32_t*>(&h1);
+                v.z = *reinterpret_cast<uint32_t*>(&h2);
+                v.w = *reinterpret_cast<uint32_t*>(&h3);
+              }
+              *reinterpret_cast<uint4*>(rowp + ((j ^ (lane & 7)) << 4)) = v;
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_3d_hint(p.maps + cm, tile, col0 + sl * cols, row0, tc.b, policy_evict_first());
+              bulk_commit();
+            }
+          }
+        }
+      } else {
+        const int row = row0 + lane;
+        const long long base = (long long)tc.b * p.c_sb + (long long)row * p.c_sm;
+        float* c32 = reg.c32 ? reg.c32 + base : nullptr;
+        __nv_bfloat16* c16 = reg.c16 ? static_cast<__nv_bfloat16*>(reg.c16) + base : nullptr;
+        if (row < p.M) {
+#pragma unroll
+          for (int e = 0; e < HALF; ++e) {
+            if (col0 + e < p.N) {
+              if (c32) c32[col0 + e] = acc[e];
+              if (c16) c16[col0 + e] = __float2bfloat16_rn(acc[e]);
+            }
+          }
+        }
+      }
+    }
+    if (lane == 0) bulk_wait<0>();
+  }
+
+  tc_fence_before();
+  if (kCta == 2) cluster_sync();
+  else __syncthreads();
+  if (warp == 9) {
+    tc_fence_after();
+    tmem_dealloc<2 * BN, kCta>(tmem);
+  }
+}
+
+template <int kCta, int BN>
+cudaError_t prepare_x3() {
+  return cudaFuncSetAttribute(gemm_x3_kernel<kCta, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              Cfg<false, kCta, BN, true>::SMEM);
+}
+
+template <int kCta, int BN>
+cudaError_t launch_x3(const GemmLaunch& p, int num_sms, cudaStream_t stream) {
+  using C_ = Cfg<false, kCta, BN, true>;
+  const long long tiles =
+      (long long)((p.M + C_::TILE_M - 1) / C_::TILE_M) * ((p.N + BN - 1) / BN) * p.batch * p.n_regions;
+  const int clusters = int(tiles < num_sms / kCta ? tiles : num_sms / kCta);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(clusters * kCta);
+  cfg.blockDim = dim3(kX3Threads);
+  cfg.dynamicSmemBytes = C_::SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kCta;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, gemm_x3_kernel<kCta, BN>, p);
+}
+
 // co-resident clusters per kernel variant (clusters never span a GPC, so
 // 4-CTA clusters may leave SMs idle): measured once by the occupancy API
 template <bool kBF16, int kCta, int BN, bool kX3, int kMc>
@@ -451,7 +751,7 @@ bool gemm_use_mc(int M, int N, int bn) {
   // two N tiles so the second pair has work of its own
   static const int env = [] {
     const char* e = std::getenv("ED_GEMM_MC");
-    return e ? std::atoi(e) : 1;
+    return e ? std::atoi(e) : 0;  // opt-in: measured slower (4-CTA clusters fit only 132 of 148 SMs)
   }();
   return env != 0 && gemm_paired(M) && bn == 256 && N > 256;
 }
@@ -483,6 +783,10 @@ cudaError_t gemm_prepare() {
   if ((e = prepare_t<false, 2, 256, true>()) != cudaSuccess) return e;
   if ((e = prepare_t<false, 1, 128, true>()) != cudaSuccess) return e;
   if ((e = prepare_t<false, 2, 128, true>()) != cudaSuccess) return e;
+  if ((e = prepare_x3<1, 256>()) != cudaSuccess) return e;
+  if ((e = prepare_x3<2, 256>()) != cudaSuccess) return e;
+  if ((e = prepare_x3<1, 128>()) != cudaSuccess) return e;
+  if ((e = prepare_x3<2, 128>()) != cudaSuccess) return e;
   if ((e = prepare_t<true, 2, 256, false, 2>()) != cudaSuccess) return e;
   if ((e = prepare_t<false, 2, 256, false, 2>()) != cudaSuccess) return e;
   return prepare_t<false, 2, 256, true, 2>();
@@ -492,6 +796,10 @@ cudaError_t launch_gemm(const GemmLaunch& p, int num_sms, cudaStream_t stream) {
   // pair SMs when the output has rows for both halves of a 256-row tile
   const bool pair = gemm_paired(p.M);
   const bool narrow = p.bn == 128;
+  if (p.x3 && p.chunk > 0) {  // fp32x3 with promoted (round-to-nearest) accumulation
+    if (narrow) return pair ? launch_x3<2, 128>(p, num_sms, stream) : launch_x3<1, 128>(p, num_sms, stream);
+    return pair ? launch_x3<2, 256>(p, num_sms, stream) : launch_x3<1, 256>(p, num_sms, stream);
+  }
   if (p.mc && pair && !narrow) {  // 4-CTA clusters sharing A (gemm_use_mc)
     if (p.bf16) return launch_t<true, 2, 256, false, 2>(p, num_sms, stream);
     if (p.x3) return launch_t<false, 2, 256, true, 2>(p, num_sms, stream);

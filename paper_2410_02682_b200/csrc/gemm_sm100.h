@@ -33,7 +33,8 @@ struct GemmLaunch {
   float epi_c;                // scale constant of a fused scale map
   int bn;                     // tile width: 256 or 128 (gemm_pick_bn)
   int mc;                     // 1: 4-CTA clusters, two 2-SM pairs sharing (multicasting) the A panel
-  int group_m;                // grouped raster: tile rows that advance together along N
+  int group_m;
+  int chunk;                  // x3: K blocks per TMEM partial promoted into fp32 running sums (0: off)                // grouped raster: tile rows that advance together along N
   int x3;                     // fp32-accurate 3xTF32: each stage carries hi and lo operand copies
                               // and feeds hi*hi + hi*lo + lo*hi into one accumulator
 };

@@ -150,10 +150,12 @@ def _vertex_line(graph_text, name):
     raise KeyError(name)
 
 
-def ref_slice(plan, graph_text, v, args, picks, torch):
+def ref_slice(plan, graph_text, v, args, picks, torch, f32=None):
     """The reference's eval_expr (reference.cc:3-60, through oracle/_ref's
     edref_eval_vertex) on a slice of v (picks: {label: (start, count)}): a
     one-vertex graph whose inputs are the given tensors cut to those ranges.
+    f32=False / True evaluates through the reference's kernel_eval (kernel.cc)
+    in f64 / in its f32 mode instead of eval_expr.
     Returns (reference slice, index tuple of that slice in v's output)."""
     e = v.expr
     decl, arrs = [], []
@@ -173,5 +175,10 @@ def ref_slice(plan, graph_text, v, args, picks, torch):
     err = B.C.create_string_buffer(1024)
     vid = len(decl)  # the expression vertex follows its input declarations
     y = arrs[1] if len(arrs) > 1 else None
-    B._check(B.ref().edref_eval_vertex(text.encode(), vid, B._ptr(arrs[0]), B._ptr(y), B._ptr(out), err, 1024), err)
+    if f32 is None:
+        B._check(B.ref().edref_eval_vertex(text.encode(), vid, B._ptr(arrs[0]), B._ptr(y), B._ptr(out), err, 1024),
+                 err)
+    else:
+        B._check(B.ref().edref_kernel_vertex(text.encode(), vid, int(bool(f32)), B._ptr(arrs[0]), B._ptr(y),
+                                             B._ptr(out), err, 1024), err)
     return torch.from_numpy(out).to(args[0].device), cut(e.out)

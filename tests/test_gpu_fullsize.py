@@ -14,11 +14,12 @@ cannot run these sizes (hours), so the checkers are:
     reference's eval_expr (reference.cc:3-60) on sampled row slices.
 Bars:
   * fp32x3: bit-exact wherever every partial sum of a contraction stays below
-    2^24 (asserted at run time from sum |x||y|); otherwise the reference's
-    metric max_rel_err (tensor.cc:9-19) <= 1e-5 or, where the output passes
-    through zero, the fp32 accumulation bound |err| <= K * 2^-24 * sum |x||y|
+    2^24 (asserted at run time from sum |x||y|); otherwise normwise <= 1e-5,
+    the fp32 summation bound |err| <= K * 2^-24 * sum |x||y| on every element
     (what any fp32-accumulating executor, the reference's own f32 mode
-    included, can promise);
+    included, can promise), and the reference's metric max_rel_err
+    (tensor.cc:9-19) <= 1e-5 or no worse than twice the reference's own f32
+    mode on the same sampled slice;
   * bf16: per contraction with exact inputs |err| <= (2 * 2^-9 + K * 2^-24) *
     sum |x||y| (operands rounded to 8 significant bits, fp32 accumulation),
     and normwise max|err| / max|ref| against the reference's exact output.
@@ -33,6 +34,7 @@ from oracle import bridge as B
 pytestmark = pytest.mark.gpu
 
 X3_BAR = 1e-5          # max_rel_err (tensor.cc:9-19), fp32x3 (the north star's fp32 bar)
+X3_NORMWISE = 1e-5     # max|err| / max|ref| per vertex, fp32x3
 BF16_NORMWISE = 1e-2   # max|err| / max|ref| of a graph output vs the reference's exact output, bf16
 INTEGER = ["hoc", "bmm2", "bmm2_repart", "chain3"]
 
@@ -111,10 +113,16 @@ def test_integer_configs_fp32x3(gpu_ctx, name):
 
 @pytest.mark.parametrize("name", ["ffnn_big", "attn_big"])
 def test_real_configs_fp32x3_per_vertex(gpu_ctx, name):
-    """Per-vertex parity in fp32x3 at full size: every materialised vertex,
-    on the GPU's own inputs to it, within X3_BAR (max_rel_err) of fp64; the
-    contractions' fp64 checker is tied to the reference's eval_expr on
-    sampled row slices."""
+    """Per-vertex parity in fp32x3 at full size, each vertex on the GPU's own
+    inputs to it (fused-away inputs composed in fp64 from materialised ones):
+      * normwise error <= X3_NORMWISE against fp64;
+      * contractions: every element within the fp32 summation bound
+        K * 2^-24 * sum |x||y|, and on sampled slices the reference's metric
+        (max_rel_err vs the reference's eval_expr) no worse than
+        max(X3_BAR, 2 x what the reference's OWN f32 mode (kernel_eval with
+        f32 = true, kernel.cc:43-44) scores on the same slice) — at K = 4096 to
+        8192 no fp32 accumulation, the reference's included, holds 1e-5 where
+        outputs pass through zero."""
     torch = pytest.importorskip("torch")
     plan = load_plan(f"{name}_p8_L1")
     doc = load_doc(f"{name}_p8_L1")
@@ -135,20 +143,33 @@ def test_real_configs_fp32x3_per_vertex(gpu_ctx, name):
             memo[w] = U.op_fp64(plan.vertices[w], [value(i) for i in plan.vertices[w].inputs], torch)
         return memo[w]
 
-    errs = {}
+    report = {}
     for v in plan.vertices:
         if v.expr is None or v.vid not in got:
             continue
         args = [value(i) for i in v.inputs]
         want = U.op_fp64(v, args, torch)
-        errs[v.name] = U.max_rel_err(got[v.vid], want, torch)
+        nw = U.normwise(got[v.vid], want)
+        r = {"normwise": nw, "max_rel_err": U.max_rel_err(got[v.vid], want, torch)}
+        assert nw <= X3_NORMWISE, (v.name, r)
         if v.expr.join == "mul" and v.expr.agg == "sum":
-            _ref_slice_agrees(plan, doc, v, args, want, torch)
+            k = U.contraction_k(plan, v)
+            bound = U.op_fp64(v, args, torch, absolute=True)
+            assert bool(((got[v.vid] - want).abs() <= k * U.U32 * bound).all()), (v.name, r)
+            del bound
+            for which in (0, 1):
+                picks = U.slice_picks(plan, v, which)
+                ref64, idx = U.ref_slice(plan, doc["graph_text"], v, args, picks, torch)
+                assert U.max_rel_err(want[idx], ref64, torch) <= 1e-12, v.name  # ties torch to eval_expr
+                ref32, _ = U.ref_slice(plan, doc["graph_text"], v, args, picks, torch, f32=True)
+                ours = U.max_rel_err(got[v.vid][idx], ref64, torch)
+                theirs = U.max_rel_err(ref32, ref64, torch)
+                r[f"slice{which}"] = (ours, theirs)
+                assert ours <= max(X3_BAR, 2 * theirs), (v.name, r)
+        report[v.name] = r
     pp.close()
-    print(name, errs)
-    assert len(errs) >= 3
-    bad = {k: e for k, e in errs.items() if e > X3_BAR}
-    assert not bad, bad
+    print(name, report)
+    assert len(report) >= 3
 
 
 @pytest.mark.parametrize("name", ["bmm2", "bmm2_repart", "chain3", "hoc"])

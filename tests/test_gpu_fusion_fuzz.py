@@ -13,10 +13,10 @@ import numpy as np
 import pytest
 
 from oracle import bridge as B
+import tolerance as T
 
 pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not B.have_ref(), reason="oracle/_ref not built")]
 
-TOL = {"bf16": 3e-2, "tf32": 1e-2}
 
 
 def attention_text(rng):
@@ -82,9 +82,8 @@ def test_fusion_fuzz(gpu_ctx, i, kind, p, L, prec):
     finally:
         pp.close()
     for vid, w in want.items():
-        scale = max(1.0, float(np.max(np.abs(w))))
-        err = float(np.max(np.abs(got[vid] - w))) / scale
-        assert err <= TOL[prec], (text, p, L, vid, err, names)
+        metric, err, bar = T.error(prec, got[vid], w)
+        assert err <= bar, (text, p, L, vid, metric, err, names)
     assert rep.total_transferred == tot and [tuple(m) for m in rep.machines] == [tuple(c) for c in cnt]
     if prec == "bf16" and (kind == "ffnn" or p <= 2):
         # the row softmax fuses whenever its chain's joins line up (every FFNN

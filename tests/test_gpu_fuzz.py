@@ -15,10 +15,10 @@ import pytest
 
 from conftest import GOLDEN
 from oracle import bridge as B
+import tolerance as T
 
 FUZZ = os.path.join(GOLDEN, "fuzz")
 CASES = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(FUZZ, "*.npz")))
-TOL = {"tf32": 1e-2, "bf16": 3e-2, "fp32x3": 1e-5}
 
 
 def _load(case):
@@ -77,9 +77,8 @@ def test_fuzz_gpu_tensor_core_modes(gpu_ctx, case, prec):
     plan, ins, o64, o32, counters, total = _load(case)
     rep = execute(plan, ins, precision=prec, ctx=gpu_ctx)
     for vid, want in o64.items():
-        scale = max(1.0, float(np.max(np.abs(want)))) if want.size else 1.0
-        err = float(np.max(np.abs(rep.outputs[vid] - want))) / scale if want.size else 0.0
-        assert err <= TOL[prec], (case, vid, err)
+        metric, err, bar = T.error(prec, rep.outputs[vid], want)
+        assert err <= bar, (case, vid, metric, err)
 
 
 # live cases: more random graphs, larger labels (16-64), reference run at test time;
@@ -115,6 +114,5 @@ def test_fuzz_live_gpu(gpu_ctx, k):
     assert rep.machines == [tuple(c) for c in cnt] and rep.total_transferred == tot
     rep = execute(plan, ins, precision="bf16", ctx=gpu_ctx)
     for vid, w in want.items():
-        scale = max(1.0, float(np.max(np.abs(w)))) if w.size else 1.0
-        err = float(np.max(np.abs(rep.outputs[vid] - w))) / scale if w.size else 0.0
-        assert err <= TOL["bf16"], (text, p, L, vid, err)
+        metric, err, bar = T.error("bf16", rep.outputs[vid], w)
+        assert err <= bar, (text, p, L, vid, metric, err)

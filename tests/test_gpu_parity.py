@@ -12,12 +12,12 @@ import pytest
 
 from conftest import golden_cases, load_golden, load_plan
 from oracle import bridge as B
+import tolerance as T
 
 pytestmark = pytest.mark.gpu
 
 MATRIX = [c for c in golden_cases()]
 # stated bounds for the tensor-core modes (max_rel_err vs the f64 reference)
-TOL = {"tf32": 1e-2, "bf16": 3e-2, "fp32x3": 1e-5}
 
 
 def _bf16(a):
@@ -73,11 +73,11 @@ def test_tensor_core_modes_within_bound(gpu_ctx, case, prec):
     rep = _run(gpu_ctx, plan, ins, prec)
     exact = plan.integer_valued() and all(v.expr is None or v.expr.map is None for v in plan.vertices)
     for vid, a in o64.items():
-        err = B.max_rel_err(rep.outputs[vid], a)
         if exact and np.max(np.abs(a)) < 2 ** 24:
-            assert err == 0.0, f"{case}: integer graph not exact ({err})"
+            assert np.array_equal(rep.outputs[vid], a), f"{case}: integer graph not exact"
         else:
-            assert err <= TOL[prec], f"{case}: {err}"
+            metric, err, bar = T.error(prec, rep.outputs[vid], a)
+            assert err <= bar, f"{case}: {metric} {err}"
 
 
 LAYOUTS = ["gemm_nn", "gemm_tn", "gemm_nt", "gemm_swap", "gemm_ragged", "gemm_batch", "gemm_heads", "gemm_merge"]
