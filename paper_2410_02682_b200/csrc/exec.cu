@@ -3,10 +3,18 @@
 // captured once into a CUDA graph (record) and replayed by ed_run.
 #include "runtime.h"
 
-void ed_plan_h::launch_op(size_t i, cudaStream_t s) {
+void ed_plan_h::launch_op(size_t i, cudaStream_t s, bool branch) {
   Op& op = ops[i];
   switch (op.kind) {
-    case OpKind::GEMM: CUDA_OK(launch_gemm(op.gemm, ctx->num_sms, s)); break;
+    case OpKind::GEMM:
+      if (branch && op.gemm.sync) {  // a parallel branch shares the SMs: no producer lockstep
+        GemmLaunch g = op.gemm;
+        g.sync = nullptr;
+        CUDA_OK(launch_gemm(g, ctx->num_sms, s));
+      } else {
+        CUDA_OK(launch_gemm(op.gemm, ctx->num_sms, s));
+      }
+      break;
     case OpKind::GENERIC: CUDA_OK(launch_generic(op.gen, f64, s)); break;
     case OpKind::REFINE:
       if (!op.groups.empty()) CUDA_OK(launch_rect(op.rect, int(op.groups.size()), op.max_rows, f64, s));
@@ -98,11 +106,11 @@ void ed_plan_h::enqueue(cudaStream_t s) {
           a = aux[k - i - 1];
         }
         CUDA_OK(cudaStreamWaitEvent(a, fork, 0));
-        launch_op(k, a);
+        launch_op(k, a, true);
         joins.push_back(next_event());
         CUDA_OK(cudaEventRecord(joins.back(), a));
       }
-      launch_op(i, s);
+      launch_op(i, s, true);
       for (cudaEvent_t e : joins) CUDA_OK(cudaStreamWaitEvent(s, e, 0));
       i = g;
       continue;
@@ -196,6 +204,7 @@ void ed_plan_h::destroy() {
   if (d_attn) cudaFree(d_attn);
   if (d_rowsegs) cudaFree(d_rowsegs);
   if (d_regions) cudaFree(d_regions);
+  if (d_sync) cudaFree(d_sync);
   if (d_ptrs) cudaFree(d_ptrs);
   if (d_err) cudaFree(d_err);
   if (staging) cudaFree(staging);

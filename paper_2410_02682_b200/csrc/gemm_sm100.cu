@@ -104,6 +104,45 @@ __device__ __forceinline__ void epi32(const GemmLaunch& p, uint32_t* r) {
   }
 }
 
+// Loose lockstep of the TMA producers (GemmLaunch::sync): before issuing its
+// K block k, a CTA announces the epoch it finished (sync_g K blocks each) and
+// waits until every CTA of the grid has issued epoch e - sync_lag, so the
+// grid's CTAs stay within ~sync_lag epochs of each other along K and the A /
+// B panels one wave shares are still in L2 when the slower CTAs read them
+// (hoc fp32x3: DRAM reads 89 -> 37 GB per launch). A wait that exceeds 200 us
+// (CTAs not co-resident, e.g. other kernels on the SMs) switches the wait
+// off for the rest of the launch: a hint, never a hang.
+__device__ __forceinline__ void producer_lockstep(const GemmLaunch& p, int k, bool& on) {
+  if (k % p.sync_g) return;
+  const int e = k / p.sync_g;
+  if (e > 0) atomicAdd(&p.sync[e - 1], 1u);  // this CTA has issued epoch e - 1
+  if (!on || e < p.sync_lag) return;
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    unsigned int v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.sync + (e - p.sync_lag)) : "memory");
+    if (v >= gridDim.x) return;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 200000ull) {
+      on = false;
+      return;
+    }
+    __nanosleep(64);
+  }
+}
+
+// After the producer's last load: epochs this CTA never issues count as
+// issued; the last CTA out re-zeroes the counters for the op's next launch.
+__device__ __forceinline__ void producer_lockstep_exit(const GemmLaunch& p, int issued) {
+  for (int e = (issued + p.sync_g - 1) / p.sync_g - 1; e < p.sync_epochs; ++e)
+    if (e >= 0) atomicAdd(&p.sync[e], 1u);
+  if (atomicAdd(&p.sync[p.sync_epochs], 1u) == gridDim.x - 1) {
+    __threadfence();
+    for (int e = 0; e <= p.sync_epochs; ++e) atomicExch(&p.sync[e], 0u);
+  }
+}
+
 // kMc = 2: two 2-SM pairs form one 4-CTA cluster over a 256 x 2BN tile; they
 // share the A panel, each pair loading half of every A box and multicasting it
 // to both pairs, so each A byte leaves L2 once per cluster instead of twice.
@@ -163,6 +202,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     // ---- TMA producer (both CTAs of a pair load their halves) ----
     if (lane == 0) {
       int it = 0;
+      bool sync_on = p.sync != nullptr;
       for (int t = first; t < total; t += stride) {
         if (t + stride >= total) griddep_launch();  // last tile: the next kernel may launch
         const TileCoord tc = coord(t);
@@ -174,6 +214,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           const CUtensorMap* ma = p.maps + reg.map0 + C_::NMAP * sib;
           const CUtensorMap* mb = ma + 1;
           for (int kb = 0; kb < kblocks; ++kb, ++it) {
+            if (p.sync) producer_lockstep(p, it, sync_on);
             const int s = it % STAGES;
             const uint32_t ph = (it / STAGES) & 1;
             mbar_wait(&empty_bar[s], ph ^ 1);
@@ -221,6 +262,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           }
         }
       }
+      if (p.sync) producer_lockstep_exit(p, it);
     }
   } else if (warp == 1) {
     // ---- MMA issuer (one thread of the leader CTA) ----
@@ -454,6 +496,7 @@ __global__ void __launch_bounds__(kX3Threads, 1) gemm_x3_kernel(const __grid_con
     // ---- TMA producer: A_hi | B_hi | A_lo | B_lo per stage ----
     if (lane == 0) {
       int it = 0;
+      bool sync_on = p.sync != nullptr;
       for (int t = first; t < total; t += stride) {
         if (t + stride >= total) griddep_launch();
         const TileCoord tc = tile_coord<C_::TILE_M, BN>(p, t, tiles_m, tiles_n);
@@ -462,6 +505,7 @@ __global__ void __launch_bounds__(kX3Threads, 1) gemm_x3_kernel(const __grid_con
         for (int sib = 0; sib < reg.n_sib; ++sib) {
           const CUtensorMap* ma = p.maps + reg.map0 + C_::NMAP * sib;
           for (int kb = 0; kb < kblocks; ++kb, ++it) {
+            if (p.sync) producer_lockstep(p, it, sync_on);
             const int s = it % STAGES;
             const uint32_t ph = (it / STAGES) & 1;
             mbar_wait(&empty_bar[s], ph ^ 1);
@@ -496,6 +540,7 @@ __global__ void __launch_bounds__(kX3Threads, 1) gemm_x3_kernel(const __grid_con
           }
         }
       }
+      if (p.sync) producer_lockstep_exit(p, it);
     }
   } else if (warp == 9) {
     // ---- MMA issuer: chunks of `chunk` K blocks into alternating buffers ----
@@ -756,6 +801,16 @@ bool gemm_use_mc(int M, int N, int bn) {
   return env != 0 && gemm_paired(M) && bn == 256 && N > 256;
 }
 int gemm_a_box_rows(bool mc) { return mc ? BM / 2 : BM; }
+
+int gemm_sync_epochs(const GemmLaunch& p, int num_sms, int max_sib) {
+  const int kcta = gemm_paired(p.M) ? 2 : 1;
+  const int tile_m = BM * kcta;
+  const long long tiles = (long long)((p.M + tile_m - 1) / tile_m) * ((p.N + p.bn - 1) / p.bn) * p.batch * p.n_regions;
+  const long long clusters = tiles < num_sms / kcta ? tiles : num_sms / kcta;
+  const long long per_cta = (tiles + clusters - 1) / clusters;
+  const long long kblocks = (p.K + gemm_bk(p.bf16) - 1) / gemm_bk(p.bf16);
+  return int((per_cta * kblocks * max_sib + p.sync_g - 1) / p.sync_g + 1);
+}
 
 int gemm_pick_bn(int M, int N, int batch, int n_regions, int num_sms) {
   // 128-wide tiles need 1.5x the L2->SMEM bytes per flop of 256-wide ones,

@@ -34,7 +34,14 @@ struct GemmLaunch {
   int bn;                     // tile width: 256 or 128 (gemm_pick_bn)
   int mc;                     // 1: 4-CTA clusters, two 2-SM pairs sharing (multicasting) the A panel
   int group_m;
-  int chunk;                  // x3: K blocks per TMEM partial promoted into fp32 running sums (0: off)                // grouped raster: tile rows that advance together along N
+  int chunk;                  // x3: K blocks per TMEM partial promoted into fp32 running sums (0: off)
+  // loose lockstep of the producers (experiment, x3 kernel): a CTA issues the
+  // loads of epoch e (sync_g K blocks) only once every CTA has issued epoch
+  // e - sync_lag, bounding how far the grid's CTAs drift apart along K so
+  // the operand panels a wave shares are still in L2. sync: sync_epochs + 1
+  // zeroed counters (the kernel re-zeroes them on exit); nullptr: off.
+  unsigned int* sync;
+  int sync_g, sync_lag, sync_epochs;                // grouped raster: tile rows that advance together along N
   int x3;                     // fp32-accurate 3xTF32: each stage carries hi and lo operand copies
                               // and feeds hi*hi + hi*lo + lo*hi into one accumulator
 };
@@ -50,5 +57,7 @@ int gemm_a_box_rows(bool mc);            // A rows per K-major TMA box (half a p
 constexpr int kStoreRows = 32;   // epilogue TMA-store box: 32 rows x 128 bytes
 cudaError_t gemm_prepare();  // sets the dynamic-smem attribute (call before capture)
 cudaError_t launch_gemm(const GemmLaunch& p, int num_sms, cudaStream_t stream);
+// epochs of sync_g K blocks the busiest CTA of this launch issues (x3 kernel)
+int gemm_sync_epochs(const GemmLaunch& p, int num_sms, int max_sib);
 
 }  // namespace ed

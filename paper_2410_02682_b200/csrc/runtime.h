@@ -237,6 +237,7 @@ struct ed_plan_h {
   DepRect* d_deps = nullptr;
   void* d_maps = nullptr;          // CUtensorMap[] of all GEMM launches
   void* d_regions = nullptr;       // GemmRegion[] of all GEMM launches
+  void* d_sync = nullptr;          // producer lockstep counters of GEMM launches (ED_GEMM_SYNC)
   void** d_ptrs = nullptr;         // chunk-pointer tables for scatter/gather
   int* d_err = nullptr;
   void* staging = nullptr;
@@ -396,7 +397,7 @@ struct ed_plan_h {
   void build();
   void allocate();
   void record();
-  void launch_op(size_t i, cudaStream_t s);
+  void launch_op(size_t i, cudaStream_t s, bool branch = false);  // branch: runs beside other launches
   void enqueue(cudaStream_t s);
   std::vector<cudaEvent_t> comm_events;  // fork / join points of the comm stream
   cudaStream_t aux[2] = {nullptr, nullptr};  // independent GEMMs run as parallel graph branches
