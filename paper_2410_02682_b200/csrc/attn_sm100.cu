@@ -3,30 +3,30 @@
 // kernel, so the [h, s, s2] logits and probabilities never reach HBM.
 //
 // A job is a pair of 128-row query tiles of one head (or a single tile in
-// the last wave, to fill the grid): K_j and V_j are loaded once per pair.
-// Each tile runs its own chain on the tensor pipe,
+// the last wave, to fill the grid): K_j and V_j are loaded once per pair
+// into a ring of shared-memory stages (K0, V0, K1, V1, ...).
 //
-//   S_t(j) -> softmax_t(j) -> PV_t(j) -> S_t(j+1) -> ...
+// One thread issues every MMA in a fixed order,
 //
-// issued by its own MMA thread; tile 1 starts half a step late so one
-// tile's softmax overlaps the other tile's MMAs.
+//   S_0(0) S_1(0) | PV_0(0) S_0(1) PV_1(0) S_1(1) | PV_0(1) S_0(2) ...
 //
-// S_t = Q_t K_j^T lands in TMEM; the softmax warps of tile t read it (one
-// thread per row), keep a reference max m (log2 domain) and sum l, write
-// P = exp2(c log2e S - m) back over S as packed bf16, and O_t += P V_j takes
-// P straight from TMEM (the A-from-TMEM form of tcgen05.mma), so P never
-// touches shared memory. O_t is rescaled in TMEM only when a row's max
-// passes the reference by more than 2^64 (P stays far inside the bf16 /
-// fp32 range); the commit that signals S_t(j) also covers PV_t(j-1), so the
-// rescale never races an MMA. Epilogue: O / l -> swizzled smem -> TMA store.
+// so while tile t's softmax works on S_t(j) the tensor pipe runs the other
+// tile's P.V and next S. S_t = Q_t K_j^T lands in TMEM; the softmax warps of
+// tile t read it (one thread per row), keep a reference max m (log2 domain),
+// post the row's rescale factor to the correction warp of its rows through
+// a named barrier, and write P = exp2(c log2e S - m) back over S as packed
+// bf16; O_t += P V_j takes P straight from TMEM (the A-from-TMEM form of
+// tcgen05.mma). P.V over the first 96 keys starts when three of P's four
+// fragments are stored. The commit that signals S_t(j) also covers
+// PV_t(j-1), so a rescale of O_t never races an MMA. O_t is rescaled only
+// when a row max passes the reference by more than 2^64.
 //
-// Warp roles (512 threads, four warpgroups): warps 0-3 softmax + epilogue
-// of tile 0, warps 4-7 of tile 1 (warp w owns TMEM lanes 32(w%4)..+32),
-// warp 8 TMA producer, warp 9 TMEM allocator + MMA issuer of tile 0, warp
-// 10 MMA issuer of tile 1, warp 11 idle, warps 12-15 the correction
-// warpgroup (O rescales, off the softmax's path). setmaxnreg moves
-// registers from the producer and correction warpgroups to the softmax
-// warpgroups, so a thread can hold its whole 128-key S row.
+// Warp roles (512 threads): warps 0-3 softmax of tile 0, 4-7 of tile 1 (warp
+// w owns TMEM lanes 32(w%4)..+32), 8-11 correction (O rescales, then the
+// epilogue O / l -> swizzled smem -> TMA store, off the softmax's path),
+// warp 12 TMEM allocator + MMA issuer, warp 13 TMA producer, 14-15 idle.
+// setmaxnreg moves registers from the producer and correction warpgroups to
+// the softmax warpgroups, so a thread holds its whole 128-key S row.
 // TMEM: S/P_0 [0,128) S/P_1 [128,256) O_0 [256,256+D) O_1 [256+D,256+2D).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -44,44 +44,34 @@ namespace {
 constexpr int BQ = 128;   // query rows per tile (TMEM lanes)
 constexpr int BKV = 128;  // keys per block
 constexpr int kThreads = 512;  // four warpgroups
-constexpr int kTmaWarp = 8, kMmaWarp = 9;
-// register split (setmaxnreg): 2 x 128 x 200 + 128 x 48 + 128 x 56 <= 64K
-constexpr int kSoftmaxRegs = 200, kProducerRegs = 48, kCorrectionRegs = 56;
+constexpr int kCorrWarp0 = 8, kMmaWarp = 12, kTmaWarp = 13;
+// register split (setmaxnreg): 2 x 128 x 184 + 128 x 96 + 128 x 48 <= 64K
+constexpr int kSoftmaxRegs = 184, kProducerRegs = 48, kCorrectionRegs = 96;
 // the softmax warpgroups can only take what the others give back from the
 // launch allocation (65536 / threads per thread), or setmaxnreg.inc never returns
 constexpr int kLaunchRegs = (65536 / kThreads) & ~7;
 static_assert(2 * (kSoftmaxRegs - kLaunchRegs) <= (kLaunchRegs - kProducerRegs) + (kLaunchRegs - kCorrectionRegs),
               "setmaxnreg split exceeds the launch allocation");
-constexpr int kCorrWarp0 = 12;  // warps 12-15: O rescale (correction) warpgroup
 // lazy rescale (log2 units): P = 2^(x - m) may reach 2^kRescale before O is
 // rescaled, and a rescale sets m = row max + kHeadroom. bf16 / fp32 keep full
 // relative precision over that span; O = sum P V keeps 2^64 / 4096 of headroom
 // for |V|, and keys more than ~2^-78 below the row max underflow to 0.
 constexpr float kRescale = 64.0f, kHeadroom = 48.0f;
-// exp2 pairs q with bit q % 8 set run on the FMA pipe (measured: 2 of 8 is
-// ~2% faster than MUFU only; more is slower, the kernel is not MUFU-bound)
+// exp2 pairs q with bit q % 8 set run on the FMA pipe (exp2_poly2), the rest on MUFU
 constexpr int kPolyPairs = 0x88;
-// 1: the two MMA threads take turns (PV_t(j) + S_t(j+1) groups alternate on
-// the tensor pipe), so the tiles' softmaxes run in anti-phase. Measured
-// slower (0.346 vs 0.32 ms on attn_big): each group then waits a whole
-// softmax for its turn, and the TS-form PV MMAs still slow down under the
-// other tile's TMEM stores (profiles/r01b_micro_tcgen05.md). Off by default.
-#ifndef ED_ATTN_ALT
-#define ED_ATTN_ALT 0
-#endif
-constexpr bool kAlternate = ED_ATTN_ALT;
 
 template <int D>
 struct ACfg {
-  static constexpr int Q_BYTES = BQ * D * 2;   // D/64 K-major chunks of 16 KiB
-  static constexpr int K_BYTES = BKV * D * 2;
-  static constexpr int V_BYTES = BKV * D * 2;  // D/64 MN atoms of 128 key-rows x 128 B
-  static constexpr int STG_BYTES = 4096;       // per softmax warp: 32 rows x 128 B
-  static constexpr int SMEM = 2 * Q_BYTES + 2 * K_BYTES + 2 * V_BYTES + 8 * STG_BYTES + 1024 + 256 + 1088;
+  static constexpr int Q_BYTES = BQ * D * 2;    // D/64 K-major chunks of 16 KiB
+  static constexpr int KV_BYTES = BKV * D * 2;  // K: D/64 K-major chunks; V: D/64 MN atoms of 128 key-rows x 128 B
+  static constexpr int KV_STAGES = D == 64 ? 6 : 3;
+  static constexpr int STG_BYTES = 4096;        // per correction warp, two of them: 32 rows x 128 B
+  static constexpr int SMEM = 2 * Q_BYTES + KV_STAGES * KV_BYTES + 8 * STG_BYTES + 1024 + 512 + 2048;
   static constexpr int TMEM_COLS = 512;
   __host__ __device__ static constexpr int s_col(int t) { return t * BKV; }
   __host__ __device__ static constexpr int o_col(int t) { return 2 * BKV + t * D; }
 };
+static_assert(ACfg<128>::SMEM <= 232448 && ACfg<64>::SMEM <= 232448, "shared memory");
 
 struct Job {
   int region, h, s0, two;
@@ -116,14 +106,6 @@ __device__ __forceinline__ Job job_of(const AttnLaunch& p, int j) {
   r.two = two;
   return r;
 }
-
-// debug tracing (ED_ATTN_TRACE=1, profile runs only): clock64 at pipeline
-// events of the first job of CTA 0, [event][tile][block]
-#define ATTN_TRACE(ev, t, j)                                                                     \
-  do {                                                                                           \
-    if (p.trace && blockIdx.x == 0 && jb == 0 && (j) < 64)                                       \
-      p.trace[((ev) * 2 + (t)) * 64 + (j)] = clock64();                                         \
-  } while (0)
 
 __device__ __forceinline__ float ex2(float x) {
   float y;
@@ -175,34 +157,37 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+__device__ __forceinline__ void named_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
 template <int D, int kPoly>
 __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant__ AttnLaunch p) {
   using C_ = ACfg<D>;
+  constexpr int NS = C_::KV_STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;                          // [2] tiles
-  uint8_t* sK = sQ + 2 * C_::Q_BYTES;          // [2] stages
-  uint8_t* sV = sK + 2 * C_::K_BYTES;          // [2] stages
-  uint8_t* sStg = sV + 2 * C_::V_BYTES;        // [8] softmax warps
+  uint8_t* sQ = smem;                           // [2] tiles
+  uint8_t* sKV = sQ + 2 * C_::Q_BYTES;          // [NS] ring: K0, V0, K1, V1, ...
+  uint8_t* sStg = sKV + NS * C_::KV_BYTES;      // [4 correction warps][2] epilogue staging
   uint64_t* bar = reinterpret_cast<uint64_t*>(sStg + 8 * C_::STG_BYTES);
-  uint64_t* q_full = bar + 0;    // [tile]
-  uint64_t* q_empty = bar + 2;   // [tile]
-  uint64_t* k_full = bar + 4;    // [stage]
-  uint64_t* k_empty = bar + 6;   // [stage]
-  uint64_t* v_full = bar + 8;    // [stage]
-  uint64_t* v_empty = bar + 10;  // [stage]
-  uint64_t* s_full = bar + 12;   // [tile]
-  uint64_t* p_full = bar + 14;   // [tile]
-  uint64_t* o_full = bar + 16;   // [tile]
-  uint64_t* o_empty = bar + 18;  // [tile]
-  uint64_t* p_half = bar + 20;   // [tile]: first 64 keys of P published
-  uint64_t* t1_go = bar + 22;    // tile 1 starts half a step behind tile 0
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 23);
-  uint64_t* corr_req = bar + 24;   // [tile] softmax -> correction: factors posted
-  uint64_t* corr_done = bar + 26;  // [tile] correction -> MMA: O_t rescaled
-  uint64_t* turn = bar + 28;       // [tile] the tensor pipe alternates PV+S groups between tiles
-  float* fac = reinterpret_cast<float*>(bar + 32);      // [tile][row] rescale factor
-  int* fac_any = reinterpret_cast<int*>(fac + 2 * BQ);  // [tile][lane quarter] any row grew
+  uint64_t* q_full = bar + 0;     // [tile] TMA -> MMA
+  uint64_t* q_empty = bar + 2;    // [tile] MMA -> TMA
+  uint64_t* s_full = bar + 4;     // [tile] MMA -> softmax: S_t(j) in TMEM (and PV_t(j-1) done)
+  uint64_t* p_part = bar + 6;     // [tile] softmax -> MMA: P over the first 3/4 of the keys stored
+  uint64_t* p_full = bar + 8;     // [tile] softmax -> MMA: all of P stored
+  uint64_t* o_ok = bar + 10;      // [tile] correction -> MMA: O_t rescaled for this block
+  uint64_t* o_full = bar + 12;    // [tile] MMA -> correction: last PV_t of the job done
+  uint64_t* o_empty = bar + 14;   // [tile] correction -> MMA: epilogue has read O_t
+  uint64_t* l_ready = bar + 16;   // [tile] softmax -> correction: row sums of the job posted
+  uint64_t* kv_full = bar + 18;   // [NS]
+  uint64_t* kv_empty = bar + 18 + NS;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 18 + 2 * NS);
+  float* scl = reinterpret_cast<float*>(bar + 20 + 2 * NS);  // [tile][row] rescale factor of the block
+  float* lbuf = scl + 2 * BQ;                                // [tile][row] row sum of the job
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int nb = p.T / BKV;
@@ -212,19 +197,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
     for (int i = 0; i < 2; ++i) {
       mbar_init(&q_full[i], 1);
       mbar_init(&q_empty[i], 1);
-      mbar_init(&k_full[i], 1);
-      mbar_init(&k_empty[i], 2);  // one arrival per MMA thread
-      mbar_init(&v_full[i], 1);
-      mbar_init(&v_empty[i], 2);
       mbar_init(&s_full[i], 1);
+      mbar_init(&p_part[i], 4);
       mbar_init(&p_full[i], 4);
-      mbar_init(&p_half[i], 4);
-      if (i == 0) mbar_init(t1_go, 1);
+      mbar_init(&o_ok[i], 4);
       mbar_init(&o_full[i], 1);
       mbar_init(&o_empty[i], 4);
-      mbar_init(&corr_req[i], 4);
-      mbar_init(&corr_done[i], 4);
-      mbar_init(&turn[i], 1);
+      mbar_init(&l_ready[i], 4);
+    }
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
     }
     fence_mbar_init();
   }
@@ -235,26 +218,23 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
   const uint32_t tmem = *tmem_slot;
   griddep_wait();  // the prologue above overlapped the previous kernel (PDL)
 
-  if (warp >= kCorrWarp0) {
-    // ---------------- O rescale (correction) warpgroup ----------------
-    // Off the softmax's path: the softmax posts per-row factors right after
-    // its row max and goes on with exp2; this warp rescales its 32 rows of
-    // O_t in TMEM (only if one of them grew) and releases PV_t(j).
+  if (warp >= kCorrWarp0 && warp < kCorrWarp0 + 4) {
+    // ---------------- correction warpgroup: O rescales and the epilogue ----------------
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kCorrectionRegs));
     const int wq = warp & 3;
+    const int row = wq * 32 + lane;
     const uint32_t lane_base = uint32_t(wq * 32) << 16;
-    int cn0 = 0, cn1 = 0;
+    uint8_t* stg = sStg + wq * 2 * C_::STG_BYTES;
+    int ln[2] = {0, 0}, sb = 0;
     for (int jb = blockIdx.x; jb < jobs; jb += gridDim.x) {
       const Job J = job_of(p, jb);
       for (int j = 0; j < nb; ++j)
         for (int t = 0; t <= J.two; ++t) {
-          int& cn = t ? cn1 : cn0;
-          mbar_wait(&corr_req[t], cn & 1);
-          ++cn;
-          if (fac_any[t * 4 + wq]) {
-            // PV_t(j-1) is complete: the softmax posted after S_t(j)'s commit
+          named_sync(1 + t * 4 + wq, 64);  // the softmax warp of these rows posted its factor
+          const float f = scl[t * BQ + row];
+          if (__any_sync(0xffffffffu, f != 1.f)) {
+            // PV_t(j-1) is complete: the softmax saw S_t(j), committed after it
             tc_fence_after();
-            const float f = fac[t * BQ + wq * 32 + lane];
             const float2 f2 = make_float2(f, f);
             const uint32_t o_addr = tmem + lane_base + uint32_t(C_::o_col(t));
 #pragma unroll 1
@@ -274,164 +254,195 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           }
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&corr_done[t]);
+          if (lane == 0) mbar_arrive(&o_ok[t]);
         }
-    }
-  } else if (warp >= 8) {
-    // producer warpgroup: hand registers to the softmax warpgroups
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kProducerRegs));
-    if (warp == kTmaWarp) {
-      // ---------------- TMA producer ----------------
-      if (lane == 0) {
-        int kc = 0, vc = 0, qn0 = 0, qn1 = 0;
-        for (int jb = blockIdx.x; jb < jobs; jb += gridDim.x) {
-          if (jb + int(gridDim.x) >= jobs) griddep_launch();  // last job: the next kernel may launch
-          const Job J = job_of(p, jb);
-          const AttnRegion R = p.regions[J.region];
-          const CUtensorMap* mq = p.maps + R.q;
-          auto src_map = [&](const AttnSrc& a, int key, int dcol) {
-            return p.maps + a.base + (key / a.keys) * a.nd + dcol / a.dw;
-          };
-          for (int t = 0; t <= J.two; ++t) {
-            int& qn = t ? qn1 : qn0;
-            mbar_wait(&q_empty[t], (qn & 1) ^ 1);
-            ++qn;
-            mbar_expect_tx(&q_full[t], C_::Q_BYTES);
-  #pragma unroll
-            for (int c = 0; c < D / 64; ++c)
-              tma_load_3d(sQ + t * C_::Q_BYTES + c * 16384, mq, &q_full[t], c * 64, J.s0 + t * BQ, J.h);
+      // ---- epilogue: O_t / l -> swizzled staging -> TMA store (32 rows per warp)
+      for (int t = 0; t <= J.two; ++t) {
+        mbar_wait(&l_ready[t], ln[t] & 1);
+        const float inv = 1.0f / lbuf[t * BQ + row];
+        mbar_wait(&o_full[t], ln[t] & 1);  // both complete once per job of this tile
+        ++ln[t];
+        tc_fence_after();
+        const uint32_t o_addr = tmem + lane_base + uint32_t(C_::o_col(t));
+        const int row0 = J.s0 + t * BQ + wq * 32;
+        for (int pass = 0; pass < 2; ++pass) {
+          const int cm = pass == 0 ? p.regions[J.region].o32 : p.regions[J.region].o16;
+          if (cm < 0) continue;
+          const int cols = pass == 0 ? 32 : 64;
+#pragma unroll 1
+          for (int c = 0; c < D / cols; ++c) {
+            uint32_t v[64];
+            tmem_ld_32x32b_x32(o_addr + uint32_t(c * cols), *reinterpret_cast<uint32_t(*)[32]>(v));
+            if (pass == 1) tmem_ld_32x32b_x32(o_addr + uint32_t(c * cols + 32), *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+            tmem_ld_wait();
+            uint8_t* buf = stg + (sb & 1) * C_::STG_BYTES;
+            if (lane == 0) bulk_wait_read<1>();  // the store that last read this buffer is done
+            __syncwarp();
+            uint8_t* rowp = buf + lane * 128;
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+              uint4 q4;
+              if (pass == 0) {
+                q4 = make_uint4(__float_as_uint(__uint_as_float(v[4 * g]) * inv),
+                                __float_as_uint(__uint_as_float(v[4 * g + 1]) * inv),
+                                __float_as_uint(__uint_as_float(v[4 * g + 2]) * inv),
+                                __float_as_uint(__uint_as_float(v[4 * g + 3]) * inv));
+              } else {
+                q4 = make_uint4(pack_bf16(__uint_as_float(v[8 * g]) * inv, __uint_as_float(v[8 * g + 1]) * inv),
+                                pack_bf16(__uint_as_float(v[8 * g + 2]) * inv, __uint_as_float(v[8 * g + 3]) * inv),
+                                pack_bf16(__uint_as_float(v[8 * g + 4]) * inv, __uint_as_float(v[8 * g + 5]) * inv),
+                                pack_bf16(__uint_as_float(v[8 * g + 6]) * inv, __uint_as_float(v[8 * g + 7]) * inv));
+              }
+              *reinterpret_cast<uint4*>(rowp + ((g ^ (lane & 7)) << 4)) = q4;
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_3d(p.maps + cm, buf, c * cols, row0, J.h);
+              bulk_commit();
+            }
+            ++sb;
           }
-          for (int j = 0; j < nb; ++j) {
-            int st = kc & 1;
-            mbar_wait(&k_empty[st], ((kc >> 1) & 1) ^ 1);
-            ++kc;
-            mbar_expect_tx(&k_full[st], C_::K_BYTES);
-  #pragma unroll
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&o_empty[t]);
+      }
+    }
+    if (lane == 0) bulk_wait<0>();
+  } else if (warp >= 12) {
+    // producer warpgroup: hands registers to the softmax warpgroups
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kProducerRegs));
+    if (warp == kTmaWarp && lane == 0) {
+      // ---------------- TMA producer: Q tiles, then the K/V ring K0 V0 K1 V1 ... ----------------
+      int kvn = 0, qn0 = 0, qn1 = 0;
+      for (int jb = blockIdx.x; jb < jobs; jb += gridDim.x) {
+        if (jb + int(gridDim.x) >= jobs) griddep_launch();  // last job: the next kernel may launch
+        const Job J = job_of(p, jb);
+        const AttnRegion R = p.regions[J.region];
+        const CUtensorMap* mq = p.maps + R.q;
+        auto src_map = [&](const AttnSrc& a, int key, int dcol) {
+          return p.maps + a.base + (key / a.keys) * a.nd + dcol / a.dw;
+        };
+        for (int t = 0; t <= J.two; ++t) {
+          int& qn = t ? qn1 : qn0;
+          mbar_wait(&q_empty[t], (qn & 1) ^ 1);
+          ++qn;
+          mbar_expect_tx(&q_full[t], C_::Q_BYTES);
+#pragma unroll
+          for (int c = 0; c < D / 64; ++c)
+            tma_load_3d(sQ + t * C_::Q_BYTES + c * 16384, mq, &q_full[t], c * 64, J.s0 + t * BQ, J.h);
+        }
+        for (int j = 0; j < nb; ++j) {
+          for (int kv = 0; kv < 2; ++kv) {
+            const int st = kvn % NS;
+            mbar_wait(&kv_empty[st], ((kvn / NS) & 1) ^ 1);
+            ++kvn;
+            mbar_expect_tx(&kv_full[st], C_::KV_BYTES);
+            uint8_t* dst = sKV + st * C_::KV_BYTES;
+            const AttnSrc& a = kv ? R.v : R.k;
+#pragma unroll
             for (int c = 0; c < D / 64; ++c)
-              tma_load_3d(sK + st * C_::K_BYTES + c * 16384, src_map(R.k, j * BKV, c * 64), &k_full[st],
-                          (c * 64) % R.k.dw, (j * BKV) % R.k.keys, J.h + R.k.hoff);
-            st = vc & 1;
-            mbar_wait(&v_empty[st], ((vc >> 1) & 1) ^ 1);
-            ++vc;
-            mbar_expect_tx(&v_full[st], C_::V_BYTES);
-  #pragma unroll
-            for (int a = 0; a < D / 64; ++a)
-              tma_load_3d(sV + st * C_::V_BYTES + a * (BKV * 128), src_map(R.v, j * BKV, a * 64), &v_full[st],
-                          (a * 64) % R.v.dw, (j * BKV) % R.v.keys, J.h + R.v.hoff);
+              tma_load_3d(dst + c * 16384, src_map(a, j * BKV, c * 64), &kv_full[st], (c * 64) % a.dw,
+                          (j * BKV) % a.keys, J.h + a.hoff);
           }
         }
       }
-    } else if (warp == kMmaWarp || warp == kMmaWarp + 1) {
-      // ---------------- MMA issuers: one thread per tile ----------------
-      // Each tile's chain (S_t(j) -> softmax -> PV_t(j) -> S_t(j+1)) is issued
-      // by its own thread, so one tile's MMAs never wait behind the other
-      // tile's softmax; K/V stages are released by both (count 2).
-      const int t = warp - kMmaWarp;
-      if (lane == 0) {
-        const uint32_t idesc_s = umma_idesc(1u, BQ, BKV, 0u, 0u);  // Q, K both K-major (d)
-        const uint32_t idesc_o = umma_idesc(1u, BQ, D, 0u, 1u);    // P from TMEM (keys), V MN-major (d)
+    } else if (warp == kMmaWarp) {
+      // ---------------- MMA issuer: PV_0(j), S_0(j+1), PV_1(j), S_1(j+1) ----------------
+      // The whole warp runs this loop (uniform values); one elected lane issues.
+      // One thread, fixed order: each tile's P.V goes in as soon as its P is
+      // stored, its next S right behind it (in issue order after the P.V that
+      // reads P, so S may overwrite P's columns), while the other tile's
+      // softmax works on its own S.
+      const uint32_t idesc_s = umma_idesc(1u, BQ, BKV, 0u, 0u);  // Q, K both K-major (d)
+      const uint32_t idesc_o = umma_idesc(1u, BQ, D, 0u, 1u);    // P from TMEM (keys), V MN-major (d)
+      int kvn = 0, qn0 = 0, qn1 = 0, pn0 = 0, pn1 = 0, on0 = 0, on1 = 0;
+      auto issue_s = [&](int t, int kst) {
         const uint32_t qa = smem_u32(sQ + t * C_::Q_BYTES);
-        int kc = 0, vc = 0, qn = 0, pn = 0, on = 0, gn = 0, tn = 0;
-        auto issue_s = [&](int kst) {
-          const uint32_t ka = smem_u32(sK + kst * C_::K_BYTES);
+        const uint32_t ka = smem_u32(sKV + kst * C_::KV_BYTES);
 #pragma unroll
-          for (int k = 0; k < D / 16; ++k) {
-            const uint32_t off = (k / 4) * 16384 + (k % 4) * 32;
-            mma_f16(tmem + C_::s_col(t), umma_desc_sw128(qa + off, 16, 1024), umma_desc_sw128(ka + off, 16, 1024),
-                    idesc_s, k != 0);
-          }
-          mma_commit(&s_full[t]);
-        };
-        for (int jb = blockIdx.x; jb < jobs; jb += gridDim.x) {
-          const Job J = job_of(p, jb);
-          if (t > J.two) {  // single-tile job: tile 0's thread releases the stages twice
-            kc += nb;
-            vc += nb;
-            continue;
-          }
-          const int rel = J.two ? 1 : 2;  // k_empty / v_empty arrivals this thread owes
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off = (k / 4) * 16384 + (k % 4) * 32;
+          mma_f16_warp(tmem + C_::s_col(t), umma_desc_sw128(qa + off, 16, 1024), umma_desc_sw128(ka + off, 16, 1024),
+                  idesc_s, k != 0);
+        }
+        mma_commit_warp(&s_full[t]);
+      };
+      auto take = [&]() {  // next ring stage, full
+        const int st = kvn % NS;
+        mbar_wait(&kv_full[st], (kvn / NS) & 1);
+        ++kvn;
+        return st;
+      };
+      for (int jb = blockIdx.x; jb < jobs; jb += gridDim.x) {
+        const Job J = job_of(p, jb);
+        const int two = J.two;
+        int kst = take();
+        for (int t = 0; t <= two; ++t) {
+          int& qn = t ? qn1 : qn0;
           mbar_wait(&q_full[t], qn & 1);
           ++qn;
-          if (t == 1) {
-            // stagger: tile 1's chain starts once tile 0's first PV is issued,
-            // so each tile's softmax overlaps the other tile's MMAs
-            mbar_wait(t1_go, gn & 1);
-            ++gn;
-          }
-          int kst = kc & 1;
-          mbar_wait(&k_full[kst], (kc >> 1) & 1);
-          ++kc;
           tc_fence_after();
-          issue_s(kst);
-          ATTN_TRACE(5, t, 0);
-          if (nb == 1) mma_commit(&q_empty[t]);
-          for (int r = 0; r < rel; ++r) mma_commit(&k_empty[kst]);
-          for (int j = 0; j < nb; ++j) {
-            const int vst = vc & 1;
-            mbar_wait(&v_full[vst], (vc >> 1) & 1);
-            ++vc;
-            const uint32_t va = smem_u32(sV + vst * C_::V_BYTES);
-            mbar_wait(&p_half[t], pn & 1);
-            mbar_wait(&corr_done[t], pn & 1);
-            if (kAlternate && J.two) {  // tile 0 holds the first turn
-              mbar_wait(&turn[t], (tn & 1) ^ (t == 0 ? 1 : 0));
-              ++tn;
-            }
-            ATTN_TRACE(3, t, j);
-            if (j == 0) {  // the last job's epilogue has drained O_t
+          issue_s(t, kst);
+          if (nb == 1) mma_commit_warp(&q_empty[t]);
+        }
+        mma_commit_warp(&kv_empty[kst]);
+        for (int j = 0; j < nb; ++j) {
+          const int vst = take();
+          const uint32_t va = smem_u32(sKV + vst * C_::KV_BYTES);
+          for (int t = 0; t <= two; ++t) {
+            int& pn = t ? pn1 : pn0;
+            if (j == 0) {  // the previous job's epilogue has read O_t
+              int& on = t ? on1 : on0;
               mbar_wait(&o_empty[t], (on & 1) ^ 1);
               ++on;
             }
+            mbar_wait(&o_ok[t], pn & 1);
+            mbar_wait(&p_part[t], pn & 1);
             tc_fence_after();
-            // PV over the first 64 keys while the softmax finishes the rest
 #pragma unroll
-            for (int k = 0; k < BKV / 32; ++k)
-              mma_f16_ts(tmem + C_::o_col(t), tmem + C_::s_col(t) + k * 8,
+            for (int k = 0; k < 3 * BKV / 64; ++k)
+              mma_f16_ts_warp(tmem + C_::o_col(t), tmem + C_::s_col(t) + k * 8,
                          umma_desc_sw128(va + k * 2048, BKV * 128, 1024), idesc_o, (j | k) != 0);
-            if (t == 0 && j == 0 && J.two) mbar_arrive(t1_go);
             mbar_wait(&p_full[t], pn & 1);
             ++pn;
-            ATTN_TRACE(4, t, j);
             tc_fence_after();
 #pragma unroll
-            for (int k = BKV / 32; k < BKV / 16; ++k)
-              mma_f16_ts(tmem + C_::o_col(t), tmem + C_::s_col(t) + k * 8,
+            for (int k = 3 * BKV / 64; k < BKV / 16; ++k)
+              mma_f16_ts_warp(tmem + C_::o_col(t), tmem + C_::s_col(t) + k * 8,
                          umma_desc_sw128(va + k * 2048, BKV * 128, 1024), idesc_o, 1u);
-            for (int r = 0; r < rel; ++r) mma_commit(&v_empty[vst]);
-            if (j == nb - 1) mma_commit(&o_full[t]);
-            if (j + 1 < nb) {
-              kst = kc & 1;
-              ATTN_TRACE(9, t, j + 1);
-              mbar_wait(&k_full[kst], (kc >> 1) & 1);
-              ++kc;
-              tc_fence_after();
-              issue_s(kst);  // in issue order after PV_t(j): overwrites P_t(j) only once it is read
-              ATTN_TRACE(5, t, j + 1);
-              if (j + 1 == nb - 1) mma_commit(&q_empty[t]);
-              for (int r = 0; r < rel; ++r) mma_commit(&k_empty[kst]);
+            if (t == two) mma_commit_warp(&kv_empty[vst]);
+            if (j == nb - 1) {
+              mma_commit_warp(&o_full[t]);
+            } else {
+              if (t == 0) {
+                kst = take();
+                tc_fence_after();
+              }
+              issue_s(t, kst);
+              if (j + 1 == nb - 1) mma_commit_warp(&q_empty[t]);
+              if (t == two) mma_commit_warp(&kv_empty[kst]);
             }
-            if (kAlternate && J.two) mbar_arrive(&turn[t ^ 1]);
           }
         }
       }
     }
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kSoftmaxRegs));
-    // ---------------- softmax + epilogue (tile t = warp / 4) ----------------
+    // ---------------- softmax (tile t = warp / 4, one thread per row) ----------------
     const int t = warp >> 2, wq = warp & 3;
+    const int row = wq * 32 + lane;
     const uint32_t lane_base = uint32_t(wq * 32) << 16;
     const uint32_t s_addr = tmem + lane_base + uint32_t(C_::s_col(t));
-    const uint32_t o_addr = tmem + lane_base + uint32_t(C_::o_col(t));
     const float sc2 = p.scale * 1.4426950408889634f;  // c * log2(e)
-    uint8_t* stg = sStg + warp * C_::STG_BYTES;
-    int sn = 0, on = 0;
+    int sn = 0;
     for (int jb = blockIdx.x; jb < jobs; jb += gridDim.x) {
       const Job J = job_of(p, jb);
       if (t > J.two) continue;
       float m = 0.f, l = 0.f;  // reference max (log2 domain) and row sum
       for (int j = 0; j < nb; ++j) {
         mbar_wait(&s_full[t], sn & 1);
-        if (lane == 0 && wq == 0) ATTN_TRACE(0, t, j);
         ++sn;
         tc_fence_after();
         uint32_t v[128];
@@ -439,7 +450,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         for (int c = 0; c < 4; ++c)
           tmem_ld_32x32b_x32(s_addr + uint32_t(c * 32), *reinterpret_cast<uint32_t(*)[32]>(v + 32 * c));
         tmem_ld_wait();
-        if (lane == 0 && wq == 0) ATTN_TRACE(6, t, j);
         // row max of c*log2e*S: four independent chains
         float mx;
         {
@@ -466,114 +476,65 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             mx = fminf(fminf(a0, a1), fminf(a2, a3)) * sc2;
           }
         }
-        if (lane == 0 && wq == 0) ATTN_TRACE(7, t, j);
-        if (lane == 0 && wq != 0) ATTN_TRACE(12 + wq, t, j);
         // reference max with hysteresis: when a row's max passes m + kRescale
         // the new reference is max + kHeadroom, so P spans [2^-kHeadroom,
         // 2^kRescale] at the row max and rescales stay rare
-        bool grow = false;
         float f = 1.f;
         if (j == 0) {
           m = mx + kHeadroom;
         } else if (mx > m + kRescale) {
-          grow = true;
           const float mn = mx + kHeadroom;
           f = ex2(m - mn);
           m = mn;
         }
-        // post this row's factor to the correction warp of its lane quarter
-        {
-          const bool wgrow = __any_sync(0xffffffffu, grow);
-          fac[t * BQ + wq * 32 + lane] = f;
-          if (lane == 0) fac_any[t * 4 + wq] = wgrow;
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&corr_req[t]);
-        }
-        // P = exp2(c log2e S - m), packed bf16, written over S in two halves
-        // of 64 keys (the S values of a half are in registers before its
-        // P columns, which alias S columns [0, 64), are stored); the first
-        // half is published at once so PV over it starts early. One pair in
-        // four is evaluated on the FMA pipe (exp2_poly2) to unload MUFU.
+        scl[t * BQ + row] = f;
+        named_arrive(1 + t * 4 + wq, 64);  // the correction warp of these rows takes the factor
+        // P = exp2(c log2e S - m), packed bf16 over S's first 64 columns, in
+        // four fragments of 32 keys; the first three are published together
+        // so P.V over 96 keys starts while the last fragment is computed
         const float2 sc2v = make_float2(sc2, sc2), nm = make_float2(-m, -m);
-        float2 acc0 = make_float2(0.f, 0.f), acc1 = acc0;
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          uint32_t w[32];
+        for (int fr = 0; fr < 4; ++fr) {
+          uint32_t w[16];
 #pragma unroll
-          for (int q = 0; q < 32; ++q) {
-            const int e = hh * 64 + 2 * q;
+          for (int q = 0; q < 16; ++q) {
+            const int e = fr * 32 + 2 * q;
             const float2 x = ffma2(make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1])), sc2v, nm);
             float2 y;
-            if ((kPoly >> (q & 7)) & 1) {
+            if ((kPoly >> ((fr * 16 + q) & 7)) & 1) {
               y = exp2_poly2(x);
             } else {
               y.x = ex2(x.x);
               y.y = ex2(x.y);
             }
-            if (q & 1) acc1 = fadd2(acc1, y);
-            else acc0 = fadd2(acc0, y);
+            v[e] = __float_as_uint(y.x);
+            v[e + 1] = __float_as_uint(y.y);
             w[q] = pack_bf16(y.x, y.y);
           }
-          tmem_st_32x32b_x32(s_addr + uint32_t(hh * 32), w);
-          if (lane == 0 && wq == 0 && hh == 0) ATTN_TRACE(8, t, j);
-          tmem_st_wait();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(hh == 0 ? &p_half[t] : &p_full[t]);
-          if (lane == 0 && wq == 0) ATTN_TRACE(1 + hh, t, j);
-          if (lane == 0 && wq != 0 && hh == 1) ATTN_TRACE(9 + wq, t, j);
+          tmem_st_32x32b_x16(s_addr + uint32_t(fr * 16), w);
+          if (fr == 2 || fr == 3) {
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(fr == 2 ? &p_part[t] : &p_full[t]);
+          }
         }
-        acc0 = fadd2(acc0, acc1);
+        // row sum off the critical path (P is already with the tensor pipe)
+        float2 acc0 = make_float2(0.f, 0.f), acc1 = acc0, acc2 = acc0, acc3 = acc0;
+#pragma unroll
+        for (int e = 0; e < 128; e += 8) {
+          acc0 = fadd2(acc0, make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1])));
+          acc1 = fadd2(acc1, make_float2(__uint_as_float(v[e + 2]), __uint_as_float(v[e + 3])));
+          acc2 = fadd2(acc2, make_float2(__uint_as_float(v[e + 4]), __uint_as_float(v[e + 5])));
+          acc3 = fadd2(acc3, make_float2(__uint_as_float(v[e + 6]), __uint_as_float(v[e + 7])));
+        }
+        acc0 = fadd2(fadd2(acc0, acc1), fadd2(acc2, acc3));
         l = l * f + (acc0.x + acc0.y);
       }
-      // ---- epilogue: O_t / l -> swizzled staging -> TMA store (32 rows per warp)
-      mbar_wait(&o_full[t], on & 1);
-      ++on;
-      tc_fence_after();
-      const float inv = 1.0f / l;
-      const int row0 = J.s0 + t * BQ + wq * 32;
-      for (int pass = 0; pass < 2; ++pass) {
-        const int cm = pass == 0 ? p.regions[J.region].o32 : p.regions[J.region].o16;
-        if (cm < 0) continue;
-        const int cols = pass == 0 ? 32 : 64;
-#pragma unroll 1
-        for (int c = 0; c < D / cols; ++c) {
-          uint32_t v[64];
-          tmem_ld_32x32b_x32(o_addr + uint32_t(c * cols), *reinterpret_cast<uint32_t(*)[32]>(v));
-          if (pass == 1) tmem_ld_32x32b_x32(o_addr + uint32_t(c * cols + 32), *reinterpret_cast<uint32_t(*)[32]>(v + 32));
-          tmem_ld_wait();
-          if (lane == 0) bulk_wait_read<0>();
-          __syncwarp();
-          uint8_t* rowp = stg + lane * 128;
-#pragma unroll
-          for (int g = 0; g < 8; ++g) {
-            uint4 q4;
-            if (pass == 0) {
-              q4 = make_uint4(__float_as_uint(__uint_as_float(v[4 * g]) * inv),
-                              __float_as_uint(__uint_as_float(v[4 * g + 1]) * inv),
-                              __float_as_uint(__uint_as_float(v[4 * g + 2]) * inv),
-                              __float_as_uint(__uint_as_float(v[4 * g + 3]) * inv));
-            } else {
-              q4 = make_uint4(pack_bf16(__uint_as_float(v[8 * g]) * inv, __uint_as_float(v[8 * g + 1]) * inv),
-                              pack_bf16(__uint_as_float(v[8 * g + 2]) * inv, __uint_as_float(v[8 * g + 3]) * inv),
-                              pack_bf16(__uint_as_float(v[8 * g + 4]) * inv, __uint_as_float(v[8 * g + 5]) * inv),
-                              pack_bf16(__uint_as_float(v[8 * g + 6]) * inv, __uint_as_float(v[8 * g + 7]) * inv));
-            }
-            *reinterpret_cast<uint4*>(rowp + ((g ^ (lane & 7)) << 4)) = q4;
-          }
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            tma_store_3d(p.maps + cm, stg, c * cols, row0, J.h);
-            bulk_commit();
-          }
-        }
-      }
-      tc_fence_before();
+      lbuf[t * BQ + row] = l;
       __syncwarp();
-      if (lane == 0) mbar_arrive(&o_empty[t]);
+      if (lane == 0) mbar_arrive(&l_ready[t]);
     }
-    if (lane == 0) bulk_wait<0>();
   }
 
   tc_fence_before();
@@ -596,13 +557,6 @@ cudaError_t launch_d(const AttnLaunch& p0, int num_sms, cudaStream_t s) {
   AttnLaunch p = p0;
   attn_schedule(p, num_sms);
 
-  static const bool trace = std::getenv("ED_ATTN_TRACE") != nullptr;
-  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  cudaStreamIsCapturing(s, &cs);
-  if (trace && cs == cudaStreamCaptureStatusNone) {
-    cudaMalloc(&p.trace, 16 * 2 * 64 * sizeof(long long));
-    cudaMemsetAsync(p.trace, 0, 16 * 2 * 64 * sizeof(long long), s);
-  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(p.n_jobs < num_sms ? p.n_jobs : num_sms);
   cfg.blockDim = dim3(kThreads);
@@ -614,20 +568,6 @@ cudaError_t launch_d(const AttnLaunch& p0, int num_sms, cudaStream_t s) {
   cfg.attrs = pdl;
   cfg.numAttrs = 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, attn_kernel<D, kPolyPairs>, p);
-  if (p.trace) {
-    long long h[16 * 2 * 64];
-    cudaStreamSynchronize(s);
-    cudaMemcpy(h, p.trace, sizeof(h), cudaMemcpyDeviceToHost);
-    cudaFree(p.trace);
-    const long long t0 = h[5 * 128];
-    const char* names[16] = {"s_ready", "p_half", "p_full", "mma_got_half", "mma_got_full", "s_issued", "s_loaded", "max_done", "half0_stored", "pvb_issued", "p_full_w1", "p_full_w2", "p_full_w3", "max_w1", "max_w2", "max_w3"};
-    for (int ev = 0; ev < 16; ++ev)
-      for (int t = 0; t < 2; ++t) {
-        std::fprintf(stderr, "attn_trace %-13s t%d:", names[ev], t);
-        for (int j = 0; j < 33; ++j) std::fprintf(stderr, " %lld", h[(ev * 2 + t) * 64 + j] ? h[(ev * 2 + t) * 64 + j] - t0 : -1);
-        std::fprintf(stderr, "\n");
-      }
-  }
   return e;
 }
 

@@ -27,7 +27,6 @@ struct AttnLaunch {
   int H, S, T, D;              // heads, query rows, keys, head dim (per region)
   float scale;                 // scale of the fused T2 vertex (1 if none)
   int n_pair_jobs, n_jobs;     // set by attn_schedule (launch_attn calls it)
-  long long* trace;            // debug event timestamps (ED_ATTN_TRACE), else null
 };
 
 // Split the (region, head, 128-row tile) space into tile-pair jobs and, for

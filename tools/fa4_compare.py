@@ -4,7 +4,7 @@ forward kernels (library code, NOT on the product path) on attn_big's shape
 the fused kernel's %-of-peak can be read against what the state of the art
 reaches on the same box. Prints one JSON line per library that runs.
 
-    python tools/fa4_compare.py [iters]
+    python tools/fa4_compare.py [iters] [q/k multiplier]
 """
 import json
 import sys
@@ -17,18 +17,21 @@ FLOP = 4.0 * B * H * S * S * D
 it = int(sys.argv[1]) if len(sys.argv) > 1 else 50
 
 
-def timeit(fn):
+def timeit(fn, reps=20):
+    """median over `it` samples of (events around `reps` back-to-back calls) / reps:
+    amortises the Python launch path, which is slower than the kernel."""
     for _ in range(5):
         fn()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ts = []
-    for _ in range(it):
+    for _ in range(max(3, it // 5)):
         e0.record()
-        fn()
+        for _ in range(reps):
+            fn()
         e1.record()
         torch.cuda.synchronize()
-        ts.append(e0.elapsed_time(e1))
+        ts.append(e0.elapsed_time(e1) / reps)
     ts.sort()
     return ts[len(ts) // 2], ts[0]
 
@@ -38,6 +41,9 @@ def main():
     q = torch.randn(B, S, H, D, device="cuda", dtype=torch.bfloat16)
     k = torch.randn(B, S, H, D, device="cuda", dtype=torch.bfloat16)
     v = torch.randn(B, S, H, D, device="cuda", dtype=torch.bfloat16)
+    if len(sys.argv) > 2:  # logit scale: integer-stream-like logits (~1e3) force O rescales
+        q.mul_(float(sys.argv[2]))
+        k.mul_(float(sys.argv[2]))
     ref = torch.nn.functional.scaled_dot_product_attention(q.transpose(1, 2).float(), k.transpose(1, 2).float(),
                                                            v.transpose(1, 2).float()).transpose(1, 2)
     cands = []
