@@ -1,18 +1,20 @@
 #!/bin/bash
-# Builds a variant of libed_gpu.so with extra -D flags for one source
-# (development experiments): tools/build_variant.sh NAME SRC.cu -DFOO=1 ...
+# Builds a variant of libed_gpu.so for A/B experiments: one translation unit
+# compiled from SRC (a path, e.g. an older revision saved under /tmp, or the
+# tree's own file) with extra -D flags, every other object from the current
+# build: tools/build_variant.sh NAME UNIT SRC.cu -DFOO=1 ...
 # -> paper_2410_02682_b200/build/var/NAME.so (load with ED_LIB_PATH=...).
 set -e
 cd "$(dirname "$0")/.."
-NAME=$1; SRC=$2; shift 2
+NAME=$1; UNIT=$2; SRC=$3; shift 3
 P=paper_2410_02682_b200
 python -c "from paper_2410_02682_b200 import build as b; b.build()"
 mkdir -p $P/build/var
 OBJS=""
-for s in runtime gemm_sm100 kernels ewise attn_sm100; do
-  if [ "$s.cu" = "$SRC" ]; then
-    /usr/local/cuda/bin/nvcc -std=c++17 -O3 -lineinfo -Xcompiler -fPIC -Xcompiler -fvisibility=hidden -Iinclude -I$P/csrc \
-      -gencode arch=compute_100a,code=sm_100a "$@" -c $P/csrc/$s.cu -o $P/build/var/$NAME.$s.o
+for s in $(python -c "from paper_2410_02682_b200 import build as b; print(' '.join(x[:-3] for x in b.SOURCES))"); do
+  if [ "$s" = "$UNIT" ]; then
+    /usr/local/cuda/bin/nvcc -std=c++17 -O3 -lineinfo -Xcompiler -fPIC -Xcompiler -fvisibility=hidden -Iinclude \
+      -I$(dirname $SRC) -I$P/csrc -gencode arch=compute_100a,code=sm_100a "$@" -c $SRC -o $P/build/var/$NAME.$s.o
     OBJS="$OBJS $P/build/var/$NAME.$s.o"
   else
     OBJS="$OBJS $P/build/$s.o"

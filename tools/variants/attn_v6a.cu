@@ -46,12 +46,7 @@ constexpr int BKV = 128;  // keys per block
 constexpr int kThreads = 512;  // four warpgroups
 constexpr int kCorrWarp0 = 8, kMmaWarp = 12, kTmaWarp = 13;
 // register split (setmaxnreg): 2 x 128 x 184 + 128 x 96 + 128 x 48 <= 64K
-#ifndef ED_ATTN_SREGS
-#define ED_ATTN_SREGS 184
-#define ED_ATTN_PREGS 48
-#define ED_ATTN_CREGS 96
-#endif
-constexpr int kSoftmaxRegs = ED_ATTN_SREGS, kProducerRegs = ED_ATTN_PREGS, kCorrectionRegs = ED_ATTN_CREGS;
+constexpr int kSoftmaxRegs = 184, kProducerRegs = 48, kCorrectionRegs = 96;
 // the softmax warpgroups can only take what the others give back from the
 // launch allocation (65536 / threads per thread), or setmaxnreg.inc never returns
 constexpr int kLaunchRegs = (65536 / kThreads) & ~7;
@@ -63,17 +58,7 @@ static_assert(2 * (kSoftmaxRegs - kLaunchRegs) <= (kLaunchRegs - kProducerRegs) 
 // for |V|, and keys more than ~2^-78 below the row max underflow to 0.
 constexpr float kRescale = 64.0f, kHeadroom = 48.0f;
 // exp2 pairs q with bit q % 8 set run on the FMA pipe (exp2_poly2), the rest on MUFU
-// (attn_big: 1 of 8 on the FMA pipe 0.2378 ms, none 0.2390, 2 of 8 0.2482, 3 of 8 0.268)
-#ifndef ED_ATTN_POLY
-#define ED_ATTN_POLY 0x80
-#endif
-constexpr int kPolyPairs = ED_ATTN_POLY;
-// P fragments (32 keys each) stored before P.V over them may start
-#ifndef ED_ATTN_SPLIT
-#define ED_ATTN_SPLIT 3
-#endif
-constexpr int kSplitFr = ED_ATTN_SPLIT;
-static_assert(kSplitFr >= 1 && kSplitFr <= 3, "P.V starts after 1-3 of the 4 P fragments");
+constexpr int kPolyPairs = 0x80;
 
 template <int D>
 struct ACfg {
@@ -380,7 +365,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t off = (k / 4) * 16384 + (k % 4) * 32;
           mma_f16_warp(tmem + C_::s_col(t), umma_desc_sw128(qa + off, 16, 1024), umma_desc_sw128(ka + off, 16, 1024),
-                       idesc_s, k != 0);
+                  idesc_s, k != 0);
         }
         mma_commit_warp(&s_full[t]);
       };
@@ -417,16 +402,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             mbar_wait(&p_part[t], pn & 1);
             tc_fence_after();
 #pragma unroll
-            for (int k = 0; k < kSplitFr * 2; ++k)
+            for (int k = 0; k < 3 * BKV / 64; ++k)
               mma_f16_ts_warp(tmem + C_::o_col(t), tmem + C_::s_col(t) + k * 8,
-                              umma_desc_sw128(va + k * 2048, BKV * 128, 1024), idesc_o, (j | k) != 0);
+                         umma_desc_sw128(va + k * 2048, BKV * 128, 1024), idesc_o, (j | k) != 0);
             mbar_wait(&p_full[t], pn & 1);
             ++pn;
             tc_fence_after();
 #pragma unroll
-            for (int k = kSplitFr * 2; k < BKV / 16; ++k)
+            for (int k = 3 * BKV / 64; k < BKV / 16; ++k)
               mma_f16_ts_warp(tmem + C_::o_col(t), tmem + C_::s_col(t) + k * 8,
-                              umma_desc_sw128(va + k * 2048, BKV * 128, 1024), idesc_o, 1u);
+                         umma_desc_sw128(va + k * 2048, BKV * 128, 1024), idesc_o, 1u);
             if (t == two) mma_commit_warp(&kv_empty[vst]);
             if (j == nb - 1) {
               mma_commit_warp(&o_full[t]);
@@ -527,11 +512,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             w[q] = pack_bf16(y.x, y.y);
           }
           tmem_st_32x32b_x16(s_addr + uint32_t(fr * 16), w);
-          if (fr == kSplitFr - 1 || fr == 3) {
+          if (fr == 2 || fr == 3) {
             tmem_st_wait();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(fr == kSplitFr - 1 ? &p_part[t] : &p_full[t]);
+            if (lane == 0) mbar_arrive(fr == 2 ? &p_part[t] : &p_full[t]);
           }
         }
         // row sum off the critical path (P is already with the tensor pipe)

@@ -265,8 +265,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       if (p.sync) producer_lockstep_exit(p, it);
     }
   } else if (warp == 1) {
-    // ---- MMA issuer (the leader CTA's warp 1; one elected lane issues) ----
-    if (rank == 0) {  // the whole warp runs the loop (uniform values), one elected lane issues
+    // ---- MMA issuer (one thread of the leader CTA) ----
+    if (lane == 0 && rank == 0) {
       const uint32_t idesc = umma_idesc(kBF16 ? 1u : 2u, BM * kCta, BN, p.a_mn, p.b_mn);
       // K-major: 8-row x 128-byte swizzle atoms stacked along MN (SBO 1024),
       // K advances 32 bytes per MMA inside the atom.
@@ -304,19 +304,19 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             const uint64_t bd = umma_desc_sw128(sb + ob + kk * b_step, b_lbo, b_sbo, b_lt);
             const uint32_t acc = (i | k) != 0;
             if (kCta == 2) {
-              if (kBF16) mma_f16_2sm_warp(d_tmem, ad, bd, idesc, acc);
-              else mma_tf32_2sm_warp(d_tmem, ad, bd, idesc, acc);
+              if (kBF16) mma_f16_2sm(d_tmem, ad, bd, idesc, acc);
+              else mma_tf32_2sm(d_tmem, ad, bd, idesc, acc);
             } else {
-              if (kBF16) mma_f16_warp(d_tmem, ad, bd, idesc, acc);
-              else mma_tf32_warp(d_tmem, ad, bd, idesc, acc);
+              if (kBF16) mma_f16(d_tmem, ad, bd, idesc, acc);
+              else mma_tf32(d_tmem, ad, bd, idesc, acc);
             }
           }
           // the stage is free once every pair that reads it has consumed it
-          if (kCta == 2) mma_commit_2sm_warp(&empty_bar[s], kMc == 2 ? 0xF : 0x3);
-          else mma_commit_warp(&empty_bar[s]);
+          if (kCta == 2) mma_commit_2sm(&empty_bar[s], kMc == 2 ? 0xF : 0x3);
+          else mma_commit(&empty_bar[s]);
         }
-        if (kCta == 2) mma_commit_2sm_warp(&acc_full[as], uint16_t(0x3u << (2 * q)));
-        else mma_commit_warp(&acc_full[as]);
+        if (kCta == 2) mma_commit_2sm(&acc_full[as], uint16_t(0x3u << (2 * q)));
+        else mma_commit(&acc_full[as]);
       }
     }
   } else {
@@ -544,7 +544,7 @@ __global__ void __launch_bounds__(kX3Threads, 1) gemm_x3_kernel(const __grid_con
     }
   } else if (warp == 9) {
     // ---- MMA issuer: chunks of `chunk` K blocks into alternating buffers ----
-    if (rank == 0) {  // the whole warp runs the loop (uniform values), one elected lane issues
+    if (lane == 0 && rank == 0) {
       const uint32_t idesc = umma_idesc(2u, BM * kCta, BN, p.a_mn, p.b_mn);
       const uint32_t a_lbo = p.a_mn ? C_::BK * 128 : 16, b_lbo = p.b_mn ? C_::BK * 128 : 16;
       const uint32_t a_step = p.a_mn ? C_::UMMA_K * 128 : 32, b_step = p.b_mn ? C_::UMMA_K * 128 : 32;
@@ -576,14 +576,14 @@ __global__ void __launch_bounds__(kX3Threads, 1) gemm_x3_kernel(const __grid_con
               const uint64_t ad = umma_desc_sw128(sa + oa + kk * a_step, a_lbo, a_sbo, a_lt);
               const uint64_t bd = umma_desc_sw128(sb + ob + kk * b_step, b_lbo, b_sbo, b_lt);
               const uint32_t acc = (q | k) != 0;  // each chunk starts a fresh partial
-              if (kCta == 2) mma_tf32_2sm_warp(d_tmem, ad, bd, idesc, acc);
-              else mma_tf32_warp(d_tmem, ad, bd, idesc, acc);
+              if (kCta == 2) mma_tf32_2sm(d_tmem, ad, bd, idesc, acc);
+              else mma_tf32(d_tmem, ad, bd, idesc, acc);
             }
-            if (kCta == 2) mma_commit_2sm_warp(&empty_bar[s]);
-            else mma_commit_warp(&empty_bar[s]);
+            if (kCta == 2) mma_commit_2sm(&empty_bar[s]);
+            else mma_commit(&empty_bar[s]);
           }
-          if (kCta == 2) mma_commit_2sm_warp(&part_full[b]);
-          else mma_commit_warp(&part_full[b]);
+          if (kCta == 2) mma_commit_2sm(&part_full[b]);
+          else mma_commit(&part_full[b]);
         }
       }
     }
