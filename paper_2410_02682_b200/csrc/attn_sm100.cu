@@ -373,16 +373,27 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
       const uint32_t idesc_s = umma_idesc(1u, BQ, BKV, 0u, 0u);  // Q, K both K-major (d)
       const uint32_t idesc_o = umma_idesc(1u, BQ, D, 0u, 1u);    // P from TMEM (keys), V MN-major (d)
       int kvn = 0, qn0 = 0, qn1 = 0, pn0 = 0, pn1 = 0, on0 = 0, on1 = 0;
+      // Descriptors are built once per operand base; a K step adds its byte
+      // offset / 16 to the start-address field (no carry below 256 KiB).
+      // (attn_big: 0.2350 vs 0.2373 ms rebuilding them per MMA; TMEM
+      // addresses as compile-time constants instead of the allocated base
+      // measured slower still, 0.2434.)
       auto issue_s = [&](int t, int kst) {
-        const uint32_t qa = smem_u32(sQ + t * C_::Q_BYTES);
-        const uint32_t ka = smem_u32(sKV + kst * C_::KV_BYTES);
+        const uint64_t qd = umma_desc_sw128(smem_u32(sQ + t * C_::Q_BYTES), 16, 1024);
+        const uint64_t kd = umma_desc_sw128(smem_u32(sKV + kst * C_::KV_BYTES), 16, 1024);
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
-          const uint32_t off = (k / 4) * 16384 + (k % 4) * 32;
-          mma_f16_warp(tmem + C_::s_col(t), umma_desc_sw128(qa + off, 16, 1024), umma_desc_sw128(ka + off, 16, 1024),
-                       idesc_s, k != 0);
+          const uint64_t off = uint64_t(((k / 4) * 16384 + (k % 4) * 32) >> 4);
+          mma_f16_warp(tmem + C_::s_col(t), qd + off, kd + off, idesc_s, k != 0);
         }
         mma_commit_warp(&s_full[t]);
+      };
+      auto issue_pv = [&](int t, uint32_t va, int k0, int k1, bool fresh) {
+        const uint64_t vd = umma_desc_sw128(va, BKV * 128, 1024);
+#pragma unroll
+        for (int k = k0; k < k1; ++k)
+          mma_f16_ts_warp(tmem + C_::o_col(t), tmem + C_::s_col(t) + k * 8, vd + uint64_t((k * 2048) >> 4), idesc_o,
+                          !(fresh && k == 0));
       };
       auto take = [&]() {  // next ring stage, full
         const int st = kvn % NS;
@@ -416,17 +427,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             mbar_wait(&o_ok[t], pn & 1);
             mbar_wait(&p_part[t], pn & 1);
             tc_fence_after();
-#pragma unroll
-            for (int k = 0; k < kSplitFr * 2; ++k)
-              mma_f16_ts_warp(tmem + C_::o_col(t), tmem + C_::s_col(t) + k * 8,
-                              umma_desc_sw128(va + k * 2048, BKV * 128, 1024), idesc_o, (j | k) != 0);
+            issue_pv(t, va, 0, kSplitFr * 2, j == 0);
             mbar_wait(&p_full[t], pn & 1);
             ++pn;
             tc_fence_after();
-#pragma unroll
-            for (int k = kSplitFr * 2; k < BKV / 16; ++k)
-              mma_f16_ts_warp(tmem + C_::o_col(t), tmem + C_::s_col(t) + k * 8,
-                              umma_desc_sw128(va + k * 2048, BKV * 128, 1024), idesc_o, 1u);
+            issue_pv(t, va, kSplitFr * 2, BKV / 16, false);
             if (t == two) mma_commit_warp(&kv_empty[vst]);
             if (j == nb - 1) {
               mma_commit_warp(&o_full[t]);
