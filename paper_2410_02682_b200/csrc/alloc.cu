@@ -113,6 +113,7 @@ void ed_plan_h::allocate() {
         op.maps.clear();
         op.regions.clear();
         int total_sib = 0;
+        std::vector<const void*> b_src;  // each region's B operand buffer
         for (int head : op.heads) {
           const auto& sibs = region_sibs_.at(head);
           GemmRegion r{};
@@ -125,6 +126,13 @@ void ed_plan_h::allocate() {
           // MN-major fp32 operands need the 32-byte-atom swizzle (see gemm_sm100.cu)
           const CUtensorMapSwizzle mn_swz = b16 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
           const int es_op = b16 ? 2 : 4;
+          // batch-segmented operand: one set of sibling maps per segment, the
+          // tiles of batch b use set b / bseg (gemm_sm100.cu)
+          const BSeg* bs = bseg_.count(u.producer) ? &bseg_.at(u.producer) : nullptr;
+          const int nbs = bs ? int(bs->segs.at(sibs[0]).size()) : 1;
+          r.bseg = bs ? int(bs->bseg) : 0;
+          r.bseg_b = bs ? bs->role : 0;
+          for (int bsi = 0; bsi < nbs; ++bsi)
           for (int pseudo = 0; pseudo < r.n_sib; ++pseudo) {
             const int sidx = sibs[pseudo / nseg];
             const int seg = pseudo % nseg;
@@ -132,6 +140,22 @@ void ed_plan_h::allocate() {
             int da = resolve(j.deps[g.a_slot]), db = resolve(j.deps[g.b_slot]);
             Dim am = g.am, ak = g.ak, ab = g.ab, bn = g.bn, bk = g.bk, bb = g.bb;
             int64_t aoff = 0, boff = 0;
+            if (bs) {
+              const Seg& sg = bs->segs.at(sidx)[size_t(bsi)];
+              if (bs->role == 0) {
+                da = sg.owner;
+                am = sg.mn;
+                ak = sg.k;
+                ab = sg.b;
+                aoff = sg.off;
+              } else {
+                db = sg.owner;
+                bn = sg.mn;
+                bk = sg.k;
+                bb = sg.b;
+                boff = sg.off;
+              }
+            }
             if (ks) {
               const Seg& sg = ks->segs.at(sidx)[seg];
               if (ks->role == 0) {
@@ -158,6 +182,7 @@ void ed_plan_h::allocate() {
               if (!pa || !pb) throw ed_error(ED_ERR_PLAN, "GEMM operand buffer missing");
               pa += aoff * es_op;
               pb += boff * es_op;
+              if (bsi == 0 && pseudo == 0 && part == 0) b_src.push_back(pb);
               CUtensorMap ma, mb;
               if (!g.a_mn)
                 make_map(&ma, pa, b16, ak.ext, am.ext, am.stride, ab.ext, ab.stride, BK, uint32_t(gemm_a_box_rows(p.mc)));
@@ -189,6 +214,9 @@ void ed_plan_h::allocate() {
           op.regions.push_back(r);
         }
         p.n_regions = int(op.regions.size());
+        // regions that all read one B operand per batch: order tiles batch-major
+        p.region_inner = p.n_regions > 1 && p.batch > 1 &&
+                         std::all_of(b_src.begin(), b_src.end(), [&](const void* q) { return q == b_src[0]; });
         const double ab = double(g.am.ext) * g.ak.ext * g.ab.ext + double(g.bn.ext) * g.bk.ext * g.bb.ext;
         const double cbytes = double(g.am.ext) * g.bn.ext * g.ab.ext *
                               ((op.regions[0].c32 ? 4 : 0) + (op.regions[0].c16 ? 2 : 0));

@@ -30,6 +30,25 @@ bool merge_dim(const labels& tl, const shape& text, const labels& cls, Dim& out,
   return true;
 }
 
+// merge_dim for a sub-box of a row-major tensor: the labels `cls` keep
+// extents dst_ext of a tensor laid out with extents src_ext; fails if the kept
+// part of the class is not one strided run (an inner label cut short).
+static bool merge_sub(const labels& tl, const shape& src_ext, const shape& dst_ext, const labels& cls, Dim& out) {
+  shape strides(tl.size(), 1);
+  for (int i = int(tl.size()) - 2; i >= 0; --i) strides[i] = strides[i + 1] * src_ext[i + 1];
+  std::vector<int> pos;
+  for (size_t i = 0; i < tl.size(); ++i)
+    if (std::find(cls.begin(), cls.end(), tl[i]) != cls.end() && dst_ext[i] > 1) pos.push_back(int(i));
+  out = Dim{};
+  if (pos.empty()) return true;
+  for (size_t j = 0; j + 1 < pos.size(); ++j)
+    if (strides[pos[j]] != strides[pos[j + 1]] * dst_ext[pos[j + 1]]) return false;
+  out.ext = 1;
+  for (int q : pos) out.ext *= dst_ext[q];
+  out.stride = strides[pos.back()];
+  return true;
+}
+
 bool map_gemm(const Vtx& v, const shape& local_xy, bool bf16, GemmMap& g, std::string& why) {
   if (v.arity != 2 || v.join != ED_JOIN_MUL || v.agg != ED_AGG_SUM) {
     why = "not mul/sum";
@@ -604,6 +623,89 @@ void ed_plan_h::build() {
     }
   }
 
+  // ---- batch-segmented operands: a GEMM operand that is a refinement pasting
+  // producer regions along the batch label (e.g. C2's repartition from
+  // batch-sharded Z1 chunks to row-sharded Z2 inputs) is read in place: the
+  // tiles of batch b load it from segment b / bseg through that segment's own
+  // tensor map, offset to the sub-box the refinement keeps, so the pasted
+  // chunk is never materialised (runtime.cc:198-269 copies it) ----
+  bseg_.clear();
+  for (auto& [c, g] : gmap) {
+    if (flash_skip_.count(c) || kseg_.count(c) || g.Bc.size() != 1) continue;
+    bool c_local = true;
+    for (int id = 0; id < ne; ++id)
+      if (X[id].producer == c && !local[id]) c_local = false;
+    if (!c_local) continue;
+    for (int role = 0; role < 2 && !bseg_.count(c); ++role) {
+      const int slot = role == 0 ? g.a_slot : g.b_slot;
+      const labels& lop = slot == 0 ? V[c].lx : V[c].ly;
+      const int bd = int(std::find(lop.begin(), lop.end(), g.Bc[0]) - lop.begin());
+      if (bd >= int(lop.size())) continue;
+      const Dim& want_mn = role == 0 ? g.am : g.bn;
+      const Dim& want_k = role == 0 ? g.ak : g.bk;
+      BSeg bs;
+      bs.role = role;
+      bool ok = true;
+      std::vector<int> refs;
+      for (int jid = 0; jid < ne && ok; ++jid) {
+        if (X[jid].kind != ED_EXEC_JOIN || X[jid].producer != c) continue;
+        const int ref = X[jid].deps[slot];
+        const Ex& R = X[ref];
+        ok = R.kind == ED_EXEC_REFINEMENT && local[ref] && owner[ref] == ref && !virt[ref] && srcs[ref].size() >= 2 &&
+             R.cb.size() == lop.size();
+        if (!ok) break;
+        const shape& bound = V[R.producer].bound;
+        const shape dc = region_partition(ref);
+        std::vector<Seg> segs;
+        for (auto& sr : srcs[ref]) {
+          shape de(lop.size());
+          int64_t off = 0, st = 1;
+          for (int d = int(lop.size()) - 1; d >= 0 && ok; --d) {
+            const int64_t c0 = R.key[size_t(d)] * (bound[size_t(d)] / dc[size_t(d)]), ce = R.cb[size_t(d)];
+            if (d == bd) {
+              ok = sr.r0[d] >= c0 && sr.r0[d] + sr.ext[d] <= c0 + ce;
+              de[d] = sr.ext[d];
+            } else {
+              ok = sr.r0[d] <= c0 && sr.r0[d] + sr.ext[d] >= c0 + ce;
+              de[d] = ce;
+              off += (c0 - sr.r0[d]) * st;
+            }
+            st *= sr.ext[d];
+          }
+          ok = ok && local[sr.id];
+          if (!ok) break;
+          Seg sg;
+          sg.owner = sr.id;
+          sg.k0 = sr.r0[bd] - R.key[size_t(bd)] * (bound[size_t(bd)] / dc[size_t(bd)]);
+          sg.kext = sr.ext[bd];
+          sg.off = off;
+          const labels& mcls = role == 0 ? g.Mc : g.Nc;
+          ok = merge_sub(lop, sr.ext, de, mcls, sg.mn) && merge_sub(lop, sr.ext, de, g.Kc, sg.k) &&
+               merge_sub(lop, sr.ext, de, g.Bc, sg.b);
+          // the segment must present exactly the GEMM's operand shape
+          ok = ok && sg.mn.ext == want_mn.ext && sg.k.ext == want_k.ext && sg.b.ext == sg.kext &&
+               (sg.off * (bf16 ? 2 : 4)) % 16 == 0;
+          segs.push_back(sg);
+        }
+        if (!ok) break;
+        std::sort(segs.begin(), segs.end(), [](const Seg& a, const Seg& b) { return a.k0 < b.k0; });
+        int64_t covered = 0;
+        for (auto& sg : segs) {
+          ok = ok && sg.kext == segs[0].kext && sg.k0 == covered;
+          covered += sg.kext;
+        }
+        ok = ok && covered == R.cb[size_t(bd)] && (bs.bseg == 0 || bs.bseg == segs[0].kext);
+        if (!ok) break;
+        bs.bseg = segs[0].kext;
+        bs.segs[jid] = segs;
+        refs.push_back(ref);
+      }
+      if (!ok || refs.empty()) continue;
+      bseg_[c] = bs;
+      for (int ref : refs) virt[ref] = 1;
+    }
+  }
+
   // softmax inputs that are a paste of column segments (rank 2) are read in place
   for (auto& [y, sm] : softmax_) {
     bool ok = true;
@@ -645,6 +747,8 @@ void ed_plan_h::build() {
       const int d = X[jid].deps[k];
       if (kseg_.count(w) && k == (kseg_[w].role == 0 ? gmap[w].a_slot : gmap[w].b_slot)) {
         for (auto& sg : kseg_[w].segs.at(jid)) r.push_back(sg.owner);
+      } else if (bseg_.count(w) && k == (bseg_[w].role == 0 ? gmap[w].a_slot : gmap[w].b_slot)) {
+        for (auto& sg : bseg_[w].segs.at(jid)) r.push_back(sg.owner);
       } else {
         r.push_back(local[d] ? owner[d] : d);
       }
@@ -692,8 +796,11 @@ void ed_plan_h::build() {
         for (int k = 0; k < int(u.deps.size()); ++k) {
           const int d = u.deps[k];
           const bool segmented = kseg_.count(w) && k == (kseg_[w].role == 0 ? gmap[w].a_slot : gmap[w].b_slot);
+          const bool bsegmented = bseg_.count(w) && k == (bseg_[w].role == 0 ? gmap[w].a_slot : gmap[w].b_slot);
           if (segmented) {
             for (auto& sg : kseg_[w].segs.at(id)) reads.push_back(sg.owner);
+          } else if (bsegmented) {
+            for (auto& sg : bseg_[w].segs.at(id)) reads.push_back(sg.owner);
           } else {
             reads.push_back(local[d] ? owner[d] : d);
           }

@@ -66,11 +66,23 @@ template <int TILE_M, int BN>
 __device__ __forceinline__ TileCoord tile_coord(const GemmLaunch& p, int t, int tiles_m, int tiles_n) {
   TileCoord c;
   const int per_batch = tiles_m * tiles_n;
-  const int per_region = per_batch * p.batch;
-  c.region = t / per_region;
-  int r = t - c.region * per_region;
-  c.b = r / per_batch;
-  r -= c.b * per_batch;
+  int r;
+  if (p.region_inner) {
+    // batch-major over the regions: the regions' tiles of one batch run
+    // together, so a B operand all regions share (C2's repartitioned Z2
+    // reading W) leaves HBM once per batch instead of once per region
+    const int per_b = per_batch * p.n_regions;
+    c.b = t / per_b;
+    r = t - c.b * per_b;
+    c.region = r / per_batch;
+    r -= c.region * per_batch;
+  } else {
+    const int per_region = per_batch * p.batch;
+    c.region = t / per_region;
+    r = t - c.region * per_region;
+    c.b = r / per_batch;
+    r -= c.b * per_batch;
+  }
   // grouped raster: kGroupM tile rows advance together along N, so one wave
   // of ~74 cluster tiles touches ~8 A panels + ~9 B panels instead of
   // 3 + tiles_n, and the panels it shares stay in L2 (hoc: 8192^2 tiles)
@@ -210,8 +222,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         const int am = tc.m0 + int(rank) * BM, bn = tc.n0 + int(rank) * C_::B_ROWS;
         // kMc: CTAs with the same rank in both pairs hold the same A rows
         const uint16_t a_mask = uint16_t((1u << rank) | (1u << (2 + rank)));
+        // batch coordinates of A and B (a batch-segmented operand: its segment's)
+        const int bseg_i = reg.bseg ? tc.b / reg.bseg : 0;
+        const int ba = reg.bseg && !reg.bseg_b ? tc.b % reg.bseg : tc.b;
+        const int bb = reg.bseg && reg.bseg_b ? tc.b % reg.bseg : tc.b;
         for (int sib = 0; sib < reg.n_sib; ++sib) {
-          const CUtensorMap* ma = p.maps + reg.map0 + C_::NMAP * sib;
+          const CUtensorMap* ma = p.maps + reg.map0 + C_::NMAP * (bseg_i * reg.n_sib + sib);
           const CUtensorMap* mb = ma + 1;
           for (int kb = 0; kb < kblocks; ++kb, ++it) {
             if (p.sync) producer_lockstep(p, it, sync_on);
@@ -222,9 +238,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             uint8_t* sa = smem + s * C_::STAGE_BYTES;
             uint8_t* sb = sa + C_::A_BYTES;
             if (rank == 0) mbar_expect_tx(&full_bar[s], C_::STAGE_BYTES * kCta);
-            auto load = [&](void* dst, const CUtensorMap* m, int c0, int c1) {
-              if (kCta == 2) tma_load_3d_2sm(dst, m, &full_bar[s], c0, c1, tc.b);
-              else tma_load_3d(dst, m, &full_bar[s], c0, c1, tc.b);
+            auto load = [&](void* dst, const CUtensorMap* m, int c0, int c1, int cb) {
+              if (kCta == 2) tma_load_3d_2sm(dst, m, &full_bar[s], c0, c1, cb);
+              else tma_load_3d(dst, m, &full_bar[s], c0, c1, cb);
             };
 #pragma unroll
             for (int part = 0; part < (kX3 ? 2 : 1); ++part) {  // hi, then (kX3) lo copies
@@ -236,27 +252,27 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
                 // this pair's half of the A box, multicast to both pairs (K-major:
                 // 64 of the 128 rows; MN-major: half of the 128-byte MN atoms)
                 if (!p.a_mn) {
-                  tma_load_3d_2sm_mc(pa + q * (BM / 2) * 128, pma, &full_bar[s], k0, am + int(q) * (BM / 2), tc.b,
+                  tma_load_3d_2sm_mc(pa + q * (BM / 2) * 128, pma, &full_bar[s], k0, am + int(q) * (BM / 2), ba,
                                      a_mask);
                 } else {
                   constexpr int NA = BM / C_::MN_ATOM;
 #pragma unroll
                   for (int i = int(q) * NA / 2; i < (int(q) + 1) * NA / 2; ++i)
-                    tma_load_3d_2sm_mc(pa + i * C_::BK * 128, pma, &full_bar[s], am + i * C_::MN_ATOM, k0, tc.b,
+                    tma_load_3d_2sm_mc(pa + i * C_::BK * 128, pma, &full_bar[s], am + i * C_::MN_ATOM, k0, ba,
                                        a_mask);
                 }
               } else if (!p.a_mn) {
-                load(pa, pma, k0, am);
+                load(pa, pma, k0, am, ba);
               } else {
 #pragma unroll
-                for (int i = 0; i < BM / C_::MN_ATOM; ++i) load(pa + i * C_::BK * 128, pma, am + i * C_::MN_ATOM, k0);
+                for (int i = 0; i < BM / C_::MN_ATOM; ++i) load(pa + i * C_::BK * 128, pma, am + i * C_::MN_ATOM, k0, ba);
               }
               if (!p.b_mn) {
-                load(pb, pmb, k0, bn);
+                load(pb, pmb, k0, bn, bb);
               } else {
 #pragma unroll
                 for (int i = 0; i < C_::B_ROWS / C_::MN_ATOM; ++i)
-                  load(pb + i * C_::BK * 128, pmb, bn + i * C_::MN_ATOM, k0);
+                  load(pb + i * C_::BK * 128, pmb, bn + i * C_::MN_ATOM, k0, bb);
               }
             }
           }
@@ -502,8 +518,11 @@ __global__ void __launch_bounds__(kX3Threads, 1) gemm_x3_kernel(const __grid_con
         const TileCoord tc = tile_coord<C_::TILE_M, BN>(p, t, tiles_m, tiles_n);
         const GemmRegion reg = p.regions[tc.region];
         const int am = tc.m0 + int(rank) * BM, bn = tc.n0 + int(rank) * C_::B_ROWS;
+        const int bseg_i = reg.bseg ? tc.b / reg.bseg : 0;
+        const int ba = reg.bseg && !reg.bseg_b ? tc.b % reg.bseg : tc.b;
+        const int bb = reg.bseg && reg.bseg_b ? tc.b % reg.bseg : tc.b;
         for (int sib = 0; sib < reg.n_sib; ++sib) {
-          const CUtensorMap* ma = p.maps + reg.map0 + C_::NMAP * sib;
+          const CUtensorMap* ma = p.maps + reg.map0 + C_::NMAP * (bseg_i * reg.n_sib + sib);
           for (int kb = 0; kb < kblocks; ++kb, ++it) {
             if (p.sync) producer_lockstep(p, it, sync_on);
             const int s = it % STAGES;
@@ -513,9 +532,9 @@ __global__ void __launch_bounds__(kX3Threads, 1) gemm_x3_kernel(const __grid_con
             uint8_t* sa = smem + s * C_::STAGE_BYTES;
             uint8_t* sb = sa + C_::A_BYTES;
             if (rank == 0) mbar_expect_tx(&full_bar[s], C_::STAGE_BYTES * kCta);
-            auto load = [&](void* dst, const CUtensorMap* m, int c0, int c1) {
-              if (kCta == 2) tma_load_3d_2sm(dst, m, &full_bar[s], c0, c1, tc.b);
-              else tma_load_3d(dst, m, &full_bar[s], c0, c1, tc.b);
+            auto load = [&](void* dst, const CUtensorMap* m, int c0, int c1, int cb) {
+              if (kCta == 2) tma_load_3d_2sm(dst, m, &full_bar[s], c0, c1, cb);
+              else tma_load_3d(dst, m, &full_bar[s], c0, c1, cb);
             };
 #pragma unroll
             for (int part = 0; part < 2; ++part) {
@@ -524,17 +543,17 @@ __global__ void __launch_bounds__(kX3Threads, 1) gemm_x3_kernel(const __grid_con
               const CUtensorMap* pma = ma + 2 * part;
               const CUtensorMap* pmb = ma + 1 + 2 * part;
               if (!p.a_mn) {
-                load(pa, pma, k0, am);
+                load(pa, pma, k0, am, ba);
               } else {
 #pragma unroll
-                for (int i = 0; i < BM / C_::MN_ATOM; ++i) load(pa + i * C_::BK * 128, pma, am + i * C_::MN_ATOM, k0);
+                for (int i = 0; i < BM / C_::MN_ATOM; ++i) load(pa + i * C_::BK * 128, pma, am + i * C_::MN_ATOM, k0, ba);
               }
               if (!p.b_mn) {
-                load(pb, pmb, k0, bn);
+                load(pb, pmb, k0, bn, bb);
               } else {
 #pragma unroll
                 for (int i = 0; i < C_::B_ROWS / C_::MN_ATOM; ++i)
-                  load(pb + i * C_::BK * 128, pmb, bn + i * C_::MN_ATOM, k0);
+                  load(pb + i * C_::BK * 128, pmb, bn + i * C_::MN_ATOM, k0, bb);
               }
             }
           }

@@ -17,6 +17,10 @@ struct GemmRegion {
   int cmap16;
   float* c32;
   void* c16;
+  // batch-segmented operand (bseg > 0): the operand (A if bseg_b == 0, else
+  // B) of batch b is read in place from segment b / bseg at batch coordinate
+  // b % bseg; segment s has its own sibling maps at map0 + NMAP * n_sib * s
+  int bseg, bseg_b;
 };
 
 // One launch: every region of one einsum on this rank (same chunk shapes).
@@ -34,6 +38,7 @@ struct GemmLaunch {
   int bn;                     // tile width: 256 or 128 (gemm_pick_bn)
   int mc;                     // 1: 4-CTA clusters, two 2-SM pairs sharing (multicasting) the A panel
   int group_m;
+  int region_inner;           // 1: tiles ordered batch-major across regions (regions share their B operand)
   int chunk;                  // x3: K blocks per TMEM partial promoted into fp32 running sums (0: off)
   // loose lockstep of the producers (experiment, x3 kernel): a CTA issues the
   // loads of epoch e (sync_g K blocks) only once every CTA has issued epoch

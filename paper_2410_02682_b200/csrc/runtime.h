@@ -297,8 +297,9 @@ struct ed_plan_h {
   std::map<int, Flash> flash_;                    // O vertex -> fused attention block
   struct Seg {
     int owner;                                    // source region buffer
-    int64_t k0, kext;                             // its range along the contraction label
+    int64_t k0, kext;                             // its range along the contraction (KSeg) / batch (BSeg) label
     Dim mn, k, b;                                 // its layout for the GEMM classes
+    int64_t off = 0;                              // BSeg: element offset of the kept sub-box in the source
   };
   struct KSeg {
     int role = 0;                                 // 0: MMA-A operand segmented, 1: MMA-B
@@ -306,6 +307,12 @@ struct ed_plan_h {
     std::map<int, std::vector<Seg>> segs;         // join -> segments in K order
   };
   std::map<int, KSeg> kseg_;                      // GEMM einsum -> K-segmented operand
+  struct BSeg {
+    int role = 0;                                 // 0: MMA-A operand segmented, 1: MMA-B
+    int64_t bseg = 0;                             // batches per segment
+    std::map<int, std::vector<Seg>> segs;         // join -> segments in batch order
+  };
+  std::map<int, BSeg> bseg_;                      // GEMM einsum -> batch-segmented operand
   std::set<int> flash_skip_;                      // einsums computed inside a Flash op
   std::map<int, Softmax> softmax_;                // Y vertex -> fused row-softmax chain
   std::map<int, std::pair<int, double>> epi_;     // GEMM einsum -> epilogue map (op, c)
