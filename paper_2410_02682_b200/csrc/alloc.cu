@@ -72,6 +72,8 @@ void ed_plan_h::allocate() {
   }
 
   auto resolve = [&](int dep) { return local[dep] ? owner[dep] : dep; };
+  const bool x3 = opt.precision == ED_PREC_F32X3;
+  const bool lo_epi = x3 && x3_lo_by_producer();
   size_t gemm_maps_total = 0, gemm_regions_total = 0, jptrs_total = 0, rect_total = 0;
   size_t attn_maps_total = 0, attn_regions_total = 0, rowseg_total = 0;
   for (auto& op : ops) {
@@ -119,7 +121,6 @@ void ed_plan_h::allocate() {
           GemmRegion r{};
           r.n_sib = int(sibs.size());
           r.map0 = int(op.maps.size());
-          const bool x3 = opt.precision == ED_PREC_F32X3;
           const KSeg* ks = kseg_.count(u.producer) ? &kseg_.at(u.producer) : nullptr;
           const int nseg = ks ? int(ks->segs.at(sibs[0]).size()) : 1;
           r.n_sib = int(sibs.size()) * nseg;
@@ -196,7 +197,7 @@ void ed_plan_h::allocate() {
             total_sib += x3 ? 2 : 1;
           }
           r.c32 = static_cast<float*>(buf[head].main);
-          r.c16 = buf[head].b16;
+          r.c16 = p.x3 ? (lo_epi ? buf[head].lo : nullptr) : buf[head].b16;  // x3: the epilogue writes the lo shadow
           // output tensor maps for the TMA-store epilogue (16-byte strides only)
           auto out_map = [&](void* base, bool o16) {
             const int oes = o16 ? 2 : 4;
@@ -210,7 +211,7 @@ void ed_plan_h::allocate() {
             return int(op.maps.size()) - 1;
           };
           r.cmap32 = out_map(r.c32, false);
-          r.cmap16 = out_map(r.c16, true);
+          r.cmap16 = out_map(r.c16, !p.x3);
           op.regions.push_back(r);
         }
         p.n_regions = int(op.regions.size());
@@ -219,7 +220,7 @@ void ed_plan_h::allocate() {
                          std::all_of(b_src.begin(), b_src.end(), [&](const void* q) { return q == b_src[0]; });
         const double ab = double(g.am.ext) * g.ak.ext * g.ab.ext + double(g.bn.ext) * g.bk.ext * g.bb.ext;
         const double cbytes = double(g.am.ext) * g.bn.ext * g.ab.ext *
-                              ((op.regions[0].c32 ? 4 : 0) + (op.regions[0].c16 ? 2 : 0));
+                              ((op.regions[0].c32 ? 4 : 0) + (op.regions[0].c16 ? (p.x3 ? 4 : 2) : 0));
         op.bytes = ab * (b16 ? 2 : 4) * total_sib + cbytes * p.n_regions;
         gemm_maps_total += op.maps.size();
         gemm_regions_total += op.regions.size();
@@ -296,8 +297,9 @@ void ed_plan_h::allocate() {
         p.deps = d_deps + first;
         p.n_deps = int(n);
         p.out = buf[id].main;
-        p.out16 = buf[id].b16;
-        op.bytes = double(u.sz) * (es + (p.out16 ? 2 : 0));
+        p.out16 = x3 ? (lo_epi ? buf[id].lo : nullptr) : buf[id].b16;  // x3: the lo shadow a later fp32x3 contraction reads
+        p.lo = x3;
+        op.bytes = double(u.sz) * (es + (p.out16 ? (x3 ? 4 : 2) : 0));
         double rd = 0;
         for (auto& s : srcs_)
           if (s.ref == id) {
@@ -367,6 +369,7 @@ void ed_plan_h::allocate() {
           op.rect.rows_per_block = int(std::max<int64_t>(1, (32768 / int64_t(es)) / std::max<int64_t>(1, inner)));
           op.rect.out = p.out;
           op.rect.out16 = p.out16;
+          op.rect.lo = p.lo;
           rect_total += op.groups.size();
         } else {
           op.groups.clear();
@@ -486,10 +489,11 @@ void ed_plan_h::allocate() {
           jp.x = buf[resolve(xr)].main;
           jp.y = sm.m_refs.empty() ? nullptr : buf[resolve(sm.m_refs[k])].main;
           jp.out = buf[yj].main;
-          jp.out16 = buf[yj].b16;
+          jp.out16 = x3 ? (lo_epi ? buf[yj].lo : nullptr) : buf[yj].b16;  // x3: the lo shadow a later fp32x3 contraction reads
           op.jptrs.push_back(jp);
-          op.bytes += double(X[yj].sz) * (es + (jp.out ? es : 0) + (jp.out16 ? 2 : 0));
+          op.bytes += double(X[yj].sz) * (es + (jp.out ? es : 0) + (jp.out16 ? (x3 ? 4 : 2) : 0));
         }
+        op.sm.lo = x3;
         op.sm.rows = X[sm.pairs[0].first].sz / sm.len;
         op.sm.len = int(sm.len);
         op.rowsegs.clear();

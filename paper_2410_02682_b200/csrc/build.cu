@@ -852,7 +852,7 @@ void ed_plan_h::build() {
   ops.clear();
   contraction_flops = 0;
   std::set<int> gemm_emitted;
-  std::set<int> split_done;
+  std::set<int> split_done;  // F32X3: chunks whose lo shadow exists (split, or written by their producer)
   for (int id = 0; id < ne; ++id) {
     for (auto& [d, dst] : xfer_at[id]) {
       if (rank_of(d) == me) {
@@ -895,7 +895,10 @@ void ed_plan_h::build() {
         Op op{OpKind::SOFTMAX};
         op.name = "softmax_rows:" + w.name;
         op.ptr = reinterpret_cast<void*>(id);
-        for (auto& [yj, xr] : softmax_[u.producer].pairs) op.heads.push_back(yj);
+        for (auto& [yj, xr] : softmax_[u.producer].pairs) {
+          op.heads.push_back(yj);
+          if (x3 && x3_lo_by_producer()) split_done.insert(yj);  // the kernel writes Y's lo shadow beside Y
+        }
         ops.push_back(op);
         continue;
       }
@@ -942,6 +945,7 @@ void ed_plan_h::build() {
           if (fused_head[h] && X[h].producer == u.producer) {
             op.heads.push_back(h);
             for (int s : region_sibs[h]) op.flops += 2.0 * double(X[s].fp);
+            if (x3 && x3_lo_by_producer()) split_done.insert(h);  // the x3 epilogue writes the region's lo shadow
           }
         ops.push_back(op);
       } else if (memmap_.count(u.producer)) {
@@ -972,6 +976,7 @@ void ed_plan_h::build() {
     op.name = "refine:" + w.name;
     op.ptr = reinterpret_cast<void*>(id);
     ops.push_back(op);
+    if (x3 && x3_lo_by_producer()) split_done.insert(id);  // the fold writes the lo shadow beside the chunk
   }
   if (opt.corrupt && first_join >= 0 && local[first_join]) {
     // after the op that produced the first join

@@ -287,13 +287,16 @@ __global__ void __launch_bounds__(NT) softmax_kernel(const SoftmaxParams p) {
     sum = block_reduce(sum, false);
     const float inv = __frcp_rn(sum);
     float* yo = jp.out ? static_cast<float*>(jp.out) + row * p.len : nullptr;
-    __nv_bfloat16* y16 = jp.out16 ? static_cast<__nv_bfloat16*>(jp.out16) + row * p.len : nullptr;
+    __nv_bfloat16* y16 = jp.out16 && !p.lo ? static_cast<__nv_bfloat16*>(jp.out16) + row * p.len : nullptr;
+    float* ylo = jp.out16 && p.lo ? static_cast<float*>(jp.out16) + row * p.len : nullptr;
+    auto lo_of = [](float x) { return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); };
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
       const int i = (j * NT + t) * 4;
       if (i >= p.len) continue;
       const float a = v[4 * j] * inv, b = v[4 * j + 1] * inv, c = v[4 * j + 2] * inv, d = v[4 * j + 3] * inv;
       if (yo) __stcs(reinterpret_cast<float4*>(yo + i), make_float4(a, b, c, d));
+      if (ylo) __stcs(reinterpret_cast<float4*>(ylo + i), make_float4(lo_of(a), lo_of(b), lo_of(c), lo_of(d)));
       if (y16) {
         __nv_bfloat162 h0 = __floats2bfloat162_rn(a, b), h1 = __floats2bfloat162_rn(c, d);
         uint2 w;

@@ -47,6 +47,7 @@ struct SoftmaxParams {
   int len;
   const RowSeg* segs;     // nullable: n_seg segments per join, each seg_w columns
   int n_seg, seg_w;
+  int lo;                 // 1: out16 is the fp32 lo shadow y - tf32(y) (fp32x3 consumers), 0: bf16
 };
 
 cudaError_t launch_softmax(const SoftmaxParams& p, int n_joins, cudaStream_t s);

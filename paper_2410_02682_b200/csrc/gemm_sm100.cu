@@ -458,6 +458,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 // sub-partitions all the same).
 constexpr int kX3Threads = 384;
 
+// x - tf32(x): the part of an fp32 value a kind::tf32 MMA drops (its 13 low
+// mantissa bits); the x3 kernel writes it as the "lo" shadow of its output
+// when a later fp32x3 contraction reads that output (split_lo_kernel's value)
+__device__ __forceinline__ float lo_of(float x) { return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+
 __device__ __forceinline__ float epi_f(int op, float c, float x) {
   if (op == 0) return x > 0.0f ? x : 0.0f;
   if (op == 2) return -x;
@@ -652,38 +657,25 @@ __global__ void __launch_bounds__(kX3Threads, 1) gemm_x3_kernel(const __grid_con
         for (int pass = 0; pass < 2; ++pass) {
           const int cm = pass == 0 ? reg.cmap32 : reg.cmap16;
           if (cm < 0) continue;
-          constexpr int kMaxSlices = HALF / 32;
+          constexpr int kSlices = HALF / 32;
 #pragma unroll
-          for (int sl = 0; sl < kMaxSlices; ++sl) {
-            const int cols = pass == 0 ? 32 : 64;
-            if (sl * cols >= HALF) break;
+          for (int sl = 0; sl < kSlices; ++sl) {
             if (lane == 0) bulk_wait_read<0>();
             __syncwarp();
             uint8_t* rowp = tile + lane * 128;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-              uint4 v;
-              if (pass == 0) {
-                const int e = sl * 32 + 4 * j;
-                v = make_uint4(__float_as_uint(acc[e]), __float_as_uint(acc[e + 1]), __float_as_uint(acc[e + 2]),
-                               __float_as_uint(acc[e + 3]));
-              } else {
-                const int e = (sl * 64 + 8 * j) % HALF;  // sl * 64 < HALF here
-                __nv_bfloat162 h0 = __floats2bfloat162_rn(acc[e], acc[e + 1]);
-                __nv_bfloat162 h1 = __floats2bfloat162_rn(acc[e + 2], acc[e + 3]);
-                __nv_bfloat162 h2 = __floats2bfloat162_rn(acc[e + 4], acc[e + 5]);
-                __nv_bfloat162 h3 = __floats2bfloat162_rn(acc[e + 6], acc[e + 7]);
-                v.x = *reinterpret_cast<uint32_t*>(&h0);
-                v.y = *reinterpret_cast<uint32_t*>(&h1);
-                v.z = *reinterpret_cast<uint32_t*>(&h2);
-                v.w = *reinterpret_cast<uint32_t*>(&h3);
-              }
+              const int e = sl * 32 + 4 * j;
+              const uint4 v = pass == 0 ? make_uint4(__float_as_uint(acc[e]), __float_as_uint(acc[e + 1]),
+                                                     __float_as_uint(acc[e + 2]), __float_as_uint(acc[e + 3]))
+                                        : make_uint4(__float_as_uint(lo_of(acc[e])), __float_as_uint(lo_of(acc[e + 1])),
+                                                     __float_as_uint(lo_of(acc[e + 2])), __float_as_uint(lo_of(acc[e + 3])));
               *reinterpret_cast<uint4*>(rowp + ((j ^ (lane & 7)) << 4)) = v;
             }
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              tma_store_3d_hint(p.maps + cm, tile, col0 + sl * cols, row0, tc.b, policy_evict_first());
+              tma_store_3d_hint(p.maps + cm, tile, col0 + sl * 32, row0, tc.b, policy_evict_first());
               bulk_commit();
             }
           }
@@ -692,13 +684,13 @@ __global__ void __launch_bounds__(kX3Threads, 1) gemm_x3_kernel(const __grid_con
         const int row = row0 + lane;
         const long long base = (long long)tc.b * p.c_sb + (long long)row * p.c_sm;
         float* c32 = reg.c32 ? reg.c32 + base : nullptr;
-        __nv_bfloat16* c16 = reg.c16 ? static_cast<__nv_bfloat16*>(reg.c16) + base : nullptr;
+        float* clo = reg.c16 ? static_cast<float*>(reg.c16) + base : nullptr;
         if (row < p.M) {
 #pragma unroll
           for (int e = 0; e < HALF; ++e) {
             if (col0 + e < p.N) {
               if (c32) c32[col0 + e] = acc[e];
-              if (c16) c16[col0 + e] = __float2bfloat16_rn(acc[e]);
+              if (clo) clo[col0 + e] = lo_of(acc[e]);
             }
           }
         }

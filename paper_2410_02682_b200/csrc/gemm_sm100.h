@@ -8,7 +8,9 @@ namespace ed {
 constexpr int kMaxSib = 8;  // aggregation siblings folded in one accumulator
 
 // One output region of an einsum: the sum over its aggregation siblings s of
-// A_s * B_s (K-concatenated), written to c32 and/or its bf16 shadow c16.
+// A_s * B_s (K-concatenated), written to c32 and/or its shadow c16: bf16 in
+// the bf16 / tf32 kernels, fp32 x - tf32(x) (the "lo" operand copy a later
+// fp32x3 contraction reads) in the x3 kernel.
 struct GemmRegion {
   int n_sib;
   int map0;        // maps[map0 + 2*s] = A_s, maps[map0 + 2*s + 1] = B_s; with x3

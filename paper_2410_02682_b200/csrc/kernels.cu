@@ -17,6 +17,9 @@ namespace ed {
 
 namespace {
 
+// x - tf32(x): the fp32 "lo" shadow an fp32x3 contraction reads beside x
+__device__ __forceinline__ float lo_f(float x) { return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+
 template <typename T> __device__ __forceinline__ T from_d(double v);
 template <> __device__ __forceinline__ float from_d<float>(double v) { return __double2float_rn(v); }
 template <> __device__ __forceinline__ double from_d<double>(double v) { return v; }
@@ -103,7 +106,8 @@ __global__ void refine_kernel(const RefineParams p) {
   for (int i = threadIdx.x; i < p.n_deps; i += blockDim.x) deps[i] = p.deps[i];
   __syncthreads();
   T* out = static_cast<T*>(p.out);
-  __nv_bfloat16* o16 = static_cast<__nv_bfloat16*>(p.out16);
+  __nv_bfloat16* o16 = p.lo ? nullptr : static_cast<__nv_bfloat16*>(p.out16);
+  float* olo = p.lo ? static_cast<float*>(p.out16) : nullptr;
   for (int64_t o = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; o < p.n_out;
        o += int64_t(gridDim.x) * blockDim.x) {
     int64_t g[kMaxRank];
@@ -130,6 +134,7 @@ __global__ void refine_kernel(const RefineParams p) {
     }
     if (out) out[o] = from_d<T>(acc);
     if (o16) o16[o] = __double2bfloat16(acc);
+    if (olo) olo[o] = lo_f(__double2float_rn(acc));
   }
 }
 
@@ -137,7 +142,8 @@ template <typename T>
 __global__ void __launch_bounds__(256) rect_kernel(const RectParams p) {
   const RectGroup& g = p.groups[blockIdx.y];
   T* out = static_cast<T*>(p.out);
-  __nv_bfloat16* o16 = static_cast<__nv_bfloat16*>(p.out16);
+  __nv_bfloat16* o16 = p.lo ? nullptr : static_cast<__nv_bfloat16*>(p.out16);
+  float* olo = p.lo ? static_cast<float*>(p.out16) : nullptr;
   const int r = p.rank;
   constexpr int V = 16 / sizeof(T);
   const int W = p.vec ? V : 1;                      // elements per slot
@@ -169,12 +175,22 @@ __global__ void __launch_bounds__(256) rect_kernel(const RectParams p) {
 #pragma unroll
         for (int e = 0; e < V; ++e) o16[dofs + e] = __double2bfloat16(double(acc[e]));
       }
+      if (olo) {
+        if constexpr (sizeof(T) == 4) {
+          *reinterpret_cast<float4*>(olo + dofs) =
+              make_float4(lo_f(float(acc[0])), lo_f(float(acc[1])), lo_f(float(acc[2])), lo_f(float(acc[3])));
+        } else {
+#pragma unroll
+          for (int e = 0; e < V; ++e) olo[dofs + e] = lo_f(float(acc[e]));
+        }
+      }
     } else {
       double acc = double(static_cast<const T*>(g.src[0])[so]);
       for (int k = 1; k < g.n_src; ++k)
         acc = double(from_d<T>(agg_d(p.agg, acc, double(static_cast<const T*>(g.src[k])[so]))));
       if (out) out[dofs] = from_d<T>(acc);
       if (o16) o16[dofs] = __double2bfloat16(acc);
+      if (olo) olo[dofs] = lo_f(__double2float_rn(acc));
     }
   }
 }

@@ -43,6 +43,7 @@ struct RefineParams {
   const DepRect* deps;      // device array, fold order
   void* out;
   void* out16;
+  int lo;                   // 1: out16 is the fp32 lo shadow x - tf32(x) (fp32x3), 0: bf16
 };
 
 // Fast refinement: the overlap rectangle of one producer region with the
@@ -65,6 +66,7 @@ struct RectParams {
   const RectGroup* groups;            // device array
   void* out;
   void* out16;
+  int lo;                             // 1: out16 is the fp32 lo shadow (fp32x3), 0: bf16
 };
 
 // Whole tensor <-> chunk buffers (chunk / assemble, relation.cc:31-78).

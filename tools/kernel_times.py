@@ -23,5 +23,6 @@ for _ in range(runs):
     for k in pp.kernel_stats():
         tot[k["name"]] = tot.get(k["name"], 0.0) + k["ms"] / runs
 print(name, os.path.basename(os.environ.get("ED_LIB_PATH", "libed_gpu.so")),
-      " ".join(f"{n}={v:.4f}" for n, v in sorted(tot.items(), key=lambda x: -x[1])[:4]))
+      f"total={sum(tot.values()):.4f}",
+      " ".join(f"{n}={v:.4f}" for n, v in sorted(tot.items(), key=lambda x: -x[1])[:int(os.environ.get('KT_TOP', '4'))]))
 pp.close()
