@@ -11,7 +11,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libed_gpu.so")
 SOURCES = ["api.cu", "plan.cu", "build.cu", "alloc.cu", "exec.cu", "io.cu", "placement.cu", "gemm_sm100.cu",
-           "kernels.cu", "ewise.cu", "attn_sm100.cu"]
+           "kernels.cu", "ewise.cu", "attn_sm100.cu", "attn_x3_sm100.cu"]
 HEADERS = ["runtime.h", "libm_exp.cuh", "ptx.cuh", "gemm_sm100.h", "kernels.h", "ewise.h", "attn_sm100.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # The toolchain's libstdc++.so link is missing (only the .a resolves); a static

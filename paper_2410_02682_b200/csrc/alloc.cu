@@ -408,25 +408,48 @@ void ed_plan_h::allocate() {
         a.scale = f.scale;
         op.maps.clear();
         op.aregions.clear();
+        a.x3 = x3;
         for (auto& r : f.regions) {
           AttnRegion ar{};
-          const void* q = buf[resolve(r[0])].b16;
-          const void* k = f.ktiles[size_t(&r - f.regions.data())].tiled ? nullptr : buf[resolve(r[1])].b16;
-          const void* v = f.vtiles[size_t(&r - f.regions.data())].tiled ? nullptr : buf[resolve(r[2])].b16;
-          if (!q) throw ed_error(ED_ERR_PLAN, "attention operand buffer missing");
+          // bf16: the operands' bf16 shadows; fp32x3: fp32 values (+ lo shadows)
+          auto opnd = [&](int id2) { return x3 ? buf[id2].main : buf[id2].b16; };
+          const void* q = opnd(resolve(r[0]));
+          const void* k = f.ktiles[size_t(&r - f.regions.data())].tiled ? nullptr : opnd(resolve(r[1]));
+          const void* v = f.vtiles[size_t(&r - f.regions.data())].tiled ? nullptr : opnd(resolve(r[2]));
+          if (!q || (x3 && !buf[resolve(r[0])].lo)) throw ed_error(ED_ERR_PLAN, "attention operand buffer missing");
           CUtensorMap m;
-          make_map(&m, q, true, gs.ak.ext, gs.am.ext, gs.am.stride, gs.ab.ext, gs.ab.stride, 64, 128);
+          if (x3) make_map(&m, buf[resolve(r[0])].lo, false, gs.ak.ext, gs.am.ext, gs.am.stride, gs.ab.ext, gs.ab.stride, 32, 128);
+          else make_map(&m, q, true, gs.ak.ext, gs.am.ext, gs.am.stride, gs.ab.ext, gs.ab.stride, 64, 128);
           ar.q = int(op.maps.size());
           op.maps.push_back(m);
+          if (x3) {
+            ar.q_tm = static_cast<const float*>(q);
+            ar.q_rs = gs.am.stride;
+            ar.q_hs = gs.ab.ext > 1 ? gs.ab.stride : 0;
+          }
           const size_t ri = size_t(&r - f.regions.data());
           // K: {d, keys, h}; V: {d, keys, h} — from the pasted chunk, or from each
           // source region of the grid with that region's own strides
-          auto kv_maps = [&](const KVTiles& t, const void* chunk, const Dim& dk, const Dim& keys, const Dim& hb,
-                             const labels& lop, int keyl, int hl, AttnSrc& out) {
+          // x3 boxes: K {32, 64} K-major; V {32, 32} MN-major (32-byte-atom swizzle);
+          // the lo twins follow the hi maps (AttnSrc::lo)
+          auto kv_map = [&](const void* base, int64_t dext, int64_t kext, int64_t kstr, int64_t hext, int64_t hstr,
+                            bool is_v) {
+            if (!x3) make_map(&m, base, true, dext, kext, kstr, hext, hstr, 64, 128);
+            else if (!is_v) make_map(&m, base, false, dext, kext, kstr, hext, hstr, 32, 64);
+            else make_map(&m, base, false, dext, kext, kstr, hext, hstr, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+            op.maps.push_back(m);
+          };
+          auto kv_maps = [&](const KVTiles& t, int chunk_id, const Dim& dk, const Dim& keys, const Dim& hb,
+                             const labels& lop, int keyl, int hl, bool is_v, AttnSrc& out) {
             out.base = int(op.maps.size());
+            out.lo = 0;
             if (!t.tiled) {
-              make_map(&m, chunk, true, dk.ext, keys.ext, keys.stride, hb.ext, hb.stride, 64, 128);
-              op.maps.push_back(m);
+              kv_map(opnd(chunk_id), dk.ext, keys.ext, keys.stride, hb.ext, hb.stride, is_v);
+              if (x3) {
+                if (!buf[chunk_id].lo) throw ed_error(ED_ERR_PLAN, "attention operand lo shadow missing");
+                kv_map(buf[chunk_id].lo, dk.ext, keys.ext, keys.stride, hb.ext, hb.stride, is_v);
+                out.lo = 1;
+              }
               out.nd = 1;
               out.keys = int(keys.ext);
               out.dw = int(dk.ext);
@@ -437,12 +460,13 @@ void ed_plan_h::allocate() {
             const int hd = int(std::find(lop.begin(), lop.end(), hl) - lop.begin());
             shape st(3, 1);
             for (int i = 1; i >= 0; --i) st[i] = st[i + 1] * t.ext[i + 1];
-            for (int o2 : t.owners) {
-              const void* b = buf[o2].b16;
-              if (!b) throw ed_error(ED_ERR_PLAN, "attention source buffer missing");
-              make_map(&m, b, true, t.ext[2], t.ext[kd], st[kd], t.ext[hd], st[hd], 64, 128);
-              op.maps.push_back(m);
-            }
+            for (int part = 0; part < (x3 ? 2 : 1); ++part)
+              for (int o2 : t.owners) {
+                const void* b = part ? buf[o2].lo : opnd(o2);
+                if (!b) throw ed_error(ED_ERR_PLAN, "attention source buffer missing");
+                kv_map(b, t.ext[2], t.ext[kd], st[kd], t.ext[hd], st[hd], is_v);
+              }
+            out.lo = x3 ? int(t.owners.size()) : 0;
             out.nd = t.nd;
             out.keys = int(t.keys);
             out.dw = int(t.dw);
@@ -450,10 +474,12 @@ void ed_plan_h::allocate() {
           };
           const labels& lk = gs.b_slot == 0 ? V[f.t1].lx : V[f.t1].ly;
           const labels& lv = go.b_slot == 0 ? V[f.o].lx : V[f.o].ly;
-          kv_maps(f.ktiles[ri], k, gs.bk, gs.bn, gs.bb, lk, gs.Nc.empty() ? -1 : gs.Nc[0], gs.Bc.empty() ? -1 : gs.Bc[0],
-                  ar.k);
-          kv_maps(f.vtiles[ri], v, go.bn, go.bk, go.bb, lv, go.Kc.empty() ? -1 : go.Kc[0], go.Bc.empty() ? -1 : go.Bc[0],
-                  ar.v);
+          (void)k;
+          (void)v;
+          kv_maps(f.ktiles[ri], resolve(r[1]), gs.bk, gs.bn, gs.bb, lk, gs.Nc.empty() ? -1 : gs.Nc[0],
+                  gs.Bc.empty() ? -1 : gs.Bc[0], false, ar.k);
+          kv_maps(f.vtiles[ri], resolve(r[2]), go.bn, go.bk, go.bb, lv, go.Kc.empty() ? -1 : go.Kc[0],
+                  go.Bc.empty() ? -1 : go.Bc[0], true, ar.v);
           auto out_map = [&](void* base, bool o16) {
             const int oes = o16 ? 2 : 4;
             bool ok = base && (go.cm.ext == 1 || (go.cm.stride * oes) % 16 == 0) &&
@@ -465,17 +491,29 @@ void ed_plan_h::allocate() {
             op.maps.push_back(mc);
             return int(op.maps.size()) - 1;
           };
-          ar.o32 = out_map(buf[r[3]].main, false);
-          ar.o16 = out_map(buf[r[3]].b16, true);
-          if ((buf[r[3]].main && ar.o32 < 0) || (buf[r[3]].b16 && ar.o16 < 0))
-            throw ed_error(ED_ERR_UNSUPPORTED, "attention output not 16-byte aligned");
+          if (x3) {
+            // row-per-thread float4 stores: d contiguous, 16-byte row / head strides
+            ar.o32 = ar.o16 = -1;
+            ar.o = static_cast<float*>(buf[r[3]].main);
+            ar.o_lo = static_cast<float*>(buf[r[3]].lo);
+            ar.o_rs = go.cm.stride;
+            ar.o_hs = go.cb.ext > 1 ? go.cb.stride : 0;
+            if (!ar.o || ar.o_rs % 4 || ar.o_hs % 4 || ar.q_rs % 4 || ar.q_hs % 4)
+              throw ed_error(ED_ERR_UNSUPPORTED, "attention output not 16-byte aligned");
+          } else {
+            ar.o32 = out_map(buf[r[3]].main, false);
+            ar.o16 = out_map(buf[r[3]].b16, true);
+            if ((buf[r[3]].main && ar.o32 < 0) || (buf[r[3]].b16 && ar.o16 < 0))
+              throw ed_error(ED_ERR_UNSUPPORTED, "attention output not 16-byte aligned");
+          }
           op.aregions.push_back(ar);
         }
         a.n_regions = int(op.aregions.size());
         op.bytes = 0;
         for (auto& r : f.regions)
-          op.bytes += double(X[r[0]].sz + X[r[1]].sz + X[r[2]].sz) * 2 + double(X[r[3]].sz) * (buf[r[3]].main ? 4 : 0) +
-                      double(X[r[3]].sz) * (buf[r[3]].b16 ? 2 : 0);
+          op.bytes += double(X[r[0]].sz + X[r[1]].sz + X[r[2]].sz) * (x3 ? 8 : 2) +
+                      double(X[r[3]].sz) * (buf[r[3]].main ? 4 : 0) + double(X[r[3]].sz) * (buf[r[3]].b16 ? 2 : 0) +
+                      double(X[r[3]].sz) * (x3 && buf[r[3]].lo ? 4 : 0);
         attn_maps_total += op.maps.size();
         attn_regions_total += op.aregions.size();
         break;

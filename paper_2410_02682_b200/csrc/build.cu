@@ -425,7 +425,8 @@ void ed_plan_h::build() {
     }
     // (3) attention block: T1 = Q K^T (GEMM, maybe with a fused scale), the
     // softmax chain on T1 (or its scaled map), O = T3 V (GEMM, K = the row
-    // label) -> one kernel; T1 and T3 are never materialised (bf16 only)
+    // label) -> one kernel; T1 and T3 are never materialised (bf16:
+    // attn_sm100.cu; fp32x3: attn_x3_sm100.cu)
     static const bool ftrace = std::getenv("ED_FUSE_TRACE") != nullptr;
 #define REJECT(k)                                                                            \
   {                                                                                          \
@@ -434,7 +435,7 @@ void ed_plan_h::build() {
     continue;                                                                                \
   }
     for (auto& [yv, sm] : softmax_) {
-      if (!bf16) break;
+      if (!bf16 && !(x3 && x3_attention_fused())) break;
       if (readers[yv].size() != 1 || is_output(yv) || !sm.m_refs.empty()) REJECT(1)
       const int o = readers[yv][0];
       if (!gmap.count(o) || V[o].inputs[gmap[o].a_slot] != yv || !has_local(o) || !all_local(yv)) REJECT(2)
@@ -454,7 +455,8 @@ void ed_plan_h::build() {
       const GemmMap& go = gmap[o];
       const int64_t H = gs.ab.ext, S = gs.am.ext, T = gs.bn.ext, Dd = gs.ak.ext;
       if (gs.a_mn || gs.b_mn || !go.b_mn || go.a_mn || go.ab.ext != H || go.am.ext != S || go.ak.ext != T ||
-          go.bn.ext != Dd || T != sm.len || !attn_supported(int(S), int(T), int(Dd)))
+          go.bn.ext != Dd || T != sm.len ||
+          !(x3 ? attn_x3_supported(int(S), int(T), int(Dd)) : attn_supported(int(S), int(T), int(Dd))))
         REJECT(6)
       // region correspondence: O region <- T3 chunk <- T1 region (single siblings)
       std::map<int, int> t1_of_y;
@@ -765,13 +767,21 @@ void ed_plan_h::build() {
       for (size_t q = 0; q < f.regions.size(); ++q) {
         const auto& r = f.regions[q];
         if (r[3] != id) continue;
-        buf[local[r[0]] ? owner[r[0]] : r[0]].need_16 = true;
+        auto need = [&](int o2) {  // bf16: the shadow; fp32x3: the value and its lo shadow
+          if (x3) {
+            buf[o2].need_main = true;
+            buf[o2].need_lo = true;
+          } else {
+            buf[o2].need_16 = true;
+          }
+        };
+        need(local[r[0]] ? owner[r[0]] : r[0]);
         for (int k = 1; k < 3; ++k) {
           const KVTiles& t = k == 1 ? f.ktiles[q] : f.vtiles[q];
           if (t.tiled)
-            for (int o2 : t.owners) buf[o2].need_16 = true;
+            for (int o2 : t.owners) need(o2);
           else
-            buf[local[r[k]] ? owner[r[k]] : r[k]].need_16 = true;
+            need(local[r[k]] ? owner[r[k]] : r[k]);
         }
       }
       continue;
@@ -906,6 +916,29 @@ void ed_plan_h::build() {
         if (!fused_head[id] || gemm_emitted.count(u.producer)) continue;
         gemm_emitted.insert(u.producer);
         const Flash& f = flash_.at(u.producer);
+        if (x3) {
+          // lo shadows of operands no producer wrote (receives, element-wise outputs)
+          auto split = [&](int o2) {
+            if (X[o2].kind == ED_EXEC_INPUT_CHUNK || !split_done.insert(o2).second) return;
+            Op sp{OpKind::SPLIT};
+            sp.name = "split_tf32";
+            sp.ptr = reinterpret_cast<void*>(o2);
+            sp.bytes = double(X[o2].sz) * 8;
+            ops.push_back(sp);
+          };
+          for (size_t q = 0; q < f.regions.size(); ++q) {
+            const auto& r = f.regions[q];
+            split(local[r[0]] ? owner[r[0]] : r[0]);
+            for (int k = 1; k < 3; ++k) {
+              const KVTiles& t = k == 1 ? f.ktiles[q] : f.vtiles[q];
+              if (t.tiled)
+                for (int o2 : t.owners) split(o2);
+              else
+                split(local[r[k]] ? owner[r[k]] : r[k]);
+            }
+            split_done.insert(r[3]);  // the kernel writes O's lo shadow
+          }
+        }
         Op op{OpKind::FLASH};
         op.name = "attention_fused:" + V[f.t1].name + ".." + w.name;
         op.ptr = reinterpret_cast<void*>(id);

@@ -24,7 +24,9 @@ void ed_plan_h::launch_op(size_t i, cudaStream_t s, bool branch) {
     case OpKind::EWISE:
       CUDA_OK(launch_ewise(op.ew, int(op.jptrs.size()), f64, opt.precision == ED_PREC_FP32, s));
       break;
-    case OpKind::FLASH: CUDA_OK(launch_attn(op.attn, ctx->num_sms, s)); break;
+    case OpKind::FLASH:
+      CUDA_OK(op.attn.x3 ? launch_attn_x3(op.attn, ctx->num_sms, s) : launch_attn(op.attn, ctx->num_sms, s));
+      break;
     case OpKind::SPLIT:
       CUDA_OK(launch_split_lo(static_cast<const float*>(op.gen.x), static_cast<float*>(op.gen.out), op.gen.n_out, s));
       break;
@@ -147,6 +149,7 @@ void ed_plan_h::enqueue(cudaStream_t s) {
 void ed_plan_h::record() {
   CUDA_OK(gemm_prepare());
   CUDA_OK(attn_prepare());
+  CUDA_OK(attn_x3_prepare());
   if (!ev0) CUDA_OK(cudaEventCreate(&ev0));
   if (!ev1) CUDA_OK(cudaEventCreate(&ev1));
   if (opt.profile && op_events.size() != ops.size() + 1) {  // every entry point that enqueues (ed_run, ed_run_steps)

@@ -198,6 +198,15 @@ bool map_memory(const Vtx& v, const shape& local_xy, bool f64, MemMap& m);
 // F32X3: producers (x3 GEMM epilogue, softmax, refinement folds) write the lo
 // shadow x - tf32(x) of a chunk a later contraction reads; ED_X3_LO_EPI=0
 // falls back to a separate split launch before the consumer (A/B experiments)
+// F32X3: the attention block runs fused (attn_x3_sm100.cu); ED_ATTN_X3=0 keeps
+// it as three einsums through HBM (A/B experiments)
+inline bool x3_attention_fused() {
+  static const bool on = [] {
+    const char* e = std::getenv("ED_ATTN_X3");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 inline bool x3_lo_by_producer() {
   static const bool on = [] {
     const char* e = std::getenv("ED_X3_LO_EPI");

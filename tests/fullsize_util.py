@@ -182,3 +182,57 @@ def ref_slice(plan, graph_text, v, args, picks, torch, f32=None):
         B._check(B.ref().edref_kernel_vertex(text.encode(), vid, int(bool(f32)), B._ptr(arrs[0]), B._ptr(y),
                                              B._ptr(out), err, 1024), err)
     return torch.from_numpy(out).to(args[0].device), cut(e.out)
+
+
+def fused_chain(plan, v, got):
+    """The vertices a fused kernel computed on the way to v (graph vertices
+    between v and its materialised ancestors, in topological order), or []
+    when every input of v is materialised."""
+    if all(i in got for i in v.inputs):
+        return []
+    chain, seen = [], set()
+
+    def visit(w):
+        if w in got or w in seen:
+            return
+        seen.add(w)
+        for i in plan.vertices[w].inputs:
+            visit(i)
+        chain.append(w)
+
+    for i in v.inputs:
+        visit(i)
+    return chain
+
+
+def chain_rows(plan, graph_text, v, chain, got, want_full, which, torch):
+    """v and the fused chain before it evaluated by the reference's f32 mode
+    (kernel_eval with f32 = true, kernel.cc:43-44) vertex by vertex on two rows
+    of v's first output label, from the materialised inputs. Returns
+    (ours, theirs): max_rel_err (tensor.cc:9-19) of the GPU's v and of the
+    reference's f32 chain against want_full (v composed in fp64) on those rows."""
+    lab = v.expr.out[0]
+    n = v.bound[0]
+    start = 0 if which == 0 else (n * 5) // 7 // 2 * 2
+    f32 = {}
+    for w in chain + [v.vid]:
+        vw = plan.vertices[w]
+        args, picks = [], {}
+        for ls, i in zip(vw.expr.ins, vw.inputs):
+            if i in f32:
+                args.append(f32[i])  # already cut to the rows
+            else:
+                a = got[i]
+                if lab in ls:
+                    d = ls.index(lab)
+                    a = a.narrow(d, start, 2)
+                args.append(a)
+        if lab in vw.expr.out:
+            picks[lab] = (0, 2)
+        ref, _ = ref_slice(plan, graph_text, vw, args, picks, torch, f32=True)
+        f32[w] = ref
+    d = v.expr.out.index(lab)
+    want = want_full.narrow(d, start, 2)
+    ours = max_rel_err(got[v.vid].narrow(d, start, 2), want, torch)
+    theirs = max_rel_err(f32[v.vid], want, torch)
+    return ours, theirs

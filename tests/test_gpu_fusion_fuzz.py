@@ -1,7 +1,8 @@
 """Randomised fusion parity: attention- and FFNN-shaped graphs with random
 sizes, scales and partitions (the reference planner's choice for random p and
 L), run in the tensor-core modes where the executor fuses the epilogue maps,
-the row softmax and the attention block. Reference outputs come from the
+the row softmax and the attention block (bf16, and fp32x3 for a head dim of
+128). Reference outputs come from the
 unmodified reference executor (oracle/_ref, built in-tree) on the same inputs
 at test time, on inputs scaled to keep the logits O(1); the bar is the bf16 /
 tf32 tolerance relative to each output's scale, and the row softmax must have
@@ -60,7 +61,7 @@ for i in range(16):
     CASES.append((i, "attention" if i % 2 == 0 else "ffnn", _rng.choice([1, 2, 4, 8]), _rng.choice([1, 2])))
 
 
-@pytest.mark.parametrize("prec", ["bf16", "tf32"])
+@pytest.mark.parametrize("prec", ["bf16", "tf32", "fp32x3"])
 @pytest.mark.parametrize("i,kind,p,L", CASES)
 def test_fusion_fuzz(gpu_ctx, i, kind, p, L, prec):
     from paper_2410_02682_b200.executor import PreparedPlan
@@ -85,8 +86,11 @@ def test_fusion_fuzz(gpu_ctx, i, kind, p, L, prec):
         metric, err, bar = T.error(prec, got[vid], w)
         assert err <= bar, (text, p, L, vid, metric, err, names)
     assert rep.total_transferred == tot and [tuple(m) for m in rep.machines] == [tuple(c) for c in cnt]
-    if prec == "bf16" and (kind == "ffnn" or p <= 2):
+    head_dim = int(text.split("WQ:[")[1].split("]")[0].split(",")[2]) if kind == "attention" else 0
+    if (prec == "bf16" and (kind == "ffnn" or p <= 2)) or (prec == "fp32x3" and kind == "attention" and p <= 2 and
+                                                          head_dim == 128):
         # the row softmax fuses whenever its chain's joins line up (every FFNN
         # plan here); the attention block whenever the softmax label is not
-        # split (the planner splits it at p = 8 for these sizes)
+        # split (the planner splits it at p = 8 for these sizes) — in fp32x3
+        # for a head dim of 128 (attn_x3_sm100.cu)
         assert any(n.startswith(fused) for n in names), names
