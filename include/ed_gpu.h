@@ -344,7 +344,11 @@ ED_API ed_status ed_peer_export(struct ed_plan_h* h, void* out, size_t cap, size
 ED_API ed_status ed_peer_import(struct ed_plan_h* h, const void* blobs, size_t blob_len, int32_t n, char* err,
                                 size_t errlen);
 
-/* Per-launch-class timings of the last profiled ed_run. */
+/* Per-launch-class timings of the last profiled ed_run. A plan over several
+ * ranks in one process (ed_ctx_create_multi) lists the classes summed over its
+ * ranks, then each rank's own as "r<rank>/<class>". With the peer transport,
+ * "nccl_recv" is the time the compute stream waited for its received chunks
+ * and "peer_recv_copy" the copies themselves (prefetched on the comm stream). */
 ED_API ed_status ed_kernel_stats(struct ed_plan_h* h, ed_kernel_stat_c* out, int32_t cap,
                           int32_t* n_out, char* err, size_t errlen);
 

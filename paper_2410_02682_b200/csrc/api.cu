@@ -258,6 +258,13 @@ ed_status ed_peer_import(ed_plan_h* h, const void* blobs, size_t blob_len, int32
       CUDA_OK(cudaIpcOpenMemHandle(&f, hd.flags, cudaIpcMemLazyEnablePeerAccess));
       h->peer_arena[size_t(r)] = static_cast<char*>(a);
       h->peer_flags[size_t(r)] = static_cast<int*>(f);
+      // another process on this same GPU (a functional test without MPS): the
+      // contexts time-slice, and a receive that spins from the run's start
+      // holds the GPU for its slice while the producer's context waits —
+      // receives then stay at their consumers (no prefetch)
+      cudaPointerAttributes at{};
+      if (cudaPointerGetAttributes(&at, a) == cudaSuccess && at.device == h->ctx->device) h->prefetch_ok = false;
+      cudaGetLastError();
     }
     h->peer_ready = true;
     h->record();

@@ -1030,6 +1030,20 @@ void ed_plan_h::build() {
 
   (void)0;
   // stash what allocate() needs
+  // what each op writes (before allocate() turns some op.ptr ids into pointers)
+  for (auto& op : ops) {
+    op.writes.clear();
+    switch (op.kind) {
+      case OpKind::GEMM:
+      case OpKind::SOFTMAX:
+      case OpKind::FLASH:
+      case OpKind::EWISE:
+      case OpKind::ROWREDUCE: op.writes = op.heads; break;
+      case OpKind::GENERIC:
+      case OpKind::REFINE: op.writes.push_back(int(reinterpret_cast<intptr_t>(op.ptr))); break;
+      default: break;
+    }
+  }
   this->srcs_.clear();
   for (int id = 0; id < ne; ++id)
     for (auto& s : srcs[id]) this->srcs_.push_back({id, s.id, s.r0, s.ext});

@@ -1,6 +1,9 @@
 // Running a prepared plan: one launch per op on the compute stream, transfer
 // runs on the comm stream, independent GEMMs as parallel branches, all
 // captured once into a CUDA graph (record) and replayed by ed_run.
+#include <algorithm>
+#include <cstring>
+
 #include "runtime.h"
 
 void ed_plan_h::launch_op(size_t i, cudaStream_t s, bool branch) {
@@ -67,6 +70,7 @@ void ed_plan_h::launch_op(size_t i, cudaStream_t s, bool branch) {
 void ed_plan_h::enqueue(cudaStream_t s) {
   cudaStream_t cs = ctx->comm_stream;
   size_t ev = 0;
+  const bool prefetch = peer && peer_prefetch() && prefetch_ok;
   if (peer) {
     // new run: advance the epoch, then wait until every rank has finished its
     // previous run (its receives from our chunks are complete: write-after-read)
@@ -84,6 +88,85 @@ void ed_plan_h::enqueue(cudaStream_t s) {
     return comm_events[ev++];
   };
   auto is_comm = [&](size_t i) { return ops[i].kind == OpKind::SEND || ops[i].kind == OpKind::RECV; };
+
+  // Peer transport, prefetched: a chunk's ready signal goes right after the op
+  // that writes it (input chunks: at the start), every receive is issued on
+  // the comm stream at the run's start in schedule order (flag wait, then the
+  // copy), and the compute stream waits for a receive only where its chunk's
+  // first consumer launches — so copies run under this rank's compute.
+  std::vector<cudaEvent_t> recv_done;
+  std::vector<std::vector<size_t>> signal_after;
+  std::vector<char> moved;
+  bool recv_fork = false;
+  auto signal = [&](size_t k) { CUDA_OK(launch_peer_signal(d_pflags + 2 + ops[k].exec, d_epoch, s)); };
+  if (prefetch) {
+    recv_done.assign(ops.size(), nullptr);
+    signal_after.assign(ops.size(), {});
+    moved.assign(ops.size(), 0);
+    for (size_t k = 0; k < ops.size(); ++k) {
+      if (ops[k].kind != OpKind::SEND) continue;
+      const int o = owner[size_t(ops[k].exec)];
+      for (size_t q = k; q-- > 0;) {
+        const auto& w = ops[q].writes;
+        if (std::find(w.begin(), w.end(), o) != w.end()) {
+          signal_after[q].push_back(k);
+          moved[k] = 1;
+          break;
+        }
+      }
+      if (!moved[k] && X[size_t(o)].kind == ED_EXEC_INPUT_CHUNK) {
+        signal(k);  // uploaded before the run
+        moved[k] = 1;
+      }
+    }
+    static const bool trace = std::getenv("ED_PEER_TRACE") != nullptr;
+    if (trace && !profile_traced) {
+      profile_traced = true;
+      for (size_t q = 0; q < ops.size(); ++q) {
+        std::fprintf(stderr, "[ed] rank %d op %zu %s", ctx->rank, q, ops[q].name.c_str());
+        if (ops[q].kind == OpKind::SEND || ops[q].kind == OpKind::RECV)
+          std::fprintf(stderr, " exec %d owner %d peer %d moved %d", ops[q].exec, owner[size_t(ops[q].exec)], ops[q].peer,
+                       moved[q]);
+        for (size_t k : signal_after[q]) std::fprintf(stderr, " -> signal exec %d", ops[k].exec);
+        std::fprintf(stderr, "\n");
+      }
+    }
+    size_t r = 0;
+    for (size_t k = 0; k < ops.size(); ++k) {
+      if (ops[k].kind != OpKind::RECV) continue;
+      if (!recv_fork) {
+        cudaEvent_t fork = next_event();
+        CUDA_OK(cudaEventRecord(fork, s));
+        CUDA_OK(cudaStreamWaitEvent(cs, fork, 0));
+        recv_fork = true;
+      }
+      const Op& op = ops[k];
+      int* f = peer_flags[size_t(op.peer)] + 2 + op.exec;
+      CUDA_OK(launch_peer_wait(&f, 1, d_epoch, 0, cs, d_perr, op.exec));
+      const int64_t off = peer_off[size_t(op.peer)][size_t(op.exec)];
+      if (off < 0) throw ed_error(ED_ERR_PLAN, "peer transport: chunk not resident on its producer rank");
+      if (opt.profile) {
+        if (recv_events.size() < 2 * (r + 1)) {
+          for (int e2 = 0; e2 < 2; ++e2) {
+            cudaEvent_t e;
+            CUDA_OK(cudaEventCreate(&e));
+            recv_events.push_back(e);
+          }
+        }
+        CUDA_OK(cudaEventRecord(recv_events[2 * r], cs));
+      }
+      CUDA_OK(cudaMemcpyAsync(op.ptr, peer_arena[size_t(op.peer)] + off, op.count * es, cudaMemcpyDeviceToDevice, cs));
+      if (opt.profile) CUDA_OK(cudaEventRecord(recv_events[2 * r + 1], cs));
+      recv_done[k] = next_event();
+      CUDA_OK(cudaEventRecord(recv_done[k], cs));
+      ++r;
+    }
+  }
+  auto signals_after = [&](size_t q) {
+    if (prefetch)
+      for (size_t k : signal_after[q]) signal(k);
+  };
+
   for (size_t i = 0; i < ops.size();) {
     // consecutive GEMMs of mutually independent einsums (e.g. attention's Q, K, V
     // projections) run as parallel branches: each persistent grid's last,
@@ -114,12 +197,22 @@ void ed_plan_h::enqueue(cudaStream_t s) {
       }
       launch_op(i, s, true);
       for (cudaEvent_t e : joins) CUDA_OK(cudaStreamWaitEvent(s, e, 0));
+      for (size_t k = i; k < g; ++k) signals_after(k);
       i = g;
       continue;
     }
     if (!is_comm(i)) {
       if (opt.profile) CUDA_OK(cudaEventRecord(op_events[i], s));
       launch_op(i, s);
+      signals_after(i);
+      ++i;
+      continue;
+    }
+    if (prefetch) {
+      // the compute stream takes its received chunk (the copy ran on the comm stream)
+      if (opt.profile) CUDA_OK(cudaEventRecord(op_events[i], s));
+      if (ops[i].kind == OpKind::RECV) CUDA_OK(cudaStreamWaitEvent(s, recv_done[i], 0));
+      else if (!moved[i]) signal(i);
       ++i;
       continue;
     }
@@ -141,6 +234,11 @@ void ed_plan_h::enqueue(cudaStream_t s) {
     CUDA_OK(cudaEventRecord(join, cs));
     CUDA_OK(cudaStreamWaitEvent(s, join, 0));
     i = j;
+  }
+  if (recv_fork) {  // the comm stream rejoins (graph capture; every copy has landed anyway)
+    cudaEvent_t join = next_event();
+    CUDA_OK(cudaEventRecord(join, cs));
+    CUDA_OK(cudaStreamWaitEvent(s, join, 0));
   }
   if (opt.profile) CUDA_OK(cudaEventRecord(op_events[ops.size()], s));
   if (peer) CUDA_OK(launch_peer_signal(d_pflags, d_epoch, s));  // this run is done on this rank
@@ -188,6 +286,7 @@ void ed_plan_h::destroy() {
   if (ev1) cudaEventDestroy(ev1);
   for (auto e : op_events) cudaEventDestroy(e);
   for (auto e : comm_events) cudaEventDestroy(e);
+  for (auto e : recv_events) cudaEventDestroy(e);
   for (auto a : aux)
     if (a) cudaStreamDestroy(a);
   for (size_t r = 0; r < peer_arena.size() && !peer_inproc; ++r)
@@ -267,6 +366,23 @@ void finish_run(ed_plan_h* h, ed_report_c* rep) {
       st.ms += t;
       st.flops += op.flops;
       st.bytes += op.bytes;
+    }
+    // prefetched receives: the copies themselves (on the comm stream); the
+    // receive ops above count only what the compute stream waited for them
+    if (h->peer && peer_prefetch() && h->prefetch_ok) {
+      ed_kernel_stat_c st{};
+      std::snprintf(st.name, sizeof(st.name), "%s", "peer_recv_copy");
+      size_t r = 0;
+      for (const Op& op : h->ops) {
+        if (op.kind != OpKind::RECV) continue;
+        float t = 0;
+        CUDA_OK(cudaEventElapsedTime(&t, h->recv_events[2 * r], h->recv_events[2 * r + 1]));
+        st.launches += 1;
+        st.ms += t;
+        st.bytes += double(op.count) * double(h->es);
+        ++r;
+      }
+      if (st.launches) h->stats.push_back(st);
     }
   }
   if (flag) throw ed_error(ED_ERR_EVAL, "division by zero");
@@ -349,9 +465,17 @@ ed_status ed_kernel_stats(ed_plan_h* h, ed_kernel_stat_c* out, int32_t cap, int3
                           size_t errlen) {
   return guarded(err, errlen, [&] {
     if (!h || !n_out) throw ed_error(ED_ERR_USAGE, "null argument");
-    int k = std::min<int>(cap, int(h->stats.size()));
-    for (int i = 0; i < k; ++i) out[i] = h->stats[i];
-    *n_out = int(h->stats.size());
+    std::vector<ed_kernel_stat_c> all = h->stats;
+    for (size_t r = 0; r < h->subs.size(); ++r)  // one process over L ranks: "r<rank>/<launch class>"
+      for (ed_kernel_stat_c st : h->subs[r]->stats) {
+        char name[sizeof st.name];
+        std::snprintf(name, sizeof name, "r%zu/%s", r, st.name);
+        std::memcpy(st.name, name, sizeof name);
+        all.push_back(st);
+      }
+    int k = std::min<int>(cap, int(all.size()));
+    for (int i = 0; i < k; ++i) out[i] = all[i];
+    *n_out = int(all.size());
   });
 }
 

@@ -175,6 +175,7 @@ struct Op {
   int peer = -1;
   size_t count = 0;
   int exec = -1;      // SEND / RECV: the chunk's exec id
+  std::vector<int> writes;  // exec ids whose data this op writes (the peer transport's early ready signals)
   int einsum = -1;    // GEMM: the graph vertex it computes
 };
 
@@ -203,6 +204,18 @@ bool map_memory(const Vtx& v, const shape& local_xy, bool f64, MemMap& m);
 inline bool x3_attention_fused() {
   static const bool on = [] {
     const char* e = std::getenv("ED_ATTN_X3");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+// peer transport: every receive of a run is issued on the comm stream at the
+// run's start (each waits for its chunk's ready flag, then copies), and the
+// compute stream waits for it only at the chunk's first consumer; a chunk's
+// ready flag is raised right after the op that produces it. ED_PEER_PREFETCH=0
+// keeps each receive at its consumer (A/B experiments).
+inline bool peer_prefetch() {
+  static const bool on = [] {
+    const char* e = std::getenv("ED_PEER_PREFETCH");
     return !(e && e[0] == '0');
   }();
   return on;
@@ -278,6 +291,9 @@ struct ed_plan_h {
   cudaGraphExec_t gexec = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::vector<cudaEvent_t> op_events;
+  bool prefetch_ok = true;                // peer receives may be prefetched (not time-sliced processes)
+  bool profile_traced = false;            // ED_PEER_TRACE printed this plan's schedule
+  std::vector<cudaEvent_t> recv_events;  // profile, peer transport: [2k], [2k+1] around the k-th receive copy
   std::vector<ed_kernel_stat_c> stats;
 
   struct SrcRec {
