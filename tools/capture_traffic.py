@@ -22,7 +22,7 @@ sys.path.insert(0, ROOT)
 
 def capture(config, prec):
     cmd = ["ncu", "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
-           "--clock-control", "none", "-k", "regex:gemm_|attn_kernel", "--csv",
+           "--clock-control", "none", "-k", "regex:gemm_|attn_", "--csv",
            sys.executable, os.path.join(ROOT, "tools", "kernel_times.py"), f"{config}_p8_L1", "1", prec]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=900).stdout
     rows = list(csv.reader(io.StringIO("\n".join(l for l in out.splitlines() if l.startswith('"')))))
