@@ -52,6 +52,9 @@ cudaError_t launch_attn(const AttnLaunch& p, int num_sms, cudaStream_t s);
 // contractions as three TF32 products, P in fp32. Maps: Q box {32, 128},
 // K box {32, 64} (K-major), V box {32, 32} (MN-major, 32-byte-atom swizzle).
 bool attn_x3_supported(int S, int T, int D);
+// CTAs per cluster of the fp32x3 kernel for S query rows (2: cta_group::2 pairs,
+// K maps then box {32, 32}; ED_ATTN_X3_CTA=1 forces single CTAs)
+int attn_x3_cta(int S);
 cudaError_t attn_x3_prepare();
 cudaError_t launch_attn_x3(const AttnLaunch& p, int num_sms, cudaStream_t s);
 

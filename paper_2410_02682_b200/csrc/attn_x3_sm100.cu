@@ -34,6 +34,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 
 #include "attn_sm100.h"
 #include "ptx.cuh"
@@ -66,13 +67,16 @@ struct XJob {
   int region, h, s0;
 };
 
-__device__ __forceinline__ XJob xjob_of(const AttnLaunch& p, int j) {
-  const int tph = p.S / XQ;
-  const int rh = j / tph;
+// job j: kCta consecutive 128-row query tiles of one head, CTA `rank` of the
+// cluster taking tile rank
+template <int kCta>
+__device__ __forceinline__ XJob xjob_of(const AttnLaunch& p, int j, uint32_t rank) {
+  const int jph = p.S / (XQ * kCta);
+  const int rh = j / jph;
   XJob r;
   r.region = rh / p.H;
   r.h = rh % p.H;
-  r.s0 = (j % tph) * XQ;
+  r.s0 = (j % jph) * XQ * kCta + int(rank) * XQ;
   return r;
 }
 
@@ -87,6 +91,12 @@ __device__ __forceinline__ float pow2i(float k) {
   return k < -126.f ? 0.f : __int_as_float((127 + int(k)) << 23);
 }
 
+// kCta = 2: a CTA pair (cluster) takes two query tiles of one head and issues
+// cta_group::2 MMAs (M = 256): each CTA loads half of every K block (32 keys)
+// and half of every V block (64 of the d columns), halving the TMA writes
+// and B-operand reads per SM; the leader's MMA warp waits for both CTAs'
+// softmax / correction arrivals, commits reach both CTAs' barriers.
+template <int kCta>
 __global__ void __launch_bounds__(kXThreads, 1) attn_x3_kernel(const __grid_constant__ AttnLaunch p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -114,18 +124,25 @@ __global__ void __launch_bounds__(kXThreads, 1) attn_x3_kernel(const __grid_cons
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int nb = p.T / XKV;
+  const uint32_t rank = kCta == 2 ? cluster_ctarank() : 0;
+  const int first = blockIdx.x / kCta, stride = gridDim.x / kCta;
+  // arrive on the leader CTA's copy of a barrier (the MMA issuer's)
+  auto arrive_leader = [&](uint64_t* b) {
+    if (kCta == 2) mbar_arrive_cluster(mapa(smem_u32(b), 0));
+    else mbar_arrive(b);
+  };
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
     mbar_init(q_empty, 1);
-    mbar_init(qt_full, 4);
+    mbar_init(qt_full, 4 * kCta);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 4);
+      mbar_init(&p_full[i], 4 * kCta);
       mbar_init(&sc_full[i], 4);
     }
     mbar_init(pv_done, 1);
-    mbar_init(o_free, 4);
+    mbar_init(o_free, 4 * kCta);
     mbar_init(l_ready, 4);
     for (int i = 0; i < XNSLOT; ++i) {
       mbar_init(&slot_full[i], 1);
@@ -133,9 +150,10 @@ __global__ void __launch_bounds__(kXThreads, 1) attn_x3_kernel(const __grid_cons
     }
     fence_mbar_init();
   }
-  if (warp == kXMmaWarp) tmem_alloc<512>(tmem_slot);
+  if (warp == kXMmaWarp) tmem_alloc<512, kCta>(tmem_slot);
   tc_fence_before();
-  __syncthreads();
+  if (kCta == 2) cluster_sync();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   griddep_wait();
@@ -153,41 +171,54 @@ __global__ void __launch_bounds__(kXThreads, 1) attn_x3_kernel(const __grid_cons
         ++sn;
         return st;
       };
-      for (int jb = blockIdx.x; jb < p.n_jobs; jb += gridDim.x) {
-        if (jb + int(gridDim.x) >= p.n_jobs) griddep_launch();
-        const XJob J = xjob_of(p, jb);
+      // kCta = 2: data lands in this CTA's smem, the bytes count on the leader's barrier
+      auto load = [&](void* dst, const CUtensorMap* m, uint64_t* b, int c0, int c1, int c2) {
+        if (kCta == 2) tma_load_3d_2sm(dst, m, b, c0, c1, c2);
+        else tma_load_3d(dst, m, b, c0, c1, c2);
+      };
+      for (int jb = first; jb < p.n_jobs; jb += stride) {
+        if (jb + stride >= p.n_jobs) griddep_launch();
+        const XJob J = xjob_of<kCta>(p, jb, rank);
         const AttnRegion& R = p.regions[J.region];
         auto src_map = [&](const AttnSrc& a, int key, int dcol) {
           return p.maps + a.base + (key / a.keys) * a.nd + dcol / a.dw;
         };
         mbar_wait(q_empty, (qn & 1) ^ 1);
         ++qn;
-        mbar_expect_tx(q_full, XQ_BYTES);
+        if (rank == 0) mbar_expect_tx(q_full, XQ_BYTES * kCta);
 #pragma unroll
-        for (int c = 0; c < XD / 32; ++c) tma_load_3d(sQ + c * 16384, p.maps + R.q, q_full, c * 32, J.s0, J.h);
+        for (int c = 0; c < XD / 32; ++c) load(sQ + c * 16384, p.maps + R.q, q_full, c * 32, J.s0, J.h);
         auto load_k = [&](int j) {
           for (int part = 1; part >= 0; --part)  // lo first: consumed first
-            for (int hf = 0; hf < 2; ++hf) {     // d chunks 2 hf, 2 hf + 1
+            for (int hf = 0; hf < 2 / kCta; ++hf) {
+              // kCta 1: d chunks 2 hf, 2 hf + 1 of the 64 keys; kCta 2: all four of this CTA's 32 keys
               const int st = slot_get();
               uint8_t* dst = sKV + st * XSLOT;
-              mbar_expect_tx(&slot_full[st], XSLOT);
+              if (rank == 0) mbar_expect_tx(&slot_full[st], XSLOT * kCta);
+              const int key = j * XKV + int(rank) * (XKV / kCta);
 #pragma unroll
-              for (int c = 2 * hf; c < 2 * hf + 2; ++c)
-                tma_load_3d(dst + (c - 2 * hf) * 8192, src_map(R.k, j * XKV, c * 32) + part * R.k.lo, &slot_full[st],
-                            (c * 32) % R.k.dw, (j * XKV) % R.k.keys, J.h + R.k.hoff);
+              for (int c = 0; c < 2 * kCta; ++c) {
+                const int dc = kCta == 1 ? 2 * hf + c : c;
+                load(dst + c * (XSLOT / (2 * kCta)), src_map(R.k, key, dc * 32) + part * R.k.lo, &slot_full[st],
+                     (dc * 32) % R.k.dw, key % R.k.keys, J.h + R.k.hoff);
+              }
             }
         };
         auto load_v = [&](int j) {
           for (int part = 1; part >= 0; --part)
-            for (int kb = 0; kb < 2; ++kb) {  // keys 32 kb .. 32 kb + 31 of the block
+            for (int kb = 0; kb < 2 / kCta; ++kb) {
+              // kCta 1: keys 32 kb.. of the block, all d; kCta 2: all 64 keys, this CTA's 64 d
               const int st = slot_get();
               uint8_t* dst = sKV + st * XSLOT;
-              mbar_expect_tx(&slot_full[st], XSLOT);
-              const int key = j * XKV + kb * 32;
+              if (rank == 0) mbar_expect_tx(&slot_full[st], XSLOT * kCta);
 #pragma unroll
-              for (int a = 0; a < XD / 32; ++a)
-                tma_load_3d(dst + a * 4096, src_map(R.v, key, a * 32) + part * R.v.lo, &slot_full[st],
-                            (a * 32) % R.v.dw, key % R.v.keys, J.h + R.v.hoff);
+              for (int i = 0; i < 4; ++i) {
+                const int kk = kCta == 1 ? kb : i / 2;             // 32-key half of the block
+                const int a = kCta == 1 ? i : int(rank) * 2 + i % 2;  // 32-wide d atom
+                const int key = j * XKV + kk * 32;
+                load(dst + i * 4096, src_map(R.v, key, a * 32) + part * R.v.lo, &slot_full[st], (a * 32) % R.v.dw,
+                     key % R.v.keys, J.h + R.v.hoff);
+              }
             }
         };
         load_k(0);
@@ -198,9 +229,26 @@ __global__ void __launch_bounds__(kXThreads, 1) attn_x3_kernel(const __grid_cons
       }
     }
   } else if (warp == kXMmaWarp) {
+    if (rank != 0) goto done;  // the pair's MMAs are issued by the leader
     // ---------------- MMA issuer (whole warp; one elected lane issues) ----------------
-    const uint32_t idesc_s = umma_idesc(2u, XQ, XKV, 0u, 0u);  // Q, K both K-major (d)
-    const uint32_t idesc_o = umma_idesc(2u, XQ, XD, 0u, 1u);   // P from TMEM (keys), V MN-major (d)
+    const uint32_t idesc_s = umma_idesc(2u, XQ * kCta, XKV, 0u, 0u);  // Q, K both K-major (d)
+    const uint32_t idesc_o = umma_idesc(2u, XQ * kCta, XD, 0u, 1u);   // P from TMEM (keys), V MN-major (d)
+    auto mma_ss = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+      if (kCta == 2) mma_tf32_2sm_warp(d, a, b, id, acc);
+      else mma_tf32_warp(d, a, b, id, acc);
+    };
+    auto mma_ts = [&](uint32_t d, uint32_t a, uint64_t b, uint32_t id, uint32_t acc) {
+      if (kCta == 2) mma_tf32_ts_2sm_warp(d, a, b, id, acc);
+      else mma_tf32_ts_warp(d, a, b, id, acc);
+    };
+    auto commit = [&](uint64_t* b) {
+      if (kCta == 2) mma_commit_2sm_warp(b);
+      else mma_commit_warp(b);
+    };
+    auto wait_arrivals = [&](uint64_t* b, uint32_t ph) {  // arrivals from both CTAs' warps
+      if (kCta == 2) mbar_wait_cluster(b, ph);
+      else mbar_wait(b, ph);
+    };
     int sn = 0, qn = 0, pn0 = 0, pn1 = 0, on = 0;
 #if X3_PROF
     long long prof[4] = {0, 0, 0, 0};  // wait K slots, issue S, wait P / O free / V slots, issue PV
@@ -221,86 +269,105 @@ __global__ void __launch_bounds__(kXThreads, 1) attn_x3_kernel(const __grid_cons
       return st;
     };
     const uint64_t qd = umma_desc_sw128(smem_u32(sQ), 16, 1024);
+    // K slot layout: kCta 1, two K-major chunks (8 KiB: 64 keys x 32 d) per slot, two slots
+    // per copy; kCta 2, four chunks (4 KiB: 32 keys x 32 d) in one slot. A K step of 8 d:
+    constexpr int KCH = XSLOT / (2 * kCta);          // bytes per K chunk
+    auto k_off = [&](int k, int hf) { return uint64_t((((k / 4) - 2 * hf) * KCH + (k % 4) * 32) >> 4); };
     auto issue_s = [&](int b) {
       const uint32_t d = tmem + t_r(b, 0);
 #pragma unroll
-      for (int hf = 0; hf < 2; ++hf) {  // Q_hi K_lo over d chunks 2 hf, 2 hf + 1
+      for (int hf = 0; hf < 2 / kCta; ++hf) {  // Q_hi K_lo
         const int kl = take();
         MPROF(0)
         const uint64_t kld = umma_desc_sw128(smem_u32(sKV + kl * XSLOT), 16, 1024);
 #pragma unroll
-        for (int k = 8 * hf; k < 8 * hf + 8; ++k) {
-          const uint64_t ko = uint64_t(((k / 4 - 2 * hf) * 8192 + (k % 4) * 32) >> 4);
-          mma_tf32_ts_warp(d, tmem + T_Q + uint32_t(k * 8), kld + ko, idesc_s, k != 0);
-        }
-        mma_commit_warp(&slot_empty[kl]);
+        for (int k = 16 / (2 / kCta) * hf; k < 16 / (2 / kCta) * (hf + 1); ++k)
+          mma_ts(d, tmem + T_Q + uint32_t(k * 8), kld + k_off(k, kCta == 1 ? hf : 0), idesc_s, k != 0);
+        commit(&slot_empty[kl]);
       }
 #pragma unroll
-      for (int hf = 0; hf < 2; ++hf) {  // Q_lo K_hi + Q_hi K_hi
+      for (int hf = 0; hf < 2 / kCta; ++hf) {  // Q_lo K_hi + Q_hi K_hi
         const int kh = take();
         MPROF(0)
         const uint64_t khd = umma_desc_sw128(smem_u32(sKV + kh * XSLOT), 16, 1024);
 #pragma unroll
-        for (int k = 8 * hf; k < 8 * hf + 8; ++k) {
+        for (int k = 16 / (2 / kCta) * hf; k < 16 / (2 / kCta) * (hf + 1); ++k) {
           const uint64_t qo = uint64_t(((k / 4) * 16384 + (k % 4) * 32) >> 4);
-          const uint64_t ko = uint64_t(((k / 4 - 2 * hf) * 8192 + (k % 4) * 32) >> 4);
-          mma_tf32_warp(d, qd + qo, khd + ko, idesc_s, 1u);
-          mma_tf32_ts_warp(d, tmem + T_Q + uint32_t(k * 8), khd + ko, idesc_s, 1u);
+          const uint64_t ko = k_off(k, kCta == 1 ? hf : 0);
+          mma_ss(d, qd + qo, khd + ko, idesc_s, 1u);
+          mma_ts(d, tmem + T_Q + uint32_t(k * 8), khd + ko, idesc_s, 1u);
         }
-        mma_commit_warp(&slot_empty[kh]);
+        commit(&slot_empty[kh]);
       }
-      mma_commit_warp(&s_full[b]);
+      commit(&s_full[b]);
       MPROF(1)
+    };
+    // V slot layout: 4 MN atoms of 32 x 128 B; kCta 1, one 32-key half of the block and
+    // all four d atoms; kCta 2, both halves (atoms 0-1: keys 0-31) of this CTA's two d atoms
+    constexpr uint32_t V_LBO = kCta == 1 ? 4096u : 4096u;  // next d atom
+    auto v_off = [&](int k) {
+      return uint64_t(((kCta == 1 ? 0 : (k / 4) * 8192) + (k % 4) * 1024) >> 4);
     };
     auto issue_pv = [&](int b) {
       const uint32_t ph = tmem + t_r(b, 0), pl = tmem + t_r(b, 1);
 #pragma unroll
-      for (int kb = 0; kb < 2; ++kb) {  // P_hi V_lo over keys 32 kb.., a fresh O_j
+      for (int kb = 0; kb < 2 / kCta; ++kb) {  // P_hi V_lo, a fresh O_j
         const int vl = take();
         MPROF(2)
-        const uint64_t vld = umma_desc_sw128(smem_u32(sKV + vl * XSLOT), 4096, 512, 1);
+        const uint64_t vld = umma_desc_sw128(smem_u32(sKV + vl * XSLOT), V_LBO, 512, 1);
 #pragma unroll
-        for (int k = 4 * kb; k < 4 * kb + 4; ++k)
-          mma_tf32_ts_warp(tmem + T_O, ph + uint32_t(k * 8), vld + uint64_t(((k % 4) * 1024) >> 4), idesc_o, k != 0);
-        mma_commit_warp(&slot_empty[vl]);
+        for (int k = 8 / (2 / kCta) * kb; k < 8 / (2 / kCta) * (kb + 1); ++k)
+          mma_ts(tmem + T_O, ph + uint32_t(k * 8), vld + v_off(k), idesc_o, k != 0);
+        commit(&slot_empty[vl]);
       }
 #pragma unroll
-      for (int kb = 0; kb < 2; ++kb) {  // P_lo V_hi + P_hi V_hi
+      for (int kb = 0; kb < 2 / kCta; ++kb) {  // P_lo V_hi + P_hi V_hi
         const int vh = take();
         MPROF(2)
-        const uint64_t vhd = umma_desc_sw128(smem_u32(sKV + vh * XSLOT), 4096, 512, 1);
+        const uint64_t vhd = umma_desc_sw128(smem_u32(sKV + vh * XSLOT), V_LBO, 512, 1);
 #pragma unroll
-        for (int k = 4 * kb; k < 4 * kb + 4; ++k) {
-          const uint64_t vo = uint64_t(((k % 4) * 1024) >> 4);
-          mma_tf32_ts_warp(tmem + T_O, pl + uint32_t(k * 8), vhd + vo, idesc_o, 1u);
-          mma_tf32_ts_warp(tmem + T_O, ph + uint32_t(k * 8), vhd + vo, idesc_o, 1u);
+        for (int k = 8 / (2 / kCta) * kb; k < 8 / (2 / kCta) * (kb + 1); ++k) {
+          mma_ts(tmem + T_O, pl + uint32_t(k * 8), vhd + v_off(k), idesc_o, 1u);
+          mma_ts(tmem + T_O, ph + uint32_t(k * 8), vhd + v_off(k), idesc_o, 1u);
         }
-        mma_commit_warp(&slot_empty[vh]);
+        commit(&slot_empty[vh]);
       }
-      mma_commit_warp(pv_done);
+      commit(pv_done);
       MPROF(3)
     };
-    for (int jb = blockIdx.x; jb < p.n_jobs; jb += gridDim.x) {
-      mbar_wait(q_full, qn & 1);
-      mbar_wait(qt_full, qn & 1);
-      ++qn;
-      tc_fence_after();
+#if X3_PROF
+    long long jprof[2] = {0, 0};  // job boundary: wait Q_lo (TMA), wait Q in TMEM (softmax)
+    t0 = clock64();
+#endif
+    for (int jb = first; jb < p.n_jobs; jb += stride) {
 #if X3_PROF
       t0 = clock64();
 #endif
+      mbar_wait(q_full, qn & 1);
+#if X3_PROF
+      jprof[0] += clock64() - t0;
+      t0 = clock64();
+#endif
+      wait_arrivals(qt_full, qn & 1);
+      ++qn;
+      tc_fence_after();
+#if X3_PROF
+      jprof[1] += clock64() - t0;
+      t0 = clock64();
+#endif
       issue_s(0);
-      if (nb == 1) mma_commit_warp(q_empty);
+      if (nb == 1) commit(q_empty);
       for (int j = 0; j < nb; ++j) {
         const int b = j & 1;
         if (j + 1 < nb) {
           // S_{j+1} overwrites the buffer PV_{j-1} read: issued after it, so in order
           issue_s(b ^ 1);
-          if (j + 1 == nb - 1) mma_commit_warp(q_empty);
+          if (j + 1 == nb - 1) commit(q_empty);
         }
         int& pn = b ? pn1 : pn0;
-        mbar_wait(&p_full[b], pn & 1);
+        wait_arrivals(&p_full[b], pn & 1);
         ++pn;
-        if (on > 0) mbar_wait(o_free, (on - 1) & 1);  // the correction warps have read O_{j-1}
+        if (on > 0) wait_arrivals(o_free, (on - 1) & 1);  // the correction warps have read O_{j-1}
         ++on;
         tc_fence_after();
         issue_pv(b);
@@ -308,8 +375,8 @@ __global__ void __launch_bounds__(kXThreads, 1) attn_x3_kernel(const __grid_cons
     }
 #if X3_PROF
     if (lane == 0 && (blockIdx.x == 0 || blockIdx.x == 77))
-      printf("cta %d mma cycles: wait K %lld issue S %lld wait P/O/V %lld issue PV %lld\n", blockIdx.x, prof[0],
-             prof[1], prof[2], prof[3]);
+      printf("cta %d mma cycles: wait K %lld issue S %lld wait P/O/V %lld issue PV %lld | job: wait Q_lo %lld Q %lld\n",
+             blockIdx.x, prof[0], prof[1], prof[2], prof[3], jprof[0], jprof[1]);
 #endif
   } else if (warp >= kXCorrWarp0) {
     // ---------------- correction: O = f_j O + O_j in registers, then the epilogue ----------------
@@ -318,8 +385,8 @@ __global__ void __launch_bounds__(kXThreads, 1) attn_x3_kernel(const __grid_cons
     const int row = wq * 32 + lane;
     const uint32_t lane_base = uint32_t(wq * 32) << 16;
     int pvn = 0, sc0 = 0, sc1 = 0, ln = 0;
-    for (int jb = blockIdx.x; jb < p.n_jobs; jb += gridDim.x) {
-      const XJob J = xjob_of(p, jb);
+    for (int jb = first; jb < p.n_jobs; jb += stride) {
+      const XJob J = xjob_of<kCta>(p, jb, rank);
       const AttnRegion& R = p.regions[J.region];
       float o[XD];
 #pragma unroll
@@ -344,7 +411,7 @@ __global__ void __launch_bounds__(kXThreads, 1) attn_x3_kernel(const __grid_cons
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(o_free);
+        if (lane == 0) arrive_leader(o_free);
       }
       // ---- epilogue: O / l (and its lo shadow) -> HBM, one row per thread
       mbar_wait(l_ready, ln & 1);
@@ -379,8 +446,8 @@ __global__ void __launch_bounds__(kXThreads, 1) attn_x3_kernel(const __grid_cons
 #else
 #define SPROF(i)
 #endif
-    for (int jb = blockIdx.x; jb < p.n_jobs; jb += gridDim.x) {
-      const XJob J = xjob_of(p, jb);
+    for (int jb = first; jb < p.n_jobs; jb += stride) {
+      const XJob J = xjob_of<kCta>(p, jb, rank);
       const AttnRegion& R = p.regions[J.region];
       {
         // Q row -> TMEM (the previous job's last PV has completed: waited below)
@@ -401,7 +468,7 @@ __global__ void __launch_bounds__(kXThreads, 1) attn_x3_kernel(const __grid_cons
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(qt_full);
+        if (lane == 0) arrive_leader(qt_full);
       }
       float m = 0.f, l = 0.f;
       for (int j = 0; j < nb; ++j) {
@@ -480,7 +547,7 @@ __global__ void __launch_bounds__(kXThreads, 1) attn_x3_kernel(const __grid_cons
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
-          mbar_arrive(&p_full[b]);
+          arrive_leader(&p_full[b]);
           mbar_arrive(&sc_full[b]);
         }
         SPROF(3)
@@ -500,11 +567,13 @@ __global__ void __launch_bounds__(kXThreads, 1) attn_x3_kernel(const __grid_cons
 #endif
   }
 
+done:
   tc_fence_before();
-  __syncthreads();
+  if (kCta == 2) cluster_sync();
+  else __syncthreads();
   if (warp == kXMmaWarp) {
     tc_fence_after();
-    tmem_dealloc<512>(tmem);
+    tmem_dealloc<512, kCta>(tmem);
   }
 }
 
@@ -512,25 +581,42 @@ __global__ void __launch_bounds__(kXThreads, 1) attn_x3_kernel(const __grid_cons
 
 bool attn_x3_supported(int S, int T, int D) { return D == XD && S % XQ == 0 && T % XKV == 0 && T > 0; }
 
+int attn_x3_cta(int S) {
+  static const int force = [] {
+    const char* e = std::getenv("ED_ATTN_X3_CTA");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (force == 1) return 1;
+  return S % (2 * XQ) == 0 ? 2 : 1;
+}
+
 cudaError_t attn_x3_prepare() {
-  return cudaFuncSetAttribute(attn_x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, XSMEM);
+  cudaError_t e = cudaFuncSetAttribute(attn_x3_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, XSMEM);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(attn_x3_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, XSMEM);
 }
 
 cudaError_t launch_attn_x3(const AttnLaunch& p0, int num_sms, cudaStream_t s) {
   AttnLaunch p = p0;
+  const int cta = attn_x3_cta(p.S);
   p.n_pair_jobs = 0;
-  p.n_jobs = p.n_regions * p.H * (p.S / XQ);
+  p.n_jobs = p.n_regions * p.H * (p.S / (XQ * cta));  // one job per cluster: cta query tiles
+  const int clusters = p.n_jobs < num_sms / cta ? p.n_jobs : num_sms / cta;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(p.n_jobs < num_sms ? p.n_jobs : num_sms);
+  cfg.gridDim = dim3(clusters * cta);
   cfg.blockDim = dim3(kXThreads);
   cfg.dynamicSmemBytes = XSMEM;
   cfg.stream = s;
-  cudaLaunchAttribute pdl[1];
-  pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  pdl[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = pdl;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, attn_x3_kernel, p);
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = cta;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  return cta == 2 ? cudaLaunchKernelEx(&cfg, attn_x3_kernel<2>, p) : cudaLaunchKernelEx(&cfg, attn_x3_kernel<1>, p);
 }
 
 }  // namespace ed
