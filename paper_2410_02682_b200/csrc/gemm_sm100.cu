@@ -516,9 +516,9 @@ __global__ void __launch_bounds__(kX3Threads, 1) gemm_x3_kernel(const __grid_con
   if (warp == 8) {
     // ---- TMA producer: A_hi | B_hi | A_lo | B_lo per stage ----
     if (lane == 0) {
-      int it = 0;
+      int it = 0, ti = 0;
       bool sync_on = p.sync != nullptr;
-      for (int t = first; t < total; t += stride) {
+      for (int t = first; t < total; t += stride, ++ti) {
         if (t + stride >= total) griddep_launch();
         const TileCoord tc = tile_coord<C_::TILE_M, BN>(p, t, tiles_m, tiles_n);
         const GemmRegion reg = p.regions[tc.region];
@@ -526,9 +526,15 @@ __global__ void __launch_bounds__(kX3Threads, 1) gemm_x3_kernel(const __grid_con
         const int bseg_i = reg.bseg ? tc.b / reg.bseg : 0;
         const int ba = reg.bseg && !reg.bseg_b ? tc.b % reg.bseg : tc.b;
         const int bb = reg.bseg && reg.bseg_b ? tc.b % reg.bseg : tc.b;
-        for (int sib = 0; sib < reg.n_sib; ++sib) {
+        // serpentine K: every other wave walks (sibling, K block) backwards, so it
+        // starts on the panel slices the previous wave left in L2 (the grouped
+        // raster keeps a wave's A panels for the next few waves)
+        const bool back = p.serp && (ti & 1);
+        for (int si = 0; si < reg.n_sib; ++si) {
+          const int sib = back ? reg.n_sib - 1 - si : si;
           const CUtensorMap* ma = p.maps + reg.map0 + C_::NMAP * (bseg_i * reg.n_sib + sib);
-          for (int kb = 0; kb < kblocks; ++kb, ++it) {
+          for (int kq = 0; kq < kblocks; ++kq, ++it) {
+            const int kb = back ? kblocks - 1 - kq : kq;
             if (p.sync) producer_lockstep(p, it, sync_on);
             const int s = it % STAGES;
             const uint32_t ph = (it / STAGES) & 1;
