@@ -110,11 +110,8 @@ void ed_plan_h::allocate() {
           if (const char* ch = std::getenv("ED_GEMM_X3_CHUNK")) p.chunk = std::max(0, std::atoi(ch));
         }
         if (const char* gm = std::getenv("ED_GEMM_GROUP_M")) p.group_m = std::max(1, std::atoi(gm));  // experiments
-        p.serp = 0;
-        if (p.x3) {
-          p.serp = 1;
-          if (const char* e = std::getenv("ED_GEMM_SERP")) p.serp = std::atoi(e) != 0;
-        }
+        p.serp = 1;  // serpentine K (gemm_sm100.cu); ED_GEMM_SERP=0 walks K forwards on every tile
+        if (const char* e = std::getenv("ED_GEMM_SERP")) p.serp = std::atoi(e) != 0;
         const uint32_t BK = uint32_t(gemm_bk(b16)), BM = uint32_t(gemm_bm());
         const uint32_t ATOM = 128u / (b16 ? 2u : 4u);
         op.maps.clear();

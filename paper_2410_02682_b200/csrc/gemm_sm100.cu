@@ -213,11 +213,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   if (warp == 0) {
     // ---- TMA producer (both CTAs of a pair load their halves) ----
     if (lane == 0) {
-      int it = 0;
+      int it = 0, ti = 0;
       bool sync_on = p.sync != nullptr;
-      for (int t = first; t < total; t += stride) {
+      for (int t = first; t < total; t += stride, ++ti) {
         if (t + stride >= total) griddep_launch();  // last tile: the next kernel may launch
         const TileCoord tc = coord(t);
+        const bool back = p.serp && (ti & 1);  // serpentine K (see gemm_x3_kernel)
         const GemmRegion reg = p.regions[tc.region];
         const int am = tc.m0 + int(rank) * BM, bn = tc.n0 + int(rank) * C_::B_ROWS;
         // kMc: CTAs with the same rank in both pairs hold the same A rows
@@ -226,10 +227,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         const int bseg_i = reg.bseg ? tc.b / reg.bseg : 0;
         const int ba = reg.bseg && !reg.bseg_b ? tc.b % reg.bseg : tc.b;
         const int bb = reg.bseg && reg.bseg_b ? tc.b % reg.bseg : tc.b;
-        for (int sib = 0; sib < reg.n_sib; ++sib) {
+        for (int si = 0; si < reg.n_sib; ++si) {
+          const int sib = back ? reg.n_sib - 1 - si : si;
           const CUtensorMap* ma = p.maps + reg.map0 + C_::NMAP * (bseg_i * reg.n_sib + sib);
           const CUtensorMap* mb = ma + 1;
-          for (int kb = 0; kb < kblocks; ++kb, ++it) {
+          for (int kq = 0; kq < kblocks; ++kq, ++it) {
+            const int kb = back ? kblocks - 1 - kq : kq;
             if (p.sync) producer_lockstep(p, it, sync_on);
             const int s = it % STAGES;
             const uint32_t ph = (it / STAGES) & 1;

@@ -49,7 +49,7 @@ struct GemmLaunch {
   // zeroed counters (the kernel re-zeroes them on exit); nullptr: off.
   unsigned int* sync;
   int sync_g, sync_lag, sync_epochs;                // grouped raster: tile rows that advance together along N
-  int serp;                   // x3 kernel: odd tile iterations walk K backwards (L2 reuse across waves)
+  int serp;                   // odd tile iterations walk (sibling, K block) backwards (L2 reuse across waves)
   int x3;                     // fp32-accurate 3xTF32: each stage carries hi and lo operand copies
                               // and feeds hi*hi + hi*lo + lo*hi into one accumulator
 };
