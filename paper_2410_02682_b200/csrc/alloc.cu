@@ -54,7 +54,7 @@ void ed_plan_h::allocate() {
   CUDA_OK(cudaMalloc(&d_ptrs, sizeof(void*) * 2 * std::max(1, ne)));
 
   // refinement dependency tables, one contiguous device array
-  std::vector<DepRect> host_deps;
+  host_deps.clear();
   std::map<int, size_t> dep_off;
   for (auto& s : srcs_) {
     if (!dep_off.count(s.ref)) dep_off[s.ref] = host_deps.size();
@@ -696,5 +696,51 @@ void ed_plan_h::allocate() {
     CUDA_OK(cudaMemset(d_pflags, 0, sizeof(int) * (X.size() + 2)));
     CUDA_OK(cudaMalloc(&d_perr, sizeof(int)));
     CUDA_OK(cudaMemset(d_perr, 0, sizeof(int)));
+  }
+}
+
+// Direct receives (peer transport, prefetched): a received chunk that only
+// refinement folds read is not copied — the folds' source pointers (the
+// DepRect table and the rect groups) are rebound to the producer's chunk, and
+// the receive becomes the wait for its ready flag. Called once the peers'
+// arenas are known (ed_prepare over several ranks, ed_peer_import).
+void ed_plan_h::bind_direct() {
+  if (!peer || !peer_ready || !prefetch_ok || !peer_prefetch()) return;
+  if (const char* e = std::getenv("ED_PEER_DIRECT"))
+    if (e[0] == '0') return;  // A/B: copy every received chunk
+  std::map<const void*, const void*> remap;
+  for (Op& op : ops) {
+    if (op.kind != OpKind::RECV || !direct[size_t(op.exec)]) continue;
+    const int64_t off = peer_off[size_t(op.peer)][size_t(op.exec)];
+    if (off < 0) continue;
+    remap[buf[size_t(op.exec)].main] = peer_arena[size_t(op.peer)] + off;
+    op.direct = true;
+  }
+  if (remap.empty()) return;
+  direct_bound = true;
+  bool deps_changed = false;
+  for (DepRect& r : host_deps) {
+    auto it = remap.find(r.src);
+    if (it != remap.end()) {
+      r.src = it->second;
+      deps_changed = true;
+    }
+  }
+  if (deps_changed)
+    CUDA_OK(cudaMemcpy(d_deps, host_deps.data(), sizeof(DepRect) * host_deps.size(), cudaMemcpyHostToDevice));
+  for (Op& op : ops) {
+    if (op.kind != OpKind::REFINE || op.groups.empty()) continue;
+    bool changed = false;
+    for (RectGroup& g : op.groups)
+      for (int k = 0; k < g.n_src; ++k) {
+        auto it = remap.find(g.src[k]);
+        if (it != remap.end()) {
+          g.src[k] = it->second;
+          changed = true;
+        }
+      }
+    if (changed)
+      CUDA_OK(cudaMemcpy(const_cast<RectGroup*>(op.rect.groups), op.groups.data(), sizeof(RectGroup) * op.groups.size(),
+                         cudaMemcpyHostToDevice));
   }
 }

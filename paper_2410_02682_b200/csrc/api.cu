@@ -152,6 +152,7 @@ ed_status ed_prepare(ed_ctx* ctx, const ed_plan_c* plan, const ed_options_c* opt
           h->peer_inproc = true;
           h->peer_ready = true;
           CUDA_OK(cudaSetDevice(h->ctx->device));
+          h->bind_direct();
           h->record();
         }
       } catch (...) {
@@ -267,6 +268,7 @@ ed_status ed_peer_import(ed_plan_h* h, const void* blobs, size_t blob_len, int32
       cudaGetLastError();
     }
     h->peer_ready = true;
+    h->bind_direct();
     h->record();
   });
 }

@@ -835,6 +835,17 @@ void ed_plan_h::build() {
     if (rank_of(d) == me) buf[owner[d]].need_main = true;
   for (auto& [d, dst] : transfers)
     if (dst == me) buf[d].need_main = true;
+  // a received chunk only refinement folds read (fp32 / fp64, no shadows) can
+  // be read where it lies on its producer once the peers are wired
+  direct.assign(ne, 0);
+  for (auto& [d, dst] : transfers) {
+    if (dst != me || buf[d].need_16 || buf[d].need_lo) continue;
+    bool ok = true;
+    for (int u = 0; u < ne && ok; ++u)
+      if (local[u] && std::find(X[u].deps.begin(), X[u].deps.end(), d) != X[u].deps.end())
+        ok = X[u].kind == ED_EXEC_REFINEMENT && owner[u] == u && !virt[u];
+    direct[d] = ok;
+  }
   // every computed chunk keeps at least one representation
   for (int id = 0; id < ne; ++id)
     if (local[id] && !virt[id] && owner[id] == id && !buf[id].need_16) buf[id].need_main = true;

@@ -145,6 +145,11 @@ void ed_plan_h::enqueue(cudaStream_t s) {
       CUDA_OK(launch_peer_wait(&f, 1, d_epoch, 0, cs, d_perr, op.exec));
       const int64_t off = peer_off[size_t(op.peer)][size_t(op.exec)];
       if (off < 0) throw ed_error(ED_ERR_PLAN, "peer transport: chunk not resident on its producer rank");
+      if (op.direct) {  // its readers take the producer's chunk in place: the flag wait is the receive
+        recv_done[k] = next_event();
+        CUDA_OK(cudaEventRecord(recv_done[k], cs));
+        continue;
+      }
       if (opt.profile) {
         if (recv_events.size() < 2 * (r + 1)) {
           for (int e2 = 0; e2 < 2; ++e2) {
@@ -374,7 +379,7 @@ void finish_run(ed_plan_h* h, ed_report_c* rep) {
       std::snprintf(st.name, sizeof(st.name), "%s", "peer_recv_copy");
       size_t r = 0;
       for (const Op& op : h->ops) {
-        if (op.kind != OpKind::RECV) continue;
+        if (op.kind != OpKind::RECV || op.direct) continue;
         float t = 0;
         CUDA_OK(cudaEventElapsedTime(&t, h->recv_events[2 * r], h->recv_events[2 * r + 1]));
         st.launches += 1;

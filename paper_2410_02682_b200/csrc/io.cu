@@ -547,6 +547,8 @@ ed_status ed_download_chunk(ed_plan_h* h, int32_t exec_id, int32_t dtype, void* 
     if (u.kind == ED_EXEC_JOIN && o != exec_id && h->X[o].producer == u.producer)
       throw ed_error(ED_ERR_USAGE, "join partial was folded into its region's accumulator");
     if (h->opaque_[exec_id]) throw ed_error(ED_ERR_USAGE, "chunk was fused into its consumer's kernel");
+    if (h->direct_bound && h->direct[exec_id])
+      throw ed_error(ED_ERR_USAGE, "chunk is read in place on its producer rank (peer transport): download it there");
     CUDA_OK(cudaSetDevice(h->ctx->device));
     cudaStream_t s = h->ctx->stream;
     size_t bytes = size_t(n) * dt_size(dtype);

@@ -175,6 +175,7 @@ struct Op {
   int peer = -1;
   size_t count = 0;
   int exec = -1;      // SEND / RECV: the chunk's exec id
+  bool direct = false;  // RECV: no copy, readers use the producer's chunk (bind_direct)
   std::vector<int> writes;  // exec ids whose data this op writes (the peer transport's early ready signals)
   int einsum = -1;    // GEMM: the graph vertex it computes
 };
@@ -257,6 +258,10 @@ struct ed_plan_h {
 
   std::vector<int> owner;          // exec id -> exec id holding its data
   std::vector<char> local;         // exec id runs (or is received) on this rank
+  std::vector<char> direct;        // received chunk read by refinement folds only: with prefetched
+                                   // receives they read the producer's copy in place (bind_direct)
+  std::vector<DepRect> host_deps;  // host copy of d_deps (rebound by bind_direct)
+  bool direct_bound = false;       // bind_direct rebound at least one receive
   std::vector<Buffer> buf;         // indexed by exec id (meaningful at owners)
   std::vector<Op> ops;
   std::vector<ed_machine_c> counters;
@@ -440,6 +445,7 @@ struct ed_plan_h {
   void build();
   void allocate();
   void record();
+  void bind_direct();  // peer transport: point direct receives' readers at the producers' chunks
   void launch_op(size_t i, cudaStream_t s, bool branch = false);  // branch: runs beside other launches
   void enqueue(cudaStream_t s);
   std::vector<cudaEvent_t> comm_events;  // fork / join points of the comm stream
