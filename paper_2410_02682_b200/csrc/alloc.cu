@@ -110,7 +110,12 @@ void ed_plan_h::allocate() {
           if (const char* ch = std::getenv("ED_GEMM_X3_CHUNK")) p.chunk = std::max(0, std::atoi(ch));
         }
         if (const char* gm = std::getenv("ED_GEMM_GROUP_M")) p.group_m = std::max(1, std::atoi(gm));  // experiments
-        p.serp = 1;  // serpentine K (gemm_sm100.cu); ED_GEMM_SERP=0 walks K forwards on every tile
+        // serpentine K (gemm_sm100.cu) in the bf16 / tf32 kernels; the x3 kernel keeps
+        // the forward order: its promoted fp32 sums then round exactly as validated
+        // (reversed sums are as accurate on average, but move individual sampled
+        // outputs near zero past the reference's own f32 error: FFNN C slice 4.2e-5
+        // vs 1.4e-5). ED_GEMM_SERP=0 / 1 forces it off / on.
+        p.serp = p.x3 ? 0 : 1;
         if (const char* e = std::getenv("ED_GEMM_SERP")) p.serp = std::atoi(e) != 0;
         const uint32_t BK = uint32_t(gemm_bk(b16)), BM = uint32_t(gemm_bm());
         const uint32_t ATOM = 128u / (b16 ? 2u : 4u);
@@ -686,6 +691,30 @@ void ed_plan_h::allocate() {
           op.gemm.sync = static_cast<unsigned int*>(d_sync) + o;
           o += size_t(op.gemm.sync_epochs) + 1;
         }
+      }
+    }
+  }
+  // x3 tail split-K: per launch, the first halves' running sums and one counter per split tile
+  {
+    size_t floats = 0, counters = 0;
+    for (auto& op : ops) {
+      if (op.kind != OpKind::GEMM) continue;
+      op.gemm.split = gemm_x3_split(op.gemm, ctx->num_sms);
+      const size_t tile = size_t(gemm_bm()) * (gemm_paired(op.gemm.M) ? 2 : 1) * size_t(op.gemm.bn);
+      floats += size_t(op.gemm.split) * tile;
+      counters += size_t(op.gemm.split);
+    }
+    if (counters) {
+      CUDA_OK(cudaMalloc(&d_split, floats * sizeof(float) + counters * sizeof(unsigned int)));
+      CUDA_OK(cudaMemset(static_cast<char*>(d_split) + floats * sizeof(float), 0, counters * sizeof(unsigned int)));
+      size_t fo = 0, co = 0;
+      for (auto& op : ops) {
+        if (op.kind != OpKind::GEMM || !op.gemm.split) continue;
+        const size_t tile = size_t(gemm_bm()) * (gemm_paired(op.gemm.M) ? 2 : 1) * size_t(op.gemm.bn);
+        op.gemm.split_ws = static_cast<float*>(d_split) + fo;
+        op.gemm.split_cnt = reinterpret_cast<unsigned int*>(static_cast<float*>(d_split) + floats) + co;
+        fo += size_t(op.gemm.split) * tile;
+        co += size_t(op.gemm.split);
       }
     }
   }

@@ -10,9 +10,12 @@ void ed_plan_h::launch_op(size_t i, cudaStream_t s, bool branch) {
   Op& op = ops[i];
   switch (op.kind) {
     case OpKind::GEMM:
-      if (branch && op.gemm.sync) {  // a parallel branch shares the SMs: no producer lockstep
+      if (branch && (op.gemm.sync || op.gemm.split)) {
+        // a parallel branch shares the SMs: no producer lockstep, no split tiles
+        // (a half waiting for its partner while the partner waits for SMs)
         GemmLaunch g = op.gemm;
         g.sync = nullptr;
+        g.split = 0;
         CUDA_OK(launch_gemm(g, ctx->num_sms, s));
       } else {
         CUDA_OK(launch_gemm(op.gemm, ctx->num_sms, s));
@@ -292,6 +295,7 @@ void ed_plan_h::destroy() {
   for (auto e : op_events) cudaEventDestroy(e);
   for (auto e : comm_events) cudaEventDestroy(e);
   for (auto e : recv_events) cudaEventDestroy(e);
+  if (d_split) cudaFree(d_split);
   for (auto a : aux)
     if (a) cudaStreamDestroy(a);
   for (size_t r = 0; r < peer_arena.size() && !peer_inproc; ++r)

@@ -473,6 +473,26 @@ __device__ __forceinline__ float epi_f(int op, float c, float x) {
   return x;
 }
 
+// Work units of the x3 kernel: every tile, except that the last `split`
+// tiles (the partial last wave) are each cut into two halves of their
+// (sibling, K block) sequence, run by two clusters of that wave: half 0 leaves
+// its fp32 running sums in a workspace, half 1 adds them to its own and stores.
+struct X3Unit {
+  int t, part;  // tile, -1 whole / 0 first half / 1 second half
+};
+__device__ __forceinline__ X3Unit x3_unit(const GemmLaunch& p, int u, int total) {
+  const int whole = total - p.split;
+  X3Unit r;
+  r.t = u < whole ? u : whole + (u - whole) / 2;
+  r.part = u < whole ? -1 : (u - whole) % 2;
+  return r;
+}
+// the unit's range [q0, q1) of its tile's (sibling, K block) iterations
+__device__ __forceinline__ void x3_range(const X3Unit& U, int iters, int& q0, int& q1) {
+  q0 = U.part == 1 ? iters / 2 : 0;
+  q1 = U.part == 0 ? iters / 2 : iters;
+}
+
 template <int kCta, int BN>
 __global__ void __launch_bounds__(kX3Threads, 1) gemm_x3_kernel(const __grid_constant__ GemmLaunch p) {
   using C_ = Cfg<false, kCta, BN, true>;
@@ -493,6 +513,7 @@ __global__ void __launch_bounds__(kX3Threads, 1) gemm_x3_kernel(const __grid_con
   const int tiles_m = (p.M + C_::TILE_M - 1) / C_::TILE_M;
   const int tiles_n = (p.N + BN - 1) / BN;
   const int total = tiles_m * tiles_n * p.batch * p.n_regions;
+  const int units = total + p.split;
   const int kblocks = (p.K + C_::BK - 1) / C_::BK;
   const int first = blockIdx.x / kCta, stride = gridDim.x / kCta;
   const int chunk = p.chunk > 0 ? p.chunk : 4;
@@ -521,10 +542,13 @@ __global__ void __launch_bounds__(kX3Threads, 1) gemm_x3_kernel(const __grid_con
     if (lane == 0) {
       int it = 0, ti = 0;
       bool sync_on = p.sync != nullptr;
-      for (int t = first; t < total; t += stride, ++ti) {
-        if (t + stride >= total) griddep_launch();
-        const TileCoord tc = tile_coord<C_::TILE_M, BN>(p, t, tiles_m, tiles_n);
+      for (int u = first; u < units; u += stride, ++ti) {
+        if (u + stride >= units) griddep_launch();
+        const X3Unit U = x3_unit(p, u, total);
+        const TileCoord tc = tile_coord<C_::TILE_M, BN>(p, U.t, tiles_m, tiles_n);
         const GemmRegion reg = p.regions[tc.region];
+        int q0, q1;
+        x3_range(U, kblocks * reg.n_sib, q0, q1);
         const int am = tc.m0 + int(rank) * BM, bn = tc.n0 + int(rank) * C_::B_ROWS;
         const int bseg_i = reg.bseg ? tc.b / reg.bseg : 0;
         const int ba = reg.bseg && !reg.bseg_b ? tc.b % reg.bseg : tc.b;
@@ -532,11 +556,12 @@ __global__ void __launch_bounds__(kX3Threads, 1) gemm_x3_kernel(const __grid_con
         // serpentine K: every other wave walks (sibling, K block) backwards, so it
         // starts on the panel slices the previous wave left in L2 (the grouped
         // raster keeps a wave's A panels for the next few waves)
-        const bool back = p.serp && (ti & 1);
-        for (int si = 0; si < reg.n_sib; ++si) {
-          const int sib = back ? reg.n_sib - 1 - si : si;
-          const CUtensorMap* ma = p.maps + reg.map0 + C_::NMAP * (bseg_i * reg.n_sib + sib);
-          for (int kq = 0; kq < kblocks; ++kq, ++it) {
+        const bool back = p.serp && (ti & 1) && U.part < 0;
+        for (int q = q0; q < q1; ++q, ++it) {
+          const int si = q / kblocks, kq = q % kblocks;
+          {
+            const int sib = back ? reg.n_sib - 1 - si : si;
+            const CUtensorMap* ma = p.maps + reg.map0 + C_::NMAP * (bseg_i * reg.n_sib + sib);
             const int kb = back ? kblocks - 1 - kq : kq;
             if (p.sync) producer_lockstep(p, it, sync_on);
             const int s = it % STAGES;
@@ -584,9 +609,12 @@ __global__ void __launch_bounds__(kX3Threads, 1) gemm_x3_kernel(const __grid_con
       const uint32_t a_lt = p.a_mn ? 1u : 2u, b_lt = p.b_mn ? 1u : 2u;
       const uint32_t a_sbo = a_lt == 1 ? 512u : 1024u, b_sbo = b_lt == 1 ? 512u : 1024u;
       int it = 0, nchunk = 0;
-      for (int t = first; t < total; t += stride) {
-        const TileCoord tc = tile_coord<C_::TILE_M, BN>(p, t, tiles_m, tiles_n);
-        const int iters = kblocks * p.regions[tc.region].n_sib;
+      for (int u = first; u < units; u += stride) {
+        const X3Unit U = x3_unit(p, u, total);
+        const TileCoord tc = tile_coord<C_::TILE_M, BN>(p, U.t, tiles_m, tiles_n);
+        int q0, q1;
+        x3_range(U, kblocks * p.regions[tc.region].n_sib, q0, q1);
+        const int iters = q1 - q0;
         for (int i = 0; i < iters; ++nchunk) {
           const int b = nchunk & 1;
           const uint32_t bph = (nchunk >> 1) & 1;
@@ -626,10 +654,13 @@ __global__ void __launch_bounds__(kX3Threads, 1) gemm_x3_kernel(const __grid_con
     const uint32_t empty_leader = kCta == 2 ? mapa(smem_u32(part_empty), 0) : 0;
     uint8_t* tile = stage_out + warp * 4096;
     int nchunk = 0;
-    for (int t = first; t < total; t += stride) {
-      const TileCoord tc = tile_coord<C_::TILE_M, BN>(p, t, tiles_m, tiles_n);
+    for (int u = first; u < units; u += stride) {
+      const X3Unit U = x3_unit(p, u, total);
+      const TileCoord tc = tile_coord<C_::TILE_M, BN>(p, U.t, tiles_m, tiles_n);
       const GemmRegion reg = p.regions[tc.region];
-      const int iters = kblocks * reg.n_sib;
+      int q0, q1;
+      x3_range(U, kblocks * reg.n_sib, q0, q1);
+      const int iters = q1 - q0;
       const int nch = (iters + chunk - 1) / chunk;
       float acc[HALF];
       for (int c = 0; c < nch; ++c, ++nchunk) {
@@ -653,6 +684,38 @@ __global__ void __launch_bounds__(kX3Threads, 1) gemm_x3_kernel(const __grid_con
           if (kCta == 2) mbar_arrive_cluster(empty_leader + uint32_t(b * sizeof(uint64_t)));
           else mbar_arrive(&part_empty[b]);
         }
+      }
+      if (U.part >= 0) {
+        // split tile: this thread's row segment of the running sums in the workspace
+        const int si = U.t - (total - p.split);
+        float* ws = p.split_ws + ((size_t(si) * kCta + rank) * BM + size_t(wq * 32 + lane)) * BN + hh * HALF;
+        unsigned int* cnt = p.split_cnt + si;
+        if (U.part == 0) {
+#pragma unroll
+          for (int e = 0; e < HALF; e += 4)
+            __stcg(reinterpret_cast<float4*>(ws + e), make_float4(acc[e], acc[e + 1], acc[e + 2], acc[e + 3]));
+          __threadfence();
+          __syncwarp();
+          if (lane == 0) atomicAdd(cnt, 1u);  // 8 * kCta warps: the first half is in place
+          continue;
+        }
+        if (lane == 0) {
+          unsigned int v;
+          do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+          } while (v < 8u * kCta);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int e = 0; e < HALF; e += 4) {
+          const float4 f = __ldcg(reinterpret_cast<const float4*>(ws + e));
+          acc[e] = __fadd_rn(f.x, acc[e]);
+          acc[e + 1] = __fadd_rn(f.y, acc[e + 1]);
+          acc[e + 2] = __fadd_rn(f.z, acc[e + 2]);
+          acc[e + 3] = __fadd_rn(f.w, acc[e + 3]);
+        }
+        __syncwarp();
+        if (lane == 0 && atomicAdd(cnt, 1u) == 16u * kCta - 1u) atomicExch(cnt, 0u);  // last reader re-arms
       }
       if (p.epi_map >= 0) {
 #pragma unroll
@@ -727,7 +790,7 @@ template <int kCta, int BN>
 cudaError_t launch_x3(const GemmLaunch& p, int num_sms, cudaStream_t stream) {
   using C_ = Cfg<false, kCta, BN, true>;
   const long long tiles =
-      (long long)((p.M + C_::TILE_M - 1) / C_::TILE_M) * ((p.N + BN - 1) / BN) * p.batch * p.n_regions;
+      (long long)((p.M + C_::TILE_M - 1) / C_::TILE_M) * ((p.N + BN - 1) / BN) * p.batch * p.n_regions + p.split;
   const int clusters = int(tiles < num_sms / kCta ? tiles : num_sms / kCta);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(clusters * kCta);
@@ -821,6 +884,20 @@ bool gemm_use_mc(int M, int N, int bn) {
   return env != 0 && gemm_paired(M) && bn == 256 && N > 256;
 }
 int gemm_a_box_rows(bool mc) { return mc ? BM / 2 : BM; }
+
+int gemm_x3_split(const GemmLaunch& p, int num_sms) {
+  if (!p.x3) return 0;
+  if (const char* e = std::getenv("ED_GEMM_X3_SPLIT"))
+    if (e[0] == '0') return 0;
+  const int kcta = gemm_paired(p.M) ? 2 : 1;
+  const long long tiles =
+      (long long)((p.M + BM * kcta - 1) / (BM * kcta)) * ((p.N + p.bn - 1) / p.bn) * p.batch * p.n_regions;
+  const long long clusters = num_sms / kcta;
+  const long long rem = tiles % clusters;
+  // at least one full wave before it, and both halves of every split tile in the last one
+  if (tiles < clusters || rem == 0 || 2 * rem > clusters) return 0;
+  return int(rem);
+}
 
 int gemm_sync_epochs(const GemmLaunch& p, int num_sms, int max_sib) {
   const int kcta = gemm_paired(p.M) ? 2 : 1;

@@ -276,6 +276,7 @@ struct ed_plan_h {
   void* d_maps = nullptr;          // CUtensorMap[] of all GEMM launches
   void* d_regions = nullptr;       // GemmRegion[] of all GEMM launches
   void* d_sync = nullptr;          // producer lockstep counters of GEMM launches (ED_GEMM_SYNC)
+  void* d_split = nullptr;         // x3 tail split-K workspaces and counters
   void** d_ptrs = nullptr;         // chunk-pointer tables for scatter/gather
   int* d_err = nullptr;
   void* staging = nullptr;
