@@ -5,27 +5,26 @@
 // fp32. The [h, s, s2] logits never reach HBM (the unfused fp32x3 path moves
 // them through HBM five times: T1, softmax in/out, its lo shadow, O's reads).
 //
-// A job is one 128-row query tile of one head. TMEM (512 columns):
-//   Q [0,128) (fp32: the MMA reads it as Q_hi)  O_j [128,256)  R(b, part) = 256 + 128 b + 64 part, b = block parity:
-//   part 0 holds S_j, then P_j (fp32, the hi operand: the MMA drops its low
-//   13 bits), part 1 holds P_j - tf32(P_j).
-// Q_lo sits in shared memory (64 KiB), so only Q_lo K_hi reads its A operand
-// from shared memory (shared-memory bandwidth bounds this kernel: per key
-// block the MMAs read ~260 KiB of operands and TMA writes 128 KiB); K_j and V_j (64 keys) stream through a
-// ring of ten 16 KiB slots (half a block's lo or hi copy each) in the order
-// the MMA consumes them: K0 | K1 V0 | K2 V1 | ...  Within S_j all Q_hi K_lo
-// products go first and within PV_j all P_hi V_lo ones, so slots are
-// released an eighth of a block at a time and the loads run well ahead.
+// A job is one 128-row query tile of one head; with kCta = 2 a cluster of two
+// CTAs takes two tiles of one head and the leader issues cta_group::2 MMAs
+// (M = 256), each CTA loading half of every K block (its 64 keys) and half of
+// every V block (64 of the d columns). TMEM (512 columns) per CTA:
+//   Q [0,128) (fp32: the MMA reads it as Q_hi)   O_j [128,256)
+//   S_j, then P_j [256,384) (fp32, the hi operand)   P_j - tf32(P_j) [384,512)
+// Q_lo sits in shared memory (64 KiB); K_j and V_j (128 keys) stream through
+// a ring of five 32 KiB slots, lo and hi copies in separate slots, in the order
+// the MMA consumes them: K0 V0 K1 V1 ...
 //
-// One warp issues the MMAs in the order S_0 | S_1 PV_0 | S_2 PV_1 | ..., so
-// S_{j+1} runs while the softmax works on S_j; the two S/P buffers alternate.
-// Promoted accumulation: every PV_j starts a fresh TMEM accumulator O_j, and
-// the correction warps fold it into fp32 running sums in registers with
-// IEEE operations, O = f_j O + O_j (the tensor core's truncating accumulation
-// is confined to the 192 products of one key block, as in the x3 GEMM). The
-// softmax keeps the exact running row max m (log2 domain, rounded up to an
-// integer), so P <= 1 and the rescale factor f_j = 2^(m_{j-1} - m_j) is an
-// exact power of two.
+// Key blocks of 128 make every MMA N = 128 wide (the N = 64 logits of the
+// previous design ran at 2/3 of the tensor pipe's rate and left it idle most
+// of the time). One S/P buffer: the MMAs run S_j, then P V_j once the softmax
+// has stored P_j, then S_{j+1} (in issue order after the P V_j that reads
+// P_j's columns). Promoted accumulation: every P V_j starts a fresh TMEM
+// accumulator O_j, and the correction warps fold it into fp32 running sums in
+// registers with IEEE operations, O = f_j O + O_j (the tensor core's
+// truncating accumulation is confined to one key block's products, as in the
+// x3 GEMM). The softmax keeps the exact running row max m (log2 domain,
+// rounded up to an integer), so P <= 1 and f_j = 2^(m_{j-1} - m_j) is exact.
 //
 // Warps: 0-3 softmax (warp w: TMEM lanes 32w..32w+31, one thread per row),
 // 4-7 correction + epilogue (same rows), 8 TMEM allocator + MMA issuer, 9 TMA,
@@ -43,8 +42,8 @@ namespace ed {
 
 namespace {
 
-constexpr int XQ = 128;   // query rows per job
-constexpr int XKV = 64;   // keys per block
+constexpr int XQ = 128;   // query rows per CTA
+constexpr int XKV = 128;  // keys per block
 constexpr int XD = 128;   // head dim
 constexpr int kXThreads = 384;  // three warpgroups: one warp of each on every 16K-register sub-partition
 constexpr int kXCorrWarp0 = 4, kXMmaWarp = 8, kXTmaWarp = 9;
@@ -53,15 +52,15 @@ constexpr int kXCorrWarp0 = 4, kXMmaWarp = 8, kXTmaWarp = 9;
 // Per sub-partition: 168 (softmax) + 232 + 96 <= 512 per lane.
 constexpr int kXCorrRegs = 232, kXProdRegs = 96;
 constexpr int XQ_BYTES = XQ * XD * 4;   // 4 K-major chunks of 128 rows x 128 B
-// a slot holds half of one key block's K or V copy: K, two K-major chunks of
-// 64 rows x 128 B (32 of the 128 d); V, the 4 MN atoms of 32 keys x 128 B
-constexpr int XSLOT = XKV * XD * 2;
-constexpr int XNSLOT = 10;
-constexpr int XBAR_BYTES = 512;
+// a slot: kCta 1, half of one block's K or V copy (K: d chunks 2h, 2h+1 of the
+// 128 keys; V: keys 64h.. for all d); kCta 2, this CTA's whole half of a copy
+// (K: its 64 keys, all d; V: all 128 keys, its 64 d)
+constexpr int XSLOT = 32768;
+constexpr int XNSLOT = 5;
+constexpr int XBAR_BYTES = 256;
 constexpr int XSMEM = XQ_BYTES + XNSLOT * XSLOT + XBAR_BYTES + 3 * XQ * 4 + 1024;
 static_assert(XSMEM <= 232448, "shared memory");
-constexpr uint32_t T_Q = 0, T_O = 128;
-__device__ __forceinline__ uint32_t t_r(int b, int part) { return 256u + uint32_t(b) * 128u + uint32_t(part) * 64u; }
+constexpr uint32_t T_Q = 0, T_O = 128, T_S = 256, T_PL = 384;
 
 struct XJob {
   int region, h, s0;
@@ -91,11 +90,6 @@ __device__ __forceinline__ float pow2i(float k) {
   return k < -126.f ? 0.f : __int_as_float((127 + int(k)) << 23);
 }
 
-// kCta = 2: a CTA pair (cluster) takes two query tiles of one head and issues
-// cta_group::2 MMAs (M = 256): each CTA loads half of every K block (32 keys)
-// and half of every V block (64 of the d columns), halving the TMA writes
-// and B-operand reads per SM; the leader's MMA warp waits for both CTAs'
-// softmax / correction arrivals, commits reach both CTAs' barriers.
 template <int kCta>
 __global__ void __launch_bounds__(kXThreads, 1) attn_x3_kernel(const __grid_constant__ AttnLaunch p) {
   extern __shared__ uint8_t smem_raw[];
@@ -106,19 +100,16 @@ __global__ void __launch_bounds__(kXThreads, 1) attn_x3_kernel(const __grid_cons
   uint64_t* q_full = bar + 0;      // TMA -> MMA: Q_lo in smem
   uint64_t* q_empty = bar + 1;     // MMA -> TMA: the job's last S done
   uint64_t* qt_full = bar + 2;     // softmax -> MMA: Q in TMEM
-  uint64_t* s_full = bar + 3;      // [2] MMA -> softmax: S_j in R(j & 1)
-  // [2] softmax -> MMA: P_j stored. Per block parity: a softmax warp may
-  // finish block j+1 (S_{j+1} is ready early) before another warp has
-  // finished block j, so one barrier could complete on the wrong arrivals.
-  uint64_t* p_full = bar + 5;
-  uint64_t* sc_full = bar + 7;     // [2] softmax -> correction: f_j posted
-  uint64_t* pv_done = bar + 9;     // MMA -> softmax, correction: PV_j in O_j
-  uint64_t* o_free = bar + 10;     // correction -> MMA: O_j folded into the running sums
-  uint64_t* l_ready = bar + 11;    // softmax -> correction: the job's row sums posted
-  uint64_t* slot_full = bar + 12;  // [XNSLOT]
+  uint64_t* s_full = bar + 3;      // MMA -> softmax: S_j in TMEM (and P V_{j-1} done)
+  uint64_t* p_full = bar + 4;      // softmax -> MMA: P_j stored
+  uint64_t* sc_full = bar + 5;     // [2] softmax -> correction: f_j posted (block parity)
+  uint64_t* pv_done = bar + 7;     // MMA -> correction: P V_j in O_j
+  uint64_t* o_free = bar + 8;      // correction -> MMA: O_j folded into the running sums
+  uint64_t* l_ready = bar + 9;     // softmax -> correction: the job's row sums posted
+  uint64_t* slot_full = bar + 10;  // [XNSLOT]
   uint64_t* slot_empty = slot_full + XNSLOT;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(slot_empty + XNSLOT);
-  static_assert((12 + 2 * XNSLOT) * 8 + 4 <= XBAR_BYTES, "barrier space");
+  static_assert((10 + 2 * XNSLOT) * 8 + 4 <= XBAR_BYTES, "barrier space");
   float* scl = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bar) + XBAR_BYTES);  // [2][XQ] f_j per row
   float* lbuf = scl + 2 * XQ;                                                           // [XQ] row sums
 
@@ -136,11 +127,10 @@ __global__ void __launch_bounds__(kXThreads, 1) attn_x3_kernel(const __grid_cons
     mbar_init(q_full, 1);
     mbar_init(q_empty, 1);
     mbar_init(qt_full, 4 * kCta);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 4 * kCta);
-      mbar_init(&sc_full[i], 4);
-    }
+    mbar_init(s_full, 1);
+    mbar_init(p_full, 4 * kCta);
+    mbar_init(&sc_full[0], 4);
+    mbar_init(&sc_full[1], 4);
     mbar_init(pv_done, 1);
     mbar_init(o_free, 4 * kCta);
     mbar_init(l_ready, 4);
@@ -188,10 +178,11 @@ __global__ void __launch_bounds__(kXThreads, 1) attn_x3_kernel(const __grid_cons
         if (rank == 0) mbar_expect_tx(q_full, XQ_BYTES * kCta);
 #pragma unroll
         for (int c = 0; c < XD / 32; ++c) load(sQ + c * 16384, p.maps + R.q, q_full, c * 32, J.s0, J.h);
-        auto load_k = [&](int j) {
-          for (int part = 1; part >= 0; --part)  // lo first: consumed first
+        for (int j = 0; j < nb; ++j) {
+          // K_j: lo then hi. kCta 1: two slots per copy, d chunks {0,1} / {2,3} of the
+          // 128 keys (16 KiB each); kCta 2: one slot, this CTA's 64 keys, all four chunks (8 KiB)
+          for (int part = 1; part >= 0; --part)
             for (int hf = 0; hf < 2 / kCta; ++hf) {
-              // kCta 1: d chunks 2 hf, 2 hf + 1 of the 64 keys; kCta 2: all four of this CTA's 32 keys
               const int st = slot_get();
               uint8_t* dst = sKV + st * XSLOT;
               if (rank == 0) mbar_expect_tx(&slot_full[st], XSLOT * kCta);
@@ -203,28 +194,22 @@ __global__ void __launch_bounds__(kXThreads, 1) attn_x3_kernel(const __grid_cons
                      (dc * 32) % R.k.dw, key % R.k.keys, J.h + R.k.hoff);
               }
             }
-        };
-        auto load_v = [&](int j) {
+          // V_j: lo then hi, MN atoms of 32 keys x 32 d. kCta 1: two slots per copy
+          // (keys 64 hf..: 2 quarters x 4 atoms); kCta 2: one slot (4 quarters x this CTA's 2 atoms)
           for (int part = 1; part >= 0; --part)
-            for (int kb = 0; kb < 2 / kCta; ++kb) {
-              // kCta 1: keys 32 kb.. of the block, all d; kCta 2: all 64 keys, this CTA's 64 d
+            for (int hf = 0; hf < 2 / kCta; ++hf) {
               const int st = slot_get();
               uint8_t* dst = sKV + st * XSLOT;
               if (rank == 0) mbar_expect_tx(&slot_full[st], XSLOT * kCta);
 #pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                const int kk = kCta == 1 ? kb : i / 2;             // 32-key half of the block
-                const int a = kCta == 1 ? i : int(rank) * 2 + i % 2;  // 32-wide d atom
-                const int key = j * XKV + kk * 32;
+              for (int i = 0; i < 8; ++i) {
+                const int quarter = kCta == 1 ? 2 * hf + i / 4 : i / 2;
+                const int a = kCta == 1 ? i % 4 : int(rank) * 2 + i % 2;
+                const int key = j * XKV + quarter * 32;
                 load(dst + i * 4096, src_map(R.v, key, a * 32) + part * R.v.lo, &slot_full[st], (a * 32) % R.v.dw,
                      key % R.v.keys, J.h + R.v.hoff);
               }
             }
-        };
-        load_k(0);
-        for (int j = 0; j < nb; ++j) {
-          if (j + 1 < nb) load_k(j + 1);
-          load_v(j);
         }
       }
     }
@@ -249,19 +234,7 @@ __global__ void __launch_bounds__(kXThreads, 1) attn_x3_kernel(const __grid_cons
       if (kCta == 2) mbar_wait_cluster(b, ph);
       else mbar_wait(b, ph);
     };
-    int sn = 0, qn = 0, pn0 = 0, pn1 = 0, on = 0;
-#if X3_PROF
-    long long prof[4] = {0, 0, 0, 0};  // wait K slots, issue S, wait P / O free / V slots, issue PV
-    long long t0 = 0;
-#define MPROF(i)                    \
-  {                                 \
-    const long long t1 = clock64(); \
-    prof[i] += t1 - t0;             \
-    t0 = t1;                        \
-  }
-#else
-#define MPROF(i)
-#endif
+    int sn = 0, qn = 0, pn = 0, on = 0;
     auto take = [&]() {
       const int st = sn % XNSLOT;
       mbar_wait(&slot_full[st], (sn / XNSLOT) & 1);
@@ -269,29 +242,30 @@ __global__ void __launch_bounds__(kXThreads, 1) attn_x3_kernel(const __grid_cons
       return st;
     };
     const uint64_t qd = umma_desc_sw128(smem_u32(sQ), 16, 1024);
-    // K slot layout: kCta 1, two K-major chunks (8 KiB: 64 keys x 32 d) per slot, two slots
-    // per copy; kCta 2, four chunks (4 KiB: 32 keys x 32 d) in one slot. A K step of 8 d:
-    constexpr int KCH = XSLOT / (2 * kCta);          // bytes per K chunk
+    // K slot: kCta 1, two chunks of 128 keys x 128 B (16 KiB) of d chunks 2 hf, 2 hf + 1;
+    // kCta 2, four chunks of 64 keys x 128 B (8 KiB). A K step = 8 d = 32 B of a chunk row.
+    constexpr int KCH = XSLOT / (2 * kCta);
     auto k_off = [&](int k, int hf) { return uint64_t((((k / 4) - 2 * hf) * KCH + (k % 4) * 32) >> 4); };
-    auto issue_s = [&](int b) {
-      const uint32_t d = tmem + t_r(b, 0);
+    constexpr int KSTEPS = XD / 8 / (2 / kCta);  // K steps per K slot
+    auto issue_s = [&]() {
+      const uint32_t d = tmem + T_S;
 #pragma unroll
       for (int hf = 0; hf < 2 / kCta; ++hf) {  // Q_hi K_lo
         const int kl = take();
-        MPROF(0)
+        tc_fence_after();
         const uint64_t kld = umma_desc_sw128(smem_u32(sKV + kl * XSLOT), 16, 1024);
 #pragma unroll
-        for (int k = 16 / (2 / kCta) * hf; k < 16 / (2 / kCta) * (hf + 1); ++k)
+        for (int k = KSTEPS * hf; k < KSTEPS * (hf + 1); ++k)
           mma_ts(d, tmem + T_Q + uint32_t(k * 8), kld + k_off(k, kCta == 1 ? hf : 0), idesc_s, k != 0);
         commit(&slot_empty[kl]);
       }
 #pragma unroll
       for (int hf = 0; hf < 2 / kCta; ++hf) {  // Q_lo K_hi + Q_hi K_hi
         const int kh = take();
-        MPROF(0)
+        tc_fence_after();
         const uint64_t khd = umma_desc_sw128(smem_u32(sKV + kh * XSLOT), 16, 1024);
 #pragma unroll
-        for (int k = 16 / (2 / kCta) * hf; k < 16 / (2 / kCta) * (hf + 1); ++k) {
+        for (int k = KSTEPS * hf; k < KSTEPS * (hf + 1); ++k) {
           const uint64_t qo = uint64_t(((k / 4) * 16384 + (k % 4) * 32) >> 4);
           const uint64_t ko = k_off(k, kCta == 1 ? hf : 0);
           mma_ss(d, qd + qo, khd + ko, idesc_s, 1u);
@@ -299,85 +273,56 @@ __global__ void __launch_bounds__(kXThreads, 1) attn_x3_kernel(const __grid_cons
         }
         commit(&slot_empty[kh]);
       }
-      commit(&s_full[b]);
-      MPROF(1)
+      commit(s_full);
     };
-    // V slot layout: 4 MN atoms of 32 x 128 B; kCta 1, one 32-key half of the block and
-    // all four d atoms; kCta 2, both halves (atoms 0-1: keys 0-31) of this CTA's two d atoms
-    constexpr uint32_t V_LBO = kCta == 1 ? 4096u : 4096u;  // next d atom
-    auto v_off = [&](int k) {
-      return uint64_t(((kCta == 1 ? 0 : (k / 4) * 8192) + (k % 4) * 1024) >> 4);
-    };
-    auto issue_pv = [&](int b) {
-      const uint32_t ph = tmem + t_r(b, 0), pl = tmem + t_r(b, 1);
+    // V slot: 8 MN atoms of 32 keys x 128 B. kCta 1: [key quarter (2)][d atom (4)];
+    // kCta 2: [key quarter (4)][this CTA's d atom (2)]. A K step = 8 keys.
+    constexpr int QB = kCta == 1 ? 16384 : 8192;  // bytes per key quarter in a slot
+    constexpr int VSTEPS = XKV / 8 / (2 / kCta);  // K steps per V slot
+    auto v_off = [&](int k) { return uint64_t((((k % VSTEPS) / 4) * QB + (k % 4) * 1024) >> 4); };
+    auto issue_pv = [&]() {
+      const uint32_t ph = tmem + T_S, pl = tmem + T_PL;
 #pragma unroll
-      for (int kb = 0; kb < 2 / kCta; ++kb) {  // P_hi V_lo, a fresh O_j
+      for (int hf = 0; hf < 2 / kCta; ++hf) {  // P_hi V_lo, a fresh O_j
         const int vl = take();
-        MPROF(2)
-        const uint64_t vld = umma_desc_sw128(smem_u32(sKV + vl * XSLOT), V_LBO, 512, 1);
+        tc_fence_after();
+        const uint64_t vld = umma_desc_sw128(smem_u32(sKV + vl * XSLOT), 4096, 512, 1);
 #pragma unroll
-        for (int k = 8 / (2 / kCta) * kb; k < 8 / (2 / kCta) * (kb + 1); ++k)
+        for (int k = VSTEPS * hf; k < VSTEPS * (hf + 1); ++k)
           mma_ts(tmem + T_O, ph + uint32_t(k * 8), vld + v_off(k), idesc_o, k != 0);
         commit(&slot_empty[vl]);
       }
 #pragma unroll
-      for (int kb = 0; kb < 2 / kCta; ++kb) {  // P_lo V_hi + P_hi V_hi
+      for (int hf = 0; hf < 2 / kCta; ++hf) {  // P_lo V_hi + P_hi V_hi
         const int vh = take();
-        MPROF(2)
-        const uint64_t vhd = umma_desc_sw128(smem_u32(sKV + vh * XSLOT), V_LBO, 512, 1);
+        tc_fence_after();
+        const uint64_t vhd = umma_desc_sw128(smem_u32(sKV + vh * XSLOT), 4096, 512, 1);
 #pragma unroll
-        for (int k = 8 / (2 / kCta) * kb; k < 8 / (2 / kCta) * (kb + 1); ++k) {
+        for (int k = VSTEPS * hf; k < VSTEPS * (hf + 1); ++k) {
           mma_ts(tmem + T_O, pl + uint32_t(k * 8), vhd + v_off(k), idesc_o, 1u);
           mma_ts(tmem + T_O, ph + uint32_t(k * 8), vhd + v_off(k), idesc_o, 1u);
         }
         commit(&slot_empty[vh]);
       }
       commit(pv_done);
-      MPROF(3)
     };
-#if X3_PROF
-    long long jprof[2] = {0, 0};  // job boundary: wait Q_lo (TMA), wait Q in TMEM (softmax)
-    t0 = clock64();
-#endif
     for (int jb = first; jb < p.n_jobs; jb += stride) {
-#if X3_PROF
-      t0 = clock64();
-#endif
       mbar_wait(q_full, qn & 1);
-#if X3_PROF
-      jprof[0] += clock64() - t0;
-      t0 = clock64();
-#endif
       wait_arrivals(qt_full, qn & 1);
       ++qn;
       tc_fence_after();
-#if X3_PROF
-      jprof[1] += clock64() - t0;
-      t0 = clock64();
-#endif
-      issue_s(0);
-      if (nb == 1) commit(q_empty);
       for (int j = 0; j < nb; ++j) {
-        const int b = j & 1;
-        if (j + 1 < nb) {
-          // S_{j+1} overwrites the buffer PV_{j-1} read: issued after it, so in order
-          issue_s(b ^ 1);
-          if (j + 1 == nb - 1) commit(q_empty);
-        }
-        int& pn = b ? pn1 : pn0;
-        wait_arrivals(&p_full[b], pn & 1);
+        // S_j overwrites the columns P V_{j-1} read: issued after it, so in order
+        issue_s();
+        if (j == nb - 1) commit(q_empty);
+        wait_arrivals(p_full, pn & 1);
         ++pn;
         if (on > 0) wait_arrivals(o_free, (on - 1) & 1);  // the correction warps have read O_{j-1}
         ++on;
         tc_fence_after();
-        issue_pv(b);
+        issue_pv();
       }
     }
-#if X3_PROF
-    if (lane == 0 && (blockIdx.x == 0 || blockIdx.x == 77))
-      printf("cta %d mma cycles: wait K %lld issue S %lld wait P/O/V %lld issue PV %lld | job: wait Q_lo %lld Q %lld\n",
-             blockIdx.x, prof[0], prof[1], prof[2], prof[3], jprof[0], jprof[1]);
-#endif
   } else if (warp >= kXCorrWarp0) {
     // ---------------- correction: O = f_j O + O_j in registers, then the epilogue ----------------
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kXCorrRegs));
@@ -433,24 +378,12 @@ __global__ void __launch_bounds__(kXThreads, 1) attn_x3_kernel(const __grid_cons
     const int row = warp * 32 + lane;
     const uint32_t lane_base = uint32_t(warp * 32) << 16;
     const float sc2 = p.scale * 1.4426950408889634f;  // c * log2(e)
-    int sn0 = 0, sn1 = 0, pvn = 0;
-#if X3_PROF
-    long long sp[4] = {0, 0, 0, 0};  // wait S + load, compute P, wait PV_{j-1}, store
-    long long ts = clock64();
-#define SPROF(i)                    \
-  {                                 \
-    const long long t1 = clock64(); \
-    sp[i] += t1 - ts;               \
-    ts = t1;                        \
-  }
-#else
-#define SPROF(i)
-#endif
+    int sn = 0;
     for (int jb = first; jb < p.n_jobs; jb += stride) {
       const XJob J = xjob_of<kCta>(p, jb, rank);
       const AttnRegion& R = p.regions[J.region];
       {
-        // Q row -> TMEM (the previous job's last PV has completed: waited below)
+        // Q row -> TMEM (the previous job's last S has completed: its s_full was seen)
         const float4* src = reinterpret_cast<const float4*>(R.q_tm + J.h * R.q_hs + (long long)(J.s0 + row) * R.q_rs);
 #pragma unroll
         for (int c = 0; c < XD / 32; ++c) {
@@ -473,97 +406,64 @@ __global__ void __launch_bounds__(kXThreads, 1) attn_x3_kernel(const __grid_cons
       float m = 0.f, l = 0.f;
       for (int j = 0; j < nb; ++j) {
         const int b = j & 1;
-        int& sn = b ? sn1 : sn0;
-        mbar_wait(&s_full[b], sn & 1);
+        mbar_wait(s_full, sn & 1);
         ++sn;
         tc_fence_after();
-        uint32_t v[64];
-        tmem_ld_32x32b_x32(tmem + lane_base + t_r(b, 0), *reinterpret_cast<uint32_t(*)[32]>(v));
-        tmem_ld_32x32b_x32(tmem + lane_base + t_r(b, 0) + 32u, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
-        tmem_ld_wait();
-        SPROF(0)
-        float mx;
-        {
-          float a0, a1, a2, a3;
-          if (sc2 >= 0.f) {
-            a0 = a1 = a2 = a3 = -INFINITY;
+        // row max of c log2e S over the 128 keys, 32 columns at a time
+        float mx = sc2 >= 0.f ? -INFINITY : INFINITY;
+#pragma unroll 1
+        for (int c = 0; c < XKV / 32; ++c) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(tmem + lane_base + T_S + uint32_t(c * 32), v);
+          tmem_ld_wait();
+          float a0 = __uint_as_float(v[0]), a1 = __uint_as_float(v[1]);
 #pragma unroll
-            for (int e = 0; e < 64; e += 4) {
-              a0 = fmaxf(a0, __uint_as_float(v[e]));
-              a1 = fmaxf(a1, __uint_as_float(v[e + 1]));
-              a2 = fmaxf(a2, __uint_as_float(v[e + 2]));
-              a3 = fmaxf(a3, __uint_as_float(v[e + 3]));
-            }
-            mx = fmaxf(fmaxf(a0, a1), fmaxf(a2, a3)) * sc2;
-          } else {
-            a0 = a1 = a2 = a3 = INFINITY;
-#pragma unroll
-            for (int e = 0; e < 64; e += 4) {
-              a0 = fminf(a0, __uint_as_float(v[e]));
-              a1 = fminf(a1, __uint_as_float(v[e + 1]));
-              a2 = fminf(a2, __uint_as_float(v[e + 2]));
-              a3 = fminf(a3, __uint_as_float(v[e + 3]));
-            }
-            mx = fminf(fminf(a0, a1), fminf(a2, a3)) * sc2;
+          for (int e = 2; e < 32; e += 2) {
+            a0 = sc2 >= 0.f ? fmaxf(a0, __uint_as_float(v[e])) : fminf(a0, __uint_as_float(v[e]));
+            a1 = sc2 >= 0.f ? fmaxf(a1, __uint_as_float(v[e + 1])) : fminf(a1, __uint_as_float(v[e + 1]));
           }
+          mx = sc2 >= 0.f ? fmaxf(mx, fmaxf(a0, a1)) : fminf(mx, fminf(a0, a1));
         }
+        mx *= sc2;
         // the running max, rounded up to an integer: P <= 1, f exact
         const float mn = j == 0 ? ceilf(mx) : fmaxf(m, ceilf(mx));
         const float f = j == 0 ? 1.f : pow2i(m - mn);
         m = mn;
-        // P = 2^(c log2e S - m) in fp32 (registers), P - tf32(P) beside it
+        // P = 2^(c log2e S - m) in fp32 over S's columns, P - tf32(P) beside it
         float2 s0 = make_float2(0.f, 0.f), s1 = s0;
-        uint32_t lo[64];
+#pragma unroll 1  // one 32-column slice live at a time (a full row would not fit the registers)
+        for (int c = 0; c < XKV / 32; ++c) {
+          uint32_t v[32], lo[32];
+          tmem_ld_32x32b_x32(tmem + lane_base + T_S + uint32_t(c * 32), v);
+          tmem_ld_wait();
 #pragma unroll
-        for (int e = 0; e < 64; e += 2) {
-          const float y0 = xex2(fmaf(__uint_as_float(v[e]), sc2, -m));
-          const float y1 = xex2(fmaf(__uint_as_float(v[e + 1]), sc2, -m));
-          v[e] = __float_as_uint(y0);
-          v[e + 1] = __float_as_uint(y1);
-          lo[e] = __float_as_uint(lo_part(y0));
-          lo[e + 1] = __float_as_uint(lo_part(y1));
-          if (e & 2) s1 = make_float2(s1.x + y0, s1.y + y1);
-          else s0 = make_float2(s0.x + y0, s0.y + y1);
+          for (int e = 0; e < 32; e += 2) {
+            const float y0 = xex2(fmaf(__uint_as_float(v[e]), sc2, -m));
+            const float y1 = xex2(fmaf(__uint_as_float(v[e + 1]), sc2, -m));
+            v[e] = __float_as_uint(y0);
+            v[e + 1] = __float_as_uint(y1);
+            lo[e] = __float_as_uint(lo_part(y0));
+            lo[e + 1] = __float_as_uint(lo_part(y1));
+            if (e & 2) s1 = make_float2(s1.x + y0, s1.y + y1);
+            else s0 = make_float2(s0.x + y0, s0.y + y1);
+          }
+          tmem_st_32x32b_x32(tmem + lane_base + T_S + uint32_t(c * 32), v);
+          tmem_st_32x32b_x32(tmem + lane_base + T_PL + uint32_t(c * 32), lo);
         }
         l = fmaf(l, f, (s0.x + s0.y) + (s1.x + s1.y));
-        SPROF(1)
-        // The TMEM stores wait for PV_{j-1}: stores issued while that A-from-TMEM
-        // P.V runs slow it down (2.13 vs 2.02 ms on attn_big, same box); S_j is
-        // read and P_j computed meanwhile. (The first version of this kernel, which
-        // accumulated O across blocks in TMEM, gave wrong P.V results without this
-        // wait; this one is bit-identical with or without it.)
-        if (j > 0) {
-          mbar_wait(pv_done, uint32_t(pvn + j - 1) & 1);
-          tc_fence_after();
-        }
-        SPROF(2)
-        scl[b * XQ + row] = f;  // correction of block j-2 read it before PV_{j-1} was issued
-        tmem_st_32x32b_x32(tmem + lane_base + t_r(b, 0), *reinterpret_cast<uint32_t(*)[32]>(v));
-        tmem_st_32x32b_x32(tmem + lane_base + t_r(b, 0) + 32u, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
-        tmem_st_32x32b_x32(tmem + lane_base + t_r(b, 1), *reinterpret_cast<uint32_t(*)[32]>(lo));
-        tmem_st_32x32b_x32(tmem + lane_base + t_r(b, 1) + 32u, *reinterpret_cast<uint32_t(*)[32]>(lo + 32));
+        scl[b * XQ + row] = f;  // the correction of block j-2 read it before P V_{j-1} was issued
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
-          arrive_leader(&p_full[b]);
+          arrive_leader(p_full);
           mbar_arrive(&sc_full[b]);
         }
-        SPROF(3)
       }
       lbuf[row] = l;  // the correction warps read the previous job's sums before its last o_free
       __syncwarp();
       if (lane == 0) mbar_arrive(l_ready);
-      // the next job's Q store waits for this job's last PV (see above)
-      mbar_wait(pv_done, uint32_t(pvn + nb - 1) & 1);
-      pvn += nb;
-      tc_fence_after();
     }
-#if X3_PROF
-    if (row == 0 && (blockIdx.x == 0 || blockIdx.x == 77))
-      printf("cta %d softmax cycles: wait S %lld compute %lld wait PV %lld store %lld\n", blockIdx.x, sp[0], sp[1],
-             sp[2], sp[3]);
-#endif
   }
 
 done:
