@@ -429,7 +429,9 @@ void ed_plan_h::allocate() {
           else make_map(&m, q, true, gs.ak.ext, gs.am.ext, gs.am.stride, gs.ab.ext, gs.ab.stride, 64, 128);
           ar.q = int(op.maps.size());
           op.maps.push_back(m);
-          if (x3) {
+          if (x3) {  // maps[q + 1]: Q itself (read by the MMA as Q_hi)
+            make_map(&m, q, false, gs.ak.ext, gs.am.ext, gs.am.stride, gs.ab.ext, gs.ab.stride, 32, 128);
+            op.maps.push_back(m);
             ar.q_tm = static_cast<const float*>(q);
             ar.q_rs = gs.am.stride;
             ar.q_hs = gs.ab.ext > 1 ? gs.ab.stride : 0;

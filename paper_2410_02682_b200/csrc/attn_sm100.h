@@ -19,9 +19,9 @@ struct AttnRegion {
   int q;            // Q [s,h,d] (K-major, box {64, 128})
   AttnSrc k, v;     // K [s2,h,d] (K-major), V [s2,h,d] (MN-major), boxes {64, 128}
   int o32, o16;     // O [s,h,d] store maps (box {32|64, 32}), -1 if that dtype is not needed
-  // fp32x3 kernel (attn_x3_sm100.cu): q maps Q's lo shadow (staged in shared
-  // memory); q_tm (Q itself, staged in TMEM) and O (+ its lo shadow) are plain
-  // pointers, [s,h,d] with d contiguous; strides in elements
+  // fp32x3 kernel (attn_x3_sm100.cu): q maps Q's lo shadow, q + 1 Q itself
+  // (box {32, 128} each); q_tm (Q) and O (+ its lo shadow) are plain pointers,
+  // [s,h,d] with d contiguous; strides in elements
   const float* q_tm;
   long long q_rs, q_hs;
   float* o;

@@ -8,23 +8,21 @@
 // A job is one 128-row query tile of one head; with kCta = 2 a cluster of two
 // CTAs takes two tiles of one head and the leader issues cta_group::2 MMAs
 // (M = 256), each CTA loading half of every K block (its 64 keys) and half of
-// every V block (64 of the d columns). TMEM (512 columns) per CTA:
-//   Q [0,128) (fp32: the MMA reads it as Q_hi)   O_j [128,256)
-//   S_j, then P_j [256,384) (fp32, the hi operand)   P_j - tf32(P_j) [384,512)
-// Q_lo sits in shared memory (64 KiB); K_j and V_j (128 keys) stream through
-// a ring of five 32 KiB slots, lo and hi copies in separate slots, in the order
-// the MMA consumes them: K0 V0 K1 V1 ...
-//
-// Key blocks of 128 make every MMA N = 128 wide (the N = 64 logits of the
-// previous design ran at 2/3 of the tensor pipe's rate and left it idle most
-// of the time). One S/P buffer: the MMAs run S_j, then P V_j once the softmax
-// has stored P_j, then S_{j+1} (in issue order after the P V_j that reads
-// P_j's columns). Promoted accumulation: every P V_j starts a fresh TMEM
-// accumulator O_j, and the correction warps fold it into fp32 running sums in
-// registers with IEEE operations, O = f_j O + O_j (the tensor core's
-// truncating accumulation is confined to one key block's products, as in the
-// x3 GEMM). The softmax keeps the exact running row max m (log2 domain,
-// rounded up to an integer), so P <= 1 and f_j = 2^(m_{j-1} - m_j) is exact.
+// every V block (64 of the d columns). Key blocks of 128 keep every MMA N = 128
+// wide. Q_hi (Q itself: the MMA drops the low 13 bits) and Q_lo sit in shared
+// memory (128 KiB); K_j and V_j stream through three 32 KiB slots, lo and hi
+// copies in separate slots, in the order the MMA consumes them:
+// K0 | K1 V0 | K2 V1 | ...  TMEM (512 columns) per CTA:
+//   O_j [0,128)   S/P buffer 0 [128,256)   S/P buffer 1 [256,384)   P - tf32(P) [384,512)
+// The MMAs run S_0 | S_1 PV_0 | S_2 PV_1 | ..., so S_{j+1} lands while the
+// softmax works on S_j; the softmax writes P_j over S_j's columns at once and
+// P_j - tf32(P_j) (one buffer) once PV_{j-1} has read the previous one.
+// Promoted accumulation: every PV_j starts a fresh TMEM accumulator O_j, and
+// the correction warps fold it into fp32 running sums in registers with IEEE
+// operations, O = f_j O + O_j (the tensor core's truncating accumulation is
+// confined to one key block's products, as in the x3 GEMM). The softmax keeps
+// the exact running row max m (log2 domain, rounded up to an integer), so
+// P <= 1 and f_j = 2^(m_{j-1} - m_j) is exact.
 //
 // Warps: 0-3 softmax (warp w: TMEM lanes 32w..32w+31, one thread per row),
 // 4-7 correction + epilogue (same rows), 8 TMEM allocator + MMA issuer, 9 TMA,
@@ -51,16 +49,17 @@ constexpr int kXCorrWarp0 = 4, kXMmaWarp = 8, kXTmaWarp = 9;
 // the producer warpgroup (MMA, TMA, two idle warps) gives registers back.
 // Per sub-partition: 168 (softmax) + 232 + 96 <= 512 per lane.
 constexpr int kXCorrRegs = 232, kXProdRegs = 96;
-constexpr int XQ_BYTES = XQ * XD * 4;   // 4 K-major chunks of 128 rows x 128 B
+constexpr int XQ_BYTES = XQ * XD * 4;   // per Q copy: 4 K-major chunks of 128 rows x 128 B
 // a slot: kCta 1, half of one block's K or V copy (K: d chunks 2h, 2h+1 of the
 // 128 keys; V: keys 64h.. for all d); kCta 2, this CTA's whole half of a copy
 // (K: its 64 keys, all d; V: all 128 keys, its 64 d)
 constexpr int XSLOT = 32768;
-constexpr int XNSLOT = 5;
+constexpr int XNSLOT = 3;
 constexpr int XBAR_BYTES = 256;
-constexpr int XSMEM = XQ_BYTES + XNSLOT * XSLOT + XBAR_BYTES + 3 * XQ * 4 + 1024;
+constexpr int XSMEM = 2 * XQ_BYTES + XNSLOT * XSLOT + XBAR_BYTES + 3 * XQ * 4 + 1024;
 static_assert(XSMEM <= 232448, "shared memory");
-constexpr uint32_t T_Q = 0, T_O = 128, T_S = 256, T_PL = 384;
+constexpr uint32_t T_O = 0, T_PL = 384;
+__device__ __forceinline__ uint32_t t_s(int b) { return 128u + 128u * uint32_t(b); }
 
 struct XJob {
   int region, h, s0;
@@ -94,22 +93,24 @@ template <int kCta>
 __global__ void __launch_bounds__(kXThreads, 1) attn_x3_kernel(const __grid_constant__ AttnLaunch p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;
-  uint8_t* sKV = sQ + XQ_BYTES;
+  uint8_t* sQ = smem;             // Q_lo
+  uint8_t* sQh = sQ + XQ_BYTES;   // Q (the hi operand)
+  uint8_t* sKV = sQh + XQ_BYTES;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sKV + XNSLOT * XSLOT);
-  uint64_t* q_full = bar + 0;      // TMA -> MMA: Q_lo in smem
+  uint64_t* q_full = bar + 0;      // TMA -> MMA: Q_lo and Q in smem
   uint64_t* q_empty = bar + 1;     // MMA -> TMA: the job's last S done
-  uint64_t* qt_full = bar + 2;     // softmax -> MMA: Q in TMEM
-  uint64_t* s_full = bar + 3;      // MMA -> softmax: S_j in TMEM (and P V_{j-1} done)
-  uint64_t* p_full = bar + 4;      // softmax -> MMA: P_j stored
-  uint64_t* sc_full = bar + 5;     // [2] softmax -> correction: f_j posted (block parity)
-  uint64_t* pv_done = bar + 7;     // MMA -> correction: P V_j in O_j
-  uint64_t* o_free = bar + 8;      // correction -> MMA: O_j folded into the running sums
-  uint64_t* l_ready = bar + 9;     // softmax -> correction: the job's row sums posted
-  uint64_t* slot_full = bar + 10;  // [XNSLOT]
+  uint64_t* s_full = bar + 2;      // [2] MMA -> softmax: S_j in buffer j & 1
+  // [2] softmax -> MMA: P_j stored (block parity: a softmax warp may finish
+  // block j+1 before another has finished block j)
+  uint64_t* p_full = bar + 4;
+  uint64_t* sc_full = bar + 6;     // [2] softmax -> correction: f_j posted (block parity)
+  uint64_t* pv_done = bar + 8;     // MMA -> softmax, correction: P V_j in O_j
+  uint64_t* o_free = bar + 9;      // correction -> MMA: O_j folded into the running sums
+  uint64_t* l_ready = bar + 10;    // softmax -> correction: the job's row sums posted
+  uint64_t* slot_full = bar + 11;  // [XNSLOT]
   uint64_t* slot_empty = slot_full + XNSLOT;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(slot_empty + XNSLOT);
-  static_assert((10 + 2 * XNSLOT) * 8 + 4 <= XBAR_BYTES, "barrier space");
+  static_assert((11 + 2 * XNSLOT) * 8 + 4 <= XBAR_BYTES, "barrier space");
   float* scl = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bar) + XBAR_BYTES);  // [2][XQ] f_j per row
   float* lbuf = scl + 2 * XQ;                                                           // [XQ] row sums
 
@@ -126,11 +127,11 @@ __global__ void __launch_bounds__(kXThreads, 1) attn_x3_kernel(const __grid_cons
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
     mbar_init(q_empty, 1);
-    mbar_init(qt_full, 4 * kCta);
-    mbar_init(s_full, 1);
-    mbar_init(p_full, 4 * kCta);
-    mbar_init(&sc_full[0], 4);
-    mbar_init(&sc_full[1], 4);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 4 * kCta);
+      mbar_init(&sc_full[i], 4);
+    }
     mbar_init(pv_done, 1);
     mbar_init(o_free, 4 * kCta);
     mbar_init(l_ready, 4);
@@ -175,10 +176,13 @@ __global__ void __launch_bounds__(kXThreads, 1) attn_x3_kernel(const __grid_cons
         };
         mbar_wait(q_empty, (qn & 1) ^ 1);
         ++qn;
-        if (rank == 0) mbar_expect_tx(q_full, XQ_BYTES * kCta);
+        if (rank == 0) mbar_expect_tx(q_full, 2 * XQ_BYTES * kCta);
 #pragma unroll
-        for (int c = 0; c < XD / 32; ++c) load(sQ + c * 16384, p.maps + R.q, q_full, c * 32, J.s0, J.h);
-        for (int j = 0; j < nb; ++j) {
+        for (int c = 0; c < XD / 32; ++c) {
+          load(sQ + c * 16384, p.maps + R.q, q_full, c * 32, J.s0, J.h);
+          load(sQh + c * 16384, p.maps + R.q + 1, q_full, c * 32, J.s0, J.h);
+        }
+        auto load_k = [&](int j) {
           // K_j: lo then hi. kCta 1: two slots per copy, d chunks {0,1} / {2,3} of the
           // 128 keys (16 KiB each); kCta 2: one slot, this CTA's 64 keys, all four chunks (8 KiB)
           for (int part = 1; part >= 0; --part)
@@ -194,6 +198,8 @@ __global__ void __launch_bounds__(kXThreads, 1) attn_x3_kernel(const __grid_cons
                      (dc * 32) % R.k.dw, key % R.k.keys, J.h + R.k.hoff);
               }
             }
+        };
+        auto load_v = [&](int j) {
           // V_j: lo then hi, MN atoms of 32 keys x 32 d. kCta 1: two slots per copy
           // (keys 64 hf..: 2 quarters x 4 atoms); kCta 2: one slot (4 quarters x this CTA's 2 atoms)
           for (int part = 1; part >= 0; --part)
@@ -210,6 +216,11 @@ __global__ void __launch_bounds__(kXThreads, 1) attn_x3_kernel(const __grid_cons
                      key % R.v.keys, J.h + R.v.hoff);
               }
             }
+        };
+        load_k(0);  // the MMA's consumption order: K0 | K1 V0 | K2 V1 | ...
+        for (int j = 0; j < nb; ++j) {
+          if (j + 1 < nb) load_k(j + 1);
+          load_v(j);
         }
       }
     }
@@ -234,29 +245,32 @@ __global__ void __launch_bounds__(kXThreads, 1) attn_x3_kernel(const __grid_cons
       if (kCta == 2) mbar_wait_cluster(b, ph);
       else mbar_wait(b, ph);
     };
-    int sn = 0, qn = 0, pn = 0, on = 0;
+    int sn = 0, qn = 0, pn0 = 0, pn1 = 0, on = 0;
     auto take = [&]() {
       const int st = sn % XNSLOT;
       mbar_wait(&slot_full[st], (sn / XNSLOT) & 1);
       ++sn;
       return st;
     };
-    const uint64_t qd = umma_desc_sw128(smem_u32(sQ), 16, 1024);
+    const uint64_t qd = umma_desc_sw128(smem_u32(sQ), 16, 1024);    // Q_lo
+    const uint64_t qhd = umma_desc_sw128(smem_u32(sQh), 16, 1024);  // Q (hi)
     // K slot: kCta 1, two chunks of 128 keys x 128 B (16 KiB) of d chunks 2 hf, 2 hf + 1;
     // kCta 2, four chunks of 64 keys x 128 B (8 KiB). A K step = 8 d = 32 B of a chunk row.
     constexpr int KCH = XSLOT / (2 * kCta);
     auto k_off = [&](int k, int hf) { return uint64_t((((k / 4) - 2 * hf) * KCH + (k % 4) * 32) >> 4); };
     constexpr int KSTEPS = XD / 8 / (2 / kCta);  // K steps per K slot
-    auto issue_s = [&]() {
-      const uint32_t d = tmem + T_S;
+    auto issue_s = [&](int b) {
+      const uint32_t d = tmem + t_s(b);
 #pragma unroll
       for (int hf = 0; hf < 2 / kCta; ++hf) {  // Q_hi K_lo
         const int kl = take();
         tc_fence_after();
         const uint64_t kld = umma_desc_sw128(smem_u32(sKV + kl * XSLOT), 16, 1024);
 #pragma unroll
-        for (int k = KSTEPS * hf; k < KSTEPS * (hf + 1); ++k)
-          mma_ts(d, tmem + T_Q + uint32_t(k * 8), kld + k_off(k, kCta == 1 ? hf : 0), idesc_s, k != 0);
+        for (int k = KSTEPS * hf; k < KSTEPS * (hf + 1); ++k) {
+          const uint64_t qo = uint64_t(((k / 4) * 16384 + (k % 4) * 32) >> 4);
+          mma_ss(d, qhd + qo, kld + k_off(k, kCta == 1 ? hf : 0), idesc_s, k != 0);
+        }
         commit(&slot_empty[kl]);
       }
 #pragma unroll
@@ -269,19 +283,19 @@ __global__ void __launch_bounds__(kXThreads, 1) attn_x3_kernel(const __grid_cons
           const uint64_t qo = uint64_t(((k / 4) * 16384 + (k % 4) * 32) >> 4);
           const uint64_t ko = k_off(k, kCta == 1 ? hf : 0);
           mma_ss(d, qd + qo, khd + ko, idesc_s, 1u);
-          mma_ts(d, tmem + T_Q + uint32_t(k * 8), khd + ko, idesc_s, 1u);
+          mma_ss(d, qhd + qo, khd + ko, idesc_s, 1u);
         }
         commit(&slot_empty[kh]);
       }
-      commit(s_full);
+      commit(&s_full[b]);
     };
     // V slot: 8 MN atoms of 32 keys x 128 B. kCta 1: [key quarter (2)][d atom (4)];
     // kCta 2: [key quarter (4)][this CTA's d atom (2)]. A K step = 8 keys.
     constexpr int QB = kCta == 1 ? 16384 : 8192;  // bytes per key quarter in a slot
     constexpr int VSTEPS = XKV / 8 / (2 / kCta);  // K steps per V slot
     auto v_off = [&](int k) { return uint64_t((((k % VSTEPS) / 4) * QB + (k % 4) * 1024) >> 4); };
-    auto issue_pv = [&]() {
-      const uint32_t ph = tmem + T_S, pl = tmem + T_PL;
+    auto issue_pv = [&](int b) {
+      const uint32_t ph = tmem + t_s(b), pl = tmem + T_PL;
 #pragma unroll
       for (int hf = 0; hf < 2 / kCta; ++hf) {  // P_hi V_lo, a fresh O_j
         const int vl = take();
@@ -308,19 +322,24 @@ __global__ void __launch_bounds__(kXThreads, 1) attn_x3_kernel(const __grid_cons
     };
     for (int jb = first; jb < p.n_jobs; jb += stride) {
       mbar_wait(q_full, qn & 1);
-      wait_arrivals(qt_full, qn & 1);
       ++qn;
       tc_fence_after();
+      issue_s(0);
+      if (nb == 1) commit(q_empty);
       for (int j = 0; j < nb; ++j) {
-        // S_j overwrites the columns P V_{j-1} read: issued after it, so in order
-        issue_s();
-        if (j == nb - 1) commit(q_empty);
-        wait_arrivals(p_full, pn & 1);
+        const int b = j & 1;
+        if (j + 1 < nb) {
+          // S_{j+1} overwrites the buffer PV_{j-1} read: issued after it, so in order
+          issue_s(b ^ 1);
+          if (j + 1 == nb - 1) commit(q_empty);
+        }
+        int& pn = b ? pn1 : pn0;
+        wait_arrivals(&p_full[b], pn & 1);
         ++pn;
         if (on > 0) wait_arrivals(o_free, (on - 1) & 1);  // the correction warps have read O_{j-1}
         ++on;
         tc_fence_after();
-        issue_pv();
+        issue_pv(b);
       }
     }
   } else if (warp >= kXCorrWarp0) {
@@ -378,43 +397,22 @@ __global__ void __launch_bounds__(kXThreads, 1) attn_x3_kernel(const __grid_cons
     const int row = warp * 32 + lane;
     const uint32_t lane_base = uint32_t(warp * 32) << 16;
     const float sc2 = p.scale * 1.4426950408889634f;  // c * log2(e)
-    int sn = 0;
+    int sn0 = 0, sn1 = 0, pvn = 0;
     for (int jb = first; jb < p.n_jobs; jb += stride) {
-      const XJob J = xjob_of<kCta>(p, jb, rank);
-      const AttnRegion& R = p.regions[J.region];
-      {
-        // Q row -> TMEM (the previous job's last S has completed: its s_full was seen)
-        const float4* src = reinterpret_cast<const float4*>(R.q_tm + J.h * R.q_hs + (long long)(J.s0 + row) * R.q_rs);
-#pragma unroll
-        for (int c = 0; c < XD / 32; ++c) {
-          uint32_t w[32];
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const float4 v = __ldg(src + c * 8 + q);
-            w[4 * q] = __float_as_uint(v.x);
-            w[4 * q + 1] = __float_as_uint(v.y);
-            w[4 * q + 2] = __float_as_uint(v.z);
-            w[4 * q + 3] = __float_as_uint(v.w);
-          }
-          tmem_st_32x32b_x32(tmem + lane_base + T_Q + uint32_t(c * 32), w);
-        }
-        tmem_st_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) arrive_leader(qt_full);
-      }
       float m = 0.f, l = 0.f;
       for (int j = 0; j < nb; ++j) {
         const int b = j & 1;
-        mbar_wait(s_full, sn & 1);
+        int& sn = b ? sn1 : sn0;
+        mbar_wait(&s_full[b], sn & 1);
         ++sn;
         tc_fence_after();
+        const uint32_t ts = tmem + lane_base + t_s(b);
         // row max of c log2e S over the 128 keys, 32 columns at a time
         float mx = sc2 >= 0.f ? -INFINITY : INFINITY;
 #pragma unroll 1
         for (int c = 0; c < XKV / 32; ++c) {
           uint32_t v[32];
-          tmem_ld_32x32b_x32(tmem + lane_base + T_S + uint32_t(c * 32), v);
+          tmem_ld_32x32b_x32(ts + uint32_t(c * 32), v);
           tmem_ld_wait();
           float a0 = __uint_as_float(v[0]), a1 = __uint_as_float(v[1]);
 #pragma unroll
@@ -429,12 +427,12 @@ __global__ void __launch_bounds__(kXThreads, 1) attn_x3_kernel(const __grid_cons
         const float mn = j == 0 ? ceilf(mx) : fmaxf(m, ceilf(mx));
         const float f = j == 0 ? 1.f : pow2i(m - mn);
         m = mn;
-        // P = 2^(c log2e S - m) in fp32 over S's columns, P - tf32(P) beside it
+        // P = 2^(c log2e S - m) in fp32 over S's columns (its own buffer: at once)
         float2 s0 = make_float2(0.f, 0.f), s1 = s0;
-#pragma unroll 1  // one 32-column slice live at a time (a full row would not fit the registers)
+#pragma unroll 1  // one 32-column slice live at a time
         for (int c = 0; c < XKV / 32; ++c) {
-          uint32_t v[32], lo[32];
-          tmem_ld_32x32b_x32(tmem + lane_base + T_S + uint32_t(c * 32), v);
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(ts + uint32_t(c * 32), v);
           tmem_ld_wait();
 #pragma unroll
           for (int e = 0; e < 32; e += 2) {
@@ -442,21 +440,34 @@ __global__ void __launch_bounds__(kXThreads, 1) attn_x3_kernel(const __grid_cons
             const float y1 = xex2(fmaf(__uint_as_float(v[e + 1]), sc2, -m));
             v[e] = __float_as_uint(y0);
             v[e + 1] = __float_as_uint(y1);
-            lo[e] = __float_as_uint(lo_part(y0));
-            lo[e + 1] = __float_as_uint(lo_part(y1));
             if (e & 2) s1 = make_float2(s1.x + y0, s1.y + y1);
             else s0 = make_float2(s0.x + y0, s0.y + y1);
           }
-          tmem_st_32x32b_x32(tmem + lane_base + T_S + uint32_t(c * 32), v);
-          tmem_st_32x32b_x32(tmem + lane_base + T_PL + uint32_t(c * 32), lo);
+          tmem_st_32x32b_x32(ts + uint32_t(c * 32), v);
         }
         l = fmaf(l, f, (s0.x + s0.y) + (s1.x + s1.y));
-        scl[b * XQ + row] = f;  // the correction of block j-2 read it before P V_{j-1} was issued
+        // P - tf32(P) goes to the one P_lo buffer, which PV_{j-1} reads
+        if (j > 0 || jb != first) {
+          mbar_wait(pv_done, uint32_t(pvn - 1) & 1);
+          tc_fence_after();
+        }
+        tmem_st_wait();
+#pragma unroll 1
+        for (int c = 0; c < XKV / 32; ++c) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(ts + uint32_t(c * 32), v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] = __float_as_uint(lo_part(__uint_as_float(v[e])));
+          tmem_st_32x32b_x32(tmem + lane_base + T_PL + uint32_t(c * 32), v);
+        }
+        ++pvn;
+        scl[b * XQ + row] = f;  // the correction of block j-2 read it before PV_{j-1} was issued
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
-          arrive_leader(p_full);
+          arrive_leader(&p_full[b]);
           mbar_arrive(&sc_full[b]);
         }
       }
