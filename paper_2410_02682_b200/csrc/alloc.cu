@@ -443,7 +443,7 @@ void ed_plan_h::allocate() {
           // the lo twins follow the hi maps (AttnSrc::lo)
           auto kv_map = [&](const void* base, int64_t dext, int64_t kext, int64_t kstr, int64_t hext, int64_t hstr,
                             bool is_v) {
-            if (!x3) make_map(&m, base, true, dext, kext, kstr, hext, hstr, 64, is_v ? 128 : 128 / attn_cta(a.S, a.D));
+            if (!x3) make_map(&m, base, true, dext, kext, kstr, hext, hstr, 64, 128);
             else if (!is_v) make_map(&m, base, false, dext, kext, kstr, hext, hstr, 32, uint32_t(128 / attn_x3_cta(a.S)));
             else make_map(&m, base, false, dext, kext, kstr, hext, hstr, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
             op.maps.push_back(m);

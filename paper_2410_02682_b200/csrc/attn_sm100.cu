@@ -75,23 +75,18 @@ constexpr int kPolyPairs = ED_ATTN_POLY;
 constexpr int kSplitFr = ED_ATTN_SPLIT;
 static_assert(kSplitFr >= 1 && kSplitFr <= 3, "P.V starts after 1-3 of the 4 P fragments");
 
-// kCta = 2: a cluster pair issues cta_group::2 MMAs (M = 256, tile t of both
-// CTAs), each CTA holding half of every K block (its 64 keys) and of every V
-// block (its 64 d columns): half the TMA bytes and B-operand reads per SM,
-// twice the ring stages in the same shared memory.
-template <int D, int kCta = 1>
+template <int D>
 struct ACfg {
   static constexpr int Q_BYTES = BQ * D * 2;    // D/64 K-major chunks of 16 KiB
-  static constexpr int KV_BYTES = BKV * D * 2 / kCta;  // K: D/64 K-major chunks; V: D/64 / kCta MN atoms of 128 keys x 128 B
-  static constexpr int K_CHUNK = BKV / kCta * 128;     // bytes per 64-d chunk of K
-  static constexpr int KV_STAGES = (D == 64 ? 6 : 3) * kCta;
+  static constexpr int KV_BYTES = BKV * D * 2;  // K: D/64 K-major chunks; V: D/64 MN atoms of 128 key-rows x 128 B
+  static constexpr int KV_STAGES = D == 64 ? 6 : 3;
   static constexpr int STG_BYTES = 4096;        // per correction warp, two of them: 32 rows x 128 B
   static constexpr int SMEM = 2 * Q_BYTES + KV_STAGES * KV_BYTES + 8 * STG_BYTES + 1024 + 512 + 2048;
   static constexpr int TMEM_COLS = 512;
   __host__ __device__ static constexpr int s_col(int t) { return t * BKV; }
   __host__ __device__ static constexpr int o_col(int t) { return 2 * BKV + t * D; }
 };
-static_assert(ACfg<128>::SMEM <= 232448 && ACfg<64>::SMEM <= 232448 && ACfg<128, 2>::SMEM <= 232448, "shared memory");
+static_assert(ACfg<128>::SMEM <= 232448 && ACfg<64>::SMEM <= 232448, "shared memory");
 
 struct Job {
   int region, h, s0, two;
@@ -99,10 +94,8 @@ struct Job {
 
 // Jobs [0, n_pair) are tile pairs (2q, 2q+1) of a head; the remaining pair
 // units are split into single tiles, then the odd last tile of every head.
-// With kCta = 2 a tile is 256 rows, 128 of them in each CTA of the pair.
-template <int kCta>
 __device__ __forceinline__ Job job_of(const AttnLaunch& p, int j) {
-  const int tph = p.S / (BQ * kCta), pph = tph / 2;
+  const int tph = p.S / BQ, pph = tph / 2;
   const int units = p.n_regions * p.H * pph;
   int rh, tile, two;
   if (j < p.n_pair_jobs) {
@@ -124,7 +117,7 @@ __device__ __forceinline__ Job job_of(const AttnLaunch& p, int j) {
   Job r;
   r.region = rh / p.H;
   r.h = rh % p.H;
-  r.s0 = tile * BQ * kCta;
+  r.s0 = tile * BQ;
   r.two = two;
   return r;
 }
@@ -186,9 +179,9 @@ __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-template <int D, int kPoly, int kCta>
+template <int D, int kPoly>
 __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant__ AttnLaunch p) {
-  using C_ = ACfg<D, kCta>;
+  using C_ = ACfg<D>;
   constexpr int NS = C_::KV_STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -214,26 +207,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int nb = p.T / BKV;
   const int jobs = p.n_jobs;
-  const uint32_t rank = kCta == 2 ? cluster_ctarank() : 0;
-  const int first = blockIdx.x / kCta, jstride = gridDim.x / kCta;
-  // this CTA's rows of tile t of a job: 128 of the tile's BQ * kCta
-  auto tile_row = [&](const Job& J, int t) { return J.s0 + t * BQ * kCta + int(rank) * BQ; };
-  // arrive on the leader CTA's copy of a barrier (the MMA issuer's)
-  auto arrive_leader = [&](uint64_t* b) {
-    if (kCta == 2) mbar_arrive_cluster(mapa(smem_u32(b), 0));
-    else mbar_arrive(b);
-  };
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < 2; ++i) {
       mbar_init(&q_full[i], 1);
       mbar_init(&q_empty[i], 1);
       mbar_init(&s_full[i], 1);
-      mbar_init(&p_part[i], 4 * kCta);
-      mbar_init(&p_full[i], 4 * kCta);
-      mbar_init(&o_ok[i], 4 * kCta);
+      mbar_init(&p_part[i], 4);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&o_ok[i], 4);
       mbar_init(&o_full[i], 1);
-      mbar_init(&o_empty[i], 4 * kCta);
+      mbar_init(&o_empty[i], 4);
       mbar_init(&l_ready[i], 4);
     }
     for (int i = 0; i < NS; ++i) {
@@ -242,10 +226,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
     }
     fence_mbar_init();
   }
-  if (warp == kMmaWarp) tmem_alloc<C_::TMEM_COLS, kCta>(tmem_slot);
+  if (warp == kMmaWarp) tmem_alloc<C_::TMEM_COLS>(tmem_slot);
   tc_fence_before();
-  if (kCta == 2) cluster_sync();
-  else __syncthreads();
+  __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   griddep_wait();  // the prologue above overlapped the previous kernel (PDL)
@@ -258,8 +241,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
     const uint32_t lane_base = uint32_t(wq * 32) << 16;
     uint8_t* stg = sStg + wq * 2 * C_::STG_BYTES;
     int ln[2] = {0, 0}, sb = 0;
-    for (int jb = first; jb < jobs; jb += jstride) {
-      const Job J = job_of<kCta>(p, jb);
+    for (int jb = blockIdx.x; jb < jobs; jb += gridDim.x) {
+      const Job J = job_of(p, jb);
       for (int j = 0; j < nb; ++j)
         for (int t = 0; t <= J.two; ++t) {
           named_sync(1 + t * 4 + wq, 64);  // the softmax warp of these rows posted its factor
@@ -286,7 +269,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           }
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) arrive_leader(&o_ok[t]);
+          if (lane == 0) mbar_arrive(&o_ok[t]);
         }
       // ---- epilogue: O_t / l -> swizzled staging -> TMA store (32 rows per warp)
       for (int t = 0; t <= J.two; ++t) {
@@ -296,7 +279,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         ++ln[t];
         tc_fence_after();
         const uint32_t o_addr = tmem + lane_base + uint32_t(C_::o_col(t));
-        const int row0 = tile_row(J, t) + wq * 32;
+        const int row0 = J.s0 + t * BQ + wq * 32;
         for (int pass = 0; pass < 2; ++pass) {
           const int cm = pass == 0 ? p.regions[J.region].o32 : p.regions[J.region].o16;
           if (cm < 0) continue;
@@ -338,7 +321,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) arrive_leader(&o_empty[t]);
+        if (lane == 0) mbar_arrive(&o_empty[t]);
       }
     }
     if (lane == 0) bulk_wait<0>();
@@ -348,70 +331,47 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
     if (warp == kTmaWarp && lane == 0) {
       // ---------------- TMA producer: Q tiles, then the K/V ring K0 V0 K1 V1 ... ----------------
       int kvn = 0, qn0 = 0, qn1 = 0;
-      for (int jb = first; jb < jobs; jb += jstride) {
-        if (jb + jstride >= jobs) griddep_launch();  // last job: the next kernel may launch
-        const Job J = job_of<kCta>(p, jb);
+      for (int jb = blockIdx.x; jb < jobs; jb += gridDim.x) {
+        if (jb + int(gridDim.x) >= jobs) griddep_launch();  // last job: the next kernel may launch
+        const Job J = job_of(p, jb);
         const AttnRegion R = p.regions[J.region];
         const CUtensorMap* mq = p.maps + R.q;
         auto src_map = [&](const AttnSrc& a, int key, int dcol) {
           return p.maps + a.base + (key / a.keys) * a.nd + dcol / a.dw;
         };
-        // kCta = 2: data lands in this CTA's smem, the bytes count on the leader's barrier
-        auto load = [&](void* dst, const CUtensorMap* m, uint64_t* b, int c0, int c1, int c2) {
-          if (kCta == 2) tma_load_3d_2sm(dst, m, b, c0, c1, c2);
-          else tma_load_3d(dst, m, b, c0, c1, c2);
-        };
         for (int t = 0; t <= J.two; ++t) {
           int& qn = t ? qn1 : qn0;
           mbar_wait(&q_empty[t], (qn & 1) ^ 1);
           ++qn;
-          if (rank == 0) mbar_expect_tx(&q_full[t], C_::Q_BYTES * kCta);
+          mbar_expect_tx(&q_full[t], C_::Q_BYTES);
 #pragma unroll
           for (int c = 0; c < D / 64; ++c)
-            load(sQ + t * C_::Q_BYTES + c * 16384, mq, &q_full[t], c * 64, tile_row(J, t), J.h);
+            tma_load_3d(sQ + t * C_::Q_BYTES + c * 16384, mq, &q_full[t], c * 64, J.s0 + t * BQ, J.h);
         }
         for (int j = 0; j < nb; ++j) {
           for (int kv = 0; kv < 2; ++kv) {
             const int st = kvn % NS;
             mbar_wait(&kv_empty[st], ((kvn / NS) & 1) ^ 1);
             ++kvn;
-            if (rank == 0) mbar_expect_tx(&kv_full[st], C_::KV_BYTES * kCta);
+            mbar_expect_tx(&kv_full[st], C_::KV_BYTES);
             uint8_t* dst = sKV + st * C_::KV_BYTES;
             const AttnSrc& a = kv ? R.v : R.k;
-            if (kv == 0) {  // K: this CTA's BKV / kCta keys, every 64-d chunk
-              const int key = j * BKV + int(rank) * (BKV / kCta);
 #pragma unroll
-              for (int c = 0; c < D / 64; ++c)
-                load(dst + c * C_::K_CHUNK, src_map(a, key, c * 64), &kv_full[st], (c * 64) % a.dw, key % a.keys,
-                     J.h + a.hoff);
-            } else {  // V: this CTA's 64-d chunks, all BKV keys
-#pragma unroll
-              for (int c = 0; c < D / 64 / kCta; ++c) {
-                const int dc = int(rank) * (D / 64 / kCta) + c;
-                load(dst + c * 16384, src_map(a, j * BKV, dc * 64), &kv_full[st], (dc * 64) % a.dw,
-                     (j * BKV) % a.keys, J.h + a.hoff);
-              }
-            }
+            for (int c = 0; c < D / 64; ++c)
+              tma_load_3d(dst + c * 16384, src_map(a, j * BKV, c * 64), &kv_full[st], (c * 64) % a.dw,
+                          (j * BKV) % a.keys, J.h + a.hoff);
           }
         }
       }
-    } else if (warp == kMmaWarp && rank == 0) {  // a pair's MMAs are issued by its leader
+    } else if (warp == kMmaWarp) {
       // ---------------- MMA issuer: PV_0(j), S_0(j+1), PV_1(j), S_1(j+1) ----------------
       // The whole warp runs this loop (uniform values); one elected lane issues.
       // One thread, fixed order: each tile's P.V goes in as soon as its P is
       // stored, its next S right behind it (in issue order after the P.V that
       // reads P, so S may overwrite P's columns), while the other tile's
       // softmax works on its own S.
-      const uint32_t idesc_s = umma_idesc(1u, BQ * kCta, BKV, 0u, 0u);  // Q, K both K-major (d)
-      const uint32_t idesc_o = umma_idesc(1u, BQ * kCta, D, 0u, 1u);    // P from TMEM (keys), V MN-major (d)
-      auto commit = [&](uint64_t* b) {
-        if (kCta == 2) mma_commit_2sm_warp(b);
-        else mma_commit_warp(b);
-      };
-      auto wait_arrivals = [&](uint64_t* b, uint32_t ph) {  // arrivals from both CTAs' warps
-        if (kCta == 2) mbar_wait_cluster(b, ph);
-        else mbar_wait(b, ph);
-      };
+      const uint32_t idesc_s = umma_idesc(1u, BQ, BKV, 0u, 0u);  // Q, K both K-major (d)
+      const uint32_t idesc_o = umma_idesc(1u, BQ, D, 0u, 1u);    // P from TMEM (keys), V MN-major (d)
       int kvn = 0, qn0 = 0, qn1 = 0, pn0 = 0, pn1 = 0, on0 = 0, on1 = 0;
       // Descriptors are built once per operand base; a K step adds its byte
       // offset / 16 to the start-address field (no carry below 256 KiB).
@@ -423,23 +383,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         const uint64_t kd = umma_desc_sw128(smem_u32(sKV + kst * C_::KV_BYTES), 16, 1024);
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
-          const uint64_t qo = uint64_t(((k / 4) * 16384 + (k % 4) * 32) >> 4);
-          const uint64_t ko = uint64_t(((k / 4) * C_::K_CHUNK + (k % 4) * 32) >> 4);
-          if (kCta == 2) mma_f16_2sm_warp(tmem + C_::s_col(t), qd + qo, kd + ko, idesc_s, k != 0);
-          else mma_f16_warp(tmem + C_::s_col(t), qd + qo, kd + ko, idesc_s, k != 0);
+          const uint64_t off = uint64_t(((k / 4) * 16384 + (k % 4) * 32) >> 4);
+          mma_f16_warp(tmem + C_::s_col(t), qd + off, kd + off, idesc_s, k != 0);
         }
-        commit(&s_full[t]);
+        mma_commit_warp(&s_full[t]);
       };
       auto issue_pv = [&](int t, uint32_t va, int k0, int k1, bool fresh) {
         const uint64_t vd = umma_desc_sw128(va, BKV * 128, 1024);
 #pragma unroll
         for (int k = k0; k < k1; ++k)
-          if (kCta == 2)
-            mma_f16_ts_2sm_warp(tmem + C_::o_col(t), tmem + C_::s_col(t) + k * 8, vd + uint64_t((k * 2048) >> 4), idesc_o,
-                                !(fresh && k == 0));
-          else
-            mma_f16_ts_warp(tmem + C_::o_col(t), tmem + C_::s_col(t) + k * 8, vd + uint64_t((k * 2048) >> 4), idesc_o,
-                            !(fresh && k == 0));
+          mma_f16_ts_warp(tmem + C_::o_col(t), tmem + C_::s_col(t) + k * 8, vd + uint64_t((k * 2048) >> 4), idesc_o,
+                          !(fresh && k == 0));
       };
       auto take = [&]() {  // next ring stage, full
         const int st = kvn % NS;
@@ -447,8 +401,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         ++kvn;
         return st;
       };
-      for (int jb = first; jb < jobs; jb += jstride) {
-        const Job J = job_of<kCta>(p, jb);
+      for (int jb = blockIdx.x; jb < jobs; jb += gridDim.x) {
+        const Job J = job_of(p, jb);
         const int two = J.two;
         int kst = take();
         for (int t = 0; t <= two; ++t) {
@@ -457,9 +411,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
           ++qn;
           tc_fence_after();
           issue_s(t, kst);
-          if (nb == 1) commit(&q_empty[t]);
+          if (nb == 1) mma_commit_warp(&q_empty[t]);
         }
-        commit(&kv_empty[kst]);
+        mma_commit_warp(&kv_empty[kst]);
         for (int j = 0; j < nb; ++j) {
           const int vst = take();
           const uint32_t va = smem_u32(sKV + vst * C_::KV_BYTES);
@@ -467,28 +421,28 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             int& pn = t ? pn1 : pn0;
             if (j == 0) {  // the previous job's epilogue has read O_t
               int& on = t ? on1 : on0;
-              wait_arrivals(&o_empty[t], (on & 1) ^ 1);
+              mbar_wait(&o_empty[t], (on & 1) ^ 1);
               ++on;
             }
-            wait_arrivals(&o_ok[t], pn & 1);
-            wait_arrivals(&p_part[t], pn & 1);
+            mbar_wait(&o_ok[t], pn & 1);
+            mbar_wait(&p_part[t], pn & 1);
             tc_fence_after();
             issue_pv(t, va, 0, kSplitFr * 2, j == 0);
-            wait_arrivals(&p_full[t], pn & 1);
+            mbar_wait(&p_full[t], pn & 1);
             ++pn;
             tc_fence_after();
             issue_pv(t, va, kSplitFr * 2, BKV / 16, false);
-            if (t == two) commit(&kv_empty[vst]);
+            if (t == two) mma_commit_warp(&kv_empty[vst]);
             if (j == nb - 1) {
-              commit(&o_full[t]);
+              mma_commit_warp(&o_full[t]);
             } else {
               if (t == 0) {
                 kst = take();
                 tc_fence_after();
               }
               issue_s(t, kst);
-              if (j + 1 == nb - 1) commit(&q_empty[t]);
-              if (t == two) commit(&kv_empty[kst]);
+              if (j + 1 == nb - 1) mma_commit_warp(&q_empty[t]);
+              if (t == two) mma_commit_warp(&kv_empty[kst]);
             }
           }
         }
@@ -503,8 +457,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
     const uint32_t s_addr = tmem + lane_base + uint32_t(C_::s_col(t));
     const float sc2 = p.scale * 1.4426950408889634f;  // c * log2(e)
     int sn = 0;
-    for (int jb = first; jb < jobs; jb += jstride) {
-      const Job J = job_of<kCta>(p, jb);
+    for (int jb = blockIdx.x; jb < jobs; jb += gridDim.x) {
+      const Job J = job_of(p, jb);
       if (t > J.two) continue;
       float m = 0.f, l = 0.f;  // reference max (log2 domain) and row sum
       for (int j = 0; j < nb; ++j) {
@@ -582,7 +536,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             tmem_st_wait();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) arrive_leader(fr == kSplitFr - 1 ? &p_part[t] : &p_full[t]);
+            if (lane == 0) mbar_arrive(fr == kSplitFr - 1 ? &p_part[t] : &p_full[t]);
           }
         }
         // row sum off the critical path (P is already with the tensor pipe)
@@ -604,50 +558,45 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
   }
 
   tc_fence_before();
-  if (kCta == 2) cluster_sync();
-  else __syncthreads();
+  __syncthreads();
   if (warp == kMmaWarp) {
     tc_fence_after();
-    tmem_dealloc<C_::TMEM_COLS, kCta>(tmem);
+    tmem_dealloc<C_::TMEM_COLS>(tmem);
   }
 }
 
-template <int D, int kCta>
+template <int D>
 cudaError_t launch_d(const AttnLaunch& p0, int num_sms, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_kernel<D, kPolyPairs, kCta>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         ACfg<D, kCta>::SMEM);
+    cudaError_t e =
+        cudaFuncSetAttribute(attn_kernel<D, kPolyPairs>, cudaFuncAttributeMaxDynamicSharedMemorySize, ACfg<D>::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   AttnLaunch p = p0;
-  attn_schedule(p, num_sms / kCta, BQ * kCta);  // jobs per cluster, tiles of BQ * kCta rows
-  const int clusters = p.n_jobs < num_sms / kCta ? p.n_jobs : num_sms / kCta;
+  attn_schedule(p, num_sms);
 
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(clusters * kCta);
+  cfg.gridDim = dim3(p.n_jobs < num_sms ? p.n_jobs : num_sms);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = ACfg<D, kCta>::SMEM;
+  cfg.dynamicSmemBytes = ACfg<D>::SMEM;
   cfg.stream = s;
-  cudaLaunchAttribute attr2[2];
-  attr2[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr2[0].val.programmaticStreamSerializationAllowed = 1;
-  attr2[1].id = cudaLaunchAttributeClusterDimension;
-  attr2[1].val.clusterDim.x = kCta;
-  attr2[1].val.clusterDim.y = 1;
-  attr2[1].val.clusterDim.z = 1;
-  cfg.attrs = attr2;
-  cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, attn_kernel<D, kPolyPairs, kCta>, p);
+  cudaLaunchAttribute pdl[1];
+  pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  pdl[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = pdl;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, attn_kernel<D, kPolyPairs>, p);
+  return e;
 }
 
 }  // namespace
 
-void attn_schedule(AttnLaunch& p, int num_sms, int tile_rows) {
+void attn_schedule(AttnLaunch& p, int num_sms) {
   // waves of tile pairs, then one wave mixing pairs and single tiles so every
-  // CTA (cluster) ends at about the same time
-  const int tph = p.S / tile_rows, pph = tph / 2;
+  // CTA ends at about the same time
+  const int tph = p.S / BQ, pph = tph / 2;
   const long long tiles = (long long)p.n_regions * p.H * tph;
   const long long units = (long long)p.n_regions * p.H * pph;
   const long long G = num_sms;
@@ -662,33 +611,18 @@ void attn_schedule(AttnLaunch& p, int num_sms, int tile_rows) {
 }
 
 cudaError_t attn_prepare() {
-  cudaError_t e = cudaFuncSetAttribute(attn_kernel<64, kPolyPairs, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       ACfg<64>::SMEM);
+  cudaError_t e =
+      cudaFuncSetAttribute(attn_kernel<64, kPolyPairs>, cudaFuncAttributeMaxDynamicSharedMemorySize, ACfg<64>::SMEM);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(attn_kernel<128, kPolyPairs, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           ACfg<128, 2>::SMEM);
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(attn_kernel<128, kPolyPairs, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  return cudaFuncSetAttribute(attn_kernel<128, kPolyPairs>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               ACfg<128>::SMEM);
-}
-
-// cta_group::2 pairs are built and parity-clean but measured slower for this
-// kernel (attn_big 0.331 vs 0.244 ms, same box): each P.V waits for both CTAs'
-// softmax hand-offs through cluster barriers, and the two tiles' pipelines
-// couple. Opt-in with ED_ATTN_CTA=2.
-int attn_cta(int S, int D) {
-  static const int force = [] {
-    const char* e = std::getenv("ED_ATTN_CTA");
-    return e ? std::atoi(e) : 0;
-  }();
-  return force == 2 && D == 128 && S % (2 * BQ) == 0 ? 2 : 1;
 }
 
 bool attn_supported(int S, int T, int D) { return (D == 64 || D == 128) && S % BQ == 0 && T % BKV == 0 && T > 0; }
 
 cudaError_t launch_attn(const AttnLaunch& p, int num_sms, cudaStream_t s) {
-  if (p.D == 128) return attn_cta(p.S, p.D) == 2 ? launch_d<128, 2>(p, num_sms, s) : launch_d<128, 1>(p, num_sms, s);
-  if (p.D == 64) return launch_d<64, 1>(p, num_sms, s);
+  if (p.D == 128) return launch_d<128>(p, num_sms, s);
+  if (p.D == 64) return launch_d<64>(p, num_sms, s);
   return cudaErrorInvalidValue;
 }
 

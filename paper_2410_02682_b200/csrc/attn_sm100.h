@@ -42,11 +42,7 @@ struct AttnLaunch {
 // Split the (region, head, 128-row tile) space into tile-pair jobs and, for
 // the last wave, single-tile jobs, so that every CTA of the persistent grid
 // finishes at about the same time.
-void attn_schedule(AttnLaunch& p, int num_sms, int tile_rows = 128);
-
-// CTAs per cluster of the bf16 kernel: 1, or 2 (cta_group::2 pairs, opt-in with
-// ED_ATTN_CTA=2, D = 128 and S a multiple of 256 — its K maps then box 64 keys)
-int attn_cta(int S, int D);
+void attn_schedule(AttnLaunch& p, int num_sms);
 
 bool attn_supported(int S, int T, int D);
 cudaError_t attn_prepare();
