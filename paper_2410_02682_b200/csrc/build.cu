@@ -185,7 +185,7 @@ void ed_plan_h::build() {
   const bool x3 = opt.precision == ED_PREC_F32X3;
   const bool tc = opt.precision == ED_PREC_TF32 || opt.precision == ED_PREC_BF16 || x3;
   const bool bf16 = opt.precision == ED_PREC_BF16;
-  const int max_sib = x3 ? kMaxSib / 3 : kMaxSib;  // F32X3 runs 3 products per sibling
+  const int max_sib = kMaxSib;  // siblings K-concatenated into one accumulator (x3: one stage feeds all three products)
 
   // ---- per einsum: kernel class and region fusion ----
   std::map<int, GemmMap> gmap;
@@ -617,7 +617,7 @@ void ed_plan_h::build() {
         refs.push_back(ref);
         const int real = fused_head[owner[jid]] ? int(region_sibs[owner[jid]].size()) : 1;
         real_max = std::max(real_max, real);
-        ok = ok && real * int(segs.size()) * (x3 ? 3 : 1) <= kMaxSib;
+        ok = ok && real * int(segs.size()) <= kMaxSib;
       }
       if (!ok || refs.empty()) continue;
       kseg_[c] = ks;
