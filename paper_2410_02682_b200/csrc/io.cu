@@ -2,6 +2,8 @@
 // runtime.cc:66-84) and whole tensors chunked on the device (relation.cc:31-53),
 // generate_inputs on the device (runtime.cc:552-571), output assembly
 // (runtime.cc:432-448, relation.cc:55-78), and the pipelined serving loop.
+#include <vector>
+
 #include "runtime.h"
 
 namespace edrt {
@@ -468,6 +470,16 @@ ed_status ed_run_steps(ed_plan_h* h, int32_t n_steps, const ed_tensor_in_c* ins,
     cudaStream_t s = h->ctx->stream;
     CUDA_OK(cudaMemsetAsync(h->d_err, 0, sizeof(int), s));
     CUDA_OK(cudaEventRecord(h->ev0, s));
+    // ED_STEPS_TRACE=1: per step, when each copy and the run start / end (ms from the first step)
+    static const bool trace = std::getenv("ED_STEPS_TRACE") != nullptr;
+    std::vector<cudaEvent_t> tev;
+    auto mark = [&](cudaStream_t q) {
+      if (!trace) return;
+      cudaEvent_t e;
+      CUDA_OK(cudaEventCreate(&e));
+      CUDA_OK(cudaEventRecord(e, q));
+      tev.push_back(e);
+    };
     int bi = 0, bo = 0;
     for (int st = 0; st < n_steps; ++st) {
       // inputs: H2D on the copy-in stream, chunk() on the compute stream
@@ -477,7 +489,9 @@ ed_status ed_run_steps(ed_plan_h* h, int32_t n_steps, const ed_tensor_in_c* ins,
         const int b = bi++ & 1;
         const size_t bytes = size_t(t.n) * dt_size(t.dtype);
         CUDA_OK(cudaStreamWaitEvent(h->cs_in, in_free[b], 0));
+        mark(h->cs_in);
         CUDA_OK(cudaMemcpyAsync(h->stg_in[b], t.data, bytes, cudaMemcpyHostToDevice, h->cs_in));
+        mark(h->cs_in);
         CUDA_OK(cudaEventRecord(in_full[b], h->cs_in));
         CUDA_OK(cudaStreamWaitEvent(s, in_full[b], 0));
         cached_copy(h, t.vertex_id, true, h->stg_in[b], t.dtype, s);
@@ -487,8 +501,10 @@ ed_status ed_run_steps(ed_plan_h* h, int32_t n_steps, const ed_tensor_in_c* ins,
                                     h->X[id].sz, s));
         CUDA_OK(cudaEventRecord(in_free[b], s));
       }
+      mark(s);
       if (h->gexec) CUDA_OK(cudaGraphLaunch(h->gexec, s));
       else h->enqueue(s);
+      mark(s);
       // outputs: assemble on the compute stream, D2H on the copy-out stream,
       // overlapping the next step's uploads
       for (int k = 0; k < n_out; ++k) {
@@ -498,8 +514,10 @@ ed_status ed_run_steps(ed_plan_h* h, int32_t n_steps, const ed_tensor_in_c* ins,
         cached_copy(h, o.vertex_id, false, h->stg_out[b], o.dtype, s);
         CUDA_OK(cudaEventRecord(out_full[b], s));
         CUDA_OK(cudaStreamWaitEvent(h->cs_out, out_full[b], 0));
+        mark(h->cs_out);
         CUDA_OK(cudaMemcpyAsync(o.data, h->stg_out[b], size_t(o.n) * dt_size(o.dtype), cudaMemcpyDeviceToHost,
                                 h->cs_out));
+        mark(h->cs_out);
         CUDA_OK(cudaEventRecord(out_free[b], h->cs_out));
       }
     }
@@ -507,6 +525,20 @@ ed_status ed_run_steps(ed_plan_h* h, int32_t n_steps, const ed_tensor_in_c* ins,
     CUDA_OK(cudaStreamSynchronize(h->cs_out));
     CUDA_OK(cudaStreamSynchronize(s));
     CUDA_OK(cudaStreamSynchronize(h->cs_in));
+    if (trace && !tev.empty()) {
+      // per step: n_in x (H2D start, end), run start, end, n_out x (D2H start, end)
+      const size_t per = size_t(2 * n_in + 2 + 2 * n_out);
+      for (size_t st = 0; st * per < tev.size(); ++st) {
+        std::fprintf(stderr, "[ed] step %zu:", st);
+        for (size_t k = 0; k < per && st * per + k < tev.size(); ++k) {
+          float ms = 0;
+          CUDA_OK(cudaEventElapsedTime(&ms, tev[0], tev[st * per + k]));
+          std::fprintf(stderr, " %.2f", ms);
+        }
+        std::fprintf(stderr, "\n");
+      }
+      for (auto e : tev) cudaEventDestroy(e);
+    }
     int flag = 0;
     CUDA_OK(cudaMemcpy(&flag, h->d_err, sizeof(int), cudaMemcpyDeviceToHost));
     if (flag) throw ed_error(ED_ERR_EVAL, "division by zero");

@@ -244,30 +244,36 @@ __global__ void gather_kernel(const ChunkMapParams p, void* whole, int st_dt_, i
   }
 }
 
-// one row of one rectangle per block-iteration; threads along the inner run
+// A rectangle flattened into (row, slot) pairs spread over every thread of the
+// group's blocks: 16-byte slots when the runs allow it. (One row per block
+// left 7 of every 8 threads idle on 128-float runs: hoc's 1 GiB input chunking
+// took ~18 ms.)
 __global__ void __launch_bounds__(256) blockcopy_kernel(const BlockCopyParams p) {
   const BlockCopy& g = p.groups[blockIdx.y];
   const int r = p.rank;
   const int64_t inner = g.ext[r - 1];
-  for (int64_t row = blockIdx.x; row < g.rows; row += gridDim.x) {
-    int64_t rem = row, so = g.src_off, dofs = g.dst_off;
+  bool vec = p.in_dt == 1 && p.out_dt == 1 && !g.dst16 && inner % 4 == 0 && g.src_off % 4 == 0 && g.dst_off % 4 == 0;
+  for (int d = 0; d < r - 1; ++d) vec = vec && g.sstr[d] % 4 == 0 && g.dstr[d] % 4 == 0;
+  const int64_t per_row = vec ? inner / 4 : inner;
+  const int64_t slots = g.rows * per_row;
+  for (int64_t sl = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; sl < slots; sl += int64_t(gridDim.x) * blockDim.x) {
+    int64_t rem = sl / per_row;
+    const int64_t i = (sl - rem * per_row) * (vec ? 4 : 1);
+    int64_t so = g.src_off + i, dofs = g.dst_off + i;
     for (int d = r - 2; d >= 0; --d) {
       const int64_t c = rem % g.ext[d];
       rem /= g.ext[d];
       so += c * g.sstr[d];
       dofs += c * g.dstr[d];
     }
-    if (p.in_dt == 1 && p.out_dt == 1 && !g.dst16 && (so % 4) == 0 && (dofs % 4) == 0 && inner % 4 == 0) {
-      const float4* s4 = reinterpret_cast<const float4*>(static_cast<const float*>(g.src) + so);
-      float4* d4 = reinterpret_cast<float4*>(static_cast<float*>(g.dst) + dofs);
-      for (int64_t i = threadIdx.x; i < inner / 4; i += blockDim.x) d4[i] = s4[i];
+    if (vec) {
+      *reinterpret_cast<float4*>(static_cast<float*>(g.dst) + dofs) =
+          __ldcs(reinterpret_cast<const float4*>(static_cast<const float*>(g.src) + so));
       continue;
     }
-    for (int64_t i = threadIdx.x; i < inner; i += blockDim.x) {
-      const double v = ld_dt(g.src, p.in_dt, so + i);
-      if (g.dst) st_dt(g.dst, p.out_dt, dofs + i, v);
-      if (g.dst16) st_dt(g.dst16, 2, dofs + i, v);
-    }
+    const double v = ld_dt(g.src, p.in_dt, so);
+    if (g.dst) st_dt(g.dst, p.out_dt, dofs, v);
+    if (g.dst16) st_dt(g.dst16, 2, dofs, v);
   }
 }
 
@@ -334,8 +340,11 @@ cudaError_t launch_gather(const ChunkMapParams& p, void* whole, DT store, DT out
 }
 
 cudaError_t launch_blockcopy(const BlockCopyParams& p, int n_groups, int64_t max_rows, cudaStream_t s) {
-  const int64_t per = (148 * 16 + n_groups - 1) / n_groups;
-  dim3 grid(unsigned(max_rows < per ? (max_rows < 1 ? 1 : max_rows) : per), unsigned(n_groups));
+  // ~8 resident 256-thread blocks per SM across the launch; max_rows bounds a group's
+  // rows (its slots are at most max_rows * 256 float-runs of up to 1024 elements)
+  const int64_t per = (148 * 8 + n_groups - 1) / n_groups;
+  const int64_t want = (max_rows * 64 + 255) / 256;  // >= 64 slots per row on typical runs
+  dim3 grid(unsigned(want < per ? (want < 1 ? 1 : want) : per), unsigned(n_groups));
   blockcopy_kernel<<<grid, 256, 0, s>>>(p);
   return cudaGetLastError();
 }
