@@ -150,6 +150,8 @@ ed_status ed_prepare(ed_ctx* ctx, const ed_plan_c* plan, const ed_options_c* opt
             for (int id = 0; id < int(q->X.size()); ++id) off[size_t(id)] = q->local[id] ? q->arena_offset(id) : -1;
           }
           h->peer_inproc = true;
+          for (ed_plan_h* q : g->subs)
+            if (q != h && q->ctx->device == h->ctx->device) h->shared_device = true;
           h->peer_ready = true;
           CUDA_OK(cudaSetDevice(h->ctx->device));
           h->bind_direct();
@@ -264,7 +266,10 @@ ed_status ed_peer_import(ed_plan_h* h, const void* blobs, size_t blob_len, int32
       // holds the GPU for its slice while the producer's context waits —
       // receives then stay at their consumers (no prefetch)
       cudaPointerAttributes at{};
-      if (cudaPointerGetAttributes(&at, a) == cudaSuccess && at.device == h->ctx->device) h->prefetch_ok = false;
+      if (cudaPointerGetAttributes(&at, a) == cudaSuccess && at.device == h->ctx->device) {
+        h->prefetch_ok = false;
+        h->shared_device = true;
+      }
       cudaGetLastError();
     }
     h->peer_ready = true;

@@ -253,6 +253,12 @@ void ed_plan_h::enqueue(cudaStream_t s) {
 }
 
 void ed_plan_h::record() {
+  if (shared_device)
+    // ranks sharing one GPU run their kernels side by side: a split tile's second
+    // half could spin on an SM its partner half needs while that one waits for
+    // another rank's kernel to leave — split tiles need every cluster of the launch
+    for (Op& op : ops)
+      if (op.kind == OpKind::GEMM) op.gemm.split = 0;
   CUDA_OK(gemm_prepare());
   CUDA_OK(attn_prepare());
   CUDA_OK(attn_x3_prepare());

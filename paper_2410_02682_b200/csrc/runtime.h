@@ -298,6 +298,7 @@ struct ed_plan_h {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::vector<cudaEvent_t> op_events;
   bool prefetch_ok = true;                // peer receives may be prefetched (not time-sliced processes)
+  bool shared_device = false;             // another rank runs on this GPU (same-device functional mode)
   bool profile_traced = false;            // ED_PEER_TRACE printed this plan's schedule
   std::vector<cudaEvent_t> recv_events;  // profile, peer transport: [2k], [2k+1] around the k-th receive copy
   std::vector<ed_kernel_stat_c> stats;

@@ -25,6 +25,12 @@ from .plan import Plan
 HERE = os.path.dirname(os.path.abspath(__file__))
 # ED_LIB_PATH: a variant build of the same library (development experiments)
 LIB_PATH = os.environ.get("ED_LIB_PATH") or os.path.join(HERE, "libed_gpu.so")
+# Ranks sharing one GPU (Context.multi with a repeated device) run 2-4 streams
+# each; with CUDA's default 8 hardware queues, streams of different ranks alias
+# one queue, and a receive spinning on one rank's comm stream can block the
+# kernel of another rank that would end its wait (8 ranks on one B200 timed
+# out). Takes effect if the process has not created its CUDA context yet.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 _lib = None
 
