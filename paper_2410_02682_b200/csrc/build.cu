@@ -930,7 +930,7 @@ void ed_plan_h::build() {
         if (x3) {
           // lo shadows of operands no producer wrote (receives, element-wise outputs)
           auto split = [&](int o2) {
-            if (X[o2].kind == ED_EXEC_INPUT_CHUNK || !split_done.insert(o2).second) return;
+            if ((X[o2].kind == ED_EXEC_INPUT_CHUNK && local[o2]) || !split_done.insert(o2).second) return;
             Op sp{OpKind::SPLIT};
             sp.name = "split_tf32";
             sp.ptr = reinterpret_cast<void*>(o2);
@@ -970,7 +970,9 @@ void ed_plan_h::build() {
             for (int sidx : region_sibs[h])
               for (int o0 : gemm_reads(sidx)) {
                 const int o = o0;
-                if (X[o].kind == ED_EXEC_INPUT_CHUNK || !split_done.insert(o).second) continue;
+                // (an input chunk's shadow is made at upload, on the rank that holds it:
+                // one received from another rank is split here like any other receive)
+                if ((X[o].kind == ED_EXEC_INPUT_CHUNK && local[o]) || !split_done.insert(o).second) continue;
                 Op sp{OpKind::SPLIT};
                 sp.name = "split_tf32";
                 sp.ptr = reinterpret_cast<void*>(o);

@@ -269,8 +269,31 @@ void ed_plan_h::record() {
     op_events.assign(ops.size() + 1, nullptr);
     for (auto& e : op_events) CUDA_OK(cudaEventCreate(&e));
   }
-  if (opt.no_graph || opt.profile || (peer && !peer_ready)) return;  // peer: recorded by ed_peer_import
+  if (peer && !peer_ready) return;  // peer: recorded by ed_peer_import
   cudaStream_t s = ctx->stream;
+  if (opt.no_graph || opt.profile) {
+    if (peer) {
+      // launched op by op, a rank's first launch of a kernel loads it (lazy
+      // module loading), and a load can wait for running kernels — among them
+      // a wait spinning on a rank sharing this context whose own launches have
+      // not been issued yet. Instantiating a throwaway capture loads them all.
+      cudaGraph_t g = nullptr;
+      cudaGraphExec_t ge = nullptr;
+      CUDA_OK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+      try {
+        enqueue(s);
+      } catch (...) {
+        cudaStreamEndCapture(s, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+      }
+      CUDA_OK(cudaStreamEndCapture(s, &g));
+      CUDA_OK(cudaGraphInstantiate(&ge, g, 0));
+      cudaGraphExecDestroy(ge);
+      cudaGraphDestroy(g);
+    }
+    return;
+  }
   CUDA_OK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
   try {
     enqueue(s);

@@ -22,7 +22,8 @@ import tolerance as T
 pytestmark = pytest.mark.gpu
 
 CASES = [("attention_p8_L4_s1084", 4), ("attention_p8_L4_s1084", 2), ("ffnn_p4_L2_s23", 2),
-         ("chain8_pinned_L4_s7", 4), ("mix_p4_L2_s41", 2), ("softmax_p8_L4_s1084", 4)]
+         ("chain8_pinned_L4_s7", 4), ("mix_p4_L2_s41", 2), ("softmax_p8_L4_s1084", 4),
+         ("chain8_pinned_L8_s7", 8)]
 
 
 def _free_port():
@@ -205,7 +206,7 @@ def test_peer_transport_reupload_between_runs(name, world):
 @pytest.mark.timeout(300)
 @pytest.mark.parametrize("case,world", [("attention_p8_L4_s1084", 4), ("ffnn_p4_L2_s23", 2),
                                         ("chain8_pinned_L4_s7", 4), ("mix_p4_L2_s41", 2),
-                                        ("softmax_p8_L4_s1084", 4)])
+                                        ("softmax_p8_L4_s1084", 4), ("chain8_pinned_L8_s7", 8)])
 def test_single_process_multi_rank(case, world):
     """ed_ctx_create_multi: ONE process drives all L ranks (the reference's
     single execute() over L machines, runtime.cc:301-355) — here all on
@@ -235,6 +236,66 @@ def test_single_process_multi_rank(case, world):
             outs = pp.download()
             for vid, w in want.items():
                 assert np.array_equal(outs[vid], w), (case, prec, vid)
+            pp.close()
+    finally:
+        ctx.close()
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("case,world", [("attention_p8_L4_s1084", 4), ("chain8_pinned_L8_s7", 8),
+                                        ("softmax_p8_L4_s1084", 4)])
+def test_single_process_multi_rank_tensor_modes(case, world):
+    """The tensor-core modes across L in-process ranks on one GPU (8 ranks
+    share cuda:0's hardware queues: CUDA_DEVICE_MAX_CONNECTIONS): fp32x3
+    within the reference's own max_rel_err bar of the f64 outputs, bf16
+    within its normwise bar, the reference's counters, twice in a row."""
+    from paper_2410_02682_b200.executor import Context, PreparedPlan
+    name, ins, o64, o32, orc, counters, total = load_golden(case)
+    plan = load_plan(name)
+    ctx = Context.multi([0] * world)
+    try:
+        for prec in ("fp32x3", "bf16"):
+            pp = PreparedPlan(ctx, plan, precision=prec)
+            pp.upload(ins)
+            for _ in range(2):
+                rep = pp.run()
+                outs = pp.download()
+                for vid, w in o64.items():
+                    metric, err, bar = T.error(prec, outs[vid], w)
+                    assert err <= bar, (case, prec, vid, metric, err)
+                assert [tuple(m) for m in rep.machines] == [tuple(c) for c in counters]
+                assert rep.total_transferred == total
+            pp.close()
+    finally:
+        ctx.close()
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("case,world", [("ffnn_p4_L2_s23", 2), ("attention_p8_L4_s1084", 4),
+                                        ("chain8_pinned_L8_s7", 8)])
+def test_single_process_multi_rank_op_by_op(case, world):
+    """In-process ranks launched op by op (no CUDA graph; profile mode times
+    every op): each rank's kernels are loaded before its first run, so a
+    first launch cannot wait on a rank's receive spinning for a chunk whose
+    producer has not been launched yet. Bit-exact f64, per-rank kernel stats."""
+    from paper_2410_02682_b200.executor import Context, PreparedPlan
+    name, ins, o64, o32, orc, counters, total = load_golden(case)
+    plan = load_plan(name)
+    ctx = Context.multi([0] * world)
+    try:
+        for kw in ({"graph": False}, {"profile": True}):
+            pp = PreparedPlan(ctx, plan, precision="fp64", **kw)
+            pp.upload(ins)
+            for _ in range(2):
+                rep = pp.run()
+                outs = pp.download()
+                for vid, w in o64.items():
+                    assert np.array_equal(outs[vid], w), (case, kw, vid)
+                assert rep.total_transferred == total
+            if kw.get("profile"):
+                import re
+                ranks = {m.group(1) for k in pp.kernel_stats() for m in [re.match(r"r(\d+)/", k["name"])] if m}
+                assert ranks == {str(r) for r in range(world)}, ranks
             pp.close()
     finally:
         ctx.close()
