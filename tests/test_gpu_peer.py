@@ -299,3 +299,35 @@ def test_single_process_multi_rank_op_by_op(case, world):
             pp.close()
     finally:
         ctx.close()
+
+
+def _fuzz_multirank_all():
+    from test_gpu_fuzz import CASES
+    return [(c, int(c.split("_L")[1].split("_")[0])) for c in CASES if int(c.split("_L")[1].split("_")[0]) > 1]
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("case,world", _fuzz_multirank_all())
+def test_single_process_multi_rank_fuzz_tensor_modes(case, world):
+    """Every randomised graph with L > 1 (tests/test_gpu_fuzz.py) on L
+    in-process ranks of one GPU in each tensor-core mode: the received
+    operands (inputs included) carry what the mode needs — a bf16 copy, a
+    TF32 lo shadow — so each mode meets its bar (tests/tolerance.py) exactly
+    as on one rank."""
+    from test_gpu_fuzz import _load
+    from paper_2410_02682_b200.executor import Context, PreparedPlan
+    plan, ins, o64, o32, counters, total = _load(case)
+    ctx = Context.multi([0] * world)
+    try:
+        for prec in ("tf32", "bf16", "fp32x3"):
+            pp = PreparedPlan(ctx, plan, precision=prec)
+            pp.upload(ins)
+            rep = pp.run()
+            outs = pp.download()
+            for vid, w in o64.items():
+                metric, err, bar = T.error(prec, outs[vid], w)
+                assert err <= bar, (case, prec, vid, metric, err)
+            assert rep.total_transferred == total
+            pp.close()
+    finally:
+        ctx.close()
