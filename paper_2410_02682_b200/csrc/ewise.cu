@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(NT) softmax_kernel(const SoftmaxParams p) {
     for (int j = 0; j < NV; ++j) {
       const int i = (j * NT + t) * 4;
       const float* src = xr + i;
-      if (sg) {  // gather the row from its column segments in place
+      if (sg && i < p.len) {  // gather the row from its column segments in place (past the row: no segment)
         const RowSeg s = sg[i / p.seg_w];
         src = s.ptr + (row + s.row0) * s.stride + (i % p.seg_w);
       }
