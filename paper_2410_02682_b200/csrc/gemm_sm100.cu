@@ -950,8 +950,14 @@ int gemm_a_box_rows(bool mc) { return mc ? BM / 2 : BM; }
 
 int gemm_tail_split(const GemmLaunch& p, int num_sms) {
   if (p.mc) return 0;  // 4-CTA clusters: whole tiles only
-  if (const char* e = std::getenv(p.x3 ? "ED_GEMM_X3_SPLIT" : "ED_GEMM_SPLIT"))
+  // bf16 / tf32 (opt-in, ED_GEMM_SPLIT=1): measured slower — their K loops are short, so the
+  // workspace round trip and the partner wait cost more than the half wave saves (chain3 bf16
+  // 0.106 -> 0.114 ms per GEMM); fp32x3 (default on, ED_GEMM_X3_SPLIT=0 disables) gains
+  if (const char* e = std::getenv(p.x3 ? "ED_GEMM_X3_SPLIT" : "ED_GEMM_SPLIT")) {
     if (e[0] == '0') return 0;
+  } else if (!p.x3) {
+    return 0;
+  }
   const int kcta = gemm_paired(p.M) ? 2 : 1;
   const long long tiles =
       (long long)((p.M + BM * kcta - 1) / (BM * kcta)) * ((p.N + p.bn - 1) / p.bn) * p.batch * p.n_regions;
