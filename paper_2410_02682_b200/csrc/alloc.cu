@@ -701,7 +701,7 @@ void ed_plan_h::allocate() {
     size_t floats = 0, counters = 0;
     for (auto& op : ops) {
       if (op.kind != OpKind::GEMM) continue;
-      op.gemm.split = gemm_tail_split(op.gemm, ctx->num_sms);
+      op.gemm.split = gemm_x3_split(op.gemm, ctx->num_sms);
       const size_t tile = size_t(gemm_bm()) * (gemm_paired(op.gemm.M) ? 2 : 1) * size_t(op.gemm.bn);
       floats += size_t(op.gemm.split) * tile;
       counters += size_t(op.gemm.split);

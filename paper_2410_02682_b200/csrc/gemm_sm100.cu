@@ -155,26 +155,6 @@ __device__ __forceinline__ void producer_lockstep_exit(const GemmLaunch& p, int 
   }
 }
 
-// Work units of both kernels: every tile, except that the last `split`
-// tiles (the partial last wave) are each cut into two halves of their
-// (sibling, K block) sequence, run by two clusters of that wave: half 0 leaves
-// its fp32 running sums in a workspace, half 1 adds them to its own and stores.
-struct X3Unit {
-  int t, part;  // tile, -1 whole / 0 first half / 1 second half
-};
-__device__ __forceinline__ X3Unit x3_unit(const GemmLaunch& p, int u, int total) {
-  const int whole = total - p.split;
-  X3Unit r;
-  r.t = u < whole ? u : whole + (u - whole) / 2;
-  r.part = u < whole ? -1 : (u - whole) % 2;
-  return r;
-}
-// the unit's range [q0, q1) of its tile's (sibling, K block) iterations
-__device__ __forceinline__ void x3_range(const X3Unit& U, int iters, int& q0, int& q1) {
-  q0 = U.part == 1 ? iters / 2 : 0;
-  q1 = U.part == 0 ? iters / 2 : iters;
-}
-
 // kMc = 2: two 2-SM pairs form one 4-CTA cluster over a 256 x 2BN tile; they
 // share the A panel, each pair loading half of every A box and multicasting it
 // to both pairs, so each A byte leaves L2 once per cluster instead of twice.
@@ -201,7 +181,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   const int tiles_m = (p.M + C_::TILE_M - 1) / C_::TILE_M;
   const int tiles_n = (p.N + BN * kMc - 1) / (BN * kMc);  // cluster tiles along N
   const int total = tiles_m * tiles_n * p.batch * p.n_regions;
-  const int units = total + (kMc == 1 ? p.split : 0);  // split tiles: two half-K units each
   const int kblocks = (p.K + C_::BK - 1) / C_::BK;
   const int first = blockIdx.x / kClu, stride = gridDim.x / kClu;
   auto coord = [&](int t) {
@@ -236,11 +215,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     if (lane == 0) {
       int it = 0, ti = 0;
       bool sync_on = p.sync != nullptr;
-      for (int u = first; u < units; u += stride, ++ti) {
-        if (u + stride >= units) griddep_launch();  // last tile: the next kernel may launch
-        const X3Unit U = x3_unit(p, u, total);
-        const TileCoord tc = coord(U.t);
-        const bool back = p.serp && (ti & 1) && U.part < 0;  // serpentine K (see gemm_x3_kernel)
+      for (int t = first; t < total; t += stride, ++ti) {
+        if (t + stride >= total) griddep_launch();  // last tile: the next kernel may launch
+        const TileCoord tc = coord(t);
+        const bool back = p.serp && (ti & 1);  // serpentine K (see gemm_x3_kernel)
         const GemmRegion reg = p.regions[tc.region];
         const int am = tc.m0 + int(rank) * BM, bn = tc.n0 + int(rank) * C_::B_ROWS;
         // kMc: CTAs with the same rank in both pairs hold the same A rows
@@ -249,14 +227,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         const int bseg_i = reg.bseg ? tc.b / reg.bseg : 0;
         const int ba = reg.bseg && !reg.bseg_b ? tc.b % reg.bseg : tc.b;
         const int bb = reg.bseg && reg.bseg_b ? tc.b % reg.bseg : tc.b;
-        int q0, q1;
-        x3_range(U, kblocks * reg.n_sib, q0, q1);
-        {
-          for (int q = q0; q < q1; ++q, ++it) {
-            const int si = q / kblocks, kq = q % kblocks;
-            const int sib = back ? reg.n_sib - 1 - si : si;
-            const CUtensorMap* ma = p.maps + reg.map0 + C_::NMAP * (bseg_i * reg.n_sib + sib);
-            const CUtensorMap* mb = ma + 1;
+        for (int si = 0; si < reg.n_sib; ++si) {
+          const int sib = back ? reg.n_sib - 1 - si : si;
+          const CUtensorMap* ma = p.maps + reg.map0 + C_::NMAP * (bseg_i * reg.n_sib + sib);
+          const CUtensorMap* mb = ma + 1;
+          for (int kq = 0; kq < kblocks; ++kq, ++it) {
             const int kb = back ? kblocks - 1 - kq : kq;
             if (p.sync) producer_lockstep(p, it, sync_on);
             const int s = it % STAGES;
@@ -322,9 +297,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       const uint32_t a_lt = (!kBF16 && p.a_mn) ? 1u : 2u, b_lt = (!kBF16 && p.b_mn) ? 1u : 2u;
       const uint32_t a_sbo = a_lt == 1 ? 512u : 1024u, b_sbo = b_lt == 1 ? 512u : 1024u;
       int it = 0, local = 0;
-      for (int u = first; u < units; u += stride, ++local) {
-        const X3Unit U = x3_unit(p, u, total);
-        const TileCoord tc = coord(U.t);
+      for (int t = first; t < total; t += stride, ++local) {
+        const TileCoord tc = coord(t);
         const int n_sib = p.regions[tc.region].n_sib;
         const int as = local & 1;
         const uint32_t aph = (local >> 1) & 1;
@@ -332,9 +306,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         else mbar_wait(&acc_empty[as], aph ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem + uint32_t(as * BN);
-        int q0, q1;
-        x3_range(U, kblocks * n_sib, q0, q1);
-        const int iters = q1 - q0;
+        const int iters = kblocks * n_sib;
         for (int i = 0; i < iters; ++i, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
@@ -372,65 +344,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     const uint32_t empty_leader = kCta == 2 ? mapa(smem_u32(acc_empty), 2 * q) : 0;
     int local = 0;
     uint32_t stage_ctr = 0;
-    for (int u = first; u < units; u += stride, ++local) {
-      const X3Unit U = x3_unit(p, u, total);
-      const TileCoord tc = coord(U.t);
+    for (int t = first; t < total; t += stride, ++local) {
+      const TileCoord tc = coord(t);
       const GemmRegion reg = p.regions[tc.region];
       const int as = local & 1;
       const uint32_t aph = (local >> 1) & 1;
       mbar_wait(&acc_full[as], aph);
       tc_fence_after();
-      // split tile (kMc == 1): this thread's row of the tile in the workspace
-      float* ws = nullptr;
-      unsigned int* cnt = nullptr;
-      if (U.part >= 0) {
-        const int si = U.t - (total - p.split);
-        ws = p.split_ws + ((size_t(si) * kCta + rank) * BM + size_t(wq * 32 + lane)) * BN;
-        cnt = p.split_cnt + si;
-        if (U.part == 0) {  // first half: the raw fp32 sums go to the workspace
-          const uint32_t tb = tmem + (uint32_t(wq * 32) << 16) + uint32_t(as * BN);
-#pragma unroll 1
-          for (int c = 0; c < BN / 32; ++c) {
-            uint32_t r[32];
-            tmem_ld_32x32b_x32(tb + uint32_t(c * 32), r);
-            tmem_ld_wait();
-#pragma unroll
-            for (int e = 0; e < 32; e += 4)
-              __stcg(reinterpret_cast<float4*>(ws + c * 32 + e),
-                     make_float4(__uint_as_float(r[e]), __uint_as_float(r[e + 1]), __uint_as_float(r[e + 2]),
-                                 __uint_as_float(r[e + 3])));
-          }
-          __threadfence();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) {
-            atomicAdd(cnt, 1u);  // 4 * kCta warps: the first half is in place
-            if (kCta == 2) mbar_arrive_cluster(empty_leader + uint32_t(as * sizeof(uint64_t)));
-            else mbar_arrive(&acc_empty[as]);
-          }
-          continue;
-        }
-        if (lane == 0) {
-          unsigned int v;
-          do {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
-          } while (v < 4u * kCta);
-        }
-        __syncwarp();
-      }
-      // second half of a split tile: the first half's sums added before the epilogue op
-      auto add_ws = [&](uint32_t* r, int n, int col) {
-        if (!ws) return;
-#pragma unroll
-        for (int e = 0; e < 64; e += 4) {
-          if (e >= n) break;
-          const float4 f = __ldcg(reinterpret_cast<const float4*>(ws + col + e));
-          r[e] = __float_as_uint(__fadd_rn(f.x, __uint_as_float(r[e])));
-          r[e + 1] = __float_as_uint(__fadd_rn(f.y, __uint_as_float(r[e + 1])));
-          r[e + 2] = __float_as_uint(__fadd_rn(f.z, __uint_as_float(r[e + 2])));
-          r[e + 3] = __float_as_uint(__fadd_rn(f.w, __uint_as_float(r[e + 3])));
-        }
-      };
       const int row = tc.m0 + int(rank) * BM + wq * 32 + lane;
       const long long base = (long long)tc.b * p.c_sb + (long long)row * p.c_sm;
       float* c32 = reg.c32 ? reg.c32 + base : nullptr;
@@ -450,7 +370,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             tmem_ld_32x32b_x32(tbase + uint32_t(c * cols), *reinterpret_cast<uint32_t(*)[32]>(r));
             if (pass == 1) tmem_ld_32x32b_x32(tbase + uint32_t(c * cols + 32), *reinterpret_cast<uint32_t(*)[32]>(r + 32));
             tmem_ld_wait();
-            add_ws(r, cols, c * cols);
             if (p.epi_map >= 0) {
               epi32(p, r);
               if (pass == 1) epi32(p, r + 32);
@@ -492,7 +411,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           uint32_t r[32];
           tmem_ld_32x32b_x32(tbase + uint32_t(c * 32), r);
           tmem_ld_wait();
-          add_ws(r, 32, c * 32);
           if (p.epi_map >= 0) epi32(p, r);
           const int col = tc.n0 + c * 32;
           if (row >= p.M || col >= p.N) continue;
@@ -510,7 +428,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       if (lane == 0) {
         if (kCta == 2) mbar_arrive_cluster(empty_leader + uint32_t(as * sizeof(uint64_t)));
         else mbar_arrive(&acc_empty[as]);
-        if (ws && atomicAdd(cnt, 1u) == 8u * kCta - 1u) atomicExch(cnt, 0u);  // last reader re-arms
       }
     }
     if (lane == 0) bulk_wait<0>();
@@ -554,6 +471,26 @@ __device__ __forceinline__ float epi_f(int op, float c, float x) {
   if (op == 2) return -x;
   if (op == 3) return c * x;
   return x;
+}
+
+// Work units of the x3 kernel: every tile, except that the last `split`
+// tiles (the partial last wave) are each cut into two halves of their
+// (sibling, K block) sequence, run by two clusters of that wave: half 0 leaves
+// its fp32 running sums in a workspace, half 1 adds them to its own and stores.
+struct X3Unit {
+  int t, part;  // tile, -1 whole / 0 first half / 1 second half
+};
+__device__ __forceinline__ X3Unit x3_unit(const GemmLaunch& p, int u, int total) {
+  const int whole = total - p.split;
+  X3Unit r;
+  r.t = u < whole ? u : whole + (u - whole) / 2;
+  r.part = u < whole ? -1 : (u - whole) % 2;
+  return r;
+}
+// the unit's range [q0, q1) of its tile's (sibling, K block) iterations
+__device__ __forceinline__ void x3_range(const X3Unit& U, int iters, int& q0, int& q1) {
+  q0 = U.part == 1 ? iters / 2 : 0;
+  q1 = U.part == 0 ? iters / 2 : iters;
 }
 
 template <int kCta, int BN>
@@ -908,7 +845,7 @@ cudaError_t launch_t(const GemmLaunch& p, int num_sms, cudaStream_t stream) {
   using C_ = Cfg<kBF16, kCta, BN, kX3>;
   constexpr int kClu = kCta * kMc;
   const long long tiles = (long long)((p.M + C_::TILE_M - 1) / C_::TILE_M) * ((p.N + BN * kMc - 1) / (BN * kMc)) *
-                          p.batch * p.n_regions + (kMc == 1 ? p.split : 0);
+                          p.batch * p.n_regions;
   int cap = num_sms / kClu;
   const int resident = max_clusters<kBF16, kCta, BN, kX3, kMc>();
   if (kMc > 1 && resident > 0 && resident < cap) cap = resident;
@@ -948,16 +885,10 @@ bool gemm_use_mc(int M, int N, int bn) {
 }
 int gemm_a_box_rows(bool mc) { return mc ? BM / 2 : BM; }
 
-int gemm_tail_split(const GemmLaunch& p, int num_sms) {
-  if (p.mc) return 0;  // 4-CTA clusters: whole tiles only
-  // bf16 / tf32 (opt-in, ED_GEMM_SPLIT=1): measured slower — their K loops are short, so the
-  // workspace round trip and the partner wait cost more than the half wave saves (chain3 bf16
-  // 0.106 -> 0.114 ms per GEMM); fp32x3 (default on, ED_GEMM_X3_SPLIT=0 disables) gains
-  if (const char* e = std::getenv(p.x3 ? "ED_GEMM_X3_SPLIT" : "ED_GEMM_SPLIT")) {
+int gemm_x3_split(const GemmLaunch& p, int num_sms) {
+  if (!p.x3) return 0;
+  if (const char* e = std::getenv("ED_GEMM_X3_SPLIT"))
     if (e[0] == '0') return 0;
-  } else if (!p.x3) {
-    return 0;
-  }
   const int kcta = gemm_paired(p.M) ? 2 : 1;
   const long long tiles =
       (long long)((p.M + BM * kcta - 1) / (BM * kcta)) * ((p.N + p.bn - 1) / p.bn) * p.batch * p.n_regions;

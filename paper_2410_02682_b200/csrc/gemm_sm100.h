@@ -50,7 +50,7 @@ struct GemmLaunch {
   unsigned int* sync;
   int sync_g, sync_lag, sync_epochs;                // grouped raster: tile rows that advance together along N
   int serp;                   // odd tile iterations walk (sibling, K block) backwards (L2 reuse across waves)
-  // the last `split` tiles (a partial last wave of at most half the
+  // x3 kernel: the last `split` tiles (a partial last wave of at most half the
   // clusters) run as two half-K units each; split_ws holds the first halves'
   // running sums (split * TILE_M * BN floats), split_cnt one zeroed counter per tile
   int split;
@@ -73,7 +73,7 @@ cudaError_t gemm_prepare();  // sets the dynamic-smem attribute (call before cap
 cudaError_t launch_gemm(const GemmLaunch& p, int num_sms, cudaStream_t stream);
 // epochs of sync_g K blocks the busiest CTA of this launch issues (x3 kernel)
 int gemm_sync_epochs(const GemmLaunch& p, int num_sms, int max_sib);
-// tiles of the partial last wave to split in two along K (0: none; both kernels)
-int gemm_tail_split(const GemmLaunch& p, int num_sms);
+// x3 kernel: tiles of the partial last wave to split in two along K (0: none)
+int gemm_x3_split(const GemmLaunch& p, int num_sms);
 
 }  // namespace ed
